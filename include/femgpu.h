@@ -1,0 +1,242 @@
+/*
+ * femgpu.h — C-ABI of the B200-native (sm_100a) FP64 matrix-free finite-element
+ * action y = A(u)·x.  Drop-in for the reference `femsched` action path:
+ *
+ *   reference entry point                                   replaced by
+ *   -----------------------------------------------------   ---------------------------------
+ *   femsched::reference_action(const ProblemInstance&)        femgpu_create + femgpu_action
+ *     (/root/reference/proj/include/femsched/form.hpp:471-595)  (or femgpu_action_once)
+ *   femsched::run_schedule(inst, build_plan(sig, params))     femgpu_action(inst, &schedule, y)
+ *     (simulate.hpp:601-603, run_scpt :171, run_mlt :293)
+ *   femsched::Executor / ExecutionOutcome                     femgpu_execute (measured seconds)
+ *     (search.hpp:257-283)
+ *   femsched::usable_flops (form.hpp:164-173)                 femgpu_usable_flops
+ *
+ * All arguments are plain pointers and sizes; no C++ or torch types cross this
+ * boundary and no C++ exception escapes it.  Every function returns a
+ * femgpu_status; the message of the last failure on the calling thread is
+ * available from femgpu_last_error().  Status codes map onto the reference's
+ * exception types (form.hpp:23-31, form.hpp:492-495):
+ *   FEMGPU_E_INVALID    -> std::invalid_argument  (validate() failures)
+ *   FEMGPU_E_INFEASIBLE -> femsched::InfeasibleError (schedule cannot launch)
+ *   FEMGPU_E_NONFINITE  -> std::runtime_error "non-finite value at cell N during <stage>"
+ *
+ * Host pointers passed to femgpu_create are borrowed for the duration of the
+ * call only; the instance owns device copies afterwards (re-blocked layout).
+ */
+#ifndef FEMGPU_H
+#define FEMGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FEMGPU_ABI_VERSION 1
+
+typedef enum femgpu_status {
+    FEMGPU_OK = 0,
+    FEMGPU_E_INVALID = 1,
+    FEMGPU_E_INFEASIBLE = 2,
+    FEMGPU_E_NONFINITE = 3,
+    FEMGPU_E_CUDA = 4,
+    FEMGPU_E_JIT = 5,
+    FEMGPU_E_INTERNAL = 6
+} femgpu_status;
+
+/* PointwiseMap::Op, same numbering as femsched (form.hpp:194-204).
+ * FEMGPU_OP_INV_JACOBIAN is a B200-build extension (J^{-1}[a][b], affine only);
+ * it is not expressible in the reference map language. */
+typedef enum femgpu_map_op {
+    FEMGPU_OP_CONSTANT = 0,
+    FEMGPU_OP_SCALAR_DERIV = 1, /* a = space, b = term */
+    FEMGPU_OP_VECTOR_DERIV = 2, /* a = space, b = term */
+    FEMGPU_OP_JACOBIAN = 3,     /* a = row, b = col */
+    FEMGPU_OP_DETERMINANT = 4,
+    FEMGPU_OP_WEIGHT = 5,
+    FEMGPU_OP_COORD = 6, /* a = local vertex, b = axis */
+    FEMGPU_OP_ADD = 7,
+    FEMGPU_OP_MUL = 8,
+    FEMGPU_OP_INV_JACOBIAN = 9 /* extension */
+} femgpu_map_op;
+
+/* PointwiseMap::Node (form.hpp:205-209). */
+typedef struct femgpu_map_node {
+    int32_t op;
+    int32_t a;
+    int32_t b;
+    int32_t pad_;
+    double value;
+} femgpu_map_node;
+
+/* One trial space: ScalarSpace/VectorSpace (form.hpp:71-80) together with its
+ * tabulations (form.hpp:324-330), index map (form.hpp:49-65) and input vector
+ * (form.hpp:412-413). */
+typedef struct femgpu_space {
+    int32_t dofs;              /* local DOFs (per component for vector spaces) */
+    int32_t deriv_terms;
+    const int32_t* components; /* vector spaces: deriv_terms component indices; NULL for scalar */
+    const double* phi;         /* deriv_terms x quad_points x dofs, row-major per term */
+    const int32_t* map;        /* cell_count x dofs, row-major [cell][entry] */
+    int32_t global_count;      /* IndexMap::global_count */
+    int32_t pad_;
+    const double* input;       /* global_count (scalar) or global_count*dim (vector, [node*dim+comp]) */
+} femgpu_space;
+
+/* femsched::ProblemInstance flattened (form.hpp:407-435). */
+typedef struct femgpu_problem {
+    int32_t dim;
+    int32_t quad_points;
+    int32_t coord_dofs;
+    int32_t affine_geometry;   /* bool */
+    int32_t coordinate_space;  /* -1 when affine */
+    int32_t word_bytes;
+    int32_t n_scalar;
+    int32_t n_vector;
+    const femgpu_space* scalar_spaces;
+    const femgpu_space* vector_spaces;
+    int32_t test_dofs;
+    int32_t test_deriv_terms;
+    const double* psi;         /* test_deriv_terms x test_dofs x quad_points */
+    const double* weights;     /* quad_points */
+    int32_t cell_count;
+    int32_t test_global_count;
+    const int32_t* test_map;   /* cell_count x test_dofs */
+    const int32_t* coord_map;  /* cell_count x coord_dofs (affine only) */
+    const double* coords;      /* coord_global_count x dim (affine only) */
+    int32_t coord_global_count;
+    int32_t n_map_nodes;
+    const femgpu_map_node* map_nodes;
+    const int32_t* map_outputs; /* test_deriv_terms node ids */
+    int32_t n_map_outputs;
+    int32_t output_size;
+} femgpu_problem;
+
+/* Schedule point.  kind/tile fields mirror femsched::TilingParams
+ * (qoi.hpp:23-41); the remaining fields are B200 knobs (0 = automatic). */
+typedef enum femgpu_schedule_kind {
+    FEMGPU_SCPT = 0, /* TilingParams::scpt(): one thread per cell */
+    FEMGPU_MLT = 1   /* multi-level tiling: N_c cells x N_WI lanes per CTA */
+} femgpu_schedule_kind;
+
+typedef enum femgpu_basis {
+    FEMGPU_BASIS_AUTO = 0,
+    FEMGPU_BASIS_CONST = 1, /* tabulations in the constant bank (DFMA c[] operands) */
+    FEMGPU_BASIS_SMEM = 2   /* tabulations staged once per CTA in shared memory */
+} femgpu_basis;
+
+typedef enum femgpu_scatter {
+    FEMGPU_SCATTER_AUTO = 0,
+    FEMGPU_SCATTER_ATOMIC = 1, /* red.global.add.f64 per (cell, test DOF) */
+    FEMGPU_SCATTER_TILE = 2    /* CTA-tile aggregation in smem; global atomics only on shared DOFs */
+} femgpu_scatter;
+
+#define FEMGPU_MAX_SPACES 8
+
+typedef struct femgpu_schedule {
+    int32_t kind;
+    int32_t quad_tile;
+    int32_t eval_row_tile;
+    int32_t eval_col_tiles_scalar[FEMGPU_MAX_SPACES];
+    int32_t eval_col_tiles_vector[FEMGPU_MAX_SPACES];
+    int32_t quad_row_tile;
+    int32_t quad_col_tile;
+    int32_t cells_per_group;
+    int32_t lanes_per_cell;
+    /* B200 knobs */
+    int32_t basis;         /* femgpu_basis */
+    int32_t scatter;       /* femgpu_scatter */
+    int32_t block_cells;   /* SCPT: cells (threads) per CTA; 0 = auto */
+    int32_t reserved[5];
+} femgpu_schedule;
+
+typedef struct femgpu_instance femgpu_instance;
+
+/* ---- library --------------------------------------------------------- */
+int32_t femgpu_abi_version(void);
+const char* femgpu_last_error(void);
+/* Number of CUDA devices visible (0 on a host without a GPU). */
+int32_t femgpu_device_count(void);
+/* Select the device used by subsequent femgpu_create calls on this thread. */
+femgpu_status femgpu_set_device(int32_t device);
+
+/* ---- pure host helpers (no GPU needed) --------------------------------- */
+/* femsched::usable_flops (form.hpp:164-173) */
+femgpu_status femgpu_usable_flops(const femgpu_problem* p, int64_t* flops_per_cell);
+/* femsched::ProblemInstance::validate (form.hpp:416-434) */
+femgpu_status femgpu_validate(const femgpu_problem* p);
+/* Emit the CUDA source the JIT would compile for (problem signature+map, schedule).
+ * Writes at most cap bytes (NUL-terminated) and the full length to *len. */
+femgpu_status femgpu_emit_source(const femgpu_problem* p, const femgpu_schedule* s,
+                                 char* buf, size_t cap, size_t* len);
+/* Compile that source with NVRTC for sm_100a (works without a GPU). */
+femgpu_status femgpu_jit_check(const femgpu_problem* p, const femgpu_schedule* s);
+
+/* ---- device instance --------------------------------------------------- */
+femgpu_status femgpu_create(const femgpu_problem* p, femgpu_instance** out);
+femgpu_status femgpu_destroy(femgpu_instance* inst);
+/* Replace trial input vectors (host pointers, lengths as in the problem). */
+femgpu_status femgpu_set_inputs(femgpu_instance* inst, const double* const* scalar_inputs,
+                                const double* const* vector_inputs);
+/* y = A(u)·x into a host buffer of output_size doubles (H2D of nothing, D2H of y). */
+femgpu_status femgpu_action(femgpu_instance* inst, const femgpu_schedule* s, double* y_host);
+/* End to end: copy host inputs in (like set_inputs), run, copy y out; all on the
+ * instance stream.  Host buffers should be pinned (femgpu_host_alloc) for speed. */
+femgpu_status femgpu_action_host(femgpu_instance* inst, const femgpu_schedule* s,
+                                 const double* const* scalar_inputs,
+                                 const double* const* vector_inputs, double* y_host);
+/* Device-resident: y_dev is a device pointer of output_size doubles; stream is a
+ * cudaStream_t (NULL = the instance stream).  Asynchronous, no host sync. */
+femgpu_status femgpu_action_device(femgpu_instance* inst, const femgpu_schedule* s, double* y_dev,
+                                   void* stream);
+/* Paper timing protocol: warmup launches, then at least
+ * min_reps and at least min_seconds of [zero y + action] timed with CUDA events on
+ * the instance stream; *seconds = arithmetic mean per action. */
+femgpu_status femgpu_time_action(femgpu_instance* inst, const femgpu_schedule* s, int32_t warmup,
+                                 int32_t min_reps, double min_seconds, double* seconds);
+/* Executor seam (search.hpp:257-283): run, verify finiteness, report output and
+ * measured seconds (mean of the timing protocol above). */
+femgpu_status femgpu_execute(femgpu_instance* inst, const femgpu_schedule* s, double* y_host,
+                             double* measured_seconds);
+/* The schedule femgpu picks for this instance when s == NULL or all-auto. */
+femgpu_status femgpu_default_schedule(const femgpu_instance* inst, femgpu_schedule* s);
+/* Introspection: kernel launches issued by the last action, device bytes held. */
+femgpu_status femgpu_stats(const femgpu_instance* inst, int64_t* launches_last_action,
+                           int64_t* device_bytes, int64_t* tiles, int64_t* max_tile_dofs);
+/* Device pointers (for zero-copy callers): output buffer of the instance. */
+femgpu_status femgpu_device_output(femgpu_instance* inst, double** y_dev);
+/* The CUDA stream (cudaStream_t) the instance launches on. */
+femgpu_status femgpu_stream(femgpu_instance* inst, void** stream);
+
+/* One-shot, reference_action-shaped: create, run (default schedule), destroy. */
+femgpu_status femgpu_action_once(const femgpu_problem* p, double* y_host);
+
+/* Pinned host memory helpers. */
+femgpu_status femgpu_host_alloc(size_t bytes, void** ptr);
+femgpu_status femgpu_host_free(void* ptr);
+
+/* ---- structured meshes (synthetic unit square / unit cube) -------------
+ * Unit square: n x n squares, 2 triangles each; unit cube: n^3 cubes, 6 Kuhn
+ * tetrahedra each.  P_degree nodes live on the degree-refined lattice and the
+ * global DOF number is the lattice index, so shared edges and faces agree.
+ * Cells are ordered brick-major (brick x brick [x brick] squares/cubes) so a
+ * run of consecutive cells is spatially compact.  Vertex v has lattice index
+ * and coordinates lattice/n.  Node ordering per cell: the dim+1 vertices
+ * first, then the remaining barycentric multi-indices in lexicographic order. */
+femgpu_status femgpu_mesh_counts(int32_t dim, int32_t n, int32_t degree, int64_t* cells,
+                                 int64_t* nodes, int64_t* vertices, int32_t* nodes_per_cell);
+femgpu_status femgpu_mesh_build(int32_t dim, int32_t n, int32_t degree, int32_t brick,
+                                int32_t* node_map, int32_t* vertex_map, double* coords);
+/* Greedy cell colouring: no two cells of one colour share an entry of map.
+ * colors[cell] in [0, *n_colors). Deterministic (cells in ascending order,
+ * smallest free colour). */
+femgpu_status femgpu_color_cells(const int32_t* map, int32_t cells, int32_t entries,
+                                 int32_t global_count, int32_t* colors, int32_t* n_colors);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FEMGPU_H */

@@ -1,0 +1,261 @@
+"""The B200 action path behind the reference's operator/plugin seams.
+
+  gpu_action(inst, params=None)      <- femsched::reference_action (form.hpp:471-472): same
+                                        signature shape, same exceptions (ValueError for
+                                        std::invalid_argument, RuntimeError "non-finite value at
+                                        cell N during <stage>", InfeasibleError)
+  GpuInstance.action(params)         <- femsched::run_schedule(inst, build_plan(sig, params))
+                                        (simulate.hpp:601-603)
+  gpu_executor()                     <- femsched::Executor / simulator_executor (search.hpp:257-283):
+                                        a callable (TilingParams, ProblemInstance) -> ExecutionOutcome
+                                        with measured_seconds from CUDA events
+
+Everything here is a thin ctypes layer over libfemgpu (include/femgpu.h); all
+compute runs in the sm_100a kernels the library JIT-compiles.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from . import abi
+from ._native import FemgpuError, check, lib
+from .form import FormSignature, InfeasibleError, ProblemInstance
+
+
+@dataclass
+class TilingParams:
+    """femsched::TilingParams (qoi.hpp:23-109) plus B200 knobs (0 = automatic)."""
+    kind: int = abi.MLT  # ScheduleKind: abi.SCPT or abi.MLT
+    quad_tile: int = 1
+    eval_row_tile: int = 1
+    eval_col_tiles_scalar: List[int] = field(default_factory=list)
+    eval_col_tiles_vector: List[int] = field(default_factory=list)
+    quad_row_tile: int = 1
+    quad_col_tile: int = 1
+    cells_per_group: int = 1
+    lanes_per_cell: int = 1
+    # B200 knobs
+    basis: int = abi.BASIS_AUTO
+    scatter: int = abi.SCATTER_AUTO
+    block_cells: int = 0
+    strict: bool = False  # --fmad=false: bitwise per-cell arithmetic of the reference
+
+    @staticmethod
+    def scpt(**knobs) -> "TilingParams":
+        return TilingParams(kind=abi.SCPT, **knobs)
+
+    @staticmethod
+    def untiled(sig: FormSignature, cells_per_group: int = 1, lanes_per_cell: int = 1) -> "TilingParams":
+        return TilingParams(kind=abi.MLT, quad_tile=sig.quad_points, eval_row_tile=sig.quad_points,
+                            eval_col_tiles_scalar=[s.dofs for s in sig.scalar_spaces],
+                            eval_col_tiles_vector=[v.dofs for v in sig.vector_spaces],
+                            quad_row_tile=sig.test_dofs, quad_col_tile=sig.quad_points,
+                            cells_per_group=cells_per_group, lanes_per_cell=lanes_per_cell)
+
+    def group_size(self) -> int:
+        return 32 if self.kind == abi.SCPT else self.cells_per_group * self.lanes_per_cell
+
+    def order_key(self):  # qoi.hpp:95-107
+        return [1 if self.kind == abi.SCPT else 0, self.quad_tile, self.eval_row_tile,
+                *self.eval_col_tiles_scalar, *self.eval_col_tiles_vector, self.quad_row_tile,
+                self.quad_col_tile, self.cells_per_group, self.lanes_per_cell]
+
+    def to_c(self) -> abi.Schedule:
+        s = abi.Schedule()
+        s.kind = self.kind
+        s.quad_tile, s.eval_row_tile = self.quad_tile, self.eval_row_tile
+        for i, t in enumerate(self.eval_col_tiles_scalar):
+            s.eval_col_tiles_scalar[i] = t
+        for i, t in enumerate(self.eval_col_tiles_vector):
+            s.eval_col_tiles_vector[i] = t
+        s.quad_row_tile, s.quad_col_tile = self.quad_row_tile, self.quad_col_tile
+        s.cells_per_group, s.lanes_per_cell = self.cells_per_group, self.lanes_per_cell
+        s.basis, s.scatter, s.block_cells = self.basis, self.scatter, self.block_cells
+        s.reserved[0] = 1 if self.strict else 0
+        return s
+
+    def describe(self) -> str:  # search.hpp:301-310
+        if self.kind == abi.SCPT:
+            return "single-cell-per-work-item"
+        tc = "".join("%d," % t for t in self.eval_col_tiles_scalar + self.eval_col_tiles_vector)
+        return "mlt(TQ=%d,Ter=%d,Tc=%sTqr=%d,Tqc=%d,Nc=%d,Nwi=%d)" % (
+            self.quad_tile, self.eval_row_tile, tc, self.quad_row_tile, self.quad_col_tile,
+            self.cells_per_group, self.lanes_per_cell)
+
+
+def _raise(e: FemgpuError):
+    if e.code == abi.E_INVALID:
+        raise ValueError(str(e)) from None
+    if e.code == abi.E_INFEASIBLE:
+        raise InfeasibleError(str(e)) from None
+    raise RuntimeError(str(e)) from None
+
+
+def _call(status: int):
+    try:
+        check(status)
+    except FemgpuError as e:
+        _raise(e)
+
+
+def _sched(params: Optional[TilingParams]):
+    if params is None:
+        return None
+    s = params.to_c()
+    return C.byref(s), s
+
+
+class GpuInstance:
+    """A ProblemInstance resident in HBM (femgpu_create), reusable across actions."""
+
+    def __init__(self, problem: ProblemInstance):
+        problem.validate()
+        self.problem = problem
+        self._cp = problem.to_c()
+        h = C.c_void_p()
+        _call(lib().femgpu_create(C.byref(self._cp.desc), C.byref(h)))
+        self._h = h
+        self.output_size = problem.output_size
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().femgpu_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    @property
+    def handle(self):
+        return self._h
+
+    def action(self, params: Optional[TilingParams] = None, out: Optional[np.ndarray] = None) -> np.ndarray:
+        y = out if out is not None else np.empty(self.output_size, dtype=np.float64)
+        sp = _sched(params)
+        _call(lib().femgpu_action(self._h, sp[0] if sp else None, y.ctypes.data_as(C.POINTER(C.c_double))))
+        return y
+
+    def _ptr_array(self, arrays):
+        if not arrays:
+            return None
+        arr = (C.POINTER(C.c_double) * len(arrays))()
+        for i, a in enumerate(arrays):
+            assert a.dtype == np.float64 and a.flags.c_contiguous
+            arr[i] = a.ctypes.data_as(C.POINTER(C.c_double))
+        return arr
+
+    def set_inputs(self, scalar_inputs=None, vector_inputs=None):
+        _call(lib().femgpu_set_inputs(self._h, self._ptr_array(scalar_inputs), self._ptr_array(vector_inputs)))
+
+    def action_host(self, scalar_inputs, vector_inputs, out: np.ndarray, params: Optional[TilingParams] = None):
+        """End to end: H2D of the inputs, the action, D2H of y (femgpu_action_host)."""
+        sp = _sched(params)
+        _call(lib().femgpu_action_host(self._h, sp[0] if sp else None, self._ptr_array(scalar_inputs),
+                                       self._ptr_array(vector_inputs), out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
+    def action_device(self, params: Optional[TilingParams] = None, y_dev: int = 0, stream: int = 0):
+        sp = _sched(params)
+        _call(lib().femgpu_action_device(self._h, sp[0] if sp else None, C.c_void_p(y_dev), C.c_void_p(stream)))
+
+    def time(self, params: Optional[TilingParams] = None, warmup: int = 5, min_reps: int = 15,
+             min_seconds: float = 0.2) -> float:
+        """Mean seconds per [zero y + action], paper protocol."""
+        s = C.c_double()
+        sp = _sched(params)
+        _call(lib().femgpu_time_action(self._h, sp[0] if sp else None, warmup, min_reps, min_seconds, C.byref(s)))
+        return s.value
+
+    def stats(self):
+        v = [C.c_int64() for _ in range(4)]
+        _call(lib().femgpu_stats(self._h, *[C.byref(x) for x in v]))
+        return {"launches_last_action": v[0].value, "device_bytes": v[1].value, "tiles": v[2].value,
+                "max_tile_dofs": v[3].value}
+
+    def stream(self) -> int:
+        p = C.c_void_p()
+        _call(lib().femgpu_stream(self._h, C.byref(p)))
+        return p.value or 0
+
+    def device_output(self) -> int:
+        p = C.c_void_p()
+        _call(lib().femgpu_device_output(self._h, C.byref(p)))
+        return p.value or 0
+
+
+def gpu_action(problem: ProblemInstance, params: Optional[TilingParams] = None) -> np.ndarray:
+    """reference_action-shaped one-shot: upload, run, download (form.hpp:471)."""
+    with GpuInstance(problem) as g:
+        return g.action(params)
+
+
+@dataclass
+class ExecutionOutcome:
+    """femsched::ExecutionOutcome (search.hpp:257-264)."""
+    ok: bool = False
+    error: str = ""
+    output: Optional[np.ndarray] = None
+    measured_seconds: Optional[float] = None
+    workgroups: int = 0
+
+
+def gpu_executor(measure: bool = True, cache: bool = True):
+    """A femsched::Executor-shaped callable backed by the sm_100a kernels (search.hpp:266).
+    Instances are uploaded once and cached by identity so tune's candidates share them."""
+    instances = {}
+
+    def run(params: TilingParams, inst: ProblemInstance) -> ExecutionOutcome:
+        out = ExecutionOutcome()
+        try:
+            g = instances.get(id(inst)) if cache else None
+            if g is None:
+                g = GpuInstance(inst)
+                if cache:
+                    instances[id(inst)] = g
+            out.output = g.action(params)
+            if measure:
+                out.measured_seconds = g.time(params)
+            out.ok = True
+            n = inst.connectivity.cell_count
+            out.workgroups = -(-n // (params.cells_per_group if params.kind == abi.MLT else 32))
+        except Exception as e:  # search.hpp:278-280: failures become ok=false + message
+            out.error = str(e)
+        return out
+
+    run.instances = instances
+    return run
+
+
+def emit_source(problem: ProblemInstance, params: Optional[TilingParams] = None) -> str:
+    """The CUDA source the JIT compiles for this form (host only; no GPU needed)."""
+    cp = problem.to_c()
+    n = C.c_size_t()
+    sp = _sched(params)
+    _call(lib().femgpu_emit_source(C.byref(cp.desc), sp[0] if sp else None, None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    _call(lib().femgpu_emit_source(C.byref(cp.desc), sp[0] if sp else None, buf, n.value + 1, C.byref(n)))
+    return buf.value.decode()
+
+
+def jit_check(problem: ProblemInstance, params: Optional[TilingParams] = None) -> None:
+    """NVRTC-compiles the emitted kernel for sm_100a (host only)."""
+    cp = problem.to_c()
+    sp = _sched(params)
+    _call(lib().femgpu_jit_check(C.byref(cp.desc), sp[0] if sp else None))
+
+
+def device_count() -> int:
+    return int(lib().femgpu_device_count())

@@ -1,0 +1,304 @@
+// api.cpp — the extern "C" boundary (include/femgpu.h).  Converts every C++
+// exception into a femgpu_status + thread-local message; nothing throws across.
+#include <cstring>
+#include <string>
+
+#include "femgpu_internal.hpp"
+
+struct femgpu_instance {
+    std::unique_ptr<femgpu::Instance> impl;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+thread_local int g_device = -1;
+
+template <typename F>
+femgpu_status guard(F&& f) {
+    try {
+        f();
+        return FEMGPU_OK;
+    } catch (const femgpu::Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "out of host memory";
+        return FEMGPU_E_INTERNAL;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return FEMGPU_E_INTERNAL;
+    } catch (...) {
+        g_last_error = "unknown error";
+        return FEMGPU_E_INTERNAL;
+    }
+}
+
+void bind_device() {
+    if (g_device >= 0) FG_CUDA(cudaSetDevice(g_device));
+}
+
+femgpu::Instance& get(femgpu_instance* h) {
+    if (!h || !h->impl) femgpu::invalid("null instance");
+    return *h->impl;
+}
+
+void copy_inputs(femgpu::Instance& I, const double* const* scalar_inputs, const double* const* vector_inputs,
+                 cudaStream_t stream) {
+    for (size_t i = 0; i < I.sspaces.size(); ++i) {
+        if (!scalar_inputs || !scalar_inputs[i]) femgpu::invalid("instance: scalar input length mismatch");
+        FG_CUDA(cudaMemcpyAsync(I.sspaces[i].d_x, scalar_inputs[i], sizeof(double) * I.sspaces[i].global,
+                                cudaMemcpyHostToDevice, stream));
+    }
+    for (size_t i = 0; i < I.vspaces.size(); ++i) {
+        if (!vector_inputs || !vector_inputs[i]) femgpu::invalid("instance: vector input length mismatch");
+        FG_CUDA(cudaMemcpyAsync(I.vspaces[i].d_x, vector_inputs[i],
+                                sizeof(double) * I.vspaces[i].global * static_cast<size_t>(I.sig.dim),
+                                cudaMemcpyHostToDevice, stream));
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t femgpu_abi_version(void) { return FEMGPU_ABI_VERSION; }
+
+const char* femgpu_last_error(void) { return g_last_error.c_str(); }
+
+int32_t femgpu_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+femgpu_status femgpu_set_device(int32_t device) {
+    return guard([&] {
+        FG_CUDA(cudaSetDevice(device));
+        g_device = device;
+    });
+}
+
+femgpu_status femgpu_usable_flops(const femgpu_problem* p, int64_t* flops) {
+    return guard([&] {
+        if (!p || !flops) femgpu::invalid("null argument");
+        femgpu::validate_problem(p);
+        *flops = femgpu::signature_from(p).usable_flops();
+    });
+}
+
+femgpu_status femgpu_validate(const femgpu_problem* p) {
+    return guard([&] { femgpu::validate_problem(p); });
+}
+
+femgpu_status femgpu_emit_source(const femgpu_problem* p, const femgpu_schedule* s, char* buf, size_t cap,
+                                 size_t* len) {
+    return guard([&] {
+        femgpu::validate_problem(p);
+        femgpu::Signature sig = femgpu::signature_from(p);
+        // Host-only resolution (no device instance): SCPT with global atomics, or MLT.
+        femgpu::KernelPlan kp;
+        if (s && s->kind == FEMGPU_MLT) {
+            kp.family = femgpu::Family::Mlt;
+            kp.TQ = s->quad_tile;
+            kp.Ter = s->eval_row_tile;
+            kp.Tqr = s->quad_row_tile;
+            kp.Tqc = s->quad_col_tile;
+            kp.Nc = s->cells_per_group;
+            kp.Nwi = s->lanes_per_cell;
+            kp.block = kp.Nc * kp.Nwi;
+            kp.basis = FEMGPU_BASIS_SMEM;
+            for (int i = 0; i < sig.ns(); ++i) kp.Tcs.push_back(s->eval_col_tiles_scalar[i]);
+            for (int i = 0; i < sig.nv(); ++i) kp.Tcv.push_back(s->eval_col_tiles_vector[i]);
+        } else {
+            kp.family = femgpu::Family::Scpt;
+            kp.basis = (s && s->basis) ? s->basis : (sig.tab_size <= 3800 ? FEMGPU_BASIS_CONST : FEMGPU_BASIS_SMEM);
+            kp.block = (s && s->block_cells > 0) ? s->block_cells : 128;
+        }
+        kp.strict = s && s->reserved[0];
+        femgpu::EmitResult em = femgpu::emit_kernel(sig, kp);
+        if (len) *len = em.source.size();
+        if (buf && cap) {
+            const size_t n = std::min(cap - 1, em.source.size());
+            std::memcpy(buf, em.source.data(), n);
+            buf[n] = 0;
+        }
+    });
+}
+
+femgpu_status femgpu_jit_check(const femgpu_problem* p, const femgpu_schedule* s) {
+    return guard([&] {
+        size_t len = 0;
+        femgpu_status st = femgpu_emit_source(p, s, nullptr, 0, &len);
+        if (st != FEMGPU_OK) throw femgpu::Error(st, g_last_error);
+        std::string src(len + 1, '\0');
+        femgpu_emit_source(p, s, src.data(), src.size(), &len);
+        src.resize(len);
+        std::string log;
+        femgpu::jit_compile(src, s && s->reserved[0], &log);
+    });
+}
+
+femgpu_status femgpu_create(const femgpu_problem* p, femgpu_instance** out) {
+    return guard([&] {
+        if (!out) femgpu::invalid("null output handle");
+        *out = nullptr;
+        bind_device();
+        auto h = new femgpu_instance;
+        try {
+            h->impl = femgpu::create_instance(p);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+femgpu_status femgpu_destroy(femgpu_instance* inst) {
+    return guard([&] { delete inst; });
+}
+
+femgpu_status femgpu_set_inputs(femgpu_instance* h, const double* const* scalar_inputs,
+                                const double* const* vector_inputs) {
+    return guard([&] {
+        auto& I = get(h);
+        std::lock_guard<std::mutex> lk(I.mu);
+        FG_CUDA(cudaSetDevice(I.device));
+        copy_inputs(I, scalar_inputs, vector_inputs, I.stream);
+        FG_CUDA(cudaStreamSynchronize(I.stream));
+    });
+}
+
+femgpu_status femgpu_action(femgpu_instance* h, const femgpu_schedule* s, double* y_host) {
+    return guard([&] {
+        auto& I = get(h);
+        if (!y_host) femgpu::invalid("null output buffer");
+        std::lock_guard<std::mutex> lk(I.mu);
+        FG_CUDA(cudaSetDevice(I.device));
+        const femgpu::KernelPlan kp = femgpu::resolve_schedule(I, s);
+        femgpu::run_action(I, kp, I.d_y, I.stream);
+        FG_CUDA(cudaMemcpyAsync(y_host, I.d_y, sizeof(double) * static_cast<size_t>(I.output_size),
+                                cudaMemcpyDeviceToHost, I.stream));
+        femgpu::check_failure(I, kp, I.stream);
+    });
+}
+
+femgpu_status femgpu_action_host(femgpu_instance* h, const femgpu_schedule* s, const double* const* scalar_inputs,
+                                 const double* const* vector_inputs, double* y_host) {
+    return guard([&] {
+        auto& I = get(h);
+        if (!y_host) femgpu::invalid("null output buffer");
+        std::lock_guard<std::mutex> lk(I.mu);
+        FG_CUDA(cudaSetDevice(I.device));
+        const femgpu::KernelPlan kp = femgpu::resolve_schedule(I, s);
+        copy_inputs(I, scalar_inputs, vector_inputs, I.stream);
+        femgpu::run_action(I, kp, I.d_y, I.stream);
+        FG_CUDA(cudaMemcpyAsync(y_host, I.d_y, sizeof(double) * static_cast<size_t>(I.output_size),
+                                cudaMemcpyDeviceToHost, I.stream));
+        femgpu::check_failure(I, kp, I.stream);
+    });
+}
+
+femgpu_status femgpu_action_device(femgpu_instance* h, const femgpu_schedule* s, double* y_dev, void* stream) {
+    return guard([&] {
+        auto& I = get(h);
+        std::lock_guard<std::mutex> lk(I.mu);
+        FG_CUDA(cudaSetDevice(I.device));
+        const femgpu::KernelPlan kp = femgpu::resolve_schedule(I, s);
+        femgpu::run_action(I, kp, y_dev ? y_dev : I.d_y, stream ? static_cast<cudaStream_t>(stream) : I.stream);
+    });
+}
+
+femgpu_status femgpu_time_action(femgpu_instance* h, const femgpu_schedule* s, int32_t warmup, int32_t min_reps,
+                                 double min_seconds, double* seconds) {
+    return guard([&] {
+        auto& I = get(h);
+        if (!seconds) femgpu::invalid("null output");
+        std::lock_guard<std::mutex> lk(I.mu);
+        FG_CUDA(cudaSetDevice(I.device));
+        const femgpu::KernelPlan kp = femgpu::resolve_schedule(I, s);
+        for (int i = 0; i < warmup; ++i) femgpu::run_action(I, kp, I.d_y, I.stream);
+        femgpu::check_failure(I, kp, I.stream);
+        double total = 0.0;
+        long long reps = 0;
+        int batch = std::max(1, min_reps);
+        while (reps < min_reps || total < min_seconds) {
+            FG_CUDA(cudaEventRecord(I.ev0, I.stream));
+            for (int i = 0; i < batch; ++i) femgpu::run_action(I, kp, I.d_y, I.stream);
+            FG_CUDA(cudaEventRecord(I.ev1, I.stream));
+            FG_CUDA(cudaEventSynchronize(I.ev1));
+            float ms = 0.f;
+            FG_CUDA(cudaEventElapsedTime(&ms, I.ev0, I.ev1));
+            total += ms * 1e-3;
+            reps += batch;
+            if (reps > 1000000) break;
+        }
+        femgpu::check_failure(I, kp, I.stream);
+        *seconds = total / static_cast<double>(reps);
+    });
+}
+
+femgpu_status femgpu_execute(femgpu_instance* h, const femgpu_schedule* s, double* y_host, double* measured) {
+    femgpu_status st = femgpu_action(h, s, y_host);
+    if (st != FEMGPU_OK) return st;
+    if (measured) return femgpu_time_action(h, s, 5, 15, 0.2, measured);
+    return FEMGPU_OK;
+}
+
+femgpu_status femgpu_default_schedule(const femgpu_instance* h, femgpu_schedule* s) {
+    return guard([&] {
+        if (!h || !s) femgpu::invalid("null argument");
+        std::memset(s, 0, sizeof *s);
+        s->kind = FEMGPU_SCPT;
+    });
+}
+
+femgpu_status femgpu_stats(const femgpu_instance* h, int64_t* launches, int64_t* device_bytes, int64_t* tiles,
+                           int64_t* max_tile_dofs) {
+    return guard([&] {
+        if (!h || !h->impl) femgpu::invalid("null instance");
+        const auto& I = *h->impl;
+        if (launches) *launches = I.last_launches;
+        if (device_bytes) *device_bytes = I.device_bytes;
+        int64_t nt = 0, mx = 0;
+        for (const auto& kv : I.tiles) {
+            nt = kv.second->n_tiles;
+            mx = kv.second->groups.empty() ? 0 : kv.second->groups[I.test_group].max_unique;
+        }
+        if (tiles) *tiles = nt;
+        if (max_tile_dofs) *max_tile_dofs = mx;
+    });
+}
+
+femgpu_status femgpu_device_output(femgpu_instance* h, double** y_dev) {
+    return guard([&] { *y_dev = get(h).d_y; });
+}
+
+femgpu_status femgpu_stream(femgpu_instance* h, void** stream) {
+    return guard([&] { *stream = get(h).stream; });
+}
+
+femgpu_status femgpu_action_once(const femgpu_problem* p, double* y_host) {
+    femgpu_instance* h = nullptr;
+    femgpu_status st = femgpu_create(p, &h);
+    if (st != FEMGPU_OK) return st;
+    st = femgpu_action(h, nullptr, y_host);
+    std::string err = g_last_error;
+    femgpu_destroy(h);
+    g_last_error = err;
+    return st;
+}
+
+femgpu_status femgpu_host_alloc(size_t bytes, void** ptr) {
+    return guard([&] { FG_CUDA(cudaMallocHost(ptr, bytes)); });
+}
+
+femgpu_status femgpu_host_free(void* ptr) {
+    return guard([&] { FG_CUDA(cudaFreeHost(ptr)); });
+}
+
+}  // extern "C"

@@ -1,0 +1,163 @@
+// femgpu_internal.hpp — host-side runtime structures of libfemgpu (not part of the ABI).
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/femgpu.h"
+
+namespace femgpu {
+
+// Errors thrown inside the library and converted to femgpu_status at the ABI.
+struct Error : std::runtime_error {
+    femgpu_status code;
+    Error(femgpu_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void fail(femgpu_status c, const std::string& m) { throw Error(c, m); }
+inline void invalid(const std::string& m) { fail(FEMGPU_E_INVALID, m); }
+
+void cuda_check(cudaError_t e, const char* what);
+#define FG_CUDA(x) ::femgpu::cuda_check((x), #x)
+
+// Structural copy of the problem signature + pointwise map: everything the
+// kernel emitter needs (no bulk data).
+struct MapNode {
+    int op, a, b;
+    double value;
+};
+
+struct Signature {
+    int dim = 0, Q = 0, coord_dofs = 0;
+    bool affine = true;
+    int coordinate_space = -1;
+    std::vector<int> sdofs, sterms;                 // scalar spaces
+    std::vector<int> vdofs, vterms;                 // vector spaces
+    std::vector<std::vector<int>> vcomps;           // component per vector term
+    int nW = 0, Tw = 0;                             // test dofs / test terms
+    std::vector<MapNode> nodes;
+    std::vector<int> outputs;
+
+    int ns() const { return static_cast<int>(sdofs.size()); }
+    int nv() const { return static_cast<int>(vdofs.size()); }
+    long long usable_flops() const;
+    // Offsets into the packed tabulation array (phi scalar, phi vector, psi, weights).
+    std::vector<long long> phi_off_s, phi_off_v;
+    long long psi_off = 0, w_off = 0, tab_size = 0;
+    void layout();
+};
+
+Signature signature_from(const femgpu_problem* p);
+
+// Kernel families.
+enum class Family { Scpt, Tile, Mlt };
+
+// Fully resolved launch plan (what the emitter specialises on).
+struct KernelPlan {
+    Family family = Family::Scpt;
+    int basis = FEMGPU_BASIS_CONST;    // const (param bank) or smem
+    int block = 128;                   // threads per CTA
+    int tile_cells = 0;                // Tile: cells per CTA (== block)
+    // Tile family: map-group ids per space (-1 = not staged) and smem capacities.
+    std::vector<int> sgroup, vgroup;
+    int tgroup = -1, cgroup = -1;
+    std::vector<int> group_entries, group_cap;   // per group: entries per cell, max unique per tile
+    // MLT family (TilingParams)
+    int Nc = 1, Nwi = 1, TQ = 1, Ter = 1, Tqr = 1, Tqc = 1;
+    std::vector<int> Tcs, Tcv;
+    bool strict = false;               // --fmad=false (bitwise debug mode)
+    std::string key() const;
+};
+
+struct EmitResult {
+    std::string source;
+    std::string kernel;          // fast kernel name
+    std::string kernel_checked;  // stage-checked diagnostic kernel name
+    size_t param_bytes = 0;
+    size_t smem_bytes = 0;       // dynamic shared memory per CTA
+};
+
+EmitResult emit_kernel(const Signature& sig, const KernelPlan& kp);
+
+// JIT: NVRTC compile for sm_100a, cached by source hash (memory + disk).
+struct Module {
+    cudaLibrary_t lib = nullptr;
+    cudaKernel_t fast = nullptr, checked = nullptr;
+    EmitResult emitted;
+    int regs = 0;
+};
+std::vector<char> jit_compile(const std::string& source, bool strict, std::string* log);
+std::shared_ptr<Module> get_module(const Signature& sig, const KernelPlan& kp);
+
+// Tile layout of one map group at one tile size (built in femgpu_create).
+struct TileGroup {
+    int entries = 0;
+    int max_unique = 0;
+    long long total_unique = 0;
+    int32_t* d_off = nullptr;      // n_tiles+1
+    int32_t* d_list = nullptr;     // global index | 0x80000000 if shared with another tile
+    uint16_t* d_loc = nullptr;     // [entry][cell] tile-local index
+};
+
+struct TileLayout {
+    int tile_cells = 0;
+    int n_tiles = 0;
+    std::vector<TileGroup> groups;
+};
+
+struct DeviceSpace {
+    int dofs = 0, terms = 0, global = 0;
+    double* d_x = nullptr;          // input vector
+    int32_t* d_mapT = nullptr;      // [entry][cell] (SoA, coalesced); may alias another space's
+    int group = -1;                 // content-equal map group
+};
+
+struct Instance {
+    Signature sig;
+    int device = 0;
+    int cells = 0, output_size = 0;
+    std::vector<double> tab;        // packed tabulations (host copy, goes to param bank)
+    double* d_tab = nullptr;        // packed tabulations (device, smem-staged variants)
+    std::vector<DeviceSpace> sspaces, vspaces;
+    int32_t* d_tmapT = nullptr;
+    int32_t* d_cmapT = nullptr;
+    double* d_coords = nullptr;
+    int coord_global = 0;
+    int test_group = -1, coord_group = -1;
+    std::vector<std::vector<int32_t>> group_maps;  // host copies of distinct maps ([cell][entry])
+    std::vector<int> group_global;
+    double* d_y = nullptr;
+    int32_t* d_bad = nullptr;       // first failing cell (INT32_MAX = none)
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    std::map<int, std::unique_ptr<TileLayout>> tiles;   // by tile size
+    std::vector<void*> allocations;
+    int64_t device_bytes = 0;
+    int64_t last_launches = 0;
+    std::mutex mu;                  // serialises actions on this instance (tune(jobs>1))
+
+    ~Instance();
+    template <typename T>
+    T* alloc(size_t count) {
+        void* p = nullptr;
+        FG_CUDA(cudaMalloc(&p, count * sizeof(T) + 16));
+        allocations.push_back(p);
+        device_bytes += static_cast<int64_t>(count * sizeof(T));
+        return static_cast<T*>(p);
+    }
+    const TileLayout& tile_layout(int tile_cells);
+};
+
+void validate_problem(const femgpu_problem* p);
+std::unique_ptr<Instance> create_instance(const femgpu_problem* p);
+KernelPlan resolve_schedule(Instance& inst, const femgpu_schedule* s);
+void run_action(Instance& inst, const KernelPlan& kp, double* d_y, cudaStream_t stream);
+void check_failure(Instance& inst, const KernelPlan& kp, cudaStream_t stream);
+
+}  // namespace femgpu

@@ -1,0 +1,589 @@
+// instance.cpp — device-resident problem instances, HBM layout, launches.
+//
+// femgpu_create does all re-blocking outside the timed region:
+//   * index maps are deduplicated by content (the reference keeps separate but
+//     identical trial/test/coord maps, form.hpp:371-378) and stored transposed,
+//     [entry][cell] int32, so one warp's loads of entry j are one 128-byte line;
+//   * the tabulations are packed into one array that becomes kernel-parameter
+//     (constant-bank) data or is staged per CTA in shared memory;
+//   * per tile size, each distinct map gets a tile layout: the sorted unique
+//     global indices of every tile of consecutive cells (shared-with-another-tile
+//     flag in bit 31) and a uint16 tile-local [entry][cell] map.
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <numeric>
+#include <thread>
+
+#include "femgpu_internal.hpp"
+
+namespace femgpu {
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        fail(FEMGPU_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    }
+}
+
+long long Signature::usable_flops() const {  // form.hpp:164-173
+    long long ops = 0;
+    for (int i = 0; i < ns(); ++i) ops += 2LL * sterms[i] * Q * sdofs[i];
+    for (int i = 0; i < nv(); ++i) ops += 2LL * vterms[i] * Q * vdofs[i];
+    ops += 2LL * Tw * Q * nW;
+    return ops;
+}
+
+void Signature::layout() {
+    long long off = 0;
+    phi_off_s.clear();
+    phi_off_v.clear();
+    for (int i = 0; i < ns(); ++i) {
+        phi_off_s.push_back(off);
+        off += static_cast<long long>(sterms[i]) * Q * sdofs[i];
+    }
+    for (int i = 0; i < nv(); ++i) {
+        phi_off_v.push_back(off);
+        off += static_cast<long long>(vterms[i]) * Q * vdofs[i];
+    }
+    psi_off = off;
+    off += static_cast<long long>(Tw) * nW * Q;
+    w_off = off;
+    off += Q;
+    tab_size = off;
+}
+
+Signature signature_from(const femgpu_problem* p) {
+    Signature s;
+    s.dim = p->dim;
+    s.Q = p->quad_points;
+    s.coord_dofs = p->coord_dofs;
+    s.affine = p->affine_geometry != 0;
+    s.coordinate_space = p->coordinate_space;
+    for (int i = 0; i < p->n_scalar; ++i) {
+        s.sdofs.push_back(p->scalar_spaces[i].dofs);
+        s.sterms.push_back(p->scalar_spaces[i].deriv_terms);
+    }
+    for (int i = 0; i < p->n_vector; ++i) {
+        const femgpu_space& v = p->vector_spaces[i];
+        s.vdofs.push_back(v.dofs);
+        s.vterms.push_back(v.deriv_terms);
+        s.vcomps.emplace_back(v.components, v.components + v.deriv_terms);
+    }
+    s.nW = p->test_dofs;
+    s.Tw = p->test_deriv_terms;
+    for (int i = 0; i < p->n_map_nodes; ++i) {
+        const femgpu_map_node& n = p->map_nodes[i];
+        s.nodes.push_back({n.op, n.a, n.b, n.value});
+    }
+    s.outputs.assign(p->map_outputs, p->map_outputs + p->n_map_outputs);
+    s.layout();
+    return s;
+}
+
+// ProblemInstance::validate (form.hpp:416-434), same messages.
+void validate_problem(const femgpu_problem* p) {
+    if (!p) invalid("instance: null problem");
+    if (p->dim < 1 || p->dim > 3) invalid("signature: dim must be 1..3");
+    if (p->n_scalar < 0 || p->n_vector < 0 || p->n_scalar + p->n_vector == 0)
+        invalid("signature: at least one trial space required");
+    if (p->n_scalar > FEMGPU_MAX_SPACES || p->n_vector > FEMGPU_MAX_SPACES)
+        invalid("signature: at most 8 scalar and 8 vector spaces are supported");
+    if (p->quad_points < 1) invalid("signature: quad_points must be >= 1");
+    if (p->test_dofs < 1 || p->test_deriv_terms < 1) invalid("signature: test space counts must be positive");
+    if (p->word_bytes != 4 && p->word_bytes != 8) invalid("signature: word_bytes must be 4 or 8");
+    for (int i = 0; i < p->n_scalar; ++i)
+        if (p->scalar_spaces[i].dofs < 1 || p->scalar_spaces[i].deriv_terms < 1)
+            invalid("signature: scalar space counts must be positive");
+    for (int i = 0; i < p->n_vector; ++i) {
+        const femgpu_space& v = p->vector_spaces[i];
+        if (v.dofs < 1 || v.deriv_terms < 1) invalid("signature: vector space counts must be positive");
+        if (!v.components) invalid("signature: one component index per derivative term required");
+        for (int k = 0; k < v.deriv_terms; ++k)
+            if (v.components[k] < 0 || v.components[k] >= p->dim) invalid("signature: component index out of range");
+    }
+    if (p->affine_geometry) {
+        if (p->coord_dofs != p->dim + 1) invalid("signature: affine geometry requires coord_dofs == dim+1");
+        if (p->coordinate_space != -1) invalid("signature: coordinate_space is only meaningful when non-affine");
+    } else if (p->coordinate_space < 0 || p->coordinate_space >= p->n_vector) {
+        invalid("signature: non-affine geometry requires the coordinate space to appear in the vector-space list "
+                "exactly once");
+    }
+    if (p->n_map_outputs != p->test_deriv_terms)
+        invalid("pointwise map: one expression per test derivative term required");
+    for (int o = 0; o < p->n_map_outputs; ++o)
+        if (p->map_outputs[o] < 0 || p->map_outputs[o] >= p->n_map_nodes)
+            invalid("pointwise map: output references unknown node");
+    for (int id = 0; id < p->n_map_nodes; ++id) {
+        const femgpu_map_node& n = p->map_nodes[id];
+        switch (n.op) {
+            case FEMGPU_OP_CONSTANT:
+            case FEMGPU_OP_WEIGHT: break;
+            case FEMGPU_OP_SCALAR_DERIV:
+                if (n.a < 0 || n.a >= p->n_scalar || n.b < 0 || n.b >= p->scalar_spaces[n.a].deriv_terms)
+                    invalid("pointwise map: undeclared scalar derivative input");
+                break;
+            case FEMGPU_OP_VECTOR_DERIV:
+                if (n.a < 0 || n.a >= p->n_vector || n.b < 0 || n.b >= p->vector_spaces[n.a].deriv_terms)
+                    invalid("pointwise map: undeclared vector derivative input");
+                break;
+            case FEMGPU_OP_JACOBIAN:
+            case FEMGPU_OP_INV_JACOBIAN:
+                if (!p->affine_geometry) invalid("pointwise map: jacobian input requires affine geometry");
+                if (n.a < 0 || n.a >= p->dim || n.b < 0 || n.b >= p->dim)
+                    invalid("pointwise map: jacobian index out of range");
+                break;
+            case FEMGPU_OP_DETERMINANT:
+                if (!p->affine_geometry) invalid("pointwise map: determinant input requires affine geometry");
+                break;
+            case FEMGPU_OP_COORD:
+                if (!p->affine_geometry) invalid("pointwise map: coord input requires affine geometry");
+                if (n.a < 0 || n.a >= p->coord_dofs || n.b < 0 || n.b >= p->dim)
+                    invalid("pointwise map: coord index out of range");
+                break;
+            case FEMGPU_OP_ADD:
+            case FEMGPU_OP_MUL:
+                if (n.a < 0 || n.b < 0 || n.a >= id || n.b >= id)
+                    invalid("pointwise map: child must precede its parent");
+                break;
+            default: invalid("pointwise map: unknown op");
+        }
+    }
+    const long long Q = p->quad_points;
+    auto finite = [](const double* v, long long n, const char* what) {
+        if (!v && n) invalid(std::string("tabulations: missing ") + what);
+        for (long long i = 0; i < n; ++i)
+            if (!std::isfinite(v[i])) invalid(std::string("tabulations: non-finite entry in ") + what);
+    };
+    for (int i = 0; i < p->n_scalar; ++i)
+        finite(p->scalar_spaces[i].phi, p->scalar_spaces[i].deriv_terms * Q * p->scalar_spaces[i].dofs, "scalar phi");
+    for (int i = 0; i < p->n_vector; ++i)
+        finite(p->vector_spaces[i].phi, p->vector_spaces[i].deriv_terms * Q * p->vector_spaces[i].dofs, "vector phi");
+    finite(p->psi, p->test_deriv_terms * Q * p->test_dofs, "psi");
+    if (!p->weights) invalid("tabulations: weight count mismatch");
+    for (long long i = 0; i < Q; ++i)
+        if (!std::isfinite(p->weights[i])) invalid("tabulations: non-finite weight");
+    const long long C = p->cell_count;
+    if (C < 1) invalid("connectivity: at least one cell required");
+    auto check_map = [&](const int32_t* m, int entries, int bound, const char* what) {
+        if (!m) invalid(std::string("connectivity: bad shape for ") + what);
+        const long long n = C * entries;
+        for (long long i = 0; i < n; ++i)
+            if (m[i] < 0 || m[i] >= bound) invalid(std::string("connectivity: index out of bounds in ") + what);
+    };
+    for (int i = 0; i < p->n_scalar; ++i) {
+        check_map(p->scalar_spaces[i].map, p->scalar_spaces[i].dofs, p->scalar_spaces[i].global_count,
+                  "scalar space map");
+        if (!p->scalar_spaces[i].input) invalid("instance: scalar input length mismatch");
+    }
+    for (int i = 0; i < p->n_vector; ++i) {
+        check_map(p->vector_spaces[i].map, p->vector_spaces[i].dofs, p->vector_spaces[i].global_count,
+                  "vector space map");
+        if (!p->vector_spaces[i].input) invalid("instance: vector input length mismatch");
+    }
+    check_map(p->test_map, p->test_dofs, p->test_global_count, "test space map");
+    if (p->affine_geometry) {
+        check_map(p->coord_map, p->coord_dofs, p->coord_global_count, "coordinate map");
+        if (p->coord_global_count < 1 || !p->coords) invalid("connectivity: coordinate array shape mismatch");
+    }
+    if (p->output_size != p->test_global_count) invalid("instance: output length mismatch");
+}
+
+Instance::~Instance() {
+    if (stream) {
+        cudaStreamSynchronize(stream);
+        cudaStreamDestroy(stream);
+    }
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    for (void* p : allocations) cudaFree(p);
+    cudaGetLastError();
+}
+
+namespace {
+
+template <typename F>
+void parallel_for(long long n, F&& f) {
+    const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    const long long chunks = std::min<long long>(hw, std::max<long long>(1, n / 4096));
+    if (chunks <= 1) {
+        f(0LL, n);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (long long c = 0; c < chunks; ++c)
+        th.emplace_back([&, c] { f(n * c / chunks, n * (c + 1) / chunks); });
+    for (auto& t : th) t.join();
+}
+
+// Upload a [cell][entry] map as [entry][cell].
+int32_t* upload_transposed(Instance& inst, const int32_t* m, int cells, int entries) {
+    std::vector<int32_t> t(static_cast<size_t>(cells) * entries);
+    parallel_for(cells, [&](long long b, long long e) {
+        for (long long c = b; c < e; ++c)
+            for (int j = 0; j < entries; ++j) t[static_cast<size_t>(j) * cells + c] = m[c * entries + j];
+    });
+    int32_t* d = inst.alloc<int32_t>(t.size());
+    FG_CUDA(cudaMemcpy(d, t.data(), t.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    return d;
+}
+
+}  // namespace
+
+std::unique_ptr<Instance> create_instance(const femgpu_problem* p) {
+    validate_problem(p);
+    auto inst = std::make_unique<Instance>();
+    Instance& I = *inst;
+    FG_CUDA(cudaGetDevice(&I.device));
+    I.sig = signature_from(p);
+    I.cells = p->cell_count;
+    I.output_size = p->output_size;
+    FG_CUDA(cudaStreamCreateWithFlags(&I.stream, cudaStreamNonBlocking));
+    FG_CUDA(cudaEventCreate(&I.ev0));
+    FG_CUDA(cudaEventCreate(&I.ev1));
+
+    // packed tabulations
+    const Signature& s = I.sig;
+    I.tab.assign(static_cast<size_t>(s.tab_size), 0.0);
+    for (int i = 0; i < s.ns(); ++i)
+        std::memcpy(&I.tab[s.phi_off_s[i]], p->scalar_spaces[i].phi,
+                    sizeof(double) * static_cast<size_t>(s.sterms[i]) * s.Q * s.sdofs[i]);
+    for (int i = 0; i < s.nv(); ++i)
+        std::memcpy(&I.tab[s.phi_off_v[i]], p->vector_spaces[i].phi,
+                    sizeof(double) * static_cast<size_t>(s.vterms[i]) * s.Q * s.vdofs[i]);
+    std::memcpy(&I.tab[s.psi_off], p->psi, sizeof(double) * static_cast<size_t>(s.Tw) * s.nW * s.Q);
+    std::memcpy(&I.tab[s.w_off], p->weights, sizeof(double) * s.Q);
+    I.d_tab = I.alloc<double>(I.tab.size());
+    FG_CUDA(cudaMemcpy(I.d_tab, I.tab.data(), I.tab.size() * sizeof(double), cudaMemcpyHostToDevice));
+
+    // distinct maps (content-equal maps share one device copy and one tile layout)
+    struct MapRef {
+        const int32_t* m;
+        int entries, global;
+    };
+    std::vector<MapRef> groups;
+    std::vector<int32_t*> group_dev;
+    auto group_of = [&](const int32_t* m, int entries, int global) {
+        for (size_t g = 0; g < groups.size(); ++g) {
+            if (groups[g].entries != entries || groups[g].global != global) continue;
+            if (groups[g].m == m ||
+                std::memcmp(groups[g].m, m, sizeof(int32_t) * static_cast<size_t>(I.cells) * entries) == 0)
+                return static_cast<int>(g);
+        }
+        groups.push_back({m, entries, global});
+        group_dev.push_back(upload_transposed(I, m, I.cells, entries));
+        return static_cast<int>(groups.size() - 1);
+    };
+    I.test_group = group_of(p->test_map, p->test_dofs, p->test_global_count);
+    for (int i = 0; i < s.ns(); ++i) {
+        const femgpu_space& sp = p->scalar_spaces[i];
+        DeviceSpace ds;
+        ds.dofs = sp.dofs;
+        ds.terms = sp.deriv_terms;
+        ds.global = sp.global_count;
+        ds.group = group_of(sp.map, sp.dofs, sp.global_count);
+        ds.d_mapT = group_dev[ds.group];
+        ds.d_x = I.alloc<double>(static_cast<size_t>(sp.global_count));
+        FG_CUDA(cudaMemcpy(ds.d_x, sp.input, sizeof(double) * sp.global_count, cudaMemcpyHostToDevice));
+        I.sspaces.push_back(ds);
+    }
+    for (int i = 0; i < s.nv(); ++i) {
+        const femgpu_space& sp = p->vector_spaces[i];
+        DeviceSpace ds;
+        ds.dofs = sp.dofs;
+        ds.terms = sp.deriv_terms;
+        ds.global = sp.global_count;
+        ds.group = group_of(sp.map, sp.dofs, sp.global_count);
+        ds.d_mapT = group_dev[ds.group];
+        const size_t n = static_cast<size_t>(sp.global_count) * s.dim;
+        ds.d_x = I.alloc<double>(n);
+        FG_CUDA(cudaMemcpy(ds.d_x, sp.input, sizeof(double) * n, cudaMemcpyHostToDevice));
+        I.vspaces.push_back(ds);
+    }
+    if (s.affine) {
+        I.coord_group = group_of(p->coord_map, p->coord_dofs, p->coord_global_count);
+        I.d_cmapT = group_dev[I.coord_group];
+        I.coord_global = p->coord_global_count;
+        const size_t n = static_cast<size_t>(p->coord_global_count) * s.dim;
+        I.d_coords = I.alloc<double>(n);
+        FG_CUDA(cudaMemcpy(I.d_coords, p->coords, sizeof(double) * n, cudaMemcpyHostToDevice));
+    }
+    I.d_tmapT = group_dev[I.test_group];
+    for (const auto& g : groups) {
+        I.group_maps.emplace_back(g.m, g.m + static_cast<size_t>(I.cells) * g.entries);
+        I.group_global.push_back(g.global);
+    }
+    I.d_y = I.alloc<double>(static_cast<size_t>(I.output_size));
+    I.d_bad = reinterpret_cast<int32_t*>(I.alloc<unsigned long long>(2));
+    FG_CUDA(cudaMemset(I.d_bad, 0xff, 2 * sizeof(unsigned long long)));
+    FG_CUDA(cudaDeviceSynchronize());
+    return inst;
+}
+
+const TileLayout& Instance::tile_layout(int tc) {
+    auto it = tiles.find(tc);
+    if (it != tiles.end()) return *it->second;
+    auto L = std::make_unique<TileLayout>();
+    L->tile_cells = tc;
+    L->n_tiles = static_cast<int>((static_cast<long long>(cells) + tc - 1) / tc);
+    const int nt = L->n_tiles;
+    for (size_t g = 0; g < group_maps.size(); ++g) {
+        const std::vector<int32_t>& m = group_maps[g];
+        const int entries = static_cast<int>(m.size() / cells);
+        const int global = group_global[g];
+        std::vector<std::vector<int32_t>> uniq(nt);
+        std::vector<uint16_t> loc(static_cast<size_t>(cells) * entries);
+        std::vector<int> maxu(64, 0);
+        bool overflow = false;
+        parallel_for(nt, [&](long long b, long long e) {
+            std::vector<int32_t> buf;
+            for (long long t = b; t < e; ++t) {
+                const long long c0 = t * tc, c1 = std::min<long long>(cells, c0 + tc);
+                buf.assign(m.begin() + c0 * entries, m.begin() + c1 * entries);
+                std::sort(buf.begin(), buf.end());
+                buf.erase(std::unique(buf.begin(), buf.end()), buf.end());
+                if (buf.size() > 65535) overflow = true;
+                for (long long c = c0; c < c1; ++c)
+                    for (int j = 0; j < entries; ++j) {
+                        const int32_t gi = m[c * entries + j];
+                        const auto pos = std::lower_bound(buf.begin(), buf.end(), gi) - buf.begin();
+                        loc[static_cast<size_t>(j) * cells + c] = static_cast<uint16_t>(pos);
+                    }
+                uniq[t] = buf;
+            }
+        });
+        TileGroup G;
+        G.entries = entries;
+        if (overflow) {
+            G.max_unique = INT_MAX;  // tile family infeasible at this size
+            L->groups.push_back(G);
+            continue;
+        }
+        // shared flag: global index referenced by more than one tile
+        std::vector<int32_t> ntiles(static_cast<size_t>(global), 0);
+        for (int t = 0; t < nt; ++t)
+            for (int32_t gi : uniq[t]) ++ntiles[gi];
+        std::vector<int32_t> off(nt + 1, 0);
+        for (int t = 0; t < nt; ++t) {
+            off[t + 1] = off[t] + static_cast<int32_t>(uniq[t].size());
+            G.max_unique = std::max<int>(G.max_unique, static_cast<int>(uniq[t].size()));
+        }
+        G.total_unique = off[nt];
+        std::vector<int32_t> list(static_cast<size_t>(off[nt]));
+        for (int t = 0; t < nt; ++t)
+            for (size_t u = 0; u < uniq[t].size(); ++u) {
+                const int32_t gi = uniq[t][u];
+                list[off[t] + u] = ntiles[gi] > 1 ? static_cast<int32_t>(static_cast<uint32_t>(gi) | 0x80000000u) : gi;
+            }
+        G.d_off = alloc<int32_t>(off.size());
+        G.d_list = alloc<int32_t>(std::max<size_t>(1, list.size()));
+        G.d_loc = alloc<uint16_t>(loc.size());
+        FG_CUDA(cudaMemcpy(G.d_off, off.data(), off.size() * 4, cudaMemcpyHostToDevice));
+        FG_CUDA(cudaMemcpy(G.d_list, list.data(), list.size() * 4, cudaMemcpyHostToDevice));
+        FG_CUDA(cudaMemcpy(G.d_loc, loc.data(), loc.size() * 2, cudaMemcpyHostToDevice));
+        L->groups.push_back(G);
+    }
+    auto& ref = *L;
+    tiles[tc] = std::move(L);
+    return ref;
+}
+
+namespace {
+
+constexpr long long kParamTabLimit = 3800;  // doubles in the 32 KB kernel-parameter bank
+
+int int_dim(int a) { return a; }
+
+}  // namespace
+
+// Resolves a femgpu_schedule (TilingParams + B200 knobs) into a launch plan.
+KernelPlan resolve_schedule(Instance& I, const femgpu_schedule* s) {
+    const Signature& sig = I.sig;
+    femgpu_schedule def{};
+    if (!s) s = &def;
+    KernelPlan kp;
+    kp.strict = s->reserved[0] != 0;
+    const long long tab_bytes = sig.tab_size * 8;
+    if (s->kind == FEMGPU_MLT) {
+        kp.family = Family::Mlt;
+        kp.TQ = s->quad_tile;
+        kp.Ter = s->eval_row_tile;
+        kp.Tqr = s->quad_row_tile;
+        kp.Tqc = s->quad_col_tile;
+        kp.Nc = s->cells_per_group;
+        kp.Nwi = s->lanes_per_cell;
+        for (int i = 0; i < sig.ns(); ++i) kp.Tcs.push_back(s->eval_col_tiles_scalar[i]);
+        for (int i = 0; i < sig.nv(); ++i) kp.Tcv.push_back(s->eval_col_tiles_vector[i]);
+        // TilingParams::validate (qoi.hpp:62-93)
+        if (kp.Nc < 1 || kp.Nwi < 1) invalid("tiling: work-group factors must be >= 1");
+        if (kp.TQ < 1 || kp.TQ > sig.Q) invalid("tiling: quad_tile must be in [1, quad_points]");
+        if (kp.Ter < 1 || kp.Ter > kp.TQ) invalid("tiling: eval_row_tile must be in [1, quad_tile]");
+        for (int i = 0; i < sig.ns(); ++i)
+            if (kp.Tcs[i] < 1 || kp.Tcs[i] > sig.sdofs[i]) invalid("tiling: scalar column tile out of range");
+        for (int i = 0; i < sig.nv(); ++i)
+            if (kp.Tcv[i] < 1 || kp.Tcv[i] > sig.vdofs[i]) invalid("tiling: vector column tile out of range");
+        if (kp.Tqr < 1 || kp.Tqr > sig.nW) invalid("tiling: quad_row_tile must be in [1, test_dofs]");
+        if (kp.Tqc < 1 || kp.Tqc > kp.TQ) invalid("tiling: quad_col_tile must be in [1, quad_tile]");
+        if (kp.Nc * kp.Nwi > 1024)
+            fail(FEMGPU_E_INFEASIBLE, "tiling: work-group of " + std::to_string(kp.Nc * kp.Nwi) +
+                                          " work-items exceeds the device limit of 1024");
+        kp.block = kp.Nc * kp.Nwi;
+        kp.basis = FEMGPU_BASIS_SMEM;
+        return kp;
+    }
+    // SCPT: one thread per cell.
+    int basis = s->basis;
+    if (basis == FEMGPU_BASIS_AUTO) basis = sig.tab_size <= kParamTabLimit ? FEMGPU_BASIS_CONST : FEMGPU_BASIS_SMEM;
+    if (basis == FEMGPU_BASIS_CONST && sig.tab_size > kParamTabLimit)
+        fail(FEMGPU_E_INFEASIBLE, "basis: " + std::to_string(tab_bytes) +
+                                      " bytes of tabulations exceed the 32 KB kernel-parameter bank");
+    kp.basis = basis;
+    const int scatter = s->scatter == FEMGPU_SCATTER_AUTO ? FEMGPU_SCATTER_TILE : s->scatter;
+    int block = s->block_cells > 0 ? s->block_cells : (scatter == FEMGPU_SCATTER_TILE ? (sig.dim == 3 ? 384 : 256) : 128);
+    if (block > 1024) fail(FEMGPU_E_INFEASIBLE, "schedule: more than 1024 cells per CTA");
+    kp.block = block;
+    const long long smem_tab = basis == FEMGPU_BASIS_SMEM ? tab_bytes : 0;
+    if (scatter == FEMGPU_SCATTER_TILE) {
+        const TileLayout& L = I.tile_layout(block);
+        long long smem = smem_tab;
+        bool ok = true;
+        for (const auto& G : L.groups)
+            if (G.max_unique > 65535) ok = false;
+        if (ok) {
+            smem += 8LL * L.groups[I.test_group].max_unique;
+            for (const auto& sp : I.sspaces) smem += 8LL * L.groups[sp.group].max_unique;
+            for (const auto& sp : I.vspaces) smem += 8LL * sig.dim * L.groups[sp.group].max_unique;
+            if (sig.affine) smem += 8LL * sig.dim * L.groups[I.coord_group].max_unique;
+            if (smem > 227 * 1024) ok = false;
+        }
+        if (ok) {
+            kp.family = Family::Tile;
+            kp.tile_cells = block;
+            for (const auto& G : L.groups) {
+                kp.group_entries.push_back(G.entries);
+                kp.group_cap.push_back(G.max_unique);
+            }
+            kp.tgroup = I.test_group;
+            kp.cgroup = sig.affine ? I.coord_group : -1;
+            for (const auto& sp : I.sspaces) kp.sgroup.push_back(sp.group);
+            for (const auto& sp : I.vspaces) kp.vgroup.push_back(sp.group);
+            return kp;
+        }
+        if (s->scatter == FEMGPU_SCATTER_TILE)
+            fail(FEMGPU_E_INFEASIBLE, "schedule: tile layout does not fit shared memory at this tile size");
+    }
+    if (smem_tab > 227 * 1024)
+        fail(FEMGPU_E_INFEASIBLE, "basis: tabulations exceed the shared-memory capacity of one CTA");
+    kp.family = Family::Scpt;
+    (void)int_dim;
+    return kp;
+}
+
+namespace {
+
+struct ParamBuf {
+    std::vector<unsigned char> b;
+    void align(size_t a) {
+        while (b.size() % a) b.push_back(0);
+    }
+    template <typename T>
+    void put(const T& v) {
+        align(alignof(T));
+        const unsigned char* p = reinterpret_cast<const unsigned char*>(&v);
+        b.insert(b.end(), p, p + sizeof(T));
+    }
+};
+
+// Builds the kernel-parameter block in the exact layout of the emitted `struct Params`.
+ParamBuf build_params(Instance& I, const KernelPlan& kp, double* d_y, const TileLayout* L) {
+    const Signature& sig = I.sig;
+    ParamBuf P;
+    for (const auto& sp : I.sspaces) {
+        P.put(static_cast<const void*>(sp.d_x));
+        P.put(static_cast<const void*>(sp.d_mapT));
+    }
+    for (const auto& sp : I.vspaces) {
+        P.put(static_cast<const void*>(sp.d_x));
+        P.put(static_cast<const void*>(sp.d_mapT));
+    }
+    P.put(static_cast<const void*>(I.d_tmapT));
+    P.put(static_cast<const void*>(I.d_cmapT));
+    P.put(static_cast<const void*>(I.d_coords));
+    P.put(static_cast<void*>(d_y));
+    P.put(static_cast<void*>(I.d_bad));
+    P.put(static_cast<const void*>(I.d_tab));
+    const int ngroups = static_cast<int>(kp.group_entries.size());
+    for (int g = 0; g < ngroups; ++g) {
+        P.put(static_cast<const void*>(L->groups[g].d_off));
+        P.put(static_cast<const void*>(L->groups[g].d_list));
+        P.put(static_cast<const void*>(L->groups[g].d_loc));
+    }
+    P.put(static_cast<int32_t>(I.cells));
+    P.put(static_cast<int32_t>(I.cells));  // stride of the [entry][cell] maps
+    if (kp.basis == FEMGPU_BASIS_CONST && kp.family != Family::Mlt)
+        for (double v : I.tab) P.put(v);
+    P.align(8);
+    (void)sig;
+    return P;
+}
+
+}  // namespace
+
+void run_action(Instance& I, const KernelPlan& kp, double* d_y, cudaStream_t stream) {
+    auto mod = get_module(I.sig, kp);
+    const TileLayout* L = kp.family == Family::Tile ? &I.tile_layout(kp.tile_cells) : nullptr;
+    ParamBuf P = build_params(I, kp, d_y, L);
+    void* args[] = {P.b.data()};
+    FG_CUDA(cudaMemsetAsync(d_y, 0, sizeof(double) * static_cast<size_t>(I.output_size), stream));
+    long long grid = 0;
+    if (kp.family == Family::Mlt)
+        grid = (static_cast<long long>(I.cells) + kp.Nc - 1) / kp.Nc;
+    else if (kp.family == Family::Tile)
+        grid = L->n_tiles;
+    else
+        grid = (static_cast<long long>(I.cells) + kp.block - 1) / kp.block;
+    if (grid > INT_MAX) fail(FEMGPU_E_INFEASIBLE, "launch: grid too large");
+    FG_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(mod->fast), dim3(static_cast<unsigned>(grid)),
+                             dim3(kp.block), args, mod->emitted.smem_bytes, stream));
+    I.last_launches = 1;
+}
+
+void check_failure(Instance& I, const KernelPlan& kp, cudaStream_t stream) {
+    unsigned long long flags[2];
+    FG_CUDA(cudaMemcpyAsync(flags, I.d_bad, sizeof flags, cudaMemcpyDeviceToHost, stream));
+    FG_CUDA(cudaStreamSynchronize(stream));
+    if (flags[0] == ~0ULL) return;
+    // Diagnose with the stage-checked kernel (same source, CHECKED=true): lowest failing
+    // cell and its first failing stage, like the sequential reference (form.hpp:492-595).
+    auto mod = get_module(I.sig, kp);
+    const TileLayout* L = kp.family == Family::Tile ? &I.tile_layout(kp.tile_cells) : nullptr;
+    double* scratch = I.d_y;
+    unsigned long long* second = reinterpret_cast<unsigned long long*>(I.d_bad) + 1;
+    ParamBuf P = build_params(I, kp, scratch, L);
+    // redirect the flag pointer to the second slot: patch the 'bad' field (after y)
+    {
+        size_t off = (2 * I.sspaces.size() + 2 * I.vspaces.size() + 4) * sizeof(void*);
+        std::memcpy(P.b.data() + off, &second, sizeof(void*));
+    }
+    void* args[] = {P.b.data()};
+    long long grid = kp.family == Family::Mlt ? (static_cast<long long>(I.cells) + kp.Nc - 1) / kp.Nc
+                     : kp.family == Family::Tile ? L->n_tiles
+                                                 : (static_cast<long long>(I.cells) + kp.block - 1) / kp.block;
+    FG_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(mod->checked), dim3(static_cast<unsigned>(grid)),
+                             dim3(kp.block), args, mod->emitted.smem_bytes, stream));
+    FG_CUDA(cudaMemcpyAsync(flags, I.d_bad, sizeof flags, cudaMemcpyDeviceToHost, stream));
+    FG_CUDA(cudaStreamSynchronize(stream));
+    FG_CUDA(cudaMemsetAsync(I.d_bad, 0xff, sizeof flags, stream));
+    FG_CUDA(cudaStreamSynchronize(stream));
+    static const char* stages[] = {"jacobian", "evaluation", "pointwise map", "quadrature"};
+    unsigned long long cell = flags[0];
+    const char* stage = "quadrature";
+    if (flags[1] != ~0ULL) {
+        cell = flags[1] / 4;
+        stage = stages[flags[1] % 4];
+    }
+    fail(FEMGPU_E_NONFINITE,
+         "reference_action: non-finite value at cell " + std::to_string(cell) + " during " + stage);
+}
+
+}  // namespace femgpu
