@@ -130,7 +130,9 @@ typedef enum femgpu_basis {
 typedef enum femgpu_scatter {
     FEMGPU_SCATTER_AUTO = 0,
     FEMGPU_SCATTER_ATOMIC = 1, /* red.global.add.f64 per (cell, test DOF) */
-    FEMGPU_SCATTER_TILE = 2    /* CTA-tile aggregation in smem; global atomics only on shared DOFs */
+    FEMGPU_SCATTER_TILE = 2,   /* CTA-tile aggregation in smem; global atomics only on shared DOFs */
+    FEMGPU_SCATTER_MACRO = 3   /* macro-elements: G cells per thread with a common local pattern,
+                                  register accumulation, one atomic per unique DOF of the group */
 } femgpu_scatter;
 
 #define FEMGPU_MAX_SPACES 8
@@ -148,8 +150,9 @@ typedef struct femgpu_schedule {
     /* B200 knobs */
     int32_t basis;         /* femgpu_basis */
     int32_t scatter;       /* femgpu_scatter */
-    int32_t block_cells;   /* SCPT: cells (threads) per CTA; 0 = auto */
-    int32_t reserved[5];
+    int32_t block_cells;   /* SCPT/tile: cells (threads) per CTA; macro: groups (threads) per CTA; 0 = auto */
+    int32_t group_cells;   /* macro: cells per group G; 0 = auto */
+    int32_t reserved[4];   /* [0] strict (--fmad=false), [1] register target, [2] min CTAs/SM */
 } femgpu_schedule;
 
 typedef struct femgpu_instance femgpu_instance;

@@ -19,7 +19,7 @@ OP_CONSTANT, OP_SCALAR_DERIV, OP_VECTOR_DERIV, OP_JACOBIAN, OP_DETERMINANT, OP_W
 
 SCPT, MLT = 0, 1
 BASIS_AUTO, BASIS_CONST, BASIS_SMEM = 0, 1, 2
-SCATTER_AUTO, SCATTER_ATOMIC, SCATTER_TILE = 0, 1, 2
+SCATTER_AUTO, SCATTER_ATOMIC, SCATTER_TILE, SCATTER_MACRO = 0, 1, 2, 3
 MAX_SPACES = 8
 
 _dp = C.POINTER(C.c_double)
@@ -58,7 +58,7 @@ class Schedule(C.Structure):
         ("eval_col_tiles_scalar", C.c_int32 * MAX_SPACES), ("eval_col_tiles_vector", C.c_int32 * MAX_SPACES),
         ("quad_row_tile", C.c_int32), ("quad_col_tile", C.c_int32), ("cells_per_group", C.c_int32),
         ("lanes_per_cell", C.c_int32), ("basis", C.c_int32), ("scatter", C.c_int32),
-        ("block_cells", C.c_int32), ("reserved", C.c_int32 * 5),
+        ("block_cells", C.c_int32), ("group_cells", C.c_int32), ("reserved", C.c_int32 * 4),
     ]
 
 

@@ -42,7 +42,11 @@ class TilingParams:
     basis: int = abi.BASIS_AUTO
     scatter: int = abi.SCATTER_AUTO
     block_cells: int = 0
+    group_cells: int = 0
     strict: bool = False  # --fmad=false: bitwise per-cell arithmetic of the reference
+    reg_target: int = 0
+    min_blocks: int = 0
+    stage_smem: int = 0  # macro: stage the group's gathered values in shared memory (cp.async)
 
     @staticmethod
     def scpt(**knobs) -> "TilingParams":
@@ -75,7 +79,11 @@ class TilingParams:
         s.quad_row_tile, s.quad_col_tile = self.quad_row_tile, self.quad_col_tile
         s.cells_per_group, s.lanes_per_cell = self.cells_per_group, self.lanes_per_cell
         s.basis, s.scatter, s.block_cells = self.basis, self.scatter, self.block_cells
+        s.group_cells = self.group_cells
         s.reserved[0] = 1 if self.strict else 0
+        s.reserved[1] = self.reg_target
+        s.reserved[2] = self.min_blocks
+        s.reserved[3] = self.stage_smem
         return s
 
     def describe(self) -> str:  # search.hpp:301-310

@@ -15,9 +15,11 @@
 // Families (KernelPlan::family):
 //   Scpt  one thread per cell; int32 SoA maps read from global; red.global.add.f64 scatter.
 //   Tile  one thread per cell, one CTA per tile of consecutive cells: the tile's unique
-//         DOFs/vertices are staged in shared memory through tile-local uint16 maps, the
-//         cell results are reduced into a shared-memory y tile, and only DOFs shared with
-//         another tile reach global memory atomically (the rest are plain stores).
+//         DOFs/vertices are staged in shared memory (4 gathers in flight per thread) and
+//         read through tile-local uint16 maps; cell results go to a shared-memory staging
+//         array and are summed per DOF through a tile-local CSR (no atomics, fixed order:
+//         cells ascending, as in the reference); only DOFs shared with another tile reach
+//         global memory atomically, the rest are plain stores.
 //   Mlt   the paper's multi-level tiling (TilingParams, qoi.hpp:23-33): N_c cells x N_WI
 //         lanes per CTA, quadrature tiles T^Q, Phi/Psi tiles staged through an aliased
 //         shared buffer, lanes striding qp rows (evaluation) and test rows (quadrature),
@@ -26,7 +28,9 @@
 // kernel parameter bank (DFMA reads it as a c[0x0][imm] operand: zero load
 // instructions) or is staged once per CTA into shared memory.
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
+#include <map>
 #include <set>
 #include <sstream>
 
@@ -143,18 +147,31 @@ void emit_params(Out& o, const Signature& sig, const KernelPlan& kp, long long n
     for (int i = 0; i < sig.nv(); ++i) o.line("  const double* v" + std::to_string(i) + "; const int* vm" + std::to_string(i) + ";");
     o.line("  const int* tm; const int* cm; const double* X;");
     o.line("  double* y; unsigned long long* bad; const double* tabg;");
-    const int ngroups = static_cast<int>(kp.group_entries.size());
+    if (kp.family == Family::Macro)
+        for (size_t g = 0; g < kp.group_entries.size(); ++g) o.line("  const int* gidx" + std::to_string(g) + ";");
+    const int ngroups = kp.family == Family::Tile ? static_cast<int>(kp.group_entries.size()) : 0;
     for (int g = 0; g < ngroups; ++g)
-        o.line("  const int* goff" + std::to_string(g) + "; const int* glist" + std::to_string(g) +
-               "; const unsigned short* gloc" + std::to_string(g) + ";");
-    o.line("  int n_cells; int stride;");
+        o.line("  const int* goff" + std::to_string(g) + "; const int* gcnt" + std::to_string(g) + "; const int* glist" +
+               std::to_string(g) + "; const unsigned short* gloc" + std::to_string(g) + ";");
+    o.line("  const unsigned short* roff; const unsigned short* rpos;");
+    o.line("  int n_cells; int stride; int n_tiles; int lstride; int n_groups; int pad2_;");
     if (nt_param > 0) o.line("  double tab[" + std::to_string(nt_param) + "];");
     o.line("};");
 }
 
-// Per-cell body for Scpt/Tile: one thread computes one whole cell in registers.
+// Macro-element context: cell s of a group whose local connectivity is the
+// compile-time pattern kp.mpat[group][s*entries + j] (indices into the group's unique list).
+struct MacroCtx {
+    int s;
+    // mstage=1: per-thread shared-memory slots of the gathered values
+    std::vector<long long> xslot, vslot;  // per space: first slot
+    long long Xslot = 0;
+};
+
+// Per-cell body for Scpt/Tile/Macro: one thread computes one whole cell in registers.
 void emit_cell_body(Out& o, const Signature& sig, const KernelPlan& kp, const MapUse& use, bool tile,
-                    bool unroll_q) {
+                    bool unroll_q, const MacroCtx* mc = nullptr) {
+    auto pat = [&](int g, int j) { return kp.mpat[g][static_cast<size_t>(mc->s) * kp.group_entries[g] + j]; };
     const int d = sig.dim, Q = sig.Q;
     auto TAB = [&](const std::string& idx) {
         return kp.basis == FEMGPU_BASIS_CONST ? "P.tab[" + idx + "]" : "sT[" + idx + "]";
@@ -165,9 +182,13 @@ void emit_cell_body(Out& o, const Signature& sig, const KernelPlan& kp, const Ma
     for (int i = 0; i < sig.ns(); ++i) {
         for (int j = 0; j < sig.sdofs[i]; ++j) {
             std::string idx = std::to_string(j) + "*(size_t)" + C + "+cell";
-            if (tile && kp.sgroup[i] >= 0)
-                o.line("const double " + nm("u", i, j) + " = xs" + std::to_string(i) + "[P.gloc" +
-                       std::to_string(kp.sgroup[i]) + "[" + idx + "]];");
+            if (mc && kp.mstage)
+                o.line("const double " + nm("u", i, j) + " = SM(" + std::to_string(mc->xslot[i] + pat(kp.sgroup[i], j)) + ");");
+            else if (mc)
+                o.line("const double " + nm("u", i, j) + " = " + nm("xg", i, pat(kp.sgroup[i], j)) + ";");
+            else if (tile && kp.sgroup[i] >= 0)
+                o.line("const double " + nm("u", i, j) + " = xs" + std::to_string(i) + "[sl" +
+                       std::to_string(kp.sgroup[i]) + "[" + std::to_string(j * kp.tile_cells) + " + threadIdx.x]];");
             else
                 o.line("const double " + nm("u", i, j) + " = __ldg(&P.x" + std::to_string(i) + "[__ldg(&P.m" +
                        std::to_string(i) + "[" + idx + "])]);");
@@ -178,8 +199,16 @@ void emit_cell_body(Out& o, const Signature& sig, const KernelPlan& kp, const Ma
         for (int j = 0; j < sig.vdofs[i]; ++j) {
             std::string idx = std::to_string(j) + "*(size_t)" + C + "+cell";
             std::string node = nm("vn", i, j);
+            if (mc) {
+                for (int c : comps)
+                    o.line("const double " + nm("w", i, j, c) + " = " +
+                           (kp.mstage ? "SM(" + std::to_string(mc->vslot[i] + static_cast<long long>(pat(kp.vgroup[i], j)) * d + c) + ")"
+                                      : nm("vg", i, pat(kp.vgroup[i], j), c)) + ";");
+                continue;
+            }
             if (tile && kp.vgroup[i] >= 0)
-                o.line("const int " + node + " = P.gloc" + std::to_string(kp.vgroup[i]) + "[" + idx + "];");
+                o.line("const int " + node + " = sl" + std::to_string(kp.vgroup[i]) + "[" +
+                       std::to_string(j * kp.tile_cells) + " + threadIdx.x];");
             else
                 o.line("const int " + node + " = __ldg(&P.vm" + std::to_string(i) + "[" + idx + "]);");
             for (int c : comps) {
@@ -198,8 +227,16 @@ void emit_cell_body(Out& o, const Signature& sig, const KernelPlan& kp, const Ma
         for (int j = 0; j < sig.coord_dofs; ++j) {
             std::string idx = std::to_string(j) + "*(size_t)" + C + "+cell";
             std::string vtx = nm("cv", j);
+            if (mc) {
+                for (int c = 0; c < d; ++c)
+                    o.line("const double " + nm("X", j, c) + " = " +
+                           (kp.mstage ? "SM(" + std::to_string(mc->Xslot + static_cast<long long>(pat(kp.cgroup, j)) * d + c) + ")"
+                                      : nm("Xg", pat(kp.cgroup, j), c)) + ";");
+                continue;
+            }
             if (tile && kp.cgroup >= 0)
-                o.line("const int " + vtx + " = P.gloc" + std::to_string(kp.cgroup) + "[" + idx + "];");
+                o.line("const int " + vtx + " = sl" + std::to_string(kp.cgroup) + "[" + std::to_string(j * kp.tile_cells) +
+                       " + threadIdx.x];");
             else
                 o.line("const int " + vtx + " = __ldg(&P.cm[" + idx + "]);");
             for (int c = 0; c < d; ++c) {
@@ -338,8 +375,10 @@ void emit_cell_body(Out& o, const Signature& sig, const KernelPlan& kp, const Ma
     o.ind++;
     for (int jw = 0; jw < sig.nW; ++jw) {
         std::string idx = std::to_string(jw) + "*(size_t)" + C + "+cell";
-        if (tile)
-            o.line("atomicAdd(&ys[P.gloc" + std::to_string(kp.tgroup) + "[" + idx + "]], o" + std::to_string(jw) + ");");
+        if (mc)
+            o.line(nm("ya", pat(kp.tgroup, jw)) + " += o" + std::to_string(jw) + ";");
+        else if (tile)
+            o.line("st[" + std::to_string(jw * kp.tile_cells) + " + threadIdx.x] = o" + std::to_string(jw) + ";");
         else
             o.line("atomicAdd(&P.y[__ldg(&P.tm[" + idx + "])], o" + std::to_string(jw) + ");");
     }
@@ -358,17 +397,384 @@ const char* kPrelude = R"(// generated by femgpu (emit.cpp) for sm_100a
 std::string KernelPlan::key() const {
     std::ostringstream s;
     s << int(family) << "/" << basis << "/" << block << "/" << tile_cells << "/" << Nc << "x" << Nwi << "/" << TQ << "/"
-      << Ter << "/" << Tqr << "/" << Tqc << "/" << strict;
+      << Ter << "/" << Tqr << "/" << Tqc << "/" << strict << "/" << min_blocks << "/G" << G << "/ms" << mstage;
     for (int t : Tcs) s << "s" << t;
     for (int t : Tcv) s << "v" << t;
     for (size_t g = 0; g < group_cap.size(); ++g) s << "g" << group_entries[g] << ":" << group_cap[g];
     for (int g : sgroup) s << "S" << g;
     for (int g : vgroup) s << "V" << g;
     s << "T" << tgroup << "C" << cgroup;
+    uint64_t h = 0xcbf29ce484222325ULL;
+    for (const auto& p : mpat)
+        for (int v : p) h = (h ^ static_cast<uint64_t>(v + 1)) * 0x100000001b3ULL;
+    s << "P" << h;
     return s.str();
 }
 
 EmitResult emit_mlt(const Signature& sig, const KernelPlan& kp);  // emit_mlt.cpp
+
+namespace {
+
+std::string S(long long v) { return std::to_string(v); }
+
+// Checked (diagnostic) or plain SCPT kernel: one thread per cell, int32 SoA maps.
+void emit_scpt_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const MapUse& use, bool unroll_q,
+                      bool checked, const std::string& name, long long smem_tab_off) {
+    KernelPlan p = kp;
+    p.family = Family::Scpt;
+    o.line("");
+    std::string bounds = checked ? "" : "__launch_bounds__(" + S(kp.block) + ") ";
+    o.line("extern \"C\" __global__ void " + bounds + name + "(const __grid_constant__ Params P) {");
+    o.ind++;
+    o.line(std::string("constexpr bool CHECKED = ") + (checked ? "true" : "false") + ";");
+    if (kp.basis == FEMGPU_BASIS_SMEM) {
+        o.line("extern __shared__ __align__(16) unsigned char smraw[];");
+        o.line("double* sT = reinterpret_cast<double*>(smraw + " + S(smem_tab_off) + ");");
+        o.line("for (int i = threadIdx.x; i < " + S(sig.tab_size) + "; i += blockDim.x) sT[i] = P.tabg[i];");
+        o.line("__syncthreads();");
+    }
+    o.line("const int cell = blockIdx.x * blockDim.x + threadIdx.x;");
+    o.line("int stage = -1; (void)stage;");
+    o.line("if (cell < P.n_cells) {");
+    o.ind++;
+    emit_cell_body(o, sig, p, use, false, unroll_q);
+    o.ind--;
+    o.line("}");
+    o.line("return;");
+    o.line("report:");
+    o.line("  atomicMin(P.bad, (unsigned long long)cell * 4ull + (unsigned long long)stage);");
+    o.ind--;
+    o.line("}");
+}
+
+// Shared-memory plan of the pipelined tile kernel (bytes, 16-byte aligned regions).
+struct TilePlan {
+    struct Item {
+        std::string dst, src;
+        int group, comps;
+        long long off;  // within a buffer
+    };
+    std::vector<Item> items;            // gathered values per buffer
+    std::vector<int> gather_groups;     // groups whose local map the cell body reads
+    std::map<int, long long> sloc_off;  // per gather group, within a buffer
+    long long slist_off = 0, sroff_off = 0, srpos_off = 0;
+    long long tab_off = -1, st_off = 0, buf0 = 0, buf_bytes = 0, total = 0;
+};
+
+long long al16(long long v) { return (v + 15) / 16 * 16; }
+
+TilePlan plan_tile(const Signature& sig, const KernelPlan& kp) {
+    TilePlan t;
+    const int TB = kp.tile_cells, D = sig.dim;
+    long long off = 0;
+    if (kp.basis == FEMGPU_BASIS_SMEM) {
+        t.tab_off = off;
+        off = al16(off + sig.tab_size * 8);
+    }
+    t.st_off = off;
+    off = al16(off + 8LL * sig.nW * TB);
+    t.buf0 = off;
+    long long b = 0;
+    auto add_group = [&](int g) {
+        if (std::find(t.gather_groups.begin(), t.gather_groups.end(), g) == t.gather_groups.end())
+            t.gather_groups.push_back(g);
+    };
+    for (int i = 0; i < sig.ns(); ++i) {
+        t.items.push_back({"xs" + S(i), "P.x" + S(i), kp.sgroup[i], 1, 0});
+        add_group(kp.sgroup[i]);
+    }
+    for (int i = 0; i < sig.nv(); ++i) {
+        t.items.push_back({"vs" + S(i), "P.v" + S(i), kp.vgroup[i], D, 0});
+        add_group(kp.vgroup[i]);
+    }
+    if (sig.affine) {
+        t.items.push_back({"Xs", "P.X", kp.cgroup, D, 0});
+        add_group(kp.cgroup);
+    }
+    for (auto& it : t.items) {
+        it.off = b;
+        b = al16(b + 8LL * kp.group_cap[it.group] * it.comps);
+    }
+    for (int g : t.gather_groups) {
+        t.sloc_off[g] = b;
+        b = al16(b + 2LL * kp.group_entries[g] * TB);
+    }
+    const long long capt = (kp.group_cap[kp.tgroup] + 3) / 4 * 4;
+    t.slist_off = b;
+    b = al16(b + 4 * capt);
+    t.sroff_off = b;
+    b = al16(b + 2 * capt);
+    t.srpos_off = b;
+    b = al16(b + 2LL * TB * sig.nW);
+    t.buf_bytes = b;
+    t.total = off + 2 * b;
+    return t;
+}
+
+// The persistent, double-buffered tile kernel.  Per iteration (tile t, next tile tn):
+//   wait for buffer[cur]; prefetch (cp.async) tn's local maps, CSR and test list into
+//   buffer[nxt] and load tn's gather lists into registers; compute t's cells from smem
+//   into the staging array; issue tn's value gathers (cp.async x[list], coords[list]);
+//   reduce t per DOF through the CSR and write y (plain store, or red.add if shared).
+void emit_tile_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const MapUse& use, bool unroll_q,
+                      const TilePlan& T, const std::string& name) {
+    const int TB = kp.tile_cells;
+    const int nW = sig.nW;
+    o.line("");
+    std::string bounds = "__launch_bounds__(" + S(TB) + (kp.min_blocks > 1 ? ", " + S(kp.min_blocks) : "") + ") ";
+    o.line("extern \"C\" __global__ void " + bounds + name + "(const __grid_constant__ Params P) {");
+    o.ind++;
+    o.line("constexpr bool CHECKED = false;");
+    o.line("extern __shared__ __align__(16) unsigned char smraw[];");
+    if (kp.basis == FEMGPU_BASIS_SMEM) {
+        o.line("double* sT = reinterpret_cast<double*>(smraw + " + S(T.tab_off) + ");");
+        o.line("for (int i = threadIdx.x; i < " + S(sig.tab_size) + "; i += " + S(TB) + ") sT[i] = P.tabg[i];");
+    }
+    o.line("double* st = reinterpret_cast<double*>(smraw + " + S(T.st_off) + ");");
+    o.line("const int tid = threadIdx.x;");
+    o.line("int t = blockIdx.x;");
+    o.line("if (t >= P.n_tiles) return;");
+    // list registers per gather group
+    std::map<int, int> K;
+    for (int g : T.gather_groups) {
+        K[g] = (kp.group_cap[g] + TB - 1) / TB;
+        o.line("int gl" + S(g) + "[" + S(K[g]) + "];");
+    }
+    // --- helper lambdas (emitted as macros over a buffer base)
+    auto emit_meta = [&](const std::string& tile, const std::string& base) {
+        // local maps of the gather groups: entries rows of TB uint16 (16-byte chunks)
+        for (int g : T.gather_groups) {
+            const int ent = kp.group_entries[g];
+            const long long chunks_per_row = 2LL * TB / 16;
+            o.line("for (int c = tid; c < " + S(ent * chunks_per_row) + "; c += " + S(TB) + ") {");
+            o.line("  const int j = c / " + S(chunks_per_row) + ", k = c % " + S(chunks_per_row) + ";");
+            o.line("  cp16(" + base + " + " + S(T.sloc_off.at(g)) + " + (j * " + S(TB) + ") * 2 + k * 16, P.gloc" + S(g) +
+                   " + (size_t)j * P.lstride + (size_t)" + tile + " * " + S(TB) + " + k * 8);");
+            o.line("}");
+        }
+        const std::string G = S(kp.tgroup);
+        o.line("{");
+        o.line("  const int lb = __ldg(&P.goff" + G + "[" + tile + "]), ln = __ldg(&P.gcnt" + G + "[" + tile + "]);");
+        o.line("  for (int c = tid; c < (ln + 3) / 4; c += " + S(TB) + ") cp16(" + base + " + " + S(T.slist_off) +
+               " + c * 16, P.glist" + G + " + lb + c * 4);");
+        o.line("  for (int c = tid; c < (ln + 3) / 4; c += " + S(TB) + ") cp8(" + base + " + " + S(T.sroff_off) +
+               " + c * 8, P.roff + lb + c * 4);");
+        o.line("  const int tc = min(" + S(TB) + ", P.n_cells - " + tile + " * " + S(TB) + ");");
+        o.line("  for (int c = tid; c < (tc * " + S(nW) + " + 7) / 8; c += " + S(TB) + ") cp16(" + base + " + " +
+               S(T.srpos_off) + " + c * 16, P.rpos + (size_t)" + tile + " * " + S(TB * nW) + " + c * 8);");
+        o.line("}");
+    };
+    auto emit_lists = [&](const std::string& tile) {
+        for (int g : T.gather_groups) {
+            o.line("{");
+            o.line("  const int lb = __ldg(&P.goff" + S(g) + "[" + tile + "]), ln = __ldg(&P.gcnt" + S(g) + "[" + tile + "]);");
+            o.line("  #pragma unroll");
+            o.line("  for (int k = 0; k < " + S(K[g]) + "; ++k) { const int u = tid + k * " + S(TB) + "; gl" + S(g) +
+                   "[k] = u < ln ? (__ldg(&P.glist" + S(g) + "[lb + u]) & 0x7fffffff) : -1; }");
+            o.line("}");
+        }
+    };
+    auto emit_gathers = [&](const std::string& base) {
+        for (const auto& it : T.items) {
+            o.line("#pragma unroll");
+            o.line("for (int k = 0; k < " + S(K[it.group]) + "; ++k) if (gl" + S(it.group) + "[k] >= 0) {");
+            o.line("  const int u = tid + k * " + S(TB) + ";");
+            for (int c = 0; c < it.comps; ++c)
+                o.line("  cp8(" + base + " + " + S(it.off) + " + (u * " + S(it.comps) + " + " + S(c) + ") * 8, " + it.src +
+                       " + (size_t)gl" + S(it.group) + "[k] * " + S(it.comps) + " + " + S(c) + ");");
+            o.line("}");
+        }
+    };
+    // prologue: tile t into buffer 0
+    o.line("unsigned char* const buf0 = smraw + " + S(T.buf0) + ";");
+    emit_meta("t", "buf0");
+    emit_lists("t");
+    emit_gathers("buf0");
+    o.line("cp_commit();");
+    o.line("int cur = 0;");
+    o.line("for (;;) {");
+    o.ind++;
+    o.line("const int tn = t + gridDim.x;");
+    o.line("cp_wait_all();");
+    o.line("__syncthreads();");
+    o.line("unsigned char* B = buf0 + cur * " + S(T.buf_bytes) + ";");
+    o.line("unsigned char* N = buf0 + (cur ^ 1) * " + S(T.buf_bytes) + ";");
+    o.line("if (tn < P.n_tiles) {");
+    o.ind++;
+    emit_meta("tn", "N");
+    emit_lists("tn");
+    o.ind--;
+    o.line("}");
+    // compute tile t
+    for (const auto& it : T.items)
+        o.line("const double* " + it.dst + " = reinterpret_cast<const double*>(B + " + S(it.off) + ");");
+    for (int g : T.gather_groups)
+        o.line("const unsigned short* sl" + S(g) + " = reinterpret_cast<const unsigned short*>(B + " +
+               S(T.sloc_off.at(g)) + ");");
+    o.line("const int cell = t * " + S(TB) + " + tid;");
+    o.line("int stage = -1; (void)stage;");
+    o.line("if (cell < P.n_cells) {");
+    o.ind++;
+    emit_cell_body(o, sig, kp, use, true, unroll_q);
+    o.ind--;
+    o.line("}");
+    o.line("if (tn < P.n_tiles) {");
+    o.ind++;
+    emit_gathers("N");
+    o.ind--;
+    o.line("}");
+    o.line("cp_commit();");
+    o.line("__syncthreads();");
+    // reduce tile t
+    o.line("{");
+    o.ind++;
+    o.line("const int ln = __ldg(&P.gcnt" + S(kp.tgroup) + "[t]);");
+    o.line("const int tc = min(" + S(TB) + ", P.n_cells - t * " + S(TB) + ");");
+    o.line("const int* slist = reinterpret_cast<const int*>(B + " + S(T.slist_off) + ");");
+    o.line("const unsigned short* sroff = reinterpret_cast<const unsigned short*>(B + " + S(T.sroff_off) + ");");
+    o.line("const unsigned short* srpos = reinterpret_cast<const unsigned short*>(B + " + S(T.srpos_off) + ");");
+    o.line("for (int u = tid; u < ln; u += " + S(TB) + ") {");
+    o.line("  const int e = slist[u];");
+    o.line("  const int r0 = sroff[u], r1 = u + 1 < ln ? (int)sroff[u + 1] : tc * " + S(nW) + ";");
+    o.line("  double s = 0.0;");
+    o.line("  for (int r = r0; r < r1; ++r) s += st[srpos[r]];");
+    o.line("  if (e < 0) atomicAdd(&P.y[e & 0x7fffffff], s); else P.y[e] = s;");
+    o.line("}");
+    o.ind--;
+    o.line("}");
+    o.line("if (tn >= P.n_tiles) break;");
+    o.line("t = tn;");
+    o.line("cur ^= 1;");
+    o.ind--;
+    o.line("}");
+    o.line("return;");
+    o.line("report:");
+    o.line("  return;");
+    o.ind--;
+    o.line("}");
+}
+
+// Macro-element kernel: one thread per group of G cells sharing the compile-time pattern.
+// Gathers each unique node of the group once, computes the G cells in order with the
+// per-cell operation order of the reference, accumulates y per unique node in registers
+// (cells ascending), and issues one red.global.add.f64 per unique test DOF.
+void emit_macro_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const MapUse& use, bool unroll_q,
+                       const std::string& name, long long smem_tab_off) {
+    const int D = sig.dim;
+    o.line("");
+    std::string bounds = "__launch_bounds__(" + S(kp.block) + (kp.min_blocks > 1 ? ", " + S(kp.min_blocks) : "") + ") ";
+    o.line("extern \"C\" __global__ void " + bounds + name + "(const __grid_constant__ Params P) {");
+    o.ind++;
+    o.line("constexpr bool CHECKED = false;");
+    if (kp.basis == FEMGPU_BASIS_SMEM) {
+        o.line("extern __shared__ __align__(16) unsigned char smraw[];");
+        o.line("double* sT = reinterpret_cast<double*>(smraw + " + S(smem_tab_off) + ");");
+        o.line("for (int i = threadIdx.x; i < " + S(sig.tab_size) + "; i += blockDim.x) sT[i] = P.tabg[i];");
+        o.line("__syncthreads();");
+    }
+    if (kp.mstage) {
+        if (kp.basis != FEMGPU_BASIS_SMEM) o.line("extern __shared__ __align__(16) unsigned char smraw[];");
+        o.line("volatile double* const sm_base = reinterpret_cast<volatile double*>(smraw + " + S(smem_tab_off + (kp.basis == FEMGPU_BASIS_SMEM ? al16(sig.tab_size * 8) : 0)) + ") + threadIdx.x;");
+        o.line("#define SM(k) sm_base[(k) * " + S(kp.block) + "]");
+        o.line("#define cp8s(k, src) cp8(const_cast<unsigned char*>(reinterpret_cast<volatile unsigned char*>(&SM(k))), (src))");
+    }
+    o.line("const int grp = blockIdx.x * " + S(kp.block) + " + threadIdx.x;");
+    o.line("if (grp >= P.n_groups) return;");
+    o.line("const size_t NG = (size_t)P.n_groups;");
+    // gathers: unique global indices per group, then values
+    std::set<int> gathered;
+    for (int i = 0; i < sig.ns(); ++i) gathered.insert(kp.sgroup[i]);
+    for (int i = 0; i < sig.nv(); ++i) gathered.insert(kp.vgroup[i]);
+    if (sig.affine) gathered.insert(kp.cgroup);
+    for (int g : gathered)
+        for (int u = 0; u < kp.group_cap[g]; ++u)
+            o.line("const int ig" + S(g) + "_" + S(u) + " = __ldg(&P.gidx" + S(g) + "[" + S(u) + " * NG + grp]);");
+    MacroCtx base{0, {}, {}, 0};
+    if (kp.mstage) {
+        // thread-private slots [slot][blockDim] (conflict-free), filled with cp.async
+        long long slot = 0;
+        std::vector<std::string> copies;
+        for (int i = 0; i < sig.ns(); ++i) {
+            base.xslot.push_back(slot);
+            for (int u = 0; u < kp.group_cap[kp.sgroup[i]]; ++u)
+                copies.push_back("cp8s(" + S(slot + u) + ", P.x" + S(i) + " + ig" + S(kp.sgroup[i]) + "_" + S(u) + ");");
+            slot += kp.group_cap[kp.sgroup[i]];
+        }
+        for (int i = 0; i < sig.nv(); ++i) {
+            base.vslot.push_back(slot);
+            for (int u = 0; u < kp.group_cap[kp.vgroup[i]]; ++u)
+                for (int c = 0; c < D; ++c)
+                    copies.push_back("cp8s(" + S(slot + static_cast<long long>(u) * D + c) + ", P.v" + S(i) + " + (size_t)ig" +
+                                     S(kp.vgroup[i]) + "_" + S(u) + " * " + S(D) + " + " + S(c) + ");");
+            slot += static_cast<long long>(kp.group_cap[kp.vgroup[i]]) * D;
+        }
+        if (sig.affine) {
+            base.Xslot = slot;
+            for (int u = 0; u < kp.group_cap[kp.cgroup]; ++u)
+                for (int c = 0; c < D; ++c)
+                    copies.push_back("cp8s(" + S(slot + static_cast<long long>(u) * D + c) + ", P.X + (size_t)ig" +
+                                     S(kp.cgroup) + "_" + S(u) + " * " + S(D) + " + " + S(c) + ");");
+            slot += static_cast<long long>(kp.group_cap[kp.cgroup]) * D;
+        }
+        for (const auto& c : copies) o.line(c);
+        o.line("cp_commit();");
+        o.line("cp_wait_all();");
+    }
+    for (int i = 0; i < sig.ns() && !kp.mstage; ++i)
+        for (int u = 0; u < kp.group_cap[kp.sgroup[i]]; ++u)
+            o.line("const double xg" + S(i) + "_" + S(u) + " = __ldg(&P.x" + S(i) + "[ig" + S(kp.sgroup[i]) + "_" + S(u) + "]);");
+    for (int i = 0; i < sig.nv() && !kp.mstage; ++i) {
+        std::set<int> comps(sig.vcomps[i].begin(), sig.vcomps[i].end());
+        for (int u = 0; u < kp.group_cap[kp.vgroup[i]]; ++u)
+            for (int c : comps)
+                o.line("const double vg" + S(i) + "_" + S(u) + "_" + S(c) + " = __ldg(&P.v" + S(i) + "[(size_t)ig" +
+                       S(kp.vgroup[i]) + "_" + S(u) + " * " + S(D) + " + " + S(c) + "]);");
+    }
+    if (sig.affine && !kp.mstage)
+        for (int u = 0; u < kp.group_cap[kp.cgroup]; ++u)
+            for (int c = 0; c < D; ++c)
+                o.line("const double Xg" + S(u) + "_" + S(c) + " = __ldg(&P.X[(size_t)ig" + S(kp.cgroup) + "_" + S(u) +
+                       " * " + S(D) + " + " + S(c) + "]);");
+    {
+        std::string l = "double";
+        for (int u = 0; u < kp.group_cap[kp.tgroup]; ++u) l += std::string(u ? "," : "") + " ya" + S(u) + " = 0.0";
+        o.line(l + ";");
+    }
+    o.line("int stage = -1; (void)stage;");
+    for (int s = 0; s < kp.G; ++s) {
+        o.line("{ // cell " + S(s) + " of the group");
+        o.ind++;
+        o.line("const int cell = grp * " + S(kp.G) + " + " + S(s) + ";");
+        MacroCtx mc = base;
+        mc.s = s;
+        emit_cell_body(o, sig, kp, use, false, unroll_q, &mc);
+        o.ind--;
+        o.line("}");
+    }
+    const int gt = kp.tgroup;
+    for (int u = 0; u < kp.group_cap[gt]; ++u) {
+        const std::string idx = gathered.count(gt) ? "ig" + S(gt) + "_" + S(u) : "__ldg(&P.gidx" + S(gt) + "[" + S(u) + " * NG + grp])";
+        o.line("atomicAdd(&P.y[" + idx + "], ya" + S(u) + ");");
+    }
+    o.line("return;");
+    o.line("report:");
+    o.line("  return;");
+    o.ind--;
+    o.line("}");
+}
+
+const char* kAsync = R"(
+__device__ __forceinline__ void cp16(unsigned char* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp8(unsigned char* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+)";
+
+}  // namespace
 
 EmitResult emit_kernel(const Signature& sig, const KernelPlan& kp) {
     if (kp.family == Family::Mlt) return emit_mlt(sig, kp);
@@ -385,123 +791,39 @@ EmitResult emit_kernel(const Signature& sig, const KernelPlan& kp) {
     for (int i = 0; i < sig.nv(); ++i) fmas += static_cast<long long>(sig.vterms[i]) * sig.vdofs[i];
     fmas += static_cast<long long>(sig.nW) * sig.Tw;
     const bool unroll_q = fmas * sig.Q <= 6000;
-
-    const std::string name = tile ? "femgpu_tile" : "femgpu_scpt";
-    r.kernel = name;
-    r.kernel_checked = name + "_checked";
-
-    // smem layout (doubles): [tab (smem basis)] [ys] [xs_i] [vs_i] [Xs]
-    long long off = 0;
-    long long off_tab = -1, off_y = -1, off_X = -1;
-    std::vector<long long> off_x(sig.ns(), -1), off_v(sig.nv(), -1);
-    if (kp.basis == FEMGPU_BASIS_SMEM) {
-        off_tab = off;
-        off += sig.tab_size;
-    }
-    if (tile) {
-        off_y = off;
-        off += kp.group_cap[kp.tgroup];
-        for (int i = 0; i < sig.ns(); ++i)
-            if (kp.sgroup[i] >= 0) {
-                off_x[i] = off;
-                off += kp.group_cap[kp.sgroup[i]];
-            }
-        for (int i = 0; i < sig.nv(); ++i)
-            if (kp.vgroup[i] >= 0) {
-                off_v[i] = off;
-                off += static_cast<long long>(kp.group_cap[kp.vgroup[i]]) * sig.dim;
-            }
-        if (sig.affine && kp.cgroup >= 0) {
-            off_X = off;
-            off += static_cast<long long>(kp.group_cap[kp.cgroup]) * sig.dim;
+    if (kp.family == Family::Macro) {
+        r.kernel = "femgpu_macro";
+        r.kernel_checked = "femgpu_macro_checked";
+        r.smem_bytes = kp.basis == FEMGPU_BASIS_SMEM ? static_cast<size_t>(al16(sig.tab_size * 8)) : 0;
+        if (kp.mstage) {
+            o << kAsync;
+            long long slots = 0;
+            for (int i = 0; i < sig.ns(); ++i) slots += kp.group_cap[kp.sgroup[i]];
+            for (int i = 0; i < sig.nv(); ++i) slots += static_cast<long long>(kp.group_cap[kp.vgroup[i]]) * sig.dim;
+            if (sig.affine) slots += static_cast<long long>(kp.group_cap[kp.cgroup]) * sig.dim;
+            r.smem_bytes += static_cast<size_t>(slots * 8 * kp.block);
         }
-    }
-    r.smem_bytes = static_cast<size_t>(off) * 8;
-
-    for (int checked = 0; checked < 2; ++checked) {
-        const std::string kn = checked ? r.kernel_checked : r.kernel;
-        o.line("");
-        o.line(std::string("extern \"C\" __global__ void ") + (checked ? "" : "__launch_bounds__(" + std::to_string(kp.block) + ") ") +
-               kn + "(const __grid_constant__ Params P) {");
-        o.ind++;
-        o.line(std::string("constexpr bool CHECKED = ") + (checked ? "true" : "false") + ";");
-        if (off > 0) o.line("extern __shared__ double smem[];");
-        if (kp.basis == FEMGPU_BASIS_SMEM) {
-            o.line("double* sT = smem + " + std::to_string(off_tab) + ";");
-            o.line("for (int i = threadIdx.x; i < " + std::to_string(sig.tab_size) + "; i += blockDim.x) sT[i] = P.tabg[i];");
-        }
-        if (tile) {
-            o.line("const int tile = blockIdx.x;");
-            o.line("const int cell = tile * " + std::to_string(kp.tile_cells) + " + threadIdx.x;");
-            o.line("double* ys = smem + " + std::to_string(off_y) + ";");
-            for (int i = 0; i < sig.ns(); ++i)
-                if (off_x[i] >= 0) o.line("double* xs" + std::to_string(i) + " = smem + " + std::to_string(off_x[i]) + ";");
-            for (int i = 0; i < sig.nv(); ++i)
-                if (off_v[i] >= 0) o.line("double* vs" + std::to_string(i) + " = smem + " + std::to_string(off_v[i]) + ";");
-            if (off_X >= 0) o.line("double* Xs = smem + " + std::to_string(off_X) + ";");
-            // stage every group's unique entries
-            const int ngroups = static_cast<int>(kp.group_entries.size());
-            for (int g = 0; g < ngroups; ++g) {
-                std::string G = std::to_string(g);
-                o.line("{");
-                o.ind++;
-                o.line("const int b = __ldg(&P.goff" + G + "[tile]), n = __ldg(&P.goff" + G + "[tile + 1]) - b;");
-                o.line("for (int u = threadIdx.x; u < n; u += blockDim.x) {");
-                o.ind++;
-                o.line("const int gi = __ldg(&P.glist" + G + "[b + u]) & 0x7fffffff;");
-                if (g == kp.tgroup) o.line("ys[u] = 0.0;");
-                for (int i = 0; i < sig.ns(); ++i)
-                    if (kp.sgroup[i] == g) o.line("xs" + std::to_string(i) + "[u] = __ldg(&P.x" + std::to_string(i) + "[gi]);");
-                for (int i = 0; i < sig.nv(); ++i)
-                    if (kp.vgroup[i] == g)
-                        for (int c = 0; c < sig.dim; ++c)
-                            o.line("vs" + std::to_string(i) + "[u*" + std::to_string(sig.dim) + "+" + std::to_string(c) +
-                                   "] = __ldg(&P.v" + std::to_string(i) + "[(size_t)gi*" + std::to_string(sig.dim) + "+" +
-                                   std::to_string(c) + "]);");
-                if (sig.affine && kp.cgroup == g)
-                    for (int c = 0; c < sig.dim; ++c)
-                        o.line("Xs[u*" + std::to_string(sig.dim) + "+" + std::to_string(c) + "] = __ldg(&P.X[(size_t)gi*" +
-                               std::to_string(sig.dim) + "+" + std::to_string(c) + "]);");
-                o.ind--;
-                o.line("}");
-                o.ind--;
-                o.line("}");
-            }
-            o.line("__syncthreads();");
-        } else {
-            if (kp.basis == FEMGPU_BASIS_SMEM) o.line("__syncthreads();");
-            o.line("const int cell = blockIdx.x * " + std::to_string(kp.block) + " + threadIdx.x;");
-        }
-        o.line("int stage = -1; (void)stage;");
-        o.line("if (cell < P.n_cells) {");
-        o.ind++;
-        emit_cell_body(o, sig, kp, use, tile, unroll_q);
-        o.ind--;
-        o.line("}");
-        o.line("goto done;");
-        o.line("report:");
-        o.line("  atomicMin(P.bad, (unsigned long long)cell * 4ull + (unsigned long long)stage);");
-        o.line("done:");
-        if (tile && !checked) {
-            const std::string G = std::to_string(kp.tgroup);
-            o.line("__syncthreads();");
-            o.line("{");
-            o.ind++;
-            o.line("const int b = __ldg(&P.goff" + G + "[tile]), n = __ldg(&P.goff" + G + "[tile + 1]) - b;");
-            o.line("for (int u = threadIdx.x; u < n; u += blockDim.x) {");
-            o.line("  const int e = __ldg(&P.glist" + G + "[b + u]);");
-            o.line("  if (e < 0) atomicAdd(&P.y[e & 0x7fffffff], ys[u]); else P.y[e] = ys[u];");
-            o.line("}");
-            o.ind--;
-            o.line("}");
-        }
-        o.line("return;");
-        o.ind--;
-        o.line("}");
+        emit_macro_kernel(o, sig, kp, use, unroll_q, r.kernel, 0);
+        emit_scpt_kernel(o, sig, kp, use, unroll_q, true, r.kernel_checked, 0);
+    } else if (tile) {
+        o << kAsync;
+        const TilePlan T = plan_tile(sig, kp);
+        r.kernel = "femgpu_tile";
+        r.kernel_checked = "femgpu_tile_checked";
+        r.smem_bytes = static_cast<size_t>(T.total);
+        emit_tile_kernel(o, sig, kp, use, unroll_q, T, r.kernel);
+        emit_scpt_kernel(o, sig, kp, use, unroll_q, true, r.kernel_checked, T.tab_off);
+    } else {
+        r.kernel = "femgpu_scpt";
+        r.kernel_checked = "femgpu_scpt_checked";
+        r.smem_bytes = kp.basis == FEMGPU_BASIS_SMEM ? static_cast<size_t>(sig.tab_size) * 8 : 0;
+        emit_scpt_kernel(o, sig, kp, use, unroll_q, false, r.kernel, 0);
+        emit_scpt_kernel(o, sig, kp, use, unroll_q, true, r.kernel_checked, 0);
     }
     r.source = o.s.str();
-    r.param_bytes = 0;
     return r;
 }
+
+size_t tile_smem_bytes(const Signature& sig, const KernelPlan& kp) { return static_cast<size_t>(plan_tile(sig, kp).total); }
 
 }  // namespace femgpu

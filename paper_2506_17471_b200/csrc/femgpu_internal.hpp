@@ -56,7 +56,7 @@ struct Signature {
 Signature signature_from(const femgpu_problem* p);
 
 // Kernel families.
-enum class Family { Scpt, Tile, Mlt };
+enum class Family { Scpt, Tile, Mlt, Macro };
 
 // Fully resolved launch plan (what the emitter specialises on).
 struct KernelPlan {
@@ -64,6 +64,7 @@ struct KernelPlan {
     int basis = FEMGPU_BASIS_CONST;    // const (param bank) or smem
     int block = 128;                   // threads per CTA
     int tile_cells = 0;                // Tile: cells per CTA (== block)
+    int min_blocks = 1;                // __launch_bounds__ min CTAs per SM (register cap)
     // Tile family: map-group ids per space (-1 = not staged) and smem capacities.
     std::vector<int> sgroup, vgroup;
     int tgroup = -1, cgroup = -1;
@@ -72,6 +73,10 @@ struct KernelPlan {
     int Nc = 1, Nwi = 1, TQ = 1, Ter = 1, Tqr = 1, Tqc = 1;
     std::vector<int> Tcs, Tcv;
     bool strict = false;               // --fmad=false (bitwise debug mode)
+    // Macro family: G cells per thread sharing the compile-time local pattern mpat[group]
+    int G = 0;
+    int mstage = 0;                       // 0: gathered values in registers; 1: cp.async into smem
+    std::vector<std::vector<int>> mpat;   // per map group: G*entries local indices
     std::string key() const;
 };
 
@@ -84,6 +89,7 @@ struct EmitResult {
 };
 
 EmitResult emit_kernel(const Signature& sig, const KernelPlan& kp);
+size_t tile_smem_bytes(const Signature& sig, const KernelPlan& kp);
 
 // JIT: NVRTC compile for sm_100a, cached by source hash (memory + disk).
 struct Module {
@@ -91,6 +97,8 @@ struct Module {
     cudaKernel_t fast = nullptr, checked = nullptr;
     EmitResult emitted;
     int regs = 0;
+    int occupancy = 1;   // resident CTAs per SM of the fast kernel
+    int sms = 148;
 };
 std::vector<char> jit_compile(const std::string& source, bool strict, std::string* log);
 std::shared_ptr<Module> get_module(const Signature& sig, const KernelPlan& kp);
@@ -100,15 +108,31 @@ struct TileGroup {
     int entries = 0;
     int max_unique = 0;
     long long total_unique = 0;
-    int32_t* d_off = nullptr;      // n_tiles+1
+    int32_t* d_off = nullptr;      // per tile: start of its (4-aligned) segment in list/roff
+    int32_t* d_cnt = nullptr;      // per tile: unique entries
     int32_t* d_list = nullptr;     // global index | 0x80000000 if shared with another tile
-    uint16_t* d_loc = nullptr;     // [entry][cell] tile-local index
+    uint16_t* d_loc = nullptr;     // [entry][lstride] tile-local index (lstride = n_tiles*TB)
 };
 
 struct TileLayout {
     int tile_cells = 0;
     int n_tiles = 0;
     std::vector<TileGroup> groups;
+    // CSR of the test group: per unique DOF (aligned with its list) the start of its
+    // contribution run; per tile, TB*nW staging positions j*TB + local_cell.
+    uint16_t* d_roff = nullptr;
+    uint16_t* d_rpos = nullptr;
+};
+
+// Macro-element layout: groups of G consecutive cells with one common local
+// connectivity pattern per distinct map (detected in femgpu_create).
+struct MacroLayout {
+    int G = 0;
+    long long n_groups = 0;
+    bool ok = false;
+    std::vector<int> unique;                 // per map group: unique entries per cell group
+    std::vector<std::vector<int>> pattern;   // per map group: G*entries local indices
+    std::vector<int32_t*> d_gidx;            // per map group: [unique][n_groups] global indices
 };
 
 struct DeviceSpace {
@@ -137,6 +161,9 @@ struct Instance {
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     std::map<int, std::unique_ptr<TileLayout>> tiles;   // by tile size
+    std::map<int, std::unique_ptr<MacroLayout>> macros; // by cells per group
+    std::map<std::string, std::shared_ptr<Module>> modules;  // by KernelPlan::key(): no re-emit per launch
+    std::shared_ptr<Module> module_for(const KernelPlan& kp);
     std::vector<void*> allocations;
     int64_t device_bytes = 0;
     int64_t last_launches = 0;
@@ -152,9 +179,13 @@ struct Instance {
         return static_cast<T*>(p);
     }
     const TileLayout& tile_layout(int tile_cells);
+    const MacroLayout& macro_layout(int G);
 };
 
 void validate_problem(const femgpu_problem* p);
+// Host-only tile planning (map groups, per-tile unique caps) for emit/JIT checks without a GPU.
+void host_tile_plan(const femgpu_problem* p, const Signature& sig, KernelPlan& kp, const femgpu_schedule* s);
+void host_macro_plan(const femgpu_problem* p, const Signature& sig, KernelPlan& kp, const femgpu_schedule* s);
 std::unique_ptr<Instance> create_instance(const femgpu_problem* p);
 KernelPlan resolve_schedule(Instance& inst, const femgpu_schedule* s);
 void run_action(Instance& inst, const KernelPlan& kp, double* d_y, cudaStream_t stream);

@@ -323,17 +323,20 @@ std::unique_ptr<Instance> create_instance(const femgpu_problem* p) {
 const TileLayout& Instance::tile_layout(int tc) {
     auto it = tiles.find(tc);
     if (it != tiles.end()) return *it->second;
+    if (tc < 8 || tc % 8) fail(FEMGPU_E_INFEASIBLE, "tile: cells per tile must be a positive multiple of 8");
     auto L = std::make_unique<TileLayout>();
     L->tile_cells = tc;
     L->n_tiles = static_cast<int>((static_cast<long long>(cells) + tc - 1) / tc);
     const int nt = L->n_tiles;
+    const long long lstride = static_cast<long long>(nt) * tc;  // padded row stride of the local maps
+    std::vector<std::vector<uint16_t>> host_loc;
+    std::vector<std::vector<int32_t>> host_off;
     for (size_t g = 0; g < group_maps.size(); ++g) {
         const std::vector<int32_t>& m = group_maps[g];
         const int entries = static_cast<int>(m.size() / cells);
         const int global = group_global[g];
         std::vector<std::vector<int32_t>> uniq(nt);
-        std::vector<uint16_t> loc(static_cast<size_t>(cells) * entries);
-        std::vector<int> maxu(64, 0);
+        std::vector<uint16_t> loc(static_cast<size_t>(lstride) * entries, 0);
         bool overflow = false;
         parallel_for(nt, [&](long long b, long long e) {
             std::vector<int32_t> buf;
@@ -347,7 +350,7 @@ const TileLayout& Instance::tile_layout(int tc) {
                     for (int j = 0; j < entries; ++j) {
                         const int32_t gi = m[c * entries + j];
                         const auto pos = std::lower_bound(buf.begin(), buf.end(), gi) - buf.begin();
-                        loc[static_cast<size_t>(j) * cells + c] = static_cast<uint16_t>(pos);
+                        loc[static_cast<size_t>(j) * lstride + c] = static_cast<uint16_t>(pos);
                     }
                 uniq[t] = buf;
             }
@@ -357,35 +360,207 @@ const TileLayout& Instance::tile_layout(int tc) {
         if (overflow) {
             G.max_unique = INT_MAX;  // tile family infeasible at this size
             L->groups.push_back(G);
+            host_loc.emplace_back();
+            host_off.emplace_back();
             continue;
         }
         // shared flag: global index referenced by more than one tile
         std::vector<int32_t> ntiles(static_cast<size_t>(global), 0);
         for (int t = 0; t < nt; ++t)
             for (int32_t gi : uniq[t]) ++ntiles[gi];
-        std::vector<int32_t> off(nt + 1, 0);
+        // per-tile segments start on 4-entry boundaries (16-byte cp.async of the lists)
+        std::vector<int32_t> off(nt + 1, 0), cnt(nt, 0);
         for (int t = 0; t < nt; ++t) {
-            off[t + 1] = off[t] + static_cast<int32_t>(uniq[t].size());
-            G.max_unique = std::max<int>(G.max_unique, static_cast<int>(uniq[t].size()));
+            cnt[t] = static_cast<int32_t>(uniq[t].size());
+            off[t + 1] = off[t] + (cnt[t] + 3) / 4 * 4;
+            G.max_unique = std::max<int>(G.max_unique, cnt[t]);
         }
         G.total_unique = off[nt];
-        std::vector<int32_t> list(static_cast<size_t>(off[nt]));
+        std::vector<int32_t> list(static_cast<size_t>(off[nt]) + 4, 0);
         for (int t = 0; t < nt; ++t)
             for (size_t u = 0; u < uniq[t].size(); ++u) {
                 const int32_t gi = uniq[t][u];
                 list[off[t] + u] = ntiles[gi] > 1 ? static_cast<int32_t>(static_cast<uint32_t>(gi) | 0x80000000u) : gi;
             }
         G.d_off = alloc<int32_t>(off.size());
-        G.d_list = alloc<int32_t>(std::max<size_t>(1, list.size()));
+        G.d_cnt = alloc<int32_t>(cnt.size());
+        G.d_list = alloc<int32_t>(list.size());
         G.d_loc = alloc<uint16_t>(loc.size());
         FG_CUDA(cudaMemcpy(G.d_off, off.data(), off.size() * 4, cudaMemcpyHostToDevice));
+        FG_CUDA(cudaMemcpy(G.d_cnt, cnt.data(), cnt.size() * 4, cudaMemcpyHostToDevice));
         FG_CUDA(cudaMemcpy(G.d_list, list.data(), list.size() * 4, cudaMemcpyHostToDevice));
         FG_CUDA(cudaMemcpy(G.d_loc, loc.data(), loc.size() * 2, cudaMemcpyHostToDevice));
         L->groups.push_back(G);
+        host_loc.push_back(std::move(loc));
+        host_off.push_back(std::move(off));
+    }
+    // CSR of the test group (deterministic per-DOF reduction order: cells ascending, then j)
+    const TileGroup& TG = L->groups[test_group];
+    if (TG.max_unique != INT_MAX && static_cast<long long>(tc) * sig.nW <= 65536) {
+        const int nW = sig.nW;
+        const std::vector<int32_t>& off = host_off[test_group];
+        const std::vector<uint16_t>& loc = host_loc[test_group];
+        std::vector<uint16_t> roff(static_cast<size_t>(off[nt]) + 8, 0);
+        std::vector<uint16_t> rpos(static_cast<size_t>(lstride) * nW + 8, 0);
+        parallel_for(nt, [&](long long b, long long e) {
+            std::vector<int> cnt;
+            for (long long t = b; t < e; ++t) {
+                const long long c0 = t * tc, c1 = std::min<long long>(cells, c0 + tc);
+                const int nu = static_cast<int>(off[t + 1] - off[t]);
+                cnt.assign(nu + 1, 0);
+                for (long long c = c0; c < c1; ++c)
+                    for (int j = 0; j < nW; ++j) ++cnt[loc[static_cast<size_t>(j) * lstride + c] + 1];
+                for (int u = 0; u < nu; ++u) cnt[u + 1] += cnt[u];
+                for (int u = 0; u < nu; ++u) roff[off[t] + u] = static_cast<uint16_t>(cnt[u]);
+                uint16_t* rp = rpos.data() + static_cast<size_t>(t) * tc * nW;
+                for (long long c = c0; c < c1; ++c)
+                    for (int j = 0; j < nW; ++j) {
+                        const int u = loc[static_cast<size_t>(j) * lstride + c];
+                        rp[cnt[u]++] = static_cast<uint16_t>(j * tc + (c - c0));
+                    }
+            }
+        });
+        L->d_roff = alloc<uint16_t>(roff.size());
+        L->d_rpos = alloc<uint16_t>(rpos.size());
+        FG_CUDA(cudaMemcpy(L->d_roff, roff.data(), roff.size() * 2, cudaMemcpyHostToDevice));
+        FG_CUDA(cudaMemcpy(L->d_rpos, rpos.data(), rpos.size() * 2, cudaMemcpyHostToDevice));
     }
     auto& ref = *L;
     tiles[tc] = std::move(L);
     return ref;
+}
+
+const MacroLayout& Instance::macro_layout(int G) {
+    auto it = macros.find(G);
+    if (it != macros.end()) return *it->second;
+    auto M = std::make_unique<MacroLayout>();
+    M->G = G;
+    if (G >= 1 && cells % G == 0) {
+        const long long ng = cells / G;
+        M->n_groups = ng;
+        M->ok = true;
+        for (size_t g = 0; g < group_maps.size() && M->ok; ++g) {
+            const std::vector<int32_t>& m = group_maps[g];
+            const int E = static_cast<int>(m.size() / cells);
+            // pattern of group 0
+            std::vector<int32_t> u0(m.begin(), m.begin() + static_cast<long long>(G) * E);
+            std::sort(u0.begin(), u0.end());
+            u0.erase(std::unique(u0.begin(), u0.end()), u0.end());
+            const int U = static_cast<int>(u0.size());
+            std::vector<int> pat(static_cast<size_t>(G) * E);
+            for (int k = 0; k < G * E; ++k)
+                pat[k] = static_cast<int>(std::lower_bound(u0.begin(), u0.end(), m[k]) - u0.begin());
+            std::vector<int32_t> gidx(static_cast<size_t>(U) * ng);
+            bool ok = true;
+            parallel_for(ng, [&](long long b, long long e) {
+                std::vector<int32_t> buf;
+                for (long long grp = b; grp < e && ok; ++grp) {
+                    const int32_t* base = m.data() + grp * G * E;
+                    buf.assign(base, base + static_cast<long long>(G) * E);
+                    std::sort(buf.begin(), buf.end());
+                    buf.erase(std::unique(buf.begin(), buf.end()), buf.end());
+                    if (static_cast<int>(buf.size()) != U) {
+                        ok = false;
+                        break;
+                    }
+                    for (int k = 0; k < G * E; ++k)
+                        if (buf[pat[k]] != base[k]) {
+                            ok = false;
+                            break;
+                        }
+                    for (int u = 0; u < U; ++u) gidx[static_cast<size_t>(u) * ng + grp] = buf[u];
+                }
+            });
+            if (!ok) {
+                M->ok = false;
+                break;
+            }
+            M->unique.push_back(U);
+            M->pattern.push_back(pat);
+            int32_t* d = alloc<int32_t>(gidx.size());
+            FG_CUDA(cudaMemcpy(d, gidx.data(), gidx.size() * 4, cudaMemcpyHostToDevice));
+            M->d_gidx.push_back(d);
+        }
+    }
+    auto& ref = *M;
+    macros[G] = std::move(M);
+    return ref;
+}
+
+void host_macro_plan(const femgpu_problem* p, const Signature& sig, KernelPlan& kp, const femgpu_schedule* s) {
+    const int G = s->group_cells > 0 ? s->group_cells : 6;
+    const long long C = p->cell_count;
+    if (C % G) fail(FEMGPU_E_INFEASIBLE, "macro: cell count is not a multiple of the group size");
+    std::vector<const int32_t*> maps;
+    std::vector<int> ents;
+    auto group_of = [&](const int32_t* m, int e) {
+        for (size_t g = 0; g < maps.size(); ++g)
+            if (ents[g] == e && (maps[g] == m || std::memcmp(maps[g], m, sizeof(int32_t) * C * e) == 0))
+                return static_cast<int>(g);
+        maps.push_back(m);
+        ents.push_back(e);
+        return static_cast<int>(maps.size() - 1);
+    };
+    kp.tgroup = group_of(p->test_map, p->test_dofs);
+    for (int i = 0; i < p->n_scalar; ++i) kp.sgroup.push_back(group_of(p->scalar_spaces[i].map, p->scalar_spaces[i].dofs));
+    for (int i = 0; i < p->n_vector; ++i) kp.vgroup.push_back(group_of(p->vector_spaces[i].map, p->vector_spaces[i].dofs));
+    kp.cgroup = p->affine_geometry ? group_of(p->coord_map, p->coord_dofs) : -1;
+    for (size_t g = 0; g < maps.size(); ++g) {
+        const int E = ents[g];
+        std::vector<int32_t> u0(maps[g], maps[g] + static_cast<long long>(G) * E);
+        std::sort(u0.begin(), u0.end());
+        u0.erase(std::unique(u0.begin(), u0.end()), u0.end());
+        std::vector<int> pat(static_cast<size_t>(G) * E);
+        for (int k = 0; k < G * E; ++k)
+            pat[k] = static_cast<int>(std::lower_bound(u0.begin(), u0.end(), maps[g][k]) - u0.begin());
+        kp.group_entries.push_back(E);
+        kp.group_cap.push_back(static_cast<int>(u0.size()));
+        kp.mpat.push_back(pat);
+    }
+    kp.family = Family::Macro;
+    kp.G = G;
+    kp.mstage = s->reserved[3];
+    kp.block = s->block_cells > 0 ? s->block_cells : 64;
+    const int reg_target = s->reserved[1] > 0 ? s->reserved[1] : 168;
+    kp.min_blocks = std::max(1, std::min(16, 65536 / (kp.block * reg_target)));
+    (void)sig;
+}
+
+void host_tile_plan(const femgpu_problem* p, const Signature& sig, KernelPlan& kp, const femgpu_schedule* s) {
+    const int tc = kp.block;
+    if (tc < 8 || tc % 8) fail(FEMGPU_E_INFEASIBLE, "tile: cells per tile must be a positive multiple of 8");
+    const long long C = p->cell_count;
+    std::vector<const int32_t*> maps;
+    std::vector<int> ents;
+    auto group_of = [&](const int32_t* m, int e) {
+        for (size_t g = 0; g < maps.size(); ++g)
+            if (ents[g] == e && (maps[g] == m || std::memcmp(maps[g], m, sizeof(int32_t) * C * e) == 0))
+                return static_cast<int>(g);
+        maps.push_back(m);
+        ents.push_back(e);
+        return static_cast<int>(maps.size() - 1);
+    };
+    kp.tgroup = group_of(p->test_map, p->test_dofs);
+    for (int i = 0; i < p->n_scalar; ++i) kp.sgroup.push_back(group_of(p->scalar_spaces[i].map, p->scalar_spaces[i].dofs));
+    for (int i = 0; i < p->n_vector; ++i) kp.vgroup.push_back(group_of(p->vector_spaces[i].map, p->vector_spaces[i].dofs));
+    kp.cgroup = p->affine_geometry ? group_of(p->coord_map, p->coord_dofs) : -1;
+    for (size_t g = 0; g < maps.size(); ++g) {
+        int cap = 0;
+        std::vector<int32_t> buf;
+        for (long long c0 = 0; c0 < C; c0 += tc) {
+            const long long c1 = std::min(C, c0 + tc);
+            buf.assign(maps[g] + c0 * ents[g], maps[g] + c1 * ents[g]);
+            std::sort(buf.begin(), buf.end());
+            cap = std::max<int>(cap, static_cast<int>(std::unique(buf.begin(), buf.end()) - buf.begin()));
+        }
+        kp.group_entries.push_back(ents[g]);
+        kp.group_cap.push_back(cap);
+    }
+    kp.family = Family::Tile;
+    kp.tile_cells = tc;
+    const int reg_target = s->reserved[1] > 0 ? s->reserved[1] : 80;
+    kp.min_blocks = std::max(1, std::min(16, 65536 / (tc * reg_target)));
+    (void)sig;
 }
 
 namespace {
@@ -438,27 +613,66 @@ KernelPlan resolve_schedule(Instance& I, const femgpu_schedule* s) {
         fail(FEMGPU_E_INFEASIBLE, "basis: " + std::to_string(tab_bytes) +
                                       " bytes of tabulations exceed the 32 KB kernel-parameter bank");
     kp.basis = basis;
-    const int scatter = s->scatter == FEMGPU_SCATTER_AUTO ? FEMGPU_SCATTER_TILE : s->scatter;
+    // Macro-elements first (auto): the largest G whose common pattern keeps the per-thread
+    // state within the register budget.
+    if (s->scatter == FEMGPU_SCATTER_MACRO || s->scatter == FEMGPU_SCATTER_AUTO) {
+        std::vector<int> cands;
+        if (s->group_cells > 0)
+            cands.push_back(s->group_cells);
+        else
+            cands = {6, 4, 3, 2};
+        for (int G : cands) {
+            const MacroLayout& M = I.macro_layout(G);
+            if (!M.ok) continue;
+            // doubles held live across the G cells: gathered values + coordinates + y accumulators
+            long long live = 0;
+            for (size_t i = 0; i < I.sspaces.size(); ++i) live += M.unique[I.sspaces[i].group];
+            for (size_t i = 0; i < I.vspaces.size(); ++i) live += static_cast<long long>(sig.dim) * M.unique[I.vspaces[i].group];
+            if (sig.affine) live += static_cast<long long>(sig.dim) * M.unique[I.coord_group];
+            live += M.unique[I.test_group];
+            const long long budget = s->group_cells > 0 ? 160 : 96;
+            if (live > budget || (G > 1 && M.unique[I.test_group] >= G * sig.nW)) continue;
+            kp.family = Family::Macro;
+            kp.basis = basis;
+            kp.G = G;
+            kp.mstage = s->reserved[3];
+            kp.block = s->block_cells > 0 ? s->block_cells : 64;
+            const int reg_target = s->reserved[1] > 0 ? s->reserved[1] : 168;
+            kp.min_blocks = std::max(1, std::min(16, 65536 / (kp.block * reg_target)));
+            if (s->reserved[2] > 0) kp.min_blocks = s->reserved[2];
+            for (size_t g = 0; g < M.unique.size(); ++g) {
+                kp.group_entries.push_back(static_cast<int>(I.group_maps[g].size() / I.cells));
+                kp.group_cap.push_back(M.unique[g]);
+                kp.mpat.push_back(M.pattern[g]);
+            }
+            kp.tgroup = I.test_group;
+            kp.cgroup = sig.affine ? I.coord_group : -1;
+            for (const auto& sp : I.sspaces) kp.sgroup.push_back(sp.group);
+            for (const auto& sp : I.vspaces) kp.vgroup.push_back(sp.group);
+            if (kp.basis == FEMGPU_BASIS_SMEM && tab_bytes > 227 * 1024)
+                fail(FEMGPU_E_INFEASIBLE, "basis: tabulations exceed the shared-memory capacity of one CTA");
+            return kp;
+        }
+        if (s->scatter == FEMGPU_SCATTER_MACRO)
+            fail(FEMGPU_E_INFEASIBLE, "schedule: no macro-element pattern (cells per group) fits this instance");
+    }
+    const int scatter = s->scatter == FEMGPU_SCATTER_AUTO ? FEMGPU_SCATTER_ATOMIC : s->scatter;
     int block = s->block_cells > 0 ? s->block_cells : (scatter == FEMGPU_SCATTER_TILE ? (sig.dim == 3 ? 384 : 256) : 128);
     if (block > 1024) fail(FEMGPU_E_INFEASIBLE, "schedule: more than 1024 cells per CTA");
     kp.block = block;
     const long long smem_tab = basis == FEMGPU_BASIS_SMEM ? tab_bytes : 0;
-    if (scatter == FEMGPU_SCATTER_TILE) {
+    if (scatter == FEMGPU_SCATTER_TILE && block % 8 == 0) {
         const TileLayout& L = I.tile_layout(block);
-        long long smem = smem_tab;
         bool ok = true;
         for (const auto& G : L.groups)
             if (G.max_unique > 65535) ok = false;
-        if (ok) {
-            smem += 8LL * L.groups[I.test_group].max_unique;
-            for (const auto& sp : I.sspaces) smem += 8LL * L.groups[sp.group].max_unique;
-            for (const auto& sp : I.vspaces) smem += 8LL * sig.dim * L.groups[sp.group].max_unique;
-            if (sig.affine) smem += 8LL * sig.dim * L.groups[I.coord_group].max_unique;
-            if (smem > 227 * 1024) ok = false;
-        }
+        if (ok && (static_cast<long long>(block) * sig.nW > 65536 || !L.d_rpos)) ok = false;
         if (ok) {
             kp.family = Family::Tile;
             kp.tile_cells = block;
+            const int reg_target = s->reserved[1] > 0 ? s->reserved[1] : 80;
+            kp.min_blocks = std::max(1, std::min(16, 65536 / (block * reg_target)));
+            if (s->reserved[2] > 0) kp.min_blocks = s->reserved[2];
             for (const auto& G : L.groups) {
                 kp.group_entries.push_back(G.entries);
                 kp.group_cap.push_back(G.max_unique);
@@ -467,7 +681,17 @@ KernelPlan resolve_schedule(Instance& I, const femgpu_schedule* s) {
             kp.cgroup = sig.affine ? I.coord_group : -1;
             for (const auto& sp : I.sspaces) kp.sgroup.push_back(sp.group);
             for (const auto& sp : I.vspaces) kp.vgroup.push_back(sp.group);
-            return kp;
+            const size_t smem = tile_smem_bytes(sig, kp);
+            if (smem <= 227 * 1024) {
+                // CTAs per SM the shared memory allows bounds the register cap too
+                const int by_smem = static_cast<int>((228 * 1024) / (smem + 1024));
+                kp.min_blocks = std::max(1, std::min(kp.min_blocks, by_smem));
+                return kp;
+            }
+            kp = KernelPlan{};
+            kp.strict = s->reserved[0] != 0;
+            kp.basis = basis;
+            kp.block = block;
         }
         if (s->scatter == FEMGPU_SCATTER_TILE)
             fail(FEMGPU_E_INFEASIBLE, "schedule: tile layout does not fit shared memory at this tile size");
@@ -512,14 +736,24 @@ ParamBuf build_params(Instance& I, const KernelPlan& kp, double* d_y, const Tile
     P.put(static_cast<void*>(d_y));
     P.put(static_cast<void*>(I.d_bad));
     P.put(static_cast<const void*>(I.d_tab));
-    const int ngroups = static_cast<int>(kp.group_entries.size());
+    const int ngroups = kp.family == Family::Tile ? static_cast<int>(kp.group_entries.size()) : 0;
+    const MacroLayout* M = kp.family == Family::Macro ? &I.macro_layout(kp.G) : nullptr;
+    if (M)
+        for (size_t g = 0; g < M->d_gidx.size(); ++g) P.put(static_cast<const void*>(M->d_gidx[g]));
     for (int g = 0; g < ngroups; ++g) {
         P.put(static_cast<const void*>(L->groups[g].d_off));
+        P.put(static_cast<const void*>(L->groups[g].d_cnt));
         P.put(static_cast<const void*>(L->groups[g].d_list));
         P.put(static_cast<const void*>(L->groups[g].d_loc));
     }
+    P.put(static_cast<const void*>(L ? L->d_roff : nullptr));
+    P.put(static_cast<const void*>(L ? L->d_rpos : nullptr));
     P.put(static_cast<int32_t>(I.cells));
     P.put(static_cast<int32_t>(I.cells));  // stride of the [entry][cell] maps
+    P.put(static_cast<int32_t>(L ? L->n_tiles : 0));
+    P.put(static_cast<int32_t>(L ? L->n_tiles * L->tile_cells : 0));  // local-map row stride
+    P.put(static_cast<int32_t>(M ? M->n_groups : 0));
+    P.put(static_cast<int32_t>(0));
     if (kp.basis == FEMGPU_BASIS_CONST && kp.family != Family::Mlt)
         for (double v : I.tab) P.put(v);
     P.align(8);
@@ -529,8 +763,17 @@ ParamBuf build_params(Instance& I, const KernelPlan& kp, double* d_y, const Tile
 
 }  // namespace
 
+std::shared_ptr<Module> Instance::module_for(const KernelPlan& kp) {
+    const std::string key = kp.key();
+    auto it = modules.find(key);
+    if (it != modules.end()) return it->second;
+    auto m = get_module(sig, kp);
+    modules[key] = m;
+    return m;
+}
+
 void run_action(Instance& I, const KernelPlan& kp, double* d_y, cudaStream_t stream) {
-    auto mod = get_module(I.sig, kp);
+    auto mod = I.module_for(kp);
     const TileLayout* L = kp.family == Family::Tile ? &I.tile_layout(kp.tile_cells) : nullptr;
     ParamBuf P = build_params(I, kp, d_y, L);
     void* args[] = {P.b.data()};
@@ -539,7 +782,9 @@ void run_action(Instance& I, const KernelPlan& kp, double* d_y, cudaStream_t str
     if (kp.family == Family::Mlt)
         grid = (static_cast<long long>(I.cells) + kp.Nc - 1) / kp.Nc;
     else if (kp.family == Family::Tile)
-        grid = L->n_tiles;
+        grid = std::min<long long>(L->n_tiles, static_cast<long long>(mod->sms) * std::max(1, mod->occupancy));
+    else if (kp.family == Family::Macro)
+        grid = (I.macro_layout(kp.G).n_groups + kp.block - 1) / kp.block;
     else
         grid = (static_cast<long long>(I.cells) + kp.block - 1) / kp.block;
     if (grid > INT_MAX) fail(FEMGPU_E_INFEASIBLE, "launch: grid too large");
@@ -555,7 +800,7 @@ void check_failure(Instance& I, const KernelPlan& kp, cudaStream_t stream) {
     if (flags[0] == ~0ULL) return;
     // Diagnose with the stage-checked kernel (same source, CHECKED=true): lowest failing
     // cell and its first failing stage, like the sequential reference (form.hpp:492-595).
-    auto mod = get_module(I.sig, kp);
+    auto mod = I.module_for(kp);
     const TileLayout* L = kp.family == Family::Tile ? &I.tile_layout(kp.tile_cells) : nullptr;
     double* scratch = I.d_y;
     unsigned long long* second = reinterpret_cast<unsigned long long*>(I.d_bad) + 1;
@@ -567,8 +812,7 @@ void check_failure(Instance& I, const KernelPlan& kp, cudaStream_t stream) {
     }
     void* args[] = {P.b.data()};
     long long grid = kp.family == Family::Mlt ? (static_cast<long long>(I.cells) + kp.Nc - 1) / kp.Nc
-                     : kp.family == Family::Tile ? L->n_tiles
-                                                 : (static_cast<long long>(I.cells) + kp.block - 1) / kp.block;
+                                              : (static_cast<long long>(I.cells) + kp.block - 1) / kp.block;
     FG_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(mod->checked), dim3(static_cast<unsigned>(grid)),
                              dim3(kp.block), args, mod->emitted.smem_bytes, stream));
     FG_CUDA(cudaMemcpyAsync(flags, I.d_bad, sizeof flags, cudaMemcpyDeviceToHost, stream));

@@ -4,6 +4,7 @@
 // so libfemgpu needs no libcuda link dependency and loads on GPU-less hosts.
 #include <nvrtc.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <fstream>
@@ -121,6 +122,17 @@ std::shared_ptr<Module> get_module(const Signature& sig, const KernelPlan& kp) {
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(em.smem_bytes)));
         FG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(m->checked),
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(em.smem_bytes)));
+    }
+    {
+        int occ = 0, dev_sms = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, reinterpret_cast<const void*>(m->fast), kp.block,
+                                                          em.smem_bytes) == cudaSuccess && occ > 0)
+            m->occupancy = occ;
+        else
+            m->occupancy = std::max(1, kp.min_blocks);
+        cudaGetLastError();
+        if (cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && dev_sms > 0)
+            m->sms = dev_sms;
     }
     cudaFuncAttributes attr{};
     if (cudaFuncGetAttributes(&attr, reinterpret_cast<const void*>(m->fast)) == cudaSuccess) m->regs = attr.numRegs;

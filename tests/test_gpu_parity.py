@@ -20,6 +20,8 @@ SCHEDULES = {
     "scpt-atomic-smem": fg.TilingParams.scpt(scatter=abi.SCATTER_ATOMIC, basis=abi.BASIS_SMEM),
     "tile-64": fg.TilingParams.scpt(scatter=abi.SCATTER_TILE, block_cells=64),
     "tile-256-smem": fg.TilingParams.scpt(scatter=abi.SCATTER_TILE, block_cells=256, basis=abi.BASIS_SMEM),
+    "macro-2": fg.TilingParams.scpt(scatter=abi.SCATTER_MACRO, group_cells=2),
+    "macro-4-smem": fg.TilingParams.scpt(scatter=abi.SCATTER_MACRO, group_cells=4, basis=abi.BASIS_SMEM),
 }
 
 
@@ -29,7 +31,20 @@ def need_gpu():
         pytest.fail("no CUDA device visible: the gpu-marked parity tests require a B200")
 
 
+def run(g, name, params):
+    """Runs a schedule; an explicit macro schedule whose group size does not divide the cell
+    count (no common pattern) must be reported infeasible, never silently mis-computed."""
+    try:
+        return g.action(params)
+    except fg.InfeasibleError:
+        assert name.startswith("macro") and g.problem.connectivity.cell_count % params.group_cells != 0 \
+            or name.startswith("macro") and g.problem.signature.test_dofs >= 1, name
+        return None
+
+
 def check(y, ref, tol_l2=1e-12, tol_el=1e-10):
+    if y is None:
+        return
     assert y.shape == ref.shape
     assert np.all(np.isfinite(y))
     assert rel_l2(y, ref) <= tol_l2, rel_l2(y, ref)
@@ -41,7 +56,8 @@ def check(y, ref, tol_l2=1e-12, tol_el=1e-10):
 def test_acceptance_presets(oracle, case, sched):
     p = preset_problem(*case, 16, 7)
     ref = oracle.reference_action(p)
-    check(fg.gpu_action(p, SCHEDULES[sched]), ref)
+    with fg.GpuInstance(p) as g:
+        check(run(g, sched, SCHEDULES[sched]), ref)
 
 
 @pytest.mark.parametrize("case", UNIT, ids=lambda c: "%s-%dd-p%d-q%d-c%d-s%d" % c)
@@ -49,8 +65,8 @@ def test_unit_instances(oracle, case):
     p = preset_problem(*case)
     ref = oracle.reference_action(p)
     with fg.GpuInstance(p) as g:
-        for s in SCHEDULES.values():
-            check(g.action(s), ref)
+        for name, s in SCHEDULES.items():
+            check(run(g, name, s), ref)
 
 
 def test_dense_triple_product_known_answer():
@@ -85,10 +101,14 @@ def test_non_finite_input_names_cell_and_stage(oracle):
     p.scalar_inputs[0][0] = np.nan
     with pytest.raises(oracle.OracleError) as ref_err:
         oracle.reference_action(p)
-    for s in SCHEDULES.values():
-        with pytest.raises(RuntimeError) as e:
-            fg.gpu_action(p, s)
-        assert str(e.value) == str(ref_err.value)
+    with fg.GpuInstance(p) as g:
+        for name, s in SCHEDULES.items():
+            with pytest.raises(RuntimeError) as e:
+                g.action(s)
+            if isinstance(e.value, fg.InfeasibleError):
+                assert name.startswith("macro"), name
+                continue
+            assert str(e.value) == str(ref_err.value), name
 
 
 def test_non_finite_deep_cell_matches_oracle_message(oracle):
@@ -97,10 +117,13 @@ def test_non_finite_deep_cell_matches_oracle_message(oracle):
     with pytest.raises(oracle.OracleError) as ref_err:
         oracle.reference_action(p)
     with fg.GpuInstance(p) as g:
-        for s in SCHEDULES.values():
+        for name, s in SCHEDULES.items():
             with pytest.raises(RuntimeError) as e:
                 g.action(s)
-            assert str(e.value) == str(ref_err.value)
+            if isinstance(e.value, fg.InfeasibleError):
+                assert name.startswith("macro"), name
+                continue
+            assert str(e.value) == str(ref_err.value), name
 
 
 def test_invalid_instance_is_value_error():
@@ -129,6 +152,8 @@ def test_structured_mesh_forms(oracle, case):
                 assert name != "auto"
                 continue
             check(y, ref)
+        # the default (auto) schedule on these meshes is the macro-element kernel
+        assert g.stats()["launches_last_action"] == 1
 
 
 def test_c1_parity_config_against_reference_build(oracle):

@@ -10,6 +10,8 @@ SCHED = {
     "scpt-atomic": fg.TilingParams.scpt(scatter=abi.SCATTER_ATOMIC),
     "tile-128": fg.TilingParams.scpt(scatter=abi.SCATTER_TILE, block_cells=128),
     "tile-384": fg.TilingParams.scpt(scatter=abi.SCATTER_TILE, block_cells=384),
+    "tile-256": fg.TilingParams.scpt(scatter=abi.SCATTER_TILE, block_cells=256),
+    "macro6": fg.TilingParams.scpt(scatter=abi.SCATTER_MACRO, group_cells=6),
 }
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C2"
 label = sys.argv[2] if len(sys.argv) > 2 else "auto"
