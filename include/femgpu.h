@@ -199,6 +199,19 @@ femgpu_status femgpu_action_device(femgpu_instance* inst, const femgpu_schedule*
  * the instance stream; *seconds = arithmetic mean per action. */
 femgpu_status femgpu_time_action(femgpu_instance* inst, const femgpu_schedule* s, int32_t warmup,
                                  int32_t min_reps, double min_seconds, double* seconds);
+/* Exactly `steps` back-to-back actions [zero y + action] on the instance stream, bracketed by
+ * a device synchronize on both sides and timed with CUDA events: *seconds = total elapsed. */
+femgpu_status femgpu_time_steps(femgpu_instance* inst, const femgpu_schedule* s, int32_t steps,
+                                double* seconds);
+/* Split timing of the same protocol: mean seconds per step [zero y + action], per
+ * action kernel alone and per y-zeroing, each bracketed by CUDA events on the
+ * instance stream (the roofline's per-kernel duration). */
+femgpu_status femgpu_profile_action(femgpu_instance* inst, const femgpu_schedule* s, int32_t warmup,
+                                    int32_t reps, double* step_seconds, double* kernel_seconds,
+                                    double* zero_seconds);
+/* The FP64 roofline denominator, measured live: DFMA peak of the current device
+ * (TFLOP/s) and its nominal SM clock (GHz).  Ahead-of-time sm_100a kernel. */
+femgpu_status femgpu_fp64_peak(double* tflops, double* sm_clock_ghz);
 /* Executor seam (search.hpp:257-283): run, verify finiteness, report output and
  * measured seconds (mean of the timing protocol above). */
 femgpu_status femgpu_execute(femgpu_instance* inst, const femgpu_schedule* s, double* y_host,
@@ -210,6 +223,9 @@ femgpu_status femgpu_stats(const femgpu_instance* inst, int64_t* launches_last_a
                            int64_t* device_bytes, int64_t* tiles, int64_t* max_tile_dofs);
 /* Device pointers (for zero-copy callers): output buffer of the instance. */
 femgpu_status femgpu_device_output(femgpu_instance* inst, double** y_dev);
+/* Device pointer of trial input vector `space` (scalar spaces first, then vector spaces),
+ * for zero-copy halo exchanges (multi-GPU): length global_count (x dim for vector spaces). */
+femgpu_status femgpu_device_input(femgpu_instance* inst, int32_t space, double** x_dev);
 /* The CUDA stream (cudaStream_t) the instance launches on. */
 femgpu_status femgpu_stream(femgpu_instance* inst, void** stream);
 

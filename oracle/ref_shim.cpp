@@ -15,6 +15,7 @@
 // Build recipe: oracle/Makefile (outputs only into oracle/_ref/).
 #include <femsched/form.hpp>
 
+#include <algorithm>
 #include <chrono>
 #include <cstring>
 #include <memory>
@@ -117,6 +118,46 @@ ProblemInstance from_desc(const femgpu_problem* d, int cell_begin, int cell_end)
     }
     for (int o = 0; o < d->n_map_outputs; ++o) m.add_output(d->map_outputs[o]);
     p.output_size = d->output_size;
+    return p;
+}
+
+// Compact restriction of cells [b, e): every map is renumbered to the indices the range
+// touches (ascending), inputs/coords are gathered accordingly, and test_global (the local->
+// global test numbering) is returned so partial outputs can be summed into the global y.
+ProblemInstance compact_from_desc(const femgpu_problem* d, int b, int e, std::vector<int>& test_global) {
+    ProblemInstance p = from_desc(d, b, e);  // global numbering, restricted maps
+    auto compact = [](IndexMap& m, std::vector<int>& uniq) {
+        uniq.assign(m.indices.begin(), m.indices.end());
+        std::sort(uniq.begin(), uniq.end());
+        uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+        for (int& v : m.indices) v = static_cast<int>(std::lower_bound(uniq.begin(), uniq.end(), v) - uniq.begin());
+        m.global_count = static_cast<int>(uniq.size());
+    };
+    std::vector<int> u;
+    for (std::size_t i = 0; i < p.connectivity.scalar_maps.size(); ++i) {
+        compact(p.connectivity.scalar_maps[i], u);
+        std::vector<double> x(u.size());
+        for (std::size_t k = 0; k < u.size(); ++k) x[k] = p.scalar_inputs[i][u[k]];
+        p.scalar_inputs[i] = std::move(x);
+    }
+    const int dim = p.signature.dim;
+    for (std::size_t i = 0; i < p.connectivity.vector_maps.size(); ++i) {
+        compact(p.connectivity.vector_maps[i], u);
+        std::vector<double> x(u.size() * dim);
+        for (std::size_t k = 0; k < u.size(); ++k)
+            for (int c = 0; c < dim; ++c) x[k * dim + c] = p.vector_inputs[i][static_cast<std::size_t>(u[k]) * dim + c];
+        p.vector_inputs[i] = std::move(x);
+    }
+    if (p.signature.affine_geometry) {
+        compact(p.connectivity.coord_map, u);
+        std::vector<double> X(u.size() * dim);
+        for (std::size_t k = 0; k < u.size(); ++k)
+            for (int c = 0; c < dim; ++c) X[k * dim + c] = p.connectivity.coords[static_cast<std::size_t>(u[k]) * dim + c];
+        p.connectivity.coords = std::move(X);
+        p.connectivity.coord_global_count = static_cast<int>(u.size());
+    }
+    compact(p.connectivity.test_map, test_global);
+    p.output_size = p.connectivity.test_map.global_count;
     return p;
 }
 
@@ -271,22 +312,30 @@ long long ref_usable_flops(const char* op, int dim, int degree, int quad_points)
     }
 }
 
-// CPU baseline harness: T threads, each running the unmodified reference_action
-// on a contiguous cell range; outputs summed in rank order into out.  Timing
-// excludes sub-instance construction.  Returns mean seconds per action, < 0 on error.
+// CPU baseline harness: T threads, each running the unmodified reference_action on a
+// compact sub-instance of a contiguous cell range (domain decomposition); the partial
+// outputs are summed into out in rank order.  Timing excludes sub-instance construction
+// and includes the summation.  Returns mean seconds per action, < 0 on error.
 double ref_time_threads(const femgpu_problem* d, int cell_begin, int cell_end, int threads, int reps,
                         double* out, char* err, int len) {
     try {
         if (threads < 1) threads = 1;
         const int cells = cell_end - cell_begin;
         if (threads > cells) threads = cells;
-        std::vector<ProblemInstance> parts;
-        for (int t = 0; t < threads; ++t) {
-            const int b = cell_begin + static_cast<int>(static_cast<long long>(cells) * t / threads);
-            const int e = cell_begin + static_cast<int>(static_cast<long long>(cells) * (t + 1) / threads);
-            parts.push_back(from_desc(d, b, e));
+        std::vector<ProblemInstance> parts(threads);
+        std::vector<std::vector<int>> tg(threads);
+        {
+            std::vector<std::thread> pool;
+            for (int t = 0; t < threads; ++t)
+                pool.emplace_back([&, t] {
+                    const int b = cell_begin + static_cast<int>(static_cast<long long>(cells) * t / threads);
+                    const int e = cell_begin + static_cast<int>(static_cast<long long>(cells) * (t + 1) / threads);
+                    parts[t] = compact_from_desc(d, b, e, tg[t]);
+                });
+            for (auto& th : pool) th.join();
         }
         std::vector<std::vector<double>> ys(threads);
+        std::vector<double> y(static_cast<std::size_t>(d->output_size), 0.0);
         double total = 0.0;
         for (int r = 0; r < reps; ++r) {
             const auto t0 = std::chrono::steady_clock::now();
@@ -294,13 +343,13 @@ double ref_time_threads(const femgpu_problem* d, int cell_begin, int cell_end, i
             for (int t = 0; t < threads; ++t)
                 pool.emplace_back([&, t] { ys[t] = reference_action(parts[t]); });
             for (auto& th : pool) th.join();
-            std::vector<double> y(static_cast<std::size_t>(d->output_size), 0.0);
+            std::fill(y.begin(), y.end(), 0.0);
             for (int t = 0; t < threads; ++t)
-                for (std::size_t i = 0; i < y.size(); ++i) y[i] += ys[t][i];
+                for (std::size_t i = 0; i < tg[t].size(); ++i) y[tg[t][i]] += ys[t][i];
             const auto t1 = std::chrono::steady_clock::now();
             total += std::chrono::duration<double>(t1 - t0).count();
-            if (out && r == reps - 1) std::memcpy(out, y.data(), sizeof(double) * y.size());
         }
+        if (out) std::memcpy(out, y.data(), sizeof(double) * y.size());
         return total / reps;
     } catch (const std::exception& e) {
         set_err(err, len, e.what());

@@ -22,7 +22,8 @@ EXPORTS = (
     "femgpu_action_device", "femgpu_time_action", "femgpu_execute", "femgpu_default_schedule",
     "femgpu_stats", "femgpu_device_output", "femgpu_stream", "femgpu_action_once",
     "femgpu_host_alloc", "femgpu_host_free", "femgpu_mesh_counts", "femgpu_mesh_build",
-    "femgpu_color_cells",
+    "femgpu_color_cells", "femgpu_profile_action", "femgpu_fp64_peak",
+    "femgpu_time_steps", "femgpu_device_input",
 )
 
 
@@ -84,6 +85,11 @@ def lib():
                                        _P(C.c_double)], C.c_int),
                 "femgpu_color_cells": ([_P(C.c_int32), C.c_int32, C.c_int32, C.c_int32, _P(C.c_int32),
                                         _P(C.c_int32)], C.c_int),
+                "femgpu_profile_action": ([C.c_void_p, _P(abi.Schedule), C.c_int32, C.c_int32, _P(C.c_double),
+                                           _P(C.c_double), _P(C.c_double)], C.c_int),
+                "femgpu_fp64_peak": ([_P(C.c_double), _P(C.c_double)], C.c_int),
+                "femgpu_time_steps": ([C.c_void_p, _P(abi.Schedule), C.c_int32, _P(C.c_double)], C.c_int),
+                "femgpu_device_input": ([C.c_void_p, C.c_int32, _P(C.c_void_p)], C.c_int),
             }
             for name, (args, res) in sig.items():
                 f = getattr(L, name)

@@ -187,6 +187,20 @@ class GpuInstance:
         _call(lib().femgpu_time_action(self._h, sp[0] if sp else None, warmup, min_reps, min_seconds, C.byref(s)))
         return s.value
 
+    def time_steps(self, steps: int, params: Optional[TilingParams] = None) -> float:
+        """Total seconds of exactly `steps` actions, CUDA events, device sync on both sides."""
+        s = C.c_double()
+        sp = _sched(params)
+        _call(lib().femgpu_time_steps(self._h, sp[0] if sp else None, steps, C.byref(s)))
+        return s.value
+
+    def profile(self, params: Optional[TilingParams] = None, warmup: int = 5, reps: int = 50):
+        """(step, kernel-only, y-zero) mean seconds, CUDA events on the instance stream."""
+        v = [C.c_double() for _ in range(3)]
+        sp = _sched(params)
+        _call(lib().femgpu_profile_action(self._h, sp[0] if sp else None, warmup, reps, *[C.byref(x) for x in v]))
+        return tuple(x.value for x in v)
+
     def stats(self):
         v = [C.c_int64() for _ in range(4)]
         _call(lib().femgpu_stats(self._h, *[C.byref(x) for x in v]))
@@ -263,6 +277,13 @@ def jit_check(problem: ProblemInstance, params: Optional[TilingParams] = None) -
     cp = problem.to_c()
     sp = _sched(params)
     _call(lib().femgpu_jit_check(C.byref(cp.desc), sp[0] if sp else None))
+
+
+def fp64_peak():
+    """(TFLOP/s, nominal SM GHz): live DFMA peak of the current device (femgpu_fp64_peak)."""
+    t, g = C.c_double(), C.c_double()
+    _call(lib().femgpu_fp64_peak(C.byref(t), C.byref(g)))
+    return t.value, g.value
 
 
 def device_count() -> int:

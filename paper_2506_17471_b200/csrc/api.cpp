@@ -244,6 +244,62 @@ femgpu_status femgpu_time_action(femgpu_instance* h, const femgpu_schedule* s, i
     });
 }
 
+femgpu_status femgpu_time_steps(femgpu_instance* h, const femgpu_schedule* s, int32_t steps, double* seconds) {
+    return guard([&] {
+        auto& I = get(h);
+        if (steps < 1 || !seconds) femgpu::invalid("time_steps: steps >= 1 and an output are required");
+        std::lock_guard<std::mutex> lk(I.mu);
+        FG_CUDA(cudaSetDevice(I.device));
+        const femgpu::KernelPlan kp = femgpu::resolve_schedule(I, s);
+        FG_CUDA(cudaDeviceSynchronize());
+        FG_CUDA(cudaEventRecord(I.ev0, I.stream));
+        for (int i = 0; i < steps; ++i) femgpu::run_action(I, kp, I.d_y, I.stream);
+        FG_CUDA(cudaEventRecord(I.ev1, I.stream));
+        FG_CUDA(cudaEventSynchronize(I.ev1));
+        FG_CUDA(cudaDeviceSynchronize());
+        float ms = 0.f;
+        FG_CUDA(cudaEventElapsedTime(&ms, I.ev0, I.ev1));
+        femgpu::check_failure(I, kp, I.stream);
+        *seconds = ms * 1e-3;
+    });
+}
+
+femgpu_status femgpu_profile_action(femgpu_instance* h, const femgpu_schedule* s, int32_t warmup, int32_t reps,
+                                    double* step_seconds, double* kernel_seconds, double* zero_seconds) {
+    return guard([&] {
+        auto& I = get(h);
+        if (reps < 1) femgpu::invalid("profile: reps must be >= 1");
+        std::lock_guard<std::mutex> lk(I.mu);
+        FG_CUDA(cudaSetDevice(I.device));
+        const femgpu::KernelPlan kp = femgpu::resolve_schedule(I, s);
+        for (int i = 0; i < warmup; ++i) femgpu::run_action(I, kp, I.d_y, I.stream);
+        femgpu::check_failure(I, kp, I.stream);
+        std::vector<cudaEvent_t> ev(3 * static_cast<size_t>(reps));
+        for (auto& e : ev) FG_CUDA(cudaEventCreate(&e));
+        for (int i = 0; i < reps; ++i) {
+            FG_CUDA(cudaEventRecord(ev[3 * i], I.stream));
+            femgpu::run_action(I, kp, I.d_y, I.stream, ev[3 * i + 1]);
+            FG_CUDA(cudaEventRecord(ev[3 * i + 2], I.stream));
+        }
+        FG_CUDA(cudaEventSynchronize(ev.back()));
+        double step = 0, kern = 0, zero = 0;
+        for (int i = 0; i < reps; ++i) {
+            float a = 0, b = 0, c = 0;
+            FG_CUDA(cudaEventElapsedTime(&a, ev[3 * i], ev[3 * i + 2]));
+            FG_CUDA(cudaEventElapsedTime(&b, ev[3 * i + 1], ev[3 * i + 2]));
+            FG_CUDA(cudaEventElapsedTime(&c, ev[3 * i], ev[3 * i + 1]));
+            step += a;
+            kern += b;
+            zero += c;
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
+        femgpu::check_failure(I, kp, I.stream);
+        if (step_seconds) *step_seconds = step * 1e-3 / reps;
+        if (kernel_seconds) *kernel_seconds = kern * 1e-3 / reps;
+        if (zero_seconds) *zero_seconds = zero * 1e-3 / reps;
+    });
+}
+
 femgpu_status femgpu_execute(femgpu_instance* h, const femgpu_schedule* s, double* y_host, double* measured) {
     femgpu_status st = femgpu_action(h, s, y_host);
     if (st != FEMGPU_OK) return st;
@@ -278,6 +334,15 @@ femgpu_status femgpu_stats(const femgpu_instance* h, int64_t* launches, int64_t*
 
 femgpu_status femgpu_device_output(femgpu_instance* h, double** y_dev) {
     return guard([&] { *y_dev = get(h).d_y; });
+}
+
+femgpu_status femgpu_device_input(femgpu_instance* h, int32_t space, double** x_dev) {
+    return guard([&] {
+        auto& I = get(h);
+        const int ns = static_cast<int>(I.sspaces.size()), nv = static_cast<int>(I.vspaces.size());
+        if (!x_dev || space < 0 || space >= ns + nv) femgpu::invalid("device_input: space out of range");
+        *x_dev = space < ns ? I.sspaces[space].d_x : I.vspaces[space - ns].d_x;
+    });
 }
 
 femgpu_status femgpu_stream(femgpu_instance* h, void** stream) {

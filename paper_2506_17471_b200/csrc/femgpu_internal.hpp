@@ -188,7 +188,8 @@ void host_tile_plan(const femgpu_problem* p, const Signature& sig, KernelPlan& k
 void host_macro_plan(const femgpu_problem* p, const Signature& sig, KernelPlan& kp, const femgpu_schedule* s);
 std::unique_ptr<Instance> create_instance(const femgpu_problem* p);
 KernelPlan resolve_schedule(Instance& inst, const femgpu_schedule* s);
-void run_action(Instance& inst, const KernelPlan& kp, double* d_y, cudaStream_t stream);
+void run_action(Instance& inst, const KernelPlan& kp, double* d_y, cudaStream_t stream,
+                cudaEvent_t after_zero = nullptr);
 void check_failure(Instance& inst, const KernelPlan& kp, cudaStream_t stream);
 
 }  // namespace femgpu

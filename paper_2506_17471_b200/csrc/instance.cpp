@@ -772,12 +772,13 @@ std::shared_ptr<Module> Instance::module_for(const KernelPlan& kp) {
     return m;
 }
 
-void run_action(Instance& I, const KernelPlan& kp, double* d_y, cudaStream_t stream) {
+void run_action(Instance& I, const KernelPlan& kp, double* d_y, cudaStream_t stream, cudaEvent_t after_zero) {
     auto mod = I.module_for(kp);
     const TileLayout* L = kp.family == Family::Tile ? &I.tile_layout(kp.tile_cells) : nullptr;
     ParamBuf P = build_params(I, kp, d_y, L);
     void* args[] = {P.b.data()};
     FG_CUDA(cudaMemsetAsync(d_y, 0, sizeof(double) * static_cast<size_t>(I.output_size), stream));
+    if (after_zero) FG_CUDA(cudaEventRecord(after_zero, stream));
     long long grid = 0;
     if (kp.family == Family::Mlt)
         grid = (static_cast<long long>(I.cells) + kp.Nc - 1) / kp.Nc;
