@@ -115,7 +115,7 @@ femgpu_status femgpu_emit_source(const femgpu_problem* p, const femgpu_schedule*
             for (int i = 0; i < sig.nv(); ++i) kp.Tcv.push_back(s->eval_col_tiles_vector[i]);
         } else {
             kp.family = femgpu::Family::Scpt;
-            kp.basis = (s && s->basis) ? s->basis : (sig.tab_size <= 3800 ? FEMGPU_BASIS_CONST : FEMGPU_BASIS_SMEM);
+            kp.basis = (s && s->basis) ? s->basis : (sig.tab_size <= 512 ? FEMGPU_BASIS_CONST : FEMGPU_BASIS_SMEM);
             kp.block = (s && s->block_cells > 0) ? s->block_cells : 128;
             if (s && s->scatter == FEMGPU_SCATTER_TILE) femgpu::host_tile_plan(p, sig, kp, s);
             if (s && s->scatter == FEMGPU_SCATTER_MACRO) femgpu::host_macro_plan(p, sig, kp, s);

@@ -686,11 +686,58 @@ void emit_macro_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const
     for (int i = 0; i < sig.ns(); ++i) gathered.insert(kp.sgroup[i]);
     for (int i = 0; i < sig.nv(); ++i) gathered.insert(kp.vgroup[i]);
     if (sig.affine) gathered.insert(kp.cgroup);
-    for (int g : gathered)
-        for (int u = 0; u < kp.group_cap[g]; ++u)
-            o.line("const int ig" + S(g) + "_" + S(u) + " = __ldg(&P.gidx" + S(g) + "[" + S(u) + " * NG + grp]);");
+    // streaming order (mstage == 0): a unique node is loaded just before the first cell of the
+    // group that reads it, and its y contribution is issued right after the last cell that
+    // writes it, so register live ranges follow the cells instead of spanning the group.
+    auto first_use = [&](int g, int u) {
+        const int E = kp.group_entries[g];
+        for (int s = 0; s < kp.G; ++s)
+            for (int j = 0; j < E; ++j)
+                if (kp.mpat[g][static_cast<size_t>(s) * E + j] == u) return s;
+        return 0;
+    };
+    auto last_use = [&](int g, int u) {
+        const int E = kp.group_entries[g];
+        for (int s = kp.G - 1; s >= 0; --s)
+            for (int j = 0; j < E; ++j)
+                if (kp.mpat[g][static_cast<size_t>(s) * E + j] == u) return s;
+        return kp.G - 1;
+    };
+    const bool stream = !kp.mstage;
+    auto emit_loads = [&](int s_now) {
+        for (int g : gathered)
+            for (int u = 0; u < kp.group_cap[g]; ++u) {
+                if (stream && first_use(g, u) != s_now) continue;
+                o.line("const int ig" + S(g) + "_" + S(u) + " = __ldg(&P.gidx" + S(g) + "[" + S(u) + " * NG + grp]);");
+                if (kp.mstage) continue;
+                for (int i = 0; i < sig.ns(); ++i)
+                    if (kp.sgroup[i] == g)
+                        o.line("const double xg" + S(i) + "_" + S(u) + " = __ldg(&P.x" + S(i) + "[ig" + S(g) + "_" + S(u) + "]);");
+                for (int i = 0; i < sig.nv(); ++i)
+                    if (kp.vgroup[i] == g) {
+                        std::set<int> comps(sig.vcomps[i].begin(), sig.vcomps[i].end());
+                        for (int c : comps)
+                            o.line("const double vg" + S(i) + "_" + S(u) + "_" + S(c) + " = __ldg(&P.v" + S(i) + "[(size_t)ig" +
+                                   S(g) + "_" + S(u) + " * " + S(D) + " + " + S(c) + "]);");
+                    }
+                if (sig.affine && kp.cgroup == g)
+                    for (int c = 0; c < D; ++c)
+                        o.line("const double Xg" + S(u) + "_" + S(c) + " = __ldg(&P.X[(size_t)ig" + S(g) + "_" + S(u) +
+                               " * " + S(D) + " + " + S(c) + "]);");
+            }
+    };
+    const int gt = kp.tgroup;
+    auto emit_reds = [&](int s_now) {
+        for (int u = 0; u < kp.group_cap[gt]; ++u) {
+            if (stream && last_use(gt, u) != s_now) continue;
+            const std::string idx =
+                gathered.count(gt) ? "ig" + S(gt) + "_" + S(u) : "__ldg(&P.gidx" + S(gt) + "[" + S(u) + " * NG + grp])";
+            o.line("atomicAdd(&P.y[" + idx + "], ya" + S(u) + ");");
+        }
+    };
     MacroCtx base{0, {}, {}, 0};
     if (kp.mstage) {
+        emit_loads(-1);
         // thread-private slots [slot][blockDim] (conflict-free), filled with cp.async
         long long slot = 0;
         std::vector<std::string> copies;
@@ -720,28 +767,14 @@ void emit_macro_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const
         o.line("cp_commit();");
         o.line("cp_wait_all();");
     }
-    for (int i = 0; i < sig.ns() && !kp.mstage; ++i)
-        for (int u = 0; u < kp.group_cap[kp.sgroup[i]]; ++u)
-            o.line("const double xg" + S(i) + "_" + S(u) + " = __ldg(&P.x" + S(i) + "[ig" + S(kp.sgroup[i]) + "_" + S(u) + "]);");
-    for (int i = 0; i < sig.nv() && !kp.mstage; ++i) {
-        std::set<int> comps(sig.vcomps[i].begin(), sig.vcomps[i].end());
-        for (int u = 0; u < kp.group_cap[kp.vgroup[i]]; ++u)
-            for (int c : comps)
-                o.line("const double vg" + S(i) + "_" + S(u) + "_" + S(c) + " = __ldg(&P.v" + S(i) + "[(size_t)ig" +
-                       S(kp.vgroup[i]) + "_" + S(u) + " * " + S(D) + " + " + S(c) + "]);");
-    }
-    if (sig.affine && !kp.mstage)
-        for (int u = 0; u < kp.group_cap[kp.cgroup]; ++u)
-            for (int c = 0; c < D; ++c)
-                o.line("const double Xg" + S(u) + "_" + S(c) + " = __ldg(&P.X[(size_t)ig" + S(kp.cgroup) + "_" + S(u) +
-                       " * " + S(D) + " + " + S(c) + "]);");
     {
         std::string l = "double";
-        for (int u = 0; u < kp.group_cap[kp.tgroup]; ++u) l += std::string(u ? "," : "") + " ya" + S(u) + " = 0.0";
+        for (int u = 0; u < kp.group_cap[gt]; ++u) l += std::string(u ? "," : "") + " ya" + S(u) + " = 0.0";
         o.line(l + ";");
     }
     o.line("int stage = -1; (void)stage;");
     for (int s = 0; s < kp.G; ++s) {
+        if (stream) emit_loads(s);
         o.line("{ // cell " + S(s) + " of the group");
         o.ind++;
         o.line("const int cell = grp * " + S(kp.G) + " + " + S(s) + ";");
@@ -750,12 +783,9 @@ void emit_macro_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const
         emit_cell_body(o, sig, kp, use, false, unroll_q, &mc);
         o.ind--;
         o.line("}");
+        if (stream) emit_reds(s);
     }
-    const int gt = kp.tgroup;
-    for (int u = 0; u < kp.group_cap[gt]; ++u) {
-        const std::string idx = gathered.count(gt) ? "ig" + S(gt) + "_" + S(u) : "__ldg(&P.gidx" + S(gt) + "[" + S(u) + " * NG + grp])";
-        o.line("atomicAdd(&P.y[" + idx + "], ya" + S(u) + ");");
-    }
+    if (!stream) emit_reds(-1);
     o.line("return;");
     o.line("report:");
     o.line("  return;");

@@ -523,6 +523,7 @@ void host_macro_plan(const femgpu_problem* p, const Signature& sig, KernelPlan& 
     kp.block = s->block_cells > 0 ? s->block_cells : 64;
     const int reg_target = s->reserved[1] > 0 ? s->reserved[1] : 168;
     kp.min_blocks = std::max(1, std::min(16, 65536 / (kp.block * reg_target)));
+    if (s->reserved[2] > 0) kp.min_blocks = s->reserved[2];
     (void)sig;
 }
 
@@ -566,6 +567,10 @@ void host_tile_plan(const femgpu_problem* p, const Signature& sig, KernelPlan& k
 namespace {
 
 constexpr long long kParamTabLimit = 3800;  // doubles in the 32 KB kernel-parameter bank
+// Auto basis residency: the parameter (constant) bank is only chosen while the tabulations fit
+// the SM's constant cache comfortably; beyond that every LDCU risks a miss (C4: 11.5 KB of
+// tabulations ran 3x slower from the constant bank than from shared memory).
+constexpr long long kConstCacheDoubles = 512;  // 4 KB
 
 int int_dim(int a) { return a; }
 
@@ -608,7 +613,7 @@ KernelPlan resolve_schedule(Instance& I, const femgpu_schedule* s) {
     }
     // SCPT: one thread per cell.
     int basis = s->basis;
-    if (basis == FEMGPU_BASIS_AUTO) basis = sig.tab_size <= kParamTabLimit ? FEMGPU_BASIS_CONST : FEMGPU_BASIS_SMEM;
+    if (basis == FEMGPU_BASIS_AUTO) basis = sig.tab_size <= kConstCacheDoubles ? FEMGPU_BASIS_CONST : FEMGPU_BASIS_SMEM;
     if (basis == FEMGPU_BASIS_CONST && sig.tab_size > kParamTabLimit)
         fail(FEMGPU_E_INFEASIBLE, "basis: " + std::to_string(tab_bytes) +
                                       " bytes of tabulations exceed the 32 KB kernel-parameter bank");
