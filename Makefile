@@ -6,13 +6,13 @@ PKG := paper_2506_17471_b200
 SRC := $(PKG)/csrc
 OBJDIR := build/obj
 LIB := $(PKG)/_lib/libfemgpu.so
-CXXSRC := $(SRC)/api.cpp $(SRC)/instance.cpp $(SRC)/emit.cpp $(SRC)/emit_mlt.cpp $(SRC)/jit.cpp $(SRC)/mesh.cpp
+CXXSRC := $(SRC)/api.cpp $(SRC)/instance.cpp $(SRC)/emit.cpp $(SRC)/jit.cpp $(SRC)/mesh.cpp
 CUSRC := $(wildcard $(SRC)/*.cu)
 HDRS := include/femgpu.h $(SRC)/femgpu_internal.hpp
 NVFLAGS := -gencode arch=compute_100a,code=sm_100a -lineinfo -O3 -std=c++17 -Xcompiler -fPIC,-O2 --expt-relaxed-constexpr
 OBJS := $(patsubst $(SRC)/%.cpp,$(OBJDIR)/%.o,$(CXXSRC)) $(patsubst $(SRC)/%.cu,$(OBJDIR)/%.cu.o,$(CUSRC))
 
-all: $(LIB) oracle
+all: $(LIB) oracle adapter
 
 $(OBJDIR)/%.o: $(SRC)/%.cpp $(HDRS)
 	@mkdir -p $(OBJDIR)
@@ -29,7 +29,11 @@ $(LIB): $(OBJS)
 oracle:
 	$(MAKE) -s -C oracle
 
+# C++ drop-in test (needs the reference headers; skipped with a message when absent)
+adapter: $(LIB)
+	$(MAKE) -s -C tests/cpp
+
 clean:
 	rm -rf build $(LIB)
 
-.PHONY: all oracle clean
+.PHONY: all oracle adapter clean

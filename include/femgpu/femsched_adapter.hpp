@@ -1,0 +1,218 @@
+// femsched_adapter.hpp — C++ drop-in for the reference's action path (header-only).
+//
+// A femsched user keeps their own headers (proj/include/femsched/*.hpp) and swaps
+//
+//     std::vector<double> y = femsched::reference_action(inst);          // form.hpp:471-472
+//     auto res = femsched::tune(inst, dev, cfg, jobs);                    // search.hpp:338-339
+// for
+//     std::vector<double> y = femgpu::action(inst);                       // B200, same shape
+//     auto res = femsched::tune(inst, dev, cfg, jobs, femgpu::executor()); // measuring Executor
+//
+// Everything crosses into libfemgpu through the C-ABI of <femgpu.h> (plain pointers, no
+// exceptions).  Status codes come back as the reference's exception types:
+//   FEMGPU_E_INVALID -> std::invalid_argument, FEMGPU_E_INFEASIBLE -> femsched::InfeasibleError,
+//   FEMGPU_E_NONFINITE and others -> std::runtime_error (same "non-finite value at cell N during
+//   <stage>" text as form.hpp:492-495).
+// femgpu::executor() needs <femsched/search.hpp> (define FEMGPU_WITH_FEMSCHED_SEARCH first, or
+// include search.hpp before this header).
+#pragma once
+
+#include <femsched/form.hpp>
+
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../femgpu.h"
+
+#if defined(FEMGPU_WITH_FEMSCHED_SEARCH) || defined(FEMSCHED_SEARCH_HPP_INCLUDED)
+#include <femsched/search.hpp>
+#define FEMGPU_HAS_EXECUTOR 1
+#endif
+
+namespace femgpu {
+
+inline void check(femgpu_status st) {
+    if (st == FEMGPU_OK) return;
+    const std::string msg = femgpu_last_error();
+    if (st == FEMGPU_E_INVALID) throw std::invalid_argument(msg);
+    if (st == FEMGPU_E_INFEASIBLE) throw femsched::InfeasibleError(msg);
+    throw std::runtime_error(msg);
+}
+
+// Flat view of a femsched::ProblemInstance (borrowed pointers, valid while both live).
+class ProblemView {
+public:
+    explicit ProblemView(const femsched::ProblemInstance& p) {
+        const auto& sig = p.signature;
+        const int Q = sig.quad_points;
+        auto flat = [](const std::vector<femsched::Matrix>& ms) {
+            std::vector<double> out;
+            for (const auto& m : ms) out.insert(out.end(), m.data.begin(), m.data.end());
+            return out;
+        };
+        for (std::size_t i = 0; i < sig.scalar_spaces.size(); ++i) phi_.push_back(flat(p.tabulations.scalar_phi.at(i)));
+        for (std::size_t i = 0; i < sig.vector_spaces.size(); ++i) phi_.push_back(flat(p.tabulations.vector_phi.at(i)));
+        psi_ = flat(p.tabulations.psi);
+        std::size_t f = 0;
+        for (std::size_t i = 0; i < sig.scalar_spaces.size(); ++i, ++f) {
+            femgpu_space s{};
+            s.dofs = sig.scalar_spaces[i].dofs;
+            s.deriv_terms = sig.scalar_spaces[i].deriv_terms;
+            s.phi = phi_[f].data();
+            s.map = p.connectivity.scalar_maps.at(i).indices.data();
+            s.global_count = p.connectivity.scalar_maps[i].global_count;
+            s.input = p.scalar_inputs.at(i).data();
+            scalar_.push_back(s);
+        }
+        for (std::size_t i = 0; i < sig.vector_spaces.size(); ++i, ++f) {
+            femgpu_space s{};
+            s.dofs = sig.vector_spaces[i].dofs;
+            s.deriv_terms = sig.vector_spaces[i].deriv_terms;
+            s.components = sig.vector_spaces[i].components.data();
+            s.phi = phi_[f].data();
+            s.map = p.connectivity.vector_maps.at(i).indices.data();
+            s.global_count = p.connectivity.vector_maps[i].global_count;
+            s.input = p.vector_inputs.at(i).data();
+            vector_.push_back(s);
+        }
+        for (const auto& n : p.map.nodes()) {
+            femgpu_map_node m{};
+            m.op = static_cast<int32_t>(n.op);
+            m.a = n.a;
+            m.b = n.b;
+            m.value = n.value;
+            nodes_.push_back(m);
+        }
+        d_.dim = sig.dim;
+        d_.quad_points = Q;
+        d_.coord_dofs = sig.coord_dofs;
+        d_.affine_geometry = sig.affine_geometry ? 1 : 0;
+        d_.coordinate_space = sig.coordinate_space;
+        d_.word_bytes = sig.word_bytes;
+        d_.n_scalar = static_cast<int32_t>(scalar_.size());
+        d_.n_vector = static_cast<int32_t>(vector_.size());
+        d_.scalar_spaces = scalar_.data();
+        d_.vector_spaces = vector_.data();
+        d_.test_dofs = sig.test_dofs;
+        d_.test_deriv_terms = sig.test_deriv_terms;
+        d_.psi = psi_.data();
+        d_.weights = p.tabulations.weights.data();
+        d_.cell_count = p.connectivity.cell_count;
+        d_.test_global_count = p.connectivity.test_map.global_count;
+        d_.test_map = p.connectivity.test_map.indices.data();
+        d_.coord_map = sig.affine_geometry ? p.connectivity.coord_map.indices.data() : nullptr;
+        d_.coords = sig.affine_geometry ? p.connectivity.coords.data() : nullptr;
+        d_.coord_global_count = p.connectivity.coord_global_count;
+        d_.n_map_nodes = static_cast<int32_t>(nodes_.size());
+        d_.map_nodes = nodes_.data();
+        d_.map_outputs = p.map.outputs().data();
+        d_.n_map_outputs = static_cast<int32_t>(p.map.outputs().size());
+        d_.output_size = p.output_size;
+    }
+    const femgpu_problem* get() const { return &d_; }
+
+private:
+    std::vector<std::vector<double>> phi_;
+    std::vector<double> psi_;
+    std::vector<femgpu_space> scalar_, vector_;
+    std::vector<femgpu_map_node> nodes_;
+    femgpu_problem d_{};
+};
+
+// RAII device instance (femgpu_create/femgpu_destroy); re-blocking happens once here.
+class DeviceInstance {
+public:
+    explicit DeviceInstance(const femsched::ProblemInstance& p) : output_size_(p.output_size) {
+        ProblemView v(p);
+        femgpu_instance* h = nullptr;
+        check(femgpu_create(v.get(), &h));
+        h_.reset(h);
+    }
+    std::vector<double> action(const femgpu_schedule* s = nullptr) {
+        std::vector<double> y(static_cast<std::size_t>(output_size_));
+        check(femgpu_action(h_.get(), s, y.data()));
+        return y;
+    }
+    double measure(const femgpu_schedule* s = nullptr) {
+        double sec = 0.0;
+        check(femgpu_time_action(h_.get(), s, 5, 15, 0.2, &sec));
+        return sec;
+    }
+    femgpu_instance* handle() const { return h_.get(); }
+
+private:
+    struct Del {
+        void operator()(femgpu_instance* h) const { femgpu_destroy(h); }
+    };
+    std::unique_ptr<femgpu_instance, Del> h_;
+    int output_size_;
+};
+
+// reference_action-shaped entry (form.hpp:471-472): same arguments, same return, same errors.
+inline std::vector<double> action(const femsched::ProblemInstance& p) {
+    p.validate();  // identical argument checking to the reference, before any device work
+    DeviceInstance d(p);
+    return d.action();
+}
+
+#ifdef FEMGPU_HAS_EXECUTOR
+// TilingParams (qoi.hpp:23-33) -> femgpu_schedule.
+inline femgpu_schedule schedule_from(const femsched::TilingParams& t) {
+    femgpu_schedule s{};
+    if (t.kind == femsched::ScheduleKind::SingleCellPerWorkItem) {
+        s.kind = FEMGPU_SCPT;
+        return s;
+    }
+    s.kind = FEMGPU_MLT;
+    s.quad_tile = t.quad_tile;
+    s.eval_row_tile = t.eval_row_tile;
+    for (std::size_t i = 0; i < t.eval_col_tiles_scalar.size() && i < FEMGPU_MAX_SPACES; ++i)
+        s.eval_col_tiles_scalar[i] = t.eval_col_tiles_scalar[i];
+    for (std::size_t i = 0; i < t.eval_col_tiles_vector.size() && i < FEMGPU_MAX_SPACES; ++i)
+        s.eval_col_tiles_vector[i] = t.eval_col_tiles_vector[i];
+    s.quad_row_tile = t.quad_row_tile;
+    s.quad_col_tile = t.quad_col_tile;
+    s.cells_per_group = t.cells_per_group;
+    s.lanes_per_cell = t.lanes_per_cell;
+    return s;
+}
+
+// A measuring femsched::Executor (search.hpp:257-283) backed by the sm_100a kernels: uploads
+// each instance once (tune calls it for b+1 candidates, possibly from std::async threads),
+// verifies finiteness on the device, reports the CUDA-event mean of the paper's protocol.
+inline femsched::Executor executor() {
+    struct Cache {
+        std::mutex mu;
+        const femsched::ProblemInstance* key = nullptr;
+        std::shared_ptr<DeviceInstance> dev;
+    };
+    auto cache = std::make_shared<Cache>();
+    return [cache](const femsched::TilingParams& t, const femsched::ProblemInstance& inst) {
+        femsched::ExecutionOutcome out;
+        try {
+            std::shared_ptr<DeviceInstance> d;
+            {
+                std::lock_guard<std::mutex> lk(cache->mu);
+                if (cache->key != &inst || !cache->dev) {
+                    cache->dev = std::make_shared<DeviceInstance>(inst);
+                    cache->key = &inst;
+                }
+                d = cache->dev;
+            }
+            const femgpu_schedule s = schedule_from(t);
+            out.output = d->action(&s);
+            out.measured_seconds = d->measure(&s);
+            out.workgroups = femsched::ceil_div(inst.connectivity.cell_count, t.group_size() / std::max(1, t.kind == femsched::ScheduleKind::SingleCellPerWorkItem ? 1 : t.lanes_per_cell));
+            out.ok = true;
+        } catch (const std::exception& e) {
+            out.error = e.what();  // search.hpp:278-280
+        }
+        return out;
+    };
+}
+#endif
+
+}  // namespace femgpu

@@ -411,7 +411,7 @@ std::string KernelPlan::key() const {
     return s.str();
 }
 
-EmitResult emit_mlt(const Signature& sig, const KernelPlan& kp);  // emit_mlt.cpp
+EmitResult emit_mlt(const Signature& sig, const KernelPlan& kp);  // below
 
 namespace {
 
@@ -851,6 +851,240 @@ EmitResult emit_kernel(const Signature& sig, const KernelPlan& kp) {
         emit_scpt_kernel(o, sig, kp, use, unroll_q, true, r.kernel_checked, 0);
     }
     r.source = o.s.str();
+    return r;
+}
+
+
+// ---------------------------------------------------------------------------------------------
+// MLT family: the paper's multi-level tiling (TilingParams, qoi.hpp:23-33) with the execution
+// and summation semantics of run_mlt (simulate.hpp:293-598): CTA = N_c cells x N_WI lanes,
+// quadrature tiles of T^Q points; per (eval row tile, space, column tile) the cells' DOF tiles are
+// gathered and the Phi tile is prefetched cooperatively into the aliased shared buffer B (roster
+// flat = N_c*N_WI*round + N_WI*lid0 + lid1), lanes stride the rows; the map writes e_arr; per
+// (quad row tile, column tile) the Psi tile goes through B; y gets one red.add per (quad tile,
+// quad row tile) per test DOF.  Tabulations are read from global memory (L2-resident).
+EmitResult emit_mlt(const Signature& sig, const KernelPlan& kp) {
+    const MapUse use = analyse(sig);
+    EmitResult r;
+    Out o;
+    o << kPrelude;
+    emit_params(o, sig, kp, 0);
+    const int NC = kp.Nc, NW = kp.Nwi, BS = NC * NW, Q = sig.Q, D = sig.dim;
+    const int TQ = kp.TQ, TER = kp.Ter, TQR = kp.Tqr, TQC = kp.Tqc, TW = sig.Tw, NWD = sig.nW;
+    struct Sp {
+        bool vec;
+        int idx, n, terms, tc;
+        long long phi_off;
+        std::vector<int> comps;
+    };
+    std::vector<Sp> sps;
+    for (int i = 0; i < sig.ns(); ++i) sps.push_back({false, i, sig.sdofs[i], sig.sterms[i], kp.Tcs[i], sig.phi_off_s[i], {}});
+    for (int i = 0; i < sig.nv(); ++i)
+        sps.push_back({true, i, sig.vdofs[i], sig.vterms[i], kp.Tcv[i], sig.phi_off_v[i], sig.vcomps[i]});
+    long long buf = 0;
+    for (const auto& s : sps) buf = std::max<long long>(buf, static_cast<long long>(s.terms) * TER * s.tc);
+    buf = std::max<long long>(buf, static_cast<long long>(TW) * TQR * TQC);
+    long long dt = 1;
+    for (const auto& s : sps) dt = std::max<long long>(dt, static_cast<long long>(s.tc) * (s.vec ? D : 1));
+    const long long earr = static_cast<long long>(TW) * NC * TQ;
+    const int geo = sig.affine ? D * D + 1 + sig.coord_dofs * D : 0;
+    const long long off_e = buf, off_dofs = off_e + earr, off_geo = off_dofs + NC * dt;
+    r.smem_bytes = static_cast<size_t>((off_geo + static_cast<long long>(NC) * geo) * 8);
+    r.kernel = "femgpu_mlt";
+    r.kernel_checked = "femgpu_mlt_checked";
+    const int RR = (TER + NW - 1) / NW, RQ = (TQR + NW - 1) / NW;
+    auto TABG = [](const std::string& idx) { return "__ldg(&P.tabg[" + idx + "])"; };
+
+    o.line("");
+    o.line("extern \"C\" __global__ void __launch_bounds__(" + S(BS) + ") " + r.kernel + "(const __grid_constant__ Params P) {");
+    o.ind++;
+    o.line("constexpr bool CHECKED = false;");
+    o.line("extern __shared__ __align__(16) double smd[];");
+    o.line("double* Bf = smd; double* earr = smd + " + S(off_e) + "; double* dofs = smd + " + S(off_dofs) +
+           "; double* geo = smd + " + S(off_geo) + ";");
+    o.line("const int tid = threadIdx.x, lid0 = tid / " + S(NW) + ", lid1 = tid % " + S(NW) + ";");
+    o.line("const int cell = blockIdx.x * " + S(NC) + " + lid0;");
+    o.line("const bool live = cell < P.n_cells;");
+    o.line("bool nf = false;");
+    o.line("int stage = -1; (void)stage;");
+    if (sig.affine) {
+        // geometry once per cell (lane 0), shared with the cell's lanes
+        o.line("if (live && lid1 == 0) {");
+        o.ind++;
+        o.line("double* g = geo + lid0 * " + S(geo) + ";");
+        for (int j = 0; j < sig.coord_dofs; ++j) {
+            o.line("{");
+            o.line("  const int v = __ldg(&P.cm[" + S(j) + "*(size_t)P.stride + cell]);");
+            for (int c = 0; c < D; ++c)
+                o.line("  g[" + S(D * D + 1 + j * D + c) + "] = __ldg(&P.X[(size_t)v*" + S(D) + "+" + S(c) + "]);");
+            o.line("}");
+        }
+        o.ind--;
+        o.line("}");
+        o.line("__syncthreads();");
+        o.line("const double* g = geo + lid0 * " + S(geo) + ";");
+        for (int j = 0; j < sig.coord_dofs; ++j)
+            for (int c = 0; c < D; ++c) o.line("const double X" + S(j) + "_" + S(c) + " = g[" + S(D * D + 1 + j * D + c) + "];");
+        for (int c = 0; c < D; ++c)
+            for (int rr = 0; rr < D; ++rr)
+                o.line("const double J" + S(rr) + "_" + S(c) + " = X" + S(c + 1) + "_" + S(rr) + " - X0_" + S(rr) + ";");
+        if (D == 1) o.line("const double det = J0_0;");
+        if (D == 2) o.line("const double det = J0_0 * J1_1 - J0_1 * J1_0;");
+        if (D == 3)
+            o.line("const double det = J0_0 * (J1_1 * J2_2 - J1_2 * J2_1) - J0_1 * (J1_0 * J2_2 - J1_2 * J2_0) + "
+                   "J0_2 * (J1_0 * J2_1 - J1_1 * J2_0);");
+        if (use.uses_inv) {
+            if (D == 1) o.line("const double Ji0_0 = 1.0 / det;");
+            if (D == 2) o.line("const double Ji0_0 = J1_1 / det, Ji0_1 = -J0_1 / det, Ji1_0 = -J1_0 / det, Ji1_1 = J0_0 / det;");
+            if (D == 3) {
+                o.line("const double Ji0_0 = (J1_1*J2_2 - J1_2*J2_1) / det, Ji0_1 = (J0_2*J2_1 - J0_1*J2_2) / det, Ji0_2 = (J0_1*J1_2 - J0_2*J1_1) / det;");
+                o.line("const double Ji1_0 = (J1_2*J2_0 - J1_0*J2_2) / det, Ji1_1 = (J0_0*J2_2 - J0_2*J2_0) / det, Ji1_2 = (J0_2*J1_0 - J0_0*J1_2) / det;");
+                o.line("const double Ji2_0 = (J1_0*J2_1 - J1_1*J2_0) / det, Ji2_1 = (J0_1*J2_0 - J0_0*J2_1) / det, Ji2_2 = (J0_0*J1_1 - J0_1*J1_0) / det;");
+            }
+        }
+        o.line("if (live) nf = nf | NF(det);");
+    }
+    emit_nodes(o, sig, use, false, "0", TABG);
+    o.line("for (int qt = 0; qt < " + S((Q + TQ - 1) / TQ) + "; ++qt) {");
+    o.ind++;
+    o.line("const int qb = qt * " + S(TQ) + ", tq = min(" + S(TQ) + ", " + S(Q) + " - qb);");
+    // ---- evaluation phase
+    o.line("for (int rb = 0; rb < tq; rb += " + S(TER) + ") {");
+    o.ind++;
+    o.line("const int tr = min(" + S(TER) + ", tq - rb);");
+    for (size_t si = 0; si < sps.size(); ++si)
+        for (int k = 0; k < sps[si].terms; ++k) {
+            std::string l = "double";
+            for (int rr = 0; rr < RR; ++rr) l += std::string(rr ? "," : "") + " a" + S(si) + "_" + S(k) + "_" + S(rr) + " = 0.0";
+            o.line(l + ";");
+        }
+    for (size_t si = 0; si < sps.size(); ++si) {
+        const Sp& sp = sps[si];
+        const int comps = sp.vec ? D : 1;
+        const std::string X = sp.vec ? "P.v" + S(sp.idx) : "P.x" + S(sp.idx);
+        const std::string M = sp.vec ? "P.vm" + S(sp.idx) : "P.m" + S(sp.idx);
+        o.line("for (int cb = 0; cb < " + S(sp.n) + "; cb += " + S(sp.tc) + ") {");
+        o.ind++;
+        o.line("const int tc = min(" + S(sp.tc) + ", " + S(sp.n) + " - cb);");
+        // per-cell DOF tile gather (lanes of the cell share it)
+        o.line("if (live) for (int t = lid1; t < tc * " + S(comps) + "; t += " + S(NW) + ") {");
+        o.line("  const int j = t / " + S(comps) + ", c = t % " + S(comps) + ";");
+        o.line("  dofs[lid0 * " + S(dt) + " + t] = __ldg(&" + X + "[(size_t)__ldg(&" + M + "[(size_t)(cb + j) * P.stride + cell]) * " +
+               S(comps) + " + c]);");
+        o.line("}");
+        // cooperative Phi-tile prefetch into the aliased buffer (roster of simulate.hpp:414-429)
+        o.line("for (int f = tid; f < tr * tc; f += " + S(BS) + ") {");
+        o.line("  const int i = f / tc, j = f % tc;");
+        for (int k = 0; k < sp.terms; ++k)
+            o.line("  Bf[" + S(static_cast<long long>(k) * TER * sp.tc) + " + i * " + S(sp.tc) + " + j] = " +
+                   TABG(S(sp.phi_off + static_cast<long long>(k) * Q * sp.n) + " + (qb + rb + i) * " + S(sp.n) + " + cb + j") + ";");
+        o.line("}");
+        o.line("__syncthreads();");
+        for (int rr = 0; rr < RR; ++rr) {
+            o.line("if (live && lid1 + " + S(rr * NW) + " < tr) {");
+            o.ind++;
+            o.line("const int iq = lid1 + " + S(rr * NW) + ";");
+            for (int k = 0; k < sp.terms; ++k) {
+                const int comp = sp.vec ? sp.comps[k] : 0;
+                const std::string a = "a" + S(si) + "_" + S(k) + "_" + S(rr);
+                o.line("for (int j = 0; j < tc; ++j) " + a + " = FMA(Bf[" + S(static_cast<long long>(k) * TER * sp.tc) + " + iq * " +
+                       S(sp.tc) + " + j], dofs[lid0 * " + S(dt) + " + j * " + S(comps) + " + " + S(comp) + "], " + a + ");");
+            }
+            o.ind--;
+            o.line("}");
+        }
+        o.line("__syncthreads();");
+        o.ind--;
+        o.line("}");
+    }
+    // map per row (the lane that evaluated the row applies the map)
+    for (int rr = 0; rr < RR; ++rr) {
+        o.line("if (live && lid1 + " + S(rr * NW) + " < tr) {");
+        o.ind++;
+        o.line("const int iq = lid1 + " + S(rr * NW) + ";");
+        // alias derivative variables
+        for (size_t si = 0; si < sps.size(); ++si)
+            for (int k = 0; k < sps[si].terms; ++k)
+                o.line("const double " + std::string(sps[si].vec ? "t" : "s") + S(sps[si].idx) + "_" + S(k) + " = a" + S(si) + "_" +
+                       S(k) + "_" + S(rr) + ";");
+        {
+            std::string unused;
+            for (int i = 0; i < sig.ns(); ++i)
+                for (int k = 0; k < sig.sterms[i]; ++k)
+                    if (!use.sd_used.count({i, k})) unused += " | NF(s" + S(i) + "_" + S(k) + ")";
+            for (int i = 0; i < sig.nv(); ++i)
+                for (int k = 0; k < sig.vterms[i]; ++k)
+                    if (!use.vd_used.count({i, k})) unused += " | NF(t" + S(i) + "_" + S(k) + ")";
+            if (!unused.empty()) o.line("nf = nf" + unused + ";");
+        }
+        emit_nodes(o, sig, use, true, "qb + rb + iq", TABG);
+        for (int k = 0; k < TW; ++k)
+            o.line("earr[(" + S(k) + " * " + S(NC) + " + lid0) * " + S(TQ) + " + rb + iq] = n" + S(sig.outputs[k]) + ";");
+        o.ind--;
+        o.line("}");
+    }
+    o.ind--;
+    o.line("}");
+    o.line("__syncthreads();");
+    // ---- quadrature phase
+    o.line("for (int rb = 0; rb < " + S(NWD) + "; rb += " + S(TQR) + ") {");
+    o.ind++;
+    o.line("const int tr = min(" + S(TQR) + ", " + S(NWD) + " - rb);");
+    {
+        std::string l = "double";
+        for (int rr = 0; rr < RQ; ++rr) l += std::string(rr ? "," : "") + " o" + S(rr) + " = 0.0";
+        o.line(l + ";");
+    }
+    o.line("for (int cb = 0; cb < tq; cb += " + S(TQC) + ") {");
+    o.ind++;
+    o.line("const int tc = min(" + S(TQC) + ", tq - cb);");
+    o.line("for (int f = tid; f < tr * tc; f += " + S(BS) + ") {");
+    o.line("  const int i = f / tc, j = f % tc;");
+    for (int k = 0; k < TW; ++k)
+        o.line("  Bf[" + S(static_cast<long long>(k) * TQR * TQC) + " + i * " + S(TQC) + " + j] = " +
+               TABG(S(sig.psi_off + static_cast<long long>(k) * NWD * Q) + " + (rb + i) * " + S(Q) + " + qb + cb + j") + ";");
+    o.line("}");
+    o.line("__syncthreads();");
+    for (int rr = 0; rr < RQ; ++rr) {
+        o.line("if (live && lid1 + " + S(rr * NW) + " < tr) {");
+        o.line("  const int jw = lid1 + " + S(rr * NW) + ";");
+        o.line("  for (int iq = 0; iq < tc; ++iq) {");
+        for (int k = 0; k < TW; ++k)
+            o.line("    o" + S(rr) + " = FMA(Bf[" + S(static_cast<long long>(k) * TQR * TQC) + " + jw * " + S(TQC) +
+                   " + iq], earr[(" + S(k) + " * " + S(NC) + " + lid0) * " + S(TQ) + " + cb + iq], o" + S(rr) + ");");
+        o.line("  }");
+        o.line("}");
+    }
+    o.line("__syncthreads();");
+    o.ind--;
+    o.line("}");
+    // scatter this (quad tile, row tile) (simulate.hpp:578-586)
+    for (int rr = 0; rr < RQ; ++rr) {
+        o.line("if (live && lid1 + " + S(rr * NW) + " < tr) {");
+        o.line("  const int jw = lid1 + " + S(rr * NW) + ";");
+        o.line("  nf = nf | NF(o" + S(rr) + ");");
+        o.line("  atomicAdd(&P.y[__ldg(&P.tm[(size_t)(rb + jw) * P.stride + cell])], o" + S(rr) + ");");
+        o.line("}");
+    }
+    o.ind--;
+    o.line("}");
+    o.line("__syncthreads();");
+    o.ind--;
+    o.line("}");
+    o.line("if (nf) atomicMin(P.bad, (unsigned long long)cell);");
+    o.line("return;");
+    o.line("report:");
+    o.line("  return;");
+    o.ind--;
+    o.line("}");
+    // diagnostic kernel: the SCPT stage-checked kernel over the same Params
+    KernelPlan pk = kp;
+    pk.family = Family::Scpt;
+    pk.basis = FEMGPU_BASIS_SMEM;
+    const bool unroll_q = false;
+    emit_scpt_kernel(o, sig, pk, use, unroll_q, true, r.kernel_checked, 0);
+    r.source = o.s.str();
+    r.smem_bytes = std::max<size_t>(r.smem_bytes, static_cast<size_t>(sig.tab_size) * 8);
     return r;
 }
 

@@ -779,6 +779,9 @@ std::shared_ptr<Module> Instance::module_for(const KernelPlan& kp) {
 
 void run_action(Instance& I, const KernelPlan& kp, double* d_y, cudaStream_t stream, cudaEvent_t after_zero) {
     auto mod = I.module_for(kp);
+    if (mod->emitted.smem_bytes > 227 * 1024)
+        fail(FEMGPU_E_INFEASIBLE, "schedule: " + std::to_string(mod->emitted.smem_bytes) +
+                                      " bytes of shared memory per CTA exceed the 227 KB sm_100a limit");
     const TileLayout* L = kp.family == Family::Tile ? &I.tile_layout(kp.tile_cells) : nullptr;
     ParamBuf P = build_params(I, kp, d_y, L);
     void* args[] = {P.b.data()};

@@ -117,7 +117,7 @@ std::shared_ptr<Module> get_module(const Signature& sig, const KernelPlan& kp) {
     FG_CUDA(cudaLibraryLoadData(&m->lib, bin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
     FG_CUDA(cudaLibraryGetKernel(&m->fast, m->lib, em.kernel.c_str()));
     FG_CUDA(cudaLibraryGetKernel(&m->checked, m->lib, em.kernel_checked.c_str()));
-    if (em.smem_bytes > 48 * 1024) {
+    if (em.smem_bytes > 48 * 1024 && em.smem_bytes <= 227 * 1024) {
         FG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(m->fast),
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(em.smem_bytes)));
         FG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(m->checked),

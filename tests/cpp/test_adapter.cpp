@@ -1,0 +1,72 @@
+// C++ drop-in test: femgpu::action vs femsched::reference_action (the reference's own code,
+// compiled from /root/reference/proj/include), and femsched::tune with femgpu::executor().
+// Built by tests/cpp/Makefile (needs the reference headers, so it is built in the container
+// and the binary travels to the GPU box).  Exit code 0 = all checks passed; 77 = no GPU.
+#include <cmath>
+#include <cstdio>
+
+#define FEMGPU_WITH_FEMSCHED_SEARCH 1
+#include <femgpu/femsched_adapter.hpp>
+
+using namespace femsched;
+
+static double rel_l2(const std::vector<double>& a, const std::vector<double>& b) {
+    double num = 0, den = 0;
+    for (std::size_t i = 0; i < a.size(); ++i) {
+        num += (a[i] - b[i]) * (a[i] - b[i]);
+        den += b[i] * b[i];
+    }
+    return std::sqrt(num / (den > 0 ? den : 1));
+}
+
+int main() {
+    if (femgpu_device_count() < 1) {
+        std::printf("no CUDA device: skipping\n");
+        return 77;
+    }
+    int fails = 0;
+    struct Case { Operator op; int d, p, q, cells; unsigned seed; };
+    const Case cases[] = {{Operator::mass, 2, 2, 7, 16, 7}, {Operator::laplace, 2, 2, 6, 16, 7},
+                          {Operator::helmholtz, 2, 3, 12, 16, 7}, {Operator::mass, 3, 1, 5, 16, 7},
+                          {Operator::laplace, 3, 2, 8, 16, 7}, {Operator::helmholtz, 3, 1, 7, 16, 7},
+                          {Operator::elasticity, 3, 2, 4, 60, 3}, {Operator::hyperelasticity, 2, 2, 6, 33, 5}};
+    for (const auto& c : cases) {
+        const auto sig = preset_signature(c.op, c.d, c.p, c.q);
+        const auto inst = make_problem(sig, preset_map(c.op, sig), c.cells, c.seed);
+        const auto ref = reference_action(inst);
+        const auto got = femgpu::action(inst);
+        const double err = rel_l2(got, ref);
+        std::printf("%-16s d=%d p=%d Q=%2d cells=%3d  rel_l2=%.3e\n", operator_name(c.op), c.d, c.p, c.q, c.cells, err);
+        if (!(err <= 1e-12) || got.size() != ref.size()) ++fails;
+    }
+    // error mapping: invalid instance -> std::invalid_argument, NaN -> runtime_error naming the cell
+    {
+        const auto sig = preset_signature(Operator::mass, 2, 1, 2);
+        auto inst = make_problem(sig, preset_map(Operator::mass, sig), 2, 1);
+        inst.scalar_inputs[0][0] = std::nan("");
+        std::string ref_msg, got_msg;
+        try { reference_action(inst); } catch (const std::runtime_error& e) { ref_msg = e.what(); }
+        try { femgpu::action(inst); } catch (const std::runtime_error& e) { got_msg = e.what(); }
+        std::printf("non-finite: ref='%s' got='%s'\n", ref_msg.c_str(), got_msg.c_str());
+        if (ref_msg != got_msg || ref_msg.empty()) ++fails;
+    }
+    // tune through the measuring executor: b-best ranked MLT candidates + SCPT (search.hpp:338-416)
+    {
+        const auto sig = preset_signature(Operator::laplace, 2, 2, 6);
+        const auto inst = make_problem(sig, preset_map(Operator::laplace, sig), 64, 7);
+        SearchConfig cfg;
+        cfg.best_count = 3;
+        try {
+            auto res = tune(inst, titan_v_device(), cfg, 1, femgpu::executor());
+            std::printf("tune: %zu candidates verified, winner %s\n", res.records.size(),
+                        detail::describe(res.winner.params).c_str());
+            for (const auto& r : res.records)
+                if (!r.output_ok || !std::isfinite(r.selection_seconds)) ++fails;
+        } catch (const std::exception& e) {
+            std::printf("tune failed: %s\n", e.what());
+            ++fails;
+        }
+    }
+    std::printf(fails ? "FAIL (%d)\n" : "PASS\n", fails);
+    return fails ? 1 : 0;
+}
