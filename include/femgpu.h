@@ -118,7 +118,13 @@ typedef struct femgpu_problem {
  * (qoi.hpp:23-41); the remaining fields are B200 knobs (0 = automatic). */
 typedef enum femgpu_schedule_kind {
     FEMGPU_SCPT = 0, /* TilingParams::scpt(): one thread per cell */
-    FEMGPU_MLT = 1   /* multi-level tiling: N_c cells x N_WI lanes per CTA */
+    FEMGPU_MLT = 1,  /* multi-level tiling: N_c cells x N_WI lanes per CTA */
+    FEMGPU_DMMA = 2  /* B200 extension: cell-batched FP64 tensor-core (DMMA) contraction.
+                        cells_per_group = N_c cells per tile (multiple of 8), quad_tile = T^Q,
+                        lanes_per_cell = threads per cell (CTA = N_c * lanes_per_cell threads),
+                        eval_row_tile = m-blocks and quad_row_tile = n-blocks of 8 per warp task,
+                        basis SMEM = Phi/Psi fragments resident in shared memory (else L1/L2);
+                        0 = automatic for every field */
 } femgpu_schedule_kind;
 
 typedef enum femgpu_basis {

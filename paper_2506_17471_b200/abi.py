@@ -17,7 +17,7 @@ OK, E_INVALID, E_INFEASIBLE, E_NONFINITE, E_CUDA, E_JIT, E_INTERNAL = range(7)
 OP_CONSTANT, OP_SCALAR_DERIV, OP_VECTOR_DERIV, OP_JACOBIAN, OP_DETERMINANT, OP_WEIGHT, OP_COORD, \
     OP_ADD, OP_MUL, OP_INV_JACOBIAN = range(10)
 
-SCPT, MLT = 0, 1
+SCPT, MLT, DMMA = 0, 1, 2
 BASIS_AUTO, BASIS_CONST, BASIS_SMEM = 0, 1, 2
 SCATTER_AUTO, SCATTER_ATOMIC, SCATTER_TILE, SCATTER_MACRO = 0, 1, 2, 3
 MAX_SPACES = 8

@@ -53,6 +53,16 @@ class TilingParams:
         return TilingParams(kind=abi.SCPT, **knobs)
 
     @staticmethod
+    def dmma(**knobs) -> "TilingParams":
+        """FEMGPU_DMMA: cell-batched FP64 tensor-core contraction (0 = automatic for every field):
+        cells_per_group = cells per tile, quad_tile = T^Q, lanes_per_cell = threads per cell,
+        eval_row_tile / quad_row_tile = m-blocks / n-blocks of 8 per warp task."""
+        d = dict(kind=abi.DMMA, quad_tile=0, eval_row_tile=0, quad_row_tile=0, quad_col_tile=0,
+                 cells_per_group=0, lanes_per_cell=0)
+        d.update(knobs)
+        return TilingParams(**d)
+
+    @staticmethod
     def untiled(sig: FormSignature, cells_per_group: int = 1, lanes_per_cell: int = 1) -> "TilingParams":
         return TilingParams(kind=abi.MLT, quad_tile=sig.quad_points, eval_row_tile=sig.quad_points,
                             eval_col_tiles_scalar=[s.dofs for s in sig.scalar_spaces],

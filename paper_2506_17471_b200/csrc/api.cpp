@@ -101,7 +101,9 @@ femgpu_status femgpu_emit_source(const femgpu_problem* p, const femgpu_schedule*
         femgpu::Signature sig = femgpu::signature_from(p);
         // Host-only resolution (no device instance): SCPT with global atomics, or MLT.
         femgpu::KernelPlan kp;
-        if (s && s->kind == FEMGPU_MLT) {
+        if (s && s->kind == FEMGPU_DMMA) {
+            femgpu::resolve_dmma(sig, kp, s);
+        } else if (s && s->kind == FEMGPU_MLT) {
             kp.family = femgpu::Family::Mlt;
             kp.TQ = s->quad_tile;
             kp.Ter = s->eval_row_tile;

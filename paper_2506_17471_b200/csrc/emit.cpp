@@ -147,6 +147,7 @@ void emit_params(Out& o, const Signature& sig, const KernelPlan& kp, long long n
     for (int i = 0; i < sig.nv(); ++i) o.line("  const double* v" + std::to_string(i) + "; const int* vm" + std::to_string(i) + ";");
     o.line("  const int* tm; const int* cm; const double* X;");
     o.line("  double* y; unsigned long long* bad; const double* tabg;");
+    if (kp.family == Family::Dmma) o.line("  const double* afr;");
     if (kp.family == Family::Macro)
         for (size_t g = 0; g < kp.group_entries.size(); ++g) o.line("  const int* gidx" + std::to_string(g) + ";");
     const int ngroups = kp.family == Family::Tile ? static_cast<int>(kp.group_entries.size()) : 0;
@@ -174,6 +175,7 @@ void emit_cell_body(Out& o, const Signature& sig, const KernelPlan& kp, const Ma
     auto pat = [&](int g, int j) { return kp.mpat[g][static_cast<size_t>(mc->s) * kp.group_entries[g] + j]; };
     const int d = sig.dim, Q = sig.Q;
     auto TAB = [&](const std::string& idx) {
+        if (kp.basis == kBasisGlobal) return "__ldg(&P.tabg[" + idx + "])";
         return kp.basis == FEMGPU_BASIS_CONST ? "P.tab[" + idx + "]" : "sT[" + idx + "]";
     };
     const std::string C = "P.stride";
@@ -394,6 +396,67 @@ const char* kPrelude = R"(// generated by femgpu (emit.cpp) for sm_100a
 
 }  // namespace
 
+// ---- helpers shared with emit_dmma.cpp
+std::vector<char> map_live(const Signature& sig) { return analyse(sig).live; }
+std::vector<char> map_qdep(const Signature& sig) { return analyse(sig).qdep; }
+
+// Emits the live map nodes of one pass (cell-invariant or quadrature-point-dependent) as SSA;
+// the quadrature weight is read through `weight_expr`.
+void emit_map_nodes(std::ostringstream& os, const Signature& sig, const std::vector<char>& live,
+                    const std::vector<char>& qdep, bool qdep_pass, const std::string& weight_expr) {
+    for (size_t id = 0; id < sig.nodes.size(); ++id) {
+        if (!live[id] || static_cast<bool>(qdep[id]) != qdep_pass) continue;
+        const MapNode& n = sig.nodes[id];
+        std::string rhs;
+        switch (n.op) {
+            case FEMGPU_OP_CONSTANT: rhs = lit(n.value); break;
+            case FEMGPU_OP_SCALAR_DERIV: rhs = "s" + std::to_string(n.a) + "_" + std::to_string(n.b); break;
+            case FEMGPU_OP_VECTOR_DERIV: rhs = "t" + std::to_string(n.a) + "_" + std::to_string(n.b); break;
+            case FEMGPU_OP_JACOBIAN: rhs = "J" + std::to_string(n.a) + "_" + std::to_string(n.b); break;
+            case FEMGPU_OP_INV_JACOBIAN: rhs = "Ji" + std::to_string(n.a) + "_" + std::to_string(n.b); break;
+            case FEMGPU_OP_DETERMINANT: rhs = "det"; break;
+            case FEMGPU_OP_WEIGHT: rhs = weight_expr; break;
+            case FEMGPU_OP_COORD: rhs = "X" + std::to_string(n.a) + "_" + std::to_string(n.b); break;
+            case FEMGPU_OP_ADD: rhs = "n" + std::to_string(n.a) + " + n" + std::to_string(n.b); break;
+            case FEMGPU_OP_MUL: rhs = "n" + std::to_string(n.a) + " * n" + std::to_string(n.b); break;
+        }
+        os << "        const double n" << id << " = " << rhs << ";\n";
+    }
+}
+
+// Coordinates through the coordinate map, affine Jacobian and determinant (form.hpp:441-457,
+// :511-520), optionally J^-1 (extension op 9).
+void emit_geometry(std::ostringstream& os, const Signature& sig, bool uses_inv, const std::string& cell) {
+    const int d = sig.dim;
+    for (int j = 0; j < sig.coord_dofs; ++j) {
+        os << "        const int cv" << j << " = __ldg(&P.cm[" << j << " * (size_t)P.stride + " << cell << "]);\n";
+        for (int c = 0; c < d; ++c)
+            os << "        const double X" << j << "_" << c << " = __ldg(&P.X[(size_t)cv" << j << " * " << d << " + " << c
+               << "]);\n";
+    }
+    for (int c = 0; c < d; ++c)
+        for (int r = 0; r < d; ++r)
+            os << "        const double J" << r << "_" << c << " = X" << c + 1 << "_" << r << " - X0_" << r << ";\n";
+    if (d == 1) os << "        const double det = J0_0;\n";
+    if (d == 2) os << "        const double det = J0_0 * J1_1 - J0_1 * J1_0;\n";
+    if (d == 3)
+        os << "        const double det = J0_0 * (J1_1 * J2_2 - J1_2 * J2_1) - J0_1 * (J1_0 * J2_2 - J1_2 * J2_0) + "
+              "J0_2 * (J1_0 * J2_1 - J1_1 * J2_0);\n";
+    if (uses_inv) {
+        if (d == 1) os << "        const double Ji0_0 = 1.0 / det;\n";
+        if (d == 2)
+            os << "        const double Ji0_0 = J1_1 / det, Ji0_1 = -J0_1 / det, Ji1_0 = -J1_0 / det, Ji1_1 = J0_0 / det;\n";
+        if (d == 3) {
+            os << "        const double Ji0_0 = (J1_1*J2_2 - J1_2*J2_1) / det, Ji0_1 = (J0_2*J2_1 - J0_1*J2_2) / det, "
+                  "Ji0_2 = (J0_1*J1_2 - J0_2*J1_1) / det;\n";
+            os << "        const double Ji1_0 = (J1_2*J2_0 - J1_0*J2_2) / det, Ji1_1 = (J0_0*J2_2 - J0_2*J2_0) / det, "
+                  "Ji1_2 = (J0_2*J1_0 - J0_0*J1_2) / det;\n";
+            os << "        const double Ji2_0 = (J1_0*J2_1 - J1_1*J2_0) / det, Ji2_1 = (J0_1*J2_0 - J0_0*J2_1) / det, "
+                  "Ji2_2 = (J0_0*J1_1 - J0_1*J1_0) / det;\n";
+        }
+    }
+}
+
 std::string KernelPlan::key() const {
     std::ostringstream s;
     s << int(family) << "/" << basis << "/" << block << "/" << tile_cells << "/" << Nc << "x" << Nwi << "/" << TQ << "/"
@@ -412,6 +475,7 @@ std::string KernelPlan::key() const {
 }
 
 EmitResult emit_mlt(const Signature& sig, const KernelPlan& kp);  // below
+EmitResult emit_dmma(const Signature& sig, const KernelPlan& kp);  // below
 
 namespace {
 
@@ -423,7 +487,7 @@ void emit_scpt_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const 
     KernelPlan p = kp;
     p.family = Family::Scpt;
     o.line("");
-    std::string bounds = checked ? "" : "__launch_bounds__(" + S(kp.block) + ") ";
+    std::string bounds = checked ? "" : "__launch_bounds__(" + S(kp.block) + (kp.min_blocks > 1 ? ", " + S(kp.min_blocks) : "") + ") ";
     o.line("extern \"C\" __global__ void " + bounds + name + "(const __grid_constant__ Params P) {");
     o.ind++;
     o.line(std::string("constexpr bool CHECKED = ") + (checked ? "true" : "false") + ";");
@@ -808,6 +872,7 @@ __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_all;
 
 EmitResult emit_kernel(const Signature& sig, const KernelPlan& kp) {
     if (kp.family == Family::Mlt) return emit_mlt(sig, kp);
+    if (kp.family == Family::Dmma) return emit_dmma(sig, kp);
     const MapUse use = analyse(sig);
     EmitResult r;
     Out o;
@@ -1089,5 +1154,34 @@ EmitResult emit_mlt(const Signature& sig, const KernelPlan& kp) {
 }
 
 size_t tile_smem_bytes(const Signature& sig, const KernelPlan& kp) { return static_cast<size_t>(plan_tile(sig, kp).total); }
+
+
+void emit_dmma_kernel(std::ostringstream& o, const Signature& sig, const KernelPlan& kp, DmmaLayout& L,
+                      const std::string& name);
+
+EmitResult emit_dmma(const Signature& sig, const KernelPlan& kp) {
+    const MapUse use = analyse(sig);
+    EmitResult r;
+    Out o;
+    o << kPrelude;
+    o << "#define DMMA(d, a, b) asm(\"mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\" : "
+         "\"+d\"((d)[0]), \"+d\"((d)[1]) : \"d\"(a), \"d\"(b))\n";
+    emit_params(o, sig, kp, 0);
+    DmmaLayout L = dmma_layout(sig, kp);
+    r.kernel = "femgpu_dmma";
+    r.kernel_checked = "femgpu_dmma_checked";
+    emit_dmma_kernel(o.s, sig, kp, L, r.kernel);
+    r.smem_bytes = static_cast<size_t>(L.smem_doubles * 8);
+    long long fmas = 0;
+    for (int i = 0; i < sig.ns(); ++i) fmas += static_cast<long long>(sig.sterms[i]) * sig.sdofs[i];
+    for (int i = 0; i < sig.nv(); ++i) fmas += static_cast<long long>(sig.vterms[i]) * sig.vdofs[i];
+    fmas += static_cast<long long>(sig.nW) * sig.Tw;
+    KernelPlan ck = kp;
+    ck.basis = kBasisGlobal;
+    ck.min_blocks = 1;
+    emit_scpt_kernel(o, sig, ck, use, fmas * sig.Q <= 6000, true, r.kernel_checked, 0);
+    r.source = o.s.str();
+    return r;
+}
 
 }  // namespace femgpu

@@ -56,7 +56,11 @@ struct Signature {
 Signature signature_from(const femgpu_problem* p);
 
 // Kernel families.
-enum class Family { Scpt, Tile, Mlt, Macro };
+enum class Family { Scpt, Tile, Mlt, Macro, Dmma };
+
+// Internal basis residency used by the checked twin of the DMMA family (tabulations read
+// from global memory; they may exceed shared memory).
+constexpr int kBasisGlobal = 3;
 
 // Fully resolved launch plan (what the emitter specialises on).
 struct KernelPlan {
@@ -79,6 +83,29 @@ struct KernelPlan {
     std::vector<std::vector<int>> mpat;   // per map group: G*entries local indices
     std::string key() const;
 };
+
+// DMMA family (emit_dmma.cpp): evaluation groups = (space, component) with their terms.
+struct DmmaGroup {
+    bool vec = false;
+    int space = 0, comp = 0, n = 0;
+    std::vector<int> terms;
+    int KS = 0, MB = 0;          // k-steps (n/4), m-blocks (terms*TQ/8)
+    long long foff = 0;          // first fragment within a q tile
+    long long offU = 0, offS = 0;  // shared-memory offsets (doubles)
+};
+struct DmmaLayout {
+    int NC = 0, TQ = 0, NQT = 0;
+    long long LDU = 0, LDS = 0;  // row strides (doubles): B-operand tiles / accumulator tiles
+    std::vector<DmmaGroup> groups;
+    int KSq = 0, MBq = 0;
+    long long foff_q = 0, FPT = 0;  // quadrature fragments; fragments per q tile
+    long long off_A = 0, off_E = 0, off_H = 0, smem_doubles = 0;
+    int nH_cap = 0;
+};
+DmmaLayout dmma_layout(const Signature& sig, const KernelPlan& kp);
+std::vector<double> dmma_fragments(const Signature& sig, const DmmaLayout& L, const std::vector<double>& tab);
+size_t dmma_smem_bytes(const Signature& sig, const KernelPlan& kp);
+void resolve_dmma(const Signature& sig, KernelPlan& kp, const femgpu_schedule* s);
 
 struct EmitResult {
     std::string source;
@@ -162,6 +189,8 @@ struct Instance {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     std::map<int, std::unique_ptr<TileLayout>> tiles;   // by tile size
     std::map<int, std::unique_ptr<MacroLayout>> macros; // by cells per group
+    std::map<int, double*> dmma_frags;                   // by quad tile: fragment-major Phi/Psi
+    double* dmma_fragments_for(const KernelPlan& kp);
     std::map<std::string, std::shared_ptr<Module>> modules;  // by KernelPlan::key(): no re-emit per launch
     std::shared_ptr<Module> module_for(const KernelPlan& kp);
     std::vector<void*> allocations;

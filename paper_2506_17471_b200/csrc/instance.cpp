@@ -430,6 +430,62 @@ const TileLayout& Instance::tile_layout(int tc) {
     return ref;
 }
 
+double* Instance::dmma_fragments_for(const KernelPlan& kp) {
+    auto it = dmma_frags.find(kp.TQ);
+    if (it != dmma_frags.end()) return it->second;
+    const DmmaLayout L = dmma_layout(sig, kp);
+    const std::vector<double> fr = dmma_fragments(sig, L, tab);
+    double* d = alloc<double>(fr.size());
+    FG_CUDA(cudaMemcpy(d, fr.data(), fr.size() * sizeof(double), cudaMemcpyHostToDevice));
+    dmma_frags[kp.TQ] = d;
+    return d;
+}
+
+// DMMA family schedule (FEMGPU_DMMA): defaults and feasibility.
+void resolve_dmma(const Signature& sig, KernelPlan& kp, const femgpu_schedule* s) {
+    kp.family = Family::Dmma;
+    kp.Nc = s->cells_per_group > 0 ? s->cells_per_group : 32;
+    if (kp.Nc % 8) fail(FEMGPU_E_INFEASIBLE, "dmma: cells per tile must be a multiple of 8");
+    const int lanes = s->lanes_per_cell > 0 ? s->lanes_per_cell : std::max(1, 256 / kp.Nc);
+    kp.Nwi = lanes;
+    kp.block = kp.Nc * lanes;
+    if (kp.block % 32 || kp.block > 1024)
+        fail(FEMGPU_E_INFEASIBLE, "dmma: threads per CTA (cells x lanes) must be a multiple of 32 and <= 1024");
+    kp.Ter = s->eval_row_tile > 0 ? s->eval_row_tile : 2;
+    kp.Tqr = s->quad_row_tile > 0 ? s->quad_row_tile : std::min(2, kp.Nc / 8);
+    kp.min_blocks = s->reserved[2] > 0 ? s->reserved[2] : 1;
+    const long long smem_cap = 227 * 1024;
+    auto fits = [&](int TQ, int basis) {
+        KernelPlan t = kp;
+        t.TQ = TQ;
+        t.basis = basis;
+        return dmma_smem_bytes(sig, t) <= static_cast<size_t>(smem_cap);
+    };
+    int basis = s->basis == FEMGPU_BASIS_SMEM ? FEMGPU_BASIS_SMEM : kBasisGlobal;
+    if (s->quad_tile > 0) {
+        kp.TQ = std::min(s->quad_tile, sig.Q);
+    } else {
+        // largest quadrature tile whose per-CTA footprint leaves room for two CTAs per SM
+        kp.TQ = sig.Q;
+        while (kp.TQ > 1) {
+            KernelPlan t = kp;
+            t.basis = basis;
+            if (dmma_smem_bytes(sig, t) <= 100 * 1024) break;
+            kp.TQ = (kp.TQ + 1) / 2;
+        }
+    }
+    if (s->basis == FEMGPU_BASIS_AUTO) {
+        KernelPlan t = kp;
+        t.basis = FEMGPU_BASIS_SMEM;
+        const DmmaLayout L = dmma_layout(sig, t);
+        if (L.NQT * L.FPT * 256 <= 48 * 1024 && dmma_smem_bytes(sig, t) <= 110 * 1024) basis = FEMGPU_BASIS_SMEM;
+    }
+    kp.basis = basis;
+    if (!fits(kp.TQ, kp.basis))
+        fail(FEMGPU_E_INFEASIBLE, "dmma: " + std::to_string(dmma_smem_bytes(sig, kp)) +
+                                      " bytes of shared memory per CTA exceed the 227 KB sm_100a limit");
+}
+
 const MacroLayout& Instance::macro_layout(int G) {
     auto it = macros.find(G);
     if (it != macros.end()) return *it->second;
@@ -570,7 +626,7 @@ constexpr long long kParamTabLimit = 3800;  // doubles in the 32 KB kernel-param
 // Auto basis residency: the parameter (constant) bank is only chosen while the tabulations fit
 // the SM's constant cache comfortably; beyond that every LDCU risks a miss (C4: 11.5 KB of
 // tabulations ran 3x slower from the constant bank than from shared memory).
-constexpr long long kConstCacheDoubles = 512;  // 4 KB
+constexpr long long kConstCacheDoubles = 1024;  // 8 KB (measured: adv P2, 5.9 KB, 2x faster from the constant bank than from smem)
 
 int int_dim(int a) { return a; }
 
@@ -609,6 +665,10 @@ KernelPlan resolve_schedule(Instance& I, const femgpu_schedule* s) {
                                           " work-items exceeds the device limit of 1024");
         kp.block = kp.Nc * kp.Nwi;
         kp.basis = FEMGPU_BASIS_SMEM;
+        return kp;
+    }
+    if (s->kind == FEMGPU_DMMA) {
+        resolve_dmma(sig, kp, s);
         return kp;
     }
     // SCPT: one thread per cell.
@@ -704,6 +764,7 @@ KernelPlan resolve_schedule(Instance& I, const femgpu_schedule* s) {
     if (smem_tab > 227 * 1024)
         fail(FEMGPU_E_INFEASIBLE, "basis: tabulations exceed the shared-memory capacity of one CTA");
     kp.family = Family::Scpt;
+    if (s->reserved[2] > 0) kp.min_blocks = s->reserved[2];
     (void)int_dim;
     return kp;
 }
@@ -741,6 +802,7 @@ ParamBuf build_params(Instance& I, const KernelPlan& kp, double* d_y, const Tile
     P.put(static_cast<void*>(d_y));
     P.put(static_cast<void*>(I.d_bad));
     P.put(static_cast<const void*>(I.d_tab));
+    if (kp.family == Family::Dmma) P.put(static_cast<const void*>(I.dmma_fragments_for(kp)));
     const int ngroups = kp.family == Family::Tile ? static_cast<int>(kp.group_entries.size()) : 0;
     const MacroLayout* M = kp.family == Family::Macro ? &I.macro_layout(kp.G) : nullptr;
     if (M)
@@ -794,6 +856,9 @@ void run_action(Instance& I, const KernelPlan& kp, double* d_y, cudaStream_t str
         grid = std::min<long long>(L->n_tiles, static_cast<long long>(mod->sms) * std::max(1, mod->occupancy));
     else if (kp.family == Family::Macro)
         grid = (I.macro_layout(kp.G).n_groups + kp.block - 1) / kp.block;
+    else if (kp.family == Family::Dmma)
+        grid = std::min<long long>((static_cast<long long>(I.cells) + kp.Nc - 1) / kp.Nc,
+                                   static_cast<long long>(mod->sms) * std::max(1, mod->occupancy));
     else
         grid = (static_cast<long long>(I.cells) + kp.block - 1) / kp.block;
     if (grid > INT_MAX) fail(FEMGPU_E_INFEASIBLE, "launch: grid too large");
