@@ -119,11 +119,12 @@ typedef struct femgpu_problem {
 typedef enum femgpu_schedule_kind {
     FEMGPU_SCPT = 0, /* TilingParams::scpt(): one thread per cell */
     FEMGPU_MLT = 1,  /* multi-level tiling: N_c cells x N_WI lanes per CTA */
-    FEMGPU_DMMA = 2  /* B200 extension: cell-batched FP64 tensor-core (DMMA) contraction.
-                        cells_per_group = N_c cells per tile (multiple of 8), quad_tile = T^Q,
-                        lanes_per_cell = threads per cell (CTA = N_c * lanes_per_cell threads),
-                        eval_row_tile = m-blocks and quad_row_tile = n-blocks of 8 per warp task,
-                        basis SMEM = Phi/Psi fragments resident in shared memory (else L1/L2);
+    FEMGPU_DMMA = 2  /* B200 extension: warp-level FP64 tensor-core (DMMA m8n8k4) pipeline.
+                        cells_per_group = cells per warp task (8, 16, 24, 32), quad_tile = T^Q
+                        quadrature points per chunk (rounded up to a multiple of 4),
+                        lanes_per_cell = 4 (fixed by the fragment layout; 0 accepted),
+                        block_cells = threads per CTA, basis SMEM = Phi/Psi fragments staged in
+                        shared memory once per CTA (else read through L1);
                         0 = automatic for every field */
 } femgpu_schedule_kind;
 

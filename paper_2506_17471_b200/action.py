@@ -54,9 +54,10 @@ class TilingParams:
 
     @staticmethod
     def dmma(**knobs) -> "TilingParams":
-        """FEMGPU_DMMA: cell-batched FP64 tensor-core contraction (0 = automatic for every field):
-        cells_per_group = cells per tile, quad_tile = T^Q, lanes_per_cell = threads per cell,
-        eval_row_tile / quad_row_tile = m-blocks / n-blocks of 8 per warp task."""
+        """FEMGPU_DMMA: warp-level FP64 tensor-core pipeline (0 = automatic for every field):
+        cells_per_group = cells per warp task (8..32, m-blocks of 8), quad_tile = T^Q quadrature
+        points per chunk (rounded up to 4: one per lane-group), lanes_per_cell = 4 (fixed by the
+        m8n8k4 layout), block_cells = threads per CTA, basis SMEM = fragments staged per CTA."""
         d = dict(kind=abi.DMMA, quad_tile=0, eval_row_tile=0, quad_row_tile=0, quad_col_tile=0,
                  cells_per_group=0, lanes_per_cell=0)
         d.update(knobs)

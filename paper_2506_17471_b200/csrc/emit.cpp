@@ -1164,14 +1164,14 @@ EmitResult emit_dmma(const Signature& sig, const KernelPlan& kp) {
     EmitResult r;
     Out o;
     o << kPrelude;
-    o << "#define DMMA(d, a, b) asm(\"mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\" : "
-         "\"+d\"((d)[0]), \"+d\"((d)[1]) : \"d\"(a), \"d\"(b))\n";
+    o << "#define DMMA(d0, d1, a, b) asm(\"mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\" : "
+         "\"+d\"(d0), \"+d\"(d1) : \"d\"(a), \"d\"(b))\n";
     emit_params(o, sig, kp, 0);
     DmmaLayout L = dmma_layout(sig, kp);
     r.kernel = "femgpu_dmma";
     r.kernel_checked = "femgpu_dmma_checked";
     emit_dmma_kernel(o.s, sig, kp, L, r.kernel);
-    r.smem_bytes = static_cast<size_t>(L.smem_doubles * 8);
+    r.smem_bytes = dmma_smem_bytes(sig, kp);
     long long fmas = 0;
     for (int i = 0; i < sig.ns(); ++i) fmas += static_cast<long long>(sig.sterms[i]) * sig.sdofs[i];
     for (int i = 0; i < sig.nv(); ++i) fmas += static_cast<long long>(sig.vterms[i]) * sig.vdofs[i];

@@ -1,31 +1,35 @@
-// emit_dmma.cpp — the cell-batched FP64 tensor-core family (femgpu_dmma).
+// emit_dmma.cpp — the warp-level FP64 tensor-core family (femgpu_dmma).
 //
 // The reference's action (reference_action, form.hpp:497-593) contracts, per cell,
 //   evaluation   s_t(q)   = sum_j  Phi_t(q, j) u_j            (form.hpp:526-555)
 //   quadrature   y_jw    += sum_k  Psi_k(jw, q) e_k(q)        (form.hpp:575-585)
-// Over a tile of N_c cells both are small dense GEMMs with the cells as the N
-// dimension: S[(t,q)][c] = Phi[(t,q)][j] * U[j][c] and Y[jw][c] = Psi[jw][(k,q)] * E[(k,q)][c].
-// sm_100a has no FP64 kind of tcgen05 (ptxas rejects .kind::f64); its FP64 tensor
-// path is DMMA (mma.sync m8n8k4 .f64), which this family drives directly:
+// Over 8 cells both are small dense GEMMs with the cells as the M dimension:
+//   S^T[c][(t,q)] = U^T[c][j] . Phi^T[j][(t,q)]      Y^T[c][jw] = E^T[c][(k,q)] . Psi^T[(k,q)][jw]
+// sm_100a has no FP64 kind of tcgen05 (ptxas rejects .kind::f64); its FP64 tensor path is
+// DMMA (mma.sync m8n8k4 .f64).  This family keeps the whole per-cell pipeline of one warp in
+// registers, with no block-level synchronisation after the one-time fragment staging:
 //
-//   per tile of N_c cells (persistent CTAs; N_c multiple of 8):
-//     gather   U_g[k][c] (zero-padded to a multiple of 4 rows) for every evaluation
-//              group g = (space, component); per-cell geometry (affine J, det) and the
-//              cell-invariant map nodes into H[h][c]
-//     per quadrature tile of T^Q points (the paper's quad_tile, qoi.hpp:26):
-//       eval   warp tasks of R m-blocks x S n-blocks: DMMA over the k-steps, A operand
-//              = Phi fragments (fragment-major, prepared at create), B = U_g -> S_g
-//       map    one thread per (cell, quadrature point): the pointwise DAG (straight-line
-//              SSA, as in the other families) reads S and H, writes E
-//       quad   DMMA, A = Psi fragments, B = E; the accumulators Y stay in registers
-//              across the quadrature tiles
-//     scatter  red.global.add.f64 straight from the accumulator fragments
+//   warp task = CW cells (MB m-blocks of 8; persistent warps, grid-stride over tasks)
+//     geometry  lane l computes cell l's affine J / det and the cell-invariant map nodes once
+//               (no 4x lane redundancy) into a warp-private shared-memory row
+//     per m-block of 8 cells (lane = 4*r + g: cell r, lane-group g):
+//       gather  A fragments a[ks] = u[cell r][j = 4 ks + g] straight from global memory
+//       per quadrature chunk of T^Q = 4*TQL points (lane-group g owns q = chunk*T^Q + 4 s + g):
+//         eval  DMMA, B = Phi^T fragments (fragment-major, built at create) -> D[r][2g+i]:
+//               lane-group g's output slots are exactly (term, s) of its own quadrature points,
+//               so the pointwise map runs on the DMMA accumulators in place
+//         map   the pointwise DAG (straight-line SSA, as in the other families) per (cell, q)
+//         quad  DMMA with A = E^T built from the map outputs without any shuffle: k-step
+//               kappa = (k, s) takes column g from lane-group g (the K order of Psi^T is
+//               permuted at create to match, the FA2 register-reuse trick for m8n8k4)
+//       scatter red.global.add.f64 straight from the Y^T accumulator fragments
 //
-// Fragment layouts (PTX ISA, mma.m8n8k4 .f64): A a0 = A[lane>>2][lane&3];
-// B b0 = B[lane&3][lane>>2]; C/D {c0,c1} = C[lane>>2][2*(lane&3) + {0,1}].
-// Columns are independent in every GEMM, so a non-finite input of one cell only
-// reaches that cell's outputs, which the scatter flags (lowest cell, like the
-// reference's first failing cell; the stage is named by the checked twin kernel).
+// Fragment layouts (PTX ISA, mma.m8n8k4 .f64, row.col): a0 = A[lane>>2][lane&3];
+// b0 = B[lane&3][lane>>2]; {c0,c1} = C[lane>>2][2*(lane&3) + {0,1}].
+// Rows (cells) are independent in every GEMM and padded K entries are zero in both operands,
+// so a non-finite input of one cell only reaches that cell's outputs; the lane flags the lowest
+// failing cell (like the reference's first failing cell) and the stage-checked twin names the
+// stage.
 #include <algorithm>
 #include <set>
 #include <sstream>
@@ -36,22 +40,15 @@ namespace femgpu {
 
 namespace {
 std::string S(long long v) { return std::to_string(v); }
-// smallest ld >= n with ld % 16 == r (doubles): conflict-free fragment loads/stores
-long long ld_mod(long long n, long long r) {
-    long long ld = n;
-    while (ld % 16 != r) ++ld;
-    return ld;
-}
 }  // namespace
 
 DmmaLayout dmma_layout(const Signature& sig, const KernelPlan& kp) {
     DmmaLayout L;
-    L.NC = kp.Nc;
+    L.CW = kp.Nc;
+    L.MB = kp.Nc / 8;
     L.TQ = kp.TQ;
-    L.NQT = (sig.Q + kp.TQ - 1) / kp.TQ;
-    L.LDU = ld_mod(L.NC, 4);
-    if (L.LDU - L.NC > 8) L.LDU = ld_mod(L.NC, 12);
-    L.LDS = ld_mod(L.NC, 8);
+    L.TQL = kp.TQ / 4;
+    L.NCH = (sig.Q + kp.TQ - 1) / kp.TQ;
     for (int i = 0; i < sig.ns(); ++i) {
         DmmaGroup g;
         g.vec = false;
@@ -77,66 +74,49 @@ DmmaLayout dmma_layout(const Signature& sig, const KernelPlan& kp) {
     long long f = 0;
     for (auto& g : L.groups) {
         g.KS = (g.n + 3) / 4;
-        g.MB = (static_cast<int>(g.terms.size()) * L.TQ + 7) / 8;
+        g.NB = (static_cast<int>(g.terms.size()) * L.TQL + 1) / 2;
         g.foff = f;
-        f += static_cast<long long>(g.MB) * g.KS;
+        f += static_cast<long long>(g.NB) * g.KS;
     }
-    L.KSq = (sig.Tw * L.TQ + 3) / 4;
-    L.MBq = (sig.nW + 7) / 8;
+    L.KQ = sig.Tw * L.TQL;
+    L.NBQ = (sig.nW + 7) / 8;
     L.foff_q = f;
-    f += static_cast<long long>(L.MBq) * L.KSq;
-    L.FPT = f;
-    // shared-memory plan (doubles)
-    long long off = 0;
-    if (kp.basis == FEMGPU_BASIS_SMEM) {
-        L.off_A = off;
-        off += L.NQT * L.FPT * 32;
-    }
-    for (auto& g : L.groups) {
-        g.offU = off;
-        off += static_cast<long long>(g.KS) * 4 * L.LDU;
-    }
-    for (auto& g : L.groups) {
-        g.offS = off;
-        off += static_cast<long long>(g.MB) * 8 * L.LDS;
-    }
-    L.off_E = off;
-    off += static_cast<long long>(L.KSq) * 4 * L.LDU;
-    L.off_H = off;
-    L.nH_cap = 0;
-    L.smem_doubles = off;  // + H rows (set by the emitter once the hoisted set is known)
+    f += static_cast<long long>(L.NBQ) * L.KQ;
+    L.FPC = f;
+    L.nfrag = L.FPC * L.NCH;
     return L;
 }
 
-// Fragment-major A operands: [q tile][group (m-block, k-step)..., quad (m-block, k-step)][lane].
+// Fragment-major B operands: [chunk][group (n-block, k-step)..., quad (n-block, k-step)][lane].
 std::vector<double> dmma_fragments(const Signature& sig, const DmmaLayout& L, const std::vector<double>& tab) {
-    std::vector<double> fr(static_cast<size_t>(L.NQT * L.FPT * 32), 0.0);
-    const int Q = sig.Q;
-    for (int qt = 0; qt < L.NQT; ++qt) {
-        const int q0 = qt * L.TQ;
-        double* base = fr.data() + static_cast<size_t>(qt) * L.FPT * 32;
+    std::vector<double> fr(static_cast<size_t>(L.nfrag * 32), 0.0);
+    const int Q = sig.Q, TQL = L.TQL;
+    for (int ch = 0; ch < L.NCH; ++ch) {
+        double* base = fr.data() + static_cast<size_t>(ch) * L.FPC * 32;
         for (const auto& g : L.groups) {
             const long long phi = g.vec ? sig.phi_off_v[g.space] : sig.phi_off_s[g.space];
-            for (int mb = 0; mb < g.MB; ++mb)
+            const int T = static_cast<int>(g.terms.size());
+            for (int nb = 0; nb < g.NB; ++nb)
                 for (int ks = 0; ks < g.KS; ++ks)
                     for (int lane = 0; lane < 32; ++lane) {
-                        const int r = mb * 8 + (lane >> 2), k = ks * 4 + (lane & 3);
-                        const int tt = r / L.TQ, ql = r % L.TQ, q = q0 + ql;
+                        // b0 = B[k = lane&3][n = lane>>2]; column n = 2*g' + i -> slot 2*nb + i of lane-group g'
+                        const int j = ks * 4 + (lane & 3), n = lane >> 2, gq = n >> 1, slot = 2 * nb + (n & 1);
+                        const int ti = slot / TQL, s = slot % TQL, q = ch * L.TQ + 4 * s + gq;
                         double v = 0.0;
-                        if (tt < static_cast<int>(g.terms.size()) && q < Q && k < g.n)
-                            v = tab[phi + static_cast<long long>(g.terms[tt]) * Q * g.n + static_cast<long long>(q) * g.n + k];
-                        base[((g.foff + static_cast<long long>(mb) * g.KS + ks) * 32) + lane] = v;
+                        if (ti < T && q < Q && j < g.n)
+                            v = tab[phi + static_cast<long long>(g.terms[ti]) * Q * g.n + static_cast<long long>(q) * g.n + j];
+                        base[(g.foff + static_cast<long long>(nb) * g.KS + ks) * 32 + lane] = v;
                     }
         }
-        for (int mb = 0; mb < L.MBq; ++mb)
-            for (int ks = 0; ks < L.KSq; ++ks)
+        for (int nb = 0; nb < L.NBQ; ++nb)
+            for (int kq = 0; kq < L.KQ; ++kq)
                 for (int lane = 0; lane < 32; ++lane) {
-                    const int jw = mb * 8 + (lane >> 2), kk = ks * 4 + (lane & 3);
-                    const int k = kk / L.TQ, ql = kk % L.TQ, q = q0 + ql;
+                    // b0 = B[kk = lane&3][jw = lane>>2]; k-step kq = (k, s), row kk taken from lane-group kk
+                    const int k = kq / TQL, s = kq % TQL, jw = nb * 8 + (lane >> 2), q = ch * L.TQ + 4 * s + (lane & 3);
                     double v = 0.0;
-                    if (jw < sig.nW && k < sig.Tw && q < Q)
+                    if (jw < sig.nW && q < Q)
                         v = tab[sig.psi_off + (static_cast<long long>(k) * sig.nW + jw) * Q + q];
-                    base[((L.foff_q + static_cast<long long>(mb) * L.KSq + ks) * 32) + lane] = v;
+                    base[(L.foff_q + static_cast<long long>(nb) * L.KQ + kq) * 32 + lane] = v;
                 }
     }
     return fr;
@@ -146,7 +126,7 @@ namespace {
 
 // Cell-invariant map nodes the quadrature-point part reads (constants are re-emitted).
 struct Hoist {
-    std::vector<int> stored;  // node ids kept in H rows
+    std::vector<int> stored;  // node ids kept in the warp's shared-memory rows
     std::vector<int> consts;  // constant node ids re-emitted in the map phase
 };
 
@@ -181,226 +161,204 @@ void emit_map_nodes(std::ostringstream& o, const Signature& sig, const std::vect
                     const std::vector<char>& qdep, bool qdep_pass, const std::string& weight_expr);
 void emit_geometry(std::ostringstream& o, const Signature& sig, bool uses_inv, const std::string& cell);
 
-size_t dmma_smem_bytes(const Signature& sig, const KernelPlan& kp) {
-    DmmaLayout L = dmma_layout(sig, kp);
+namespace {
+struct Smem {
+    long long off_A = 0, off_H = 0, total = 0;  // doubles
+    int nH = 0;
+};
+Smem dmma_smem(const Signature& sig, const KernelPlan& kp, const DmmaLayout& L) {
+    Smem s;
     const Hoist H = hoisted(sig, map_live(sig), map_qdep(sig));
-    return static_cast<size_t>((L.off_H + static_cast<long long>(H.stored.size()) * L.LDS) * 8);
+    s.nH = static_cast<int>(H.stored.size());
+    long long off = 0;
+    if (kp.basis == FEMGPU_BASIS_SMEM) off += L.nfrag * 32;
+    s.off_H = off;
+    off += static_cast<long long>(kp.block / 32) * s.nH * L.CW;
+    s.total = off;
+    return s;
+}
+}  // namespace
+
+size_t dmma_smem_bytes(const Signature& sig, const KernelPlan& kp) {
+    const DmmaLayout L = dmma_layout(sig, kp);
+    return static_cast<size_t>(dmma_smem(sig, kp, L).total * 8);
+}
+
+// Live doubles per lane of one m-block (register-pressure estimate used by the auto schedule).
+long long dmma_live_doubles(const Signature& sig, const DmmaLayout& L) {
+    long long a = 0, s = 0;
+    for (const auto& g : L.groups) {
+        a += g.KS;
+        s += 2LL * g.NB;
+    }
+    return a + s + static_cast<long long>(sig.Tw) * L.TQL + 2LL * L.NBQ;
 }
 
 void emit_dmma_kernel(std::ostringstream& o, const Signature& sig, const KernelPlan& kp, DmmaLayout& L,
                       const std::string& name) {
     const std::vector<char> live = map_live(sig), qdep = map_qdep(sig);
     const Hoist H = hoisted(sig, live, qdep);
-    L.nH_cap = static_cast<int>(H.stored.size());
-    L.smem_doubles = L.off_H + static_cast<long long>(L.nH_cap) * L.LDS;
-    const int NC = L.NC, TQ = L.TQ, NT = kp.block, NW = NT / 32, R = kp.Ter, SB = kp.Tqr;
-    const int NB = NC / 8;
-    const int NBS = (NB + SB - 1) / SB;
+    const Smem SM = dmma_smem(sig, kp, L);
+    const int NT = kp.block, NW = NT / 32, CW = L.CW, MB = L.MB, TQL = L.TQL, nH = SM.nH;
     const bool smemA = kp.basis == FEMGPU_BASIS_SMEM;
     bool uses_inv = false;
     for (size_t id = 0; id < sig.nodes.size(); ++id)
         if (live[id] && sig.nodes[id].op == FEMGPU_OP_INV_JACOBIAN) uses_inv = true;
+    // which derivative variables the map reads (the rest are still checked for finiteness)
+    std::set<std::pair<int, int>> sd_used, vd_used;
+    for (size_t id = 0; id < sig.nodes.size(); ++id) {
+        if (!live[id]) continue;
+        if (sig.nodes[id].op == FEMGPU_OP_SCALAR_DERIV) sd_used.insert({sig.nodes[id].a, sig.nodes[id].b});
+        if (sig.nodes[id].op == FEMGPU_OP_VECTOR_DERIV) vd_used.insert({sig.nodes[id].a, sig.nodes[id].b});
+    }
 
     o << "\nextern \"C\" __global__ void __launch_bounds__(" << NT << (kp.min_blocks > 1 ? ", " + S(kp.min_blocks) : "")
       << ") " << name << "(const __grid_constant__ Params P) {\n";
     o << "  extern __shared__ __align__(16) double sm[];\n";
-    o << "  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5; (void)warp;\n";
+    o << "  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;\n";
+    o << "  const int r = lane >> 2, g = lane & 3;\n";
     o << "  const size_t STR = (size_t)P.stride;\n";
     if (smemA) {
-        o << "  double* const sA = sm + " << L.off_A << ";\n";
-        o << "  for (int i = tid; i < " << (L.NQT * L.FPT * 16) << "; i += " << NT
-          << ") reinterpret_cast<double2*>(sA)[i] = __ldg(reinterpret_cast<const double2*>(P.afr) + i);\n";
+        o << "  for (int i = tid; i < " << L.nfrag * 16 << "; i += " << NT
+          << ") reinterpret_cast<double2*>(sm)[i] = __ldg(reinterpret_cast<const double2*>(P.afr) + i);\n";
+        o << "  __syncthreads();\n";
+        o << "  const double* const FR = sm + lane;\n";
+    } else {
+        o << "  const double* const FR = P.afr + lane;\n";
     }
-    o << "  double* const sE = sm + " << L.off_E << ";\n";
-    o << "  double* const sH = sm + " << L.off_H << "; (void)sH;\n";
-    // E rows past Tw*TQ are K padding: zero once (never written afterwards)
-    const long long erows = static_cast<long long>(sig.Tw) * TQ;
-    if (L.KSq * 4 > erows)
-        o << "  for (int i = tid; i < " << (L.KSq * 4 - erows) * L.LDU << "; i += " << NT << ") sE[" << erows * L.LDU
-          << " + i] = 0.0;\n";
-    o << "  __syncthreads();\n";
-    o << "  const int n_tiles = (P.n_cells + " << NC - 1 << ") / " << NC << ";\n";
+    o << "  double* const sH = sm + " << SM.off_H << " + warp * " << static_cast<long long>(nH) * CW << "; (void)sH;\n";
+    o << "  const int n_tasks = (P.n_cells + " << CW - 1 << ") / " << CW << ";\n";
+    o << "  unsigned long long badc = ~0ULL;\n";
     o << "  #pragma unroll 1\n";
-    o << "  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {\n";
-    o << "    const int c0 = tile * " << NC << ";\n";
-    // ---- gather: one index per (space, entry, cell); all component groups of the space
-    std::vector<std::vector<int>> by_space_s(sig.ns()), by_space_v(sig.nv());
-    for (size_t gi = 0; gi < L.groups.size(); ++gi)
-        (L.groups[gi].vec ? by_space_v[L.groups[gi].space] : by_space_s[L.groups[gi].space]).push_back(static_cast<int>(gi));
-    auto gather_space = [&](bool vec, int i, const std::vector<int>& gids) {
-        const DmmaGroup& g0 = L.groups[gids[0]];
-        const long long rows = static_cast<long long>(g0.KS) * 4;
-        o << "    for (int e = tid; e < " << rows * NC << "; e += " << NT << ") {\n";
-        o << "      const int k = e / " << NC << ", c = e % " << NC << ", cell = c0 + c;\n";
-        o << "      const bool ok = k < " << g0.n << " && cell < P.n_cells;\n";
-        o << "      const int idx = ok ? __ldg(&P." << (vec ? "vm" : "m") << i << "[k * STR + cell]) : 0;\n";
-        for (int gid : gids) {
-            const DmmaGroup& g = L.groups[gid];
-            if (vec)
-                o << "      sm[" << g.offU << " + k * " << L.LDU << " + c] = ok ? __ldg(&P.v" << i << "[(size_t)idx * "
-                  << sig.dim << " + " << g.comp << "]) : 0.0;\n";
-            else
-                o << "      sm[" << g.offU << " + k * " << L.LDU << " + c] = ok ? __ldg(&P.x" << i << "[idx]) : 0.0;\n";
-        }
-        o << "    }\n";
-    };
-    for (int i = 0; i < sig.ns(); ++i) gather_space(false, i, by_space_s[i]);
-    for (int i = 0; i < sig.nv(); ++i) gather_space(true, i, by_space_v[i]);
-    // ---- geometry + cell-invariant map nodes
-    if (sig.affine || !H.stored.empty()) {
-        o << "    for (int c = tid; c < " << NC << "; c += " << NT << ") {\n";
-        o << "      const int cell = c0 + c;\n";
-        o << "      if (cell < P.n_cells) {\n";
+    o << "  for (int task = blockIdx.x * " << NW << " + warp; task < n_tasks; task += gridDim.x * " << NW << ") {\n";
+    o << "    const int c0 = task * " << CW << ";\n";
+    // ---- geometry + cell-invariant nodes, one lane per cell
+    if (sig.affine || nH > 0) {
+        o << "    if (lane < " << CW << ") {\n";
+        o << "      const bool cok = c0 + lane < P.n_cells;\n";
+        o << "      const int cell = cok ? c0 + lane : c0;\n";
         if (sig.affine) {
-            std::ostringstream g;
-            emit_geometry(g, sig, uses_inv, "cell");
-            o << g.str();
-            o << "        if (NF(det)) atomicMin(P.bad, (unsigned long long)cell);\n";
+            std::ostringstream gm;
+            emit_geometry(gm, sig, uses_inv, "cell");
+            o << gm.str();
+            o << "      if (cok && NF(det)) badc = min(badc, (unsigned long long)cell);\n";
         }
         {
             std::ostringstream m;
             emit_map_nodes(m, sig, live, qdep, false, "0.0");
             o << m.str();
         }
-        for (size_t h = 0; h < H.stored.size(); ++h)
-            o << "        sH[" << h * L.LDS << " + c] = n" << H.stored[h] << ";\n";
-        o << "      } else {\n";
-        for (size_t h = 0; h < H.stored.size(); ++h) o << "        sH[" << h * L.LDS << " + c] = 0.0;\n";
-        o << "      }\n";
+        for (int h = 0; h < nH; ++h) o << "      sH[" << static_cast<long long>(h) * CW << " + lane] = n" << H.stored[h] << ";\n";
         o << "    }\n";
+        o << "    __syncwarp();\n";
     }
-    o << "    __syncthreads();\n";
-    // ---- quadrature-tile loop
-    const int TPWq = static_cast<int>((static_cast<long long>((L.MBq + R - 1) / R) * NBS + NW - 1) / NW);
-    o << "    double yacc[" << TPWq << "][" << R << "][" << SB << "][2];\n";
-    o << "    #pragma unroll\n    for (int j = 0; j < " << TPWq << "; ++j)\n      #pragma unroll\n      for (int r = 0; r < " << R
-      << "; ++r)\n        #pragma unroll\n        for (int s = 0; s < " << SB
-      << "; ++s) { yacc[j][r][s][0] = 0.0; yacc[j][r][s][1] = 0.0; }\n";
     o << "    #pragma unroll 1\n";
-    o << "    for (int qt = 0; qt < " << L.NQT << "; ++qt) {\n";
-    o << "      const double* const Aq = " << (smemA ? "sA" : "P.afr") << " + (size_t)qt * " << L.FPT * 32 << " + lane;\n";
-    // eval tasks
-    long long ntask = 0;
-    std::vector<long long> tstart;
-    for (const auto& g : L.groups) {
-        tstart.push_back(ntask);
-        ntask += static_cast<long long>((g.MB + R - 1) / R) * NBS;
-    }
-    const std::string LDA = smemA ? "" : "__ldg";
-    o << "      for (int t = warp; t < " << ntask << "; t += " << NW << ") {\n";
+    o << "    for (int mb = 0; mb < " << MB << "; ++mb) {\n";
+    o << "      const int cr = mb * 8 + r, cell = c0 + cr;\n";
+    o << "      const bool cok = cell < P.n_cells;\n";
+    // ---- gather A fragments (one index per (space, k-step), shared by the component groups)
+    std::vector<std::vector<int>> by_space_s(sig.ns()), by_space_v(sig.nv());
+    for (size_t gi = 0; gi < L.groups.size(); ++gi)
+        (L.groups[gi].vec ? by_space_v[L.groups[gi].space] : by_space_s[L.groups[gi].space]).push_back(static_cast<int>(gi));
+    auto gather_space = [&](bool vec, int i, const std::vector<int>& gids) {
+        const DmmaGroup& g0 = L.groups[gids[0]];
+        for (int ks = 0; ks < g0.KS; ++ks) {
+            const bool partial = (ks + 1) * 4 > g0.n;
+            const std::string ok = partial ? "(cok && " + S(ks * 4) + " + g < " + S(g0.n) + ")" : "cok";
+            const std::string ix = "ix" + S(vec) + "_" + S(i) + "_" + S(ks);
+            o << "      const int " << ix << " = " << ok << " ? __ldg(&P." << (vec ? "vm" : "m") << i << "[(" << ks * 4
+              << " + g) * STR + cell]) : -1;\n";
+            for (int gid : gids) {
+                const DmmaGroup& g = L.groups[gid];
+                o << "      const double uA" << gid << "_" << ks << " = " << ix << " >= 0 ? ";
+                if (vec)
+                    o << "__ldg(&P.v" << i << "[(size_t)" << ix << " * " << sig.dim << " + " << g.comp << "])";
+                else
+                    o << "__ldg(&P.x" << i << "[" << ix << "])";
+                o << " : 0.0;\n";
+            }
+        }
+    };
+    for (int i = 0; i < sig.ns(); ++i) gather_space(false, i, by_space_s[i]);
+    for (int i = 0; i < sig.nv(); ++i) gather_space(true, i, by_space_v[i]);
+    for (int h = 0; h < nH; ++h) o << "      const double hv" << h << " = sH[" << static_cast<long long>(h) * CW << " + cr];\n";
+    for (int nb = 0; nb < L.NBQ; ++nb) o << "      double y" << nb << "_0 = 0.0, y" << nb << "_1 = 0.0;\n";
+    o << "      #pragma unroll 1\n";
+    o << "      for (int ch = 0; ch < " << L.NCH << "; ++ch) {\n";
+    o << "        const double* const Fc = FR + (size_t)ch * " << L.FPC * 32 << ";\n";
+    // ---- evaluation GEMMs
     for (size_t gi = 0; gi < L.groups.size(); ++gi) {
         const DmmaGroup& g = L.groups[gi];
-        const long long t0 = tstart[gi], t1 = t0 + static_cast<long long>((g.MB + R - 1) / R) * NBS;
-        o << "        " << (gi ? "else " : "") << "if (t < " << t1 << ") {\n";
-        o << "          const int tl = t - " << t0 << ", mb0 = (tl / " << NBS << ") * " << R << ", nb0 = (tl % " << NBS
-          << ") * " << SB << ";\n";
-        o << "          double acc[" << R << "][" << SB << "][2] = {};\n";
-        o << "          const double* Ab = Aq + (" << g.foff << " + mb0 * " << g.KS << ") * 32;\n";
-        o << "          const double* Bb = sm + " << g.offU << " + (lane & 3) * " << L.LDU << " + nb0 * 8 + (lane >> 2);\n";
-        o << "          #pragma unroll\n";
-        o << "          for (int ks = 0; ks < " << g.KS << "; ++ks) {\n";
-        o << "            double a[" << R << "], b[" << SB << "];\n";
-        o << "            #pragma unroll\n            for (int r = 0; r < " << R << "; ++r) a[r] = (mb0 + r < " << g.MB
-          << ") ? " << (smemA ? "Ab[(r * " + S(g.KS) + " + ks) * 32]" : "__ldg(&Ab[(r * " + S(g.KS) + " + ks) * 32])")
-          << " : 0.0;\n";
-        o << "            #pragma unroll\n            for (int s = 0; s < " << SB << "; ++s) b[s] = (nb0 + s < " << NB
-          << ") ? Bb[ks * " << 4 * L.LDU << " + s * 8] : 0.0;\n";
-        o << "            #pragma unroll\n            for (int r = 0; r < " << R
-          << "; ++r)\n              #pragma unroll\n              for (int s = 0; s < " << SB
-          << "; ++s) DMMA(acc[r][s], a[r], b[s]);\n";
-        o << "          }\n";
-        o << "          #pragma unroll\n          for (int r = 0; r < " << R << "; ++r)\n";
-        o << "            if (mb0 + r < " << g.MB << ") {\n";
-        o << "              #pragma unroll\n              for (int s = 0; s < " << SB << "; ++s)\n";
-        o << "                if (nb0 + s < " << NB << ") *reinterpret_cast<double2*>(sm + " << g.offS << " + ((mb0 + r) * 8 + (lane >> 2)) * "
-          << L.LDS << " + (nb0 + s) * 8 + 2 * (lane & 3)) = make_double2(acc[r][s][0], acc[r][s][1]);\n";
-        o << "            }\n";
+        for (int nb = 0; nb < g.NB; ++nb) {
+            const std::string d0 = "S" + S(gi) + "_" + S(nb) + "_0", d1 = "S" + S(gi) + "_" + S(nb) + "_1";
+            o << "        double " << d0 << " = 0.0, " << d1 << " = 0.0;\n";
+            for (int ks = 0; ks < g.KS; ++ks)
+                o << "        DMMA(" << d0 << ", " << d1 << ", uA" << gi << "_" << ks << ", Fc["
+                  << (g.foff + static_cast<long long>(nb) * g.KS + ks) * 32 << "]);\n";
+        }
+    }
+    // ---- pointwise map per owned quadrature point
+    for (int s = 0; s < TQL; ++s) {
+        o << "        double E" << s << "_0";
+        for (int k = 1; k < sig.Tw; ++k) o << ", E" << s << "_" << k;
+        o << ";\n";
+        o << "        {\n";
+        o << "          const int q = ch * " << L.TQ << " + " << 4 * s << " + g;\n";
+        o << "          const bool qok = q < " << sig.Q << ";\n";
+        o << "          const double wq = qok ? __ldg(&P.tabg[" << sig.w_off << " + q]) : 0.0;\n";
+        std::string nf = "false";
+        for (size_t gi = 0; gi < L.groups.size(); ++gi) {
+            const DmmaGroup& g = L.groups[gi];
+            for (size_t ti = 0; ti < g.terms.size(); ++ti) {
+                const int slot = static_cast<int>(ti) * TQL + s;
+                const std::string v = (g.vec ? "t" : "s") + S(g.space) + "_" + S(g.terms[ti]);
+                o << "          const double " << v << " = S" << gi << "_" << slot / 2 << "_" << slot % 2 << ";\n";
+                const bool used = g.vec ? vd_used.count({g.space, g.terms[ti]}) : sd_used.count({g.space, g.terms[ti]});
+                if (!used) nf += " | NF(" + v + ")";
+            }
+        }
+        for (int h = 0; h < nH; ++h) o << "          const double n" << H.stored[h] << " = hv" << h << ";\n";
+        for (int id : H.consts) {
+            char buf[64];
+            std::snprintf(buf, sizeof buf, "%a", sig.nodes[id].value);
+            o << "          const double n" << id << " = (" << buf << ");\n";
+        }
+        {
+            std::ostringstream m;
+            emit_map_nodes(m, sig, live, qdep, true, "wq");
+            o << m.str();
+        }
+        for (int k = 0; k < sig.Tw; ++k) {
+            o << "          E" << s << "_" << k << " = qok ? n" << sig.outputs[k] << " : 0.0;\n";
+            nf += " | NF(n" + S(sig.outputs[k]) + ")";
+        }
+        o << "          if (cok && qok && (" << nf << ")) badc = min(badc, (unsigned long long)cell);\n";
         o << "        }\n";
     }
-    o << "      }\n";
-    o << "      __syncthreads();\n";
-    // map: one thread per (cell, quadrature point of the tile)
-    o << "      for (int it = tid; it < " << NC * TQ << "; it += " << NT << ") {\n";
-    o << "        const int c = it % " << NC << ", ql = it / " << NC << ", q = qt * " << TQ << " + ql;\n";
-    o << "        if (q < " << sig.Q << ") {\n";
-    for (size_t h = 0; h < H.stored.size(); ++h)
-        o << "          const double n" << H.stored[h] << " = sH[" << h * L.LDS << " + c];\n";
-    for (int id : H.consts) {
-        char buf[64];
-        std::snprintf(buf, sizeof buf, "%a", sig.nodes[id].value);
-        o << "          const double n" << id << " = (" << buf << ");\n";
+    // ---- quadrature GEMM: k-step kappa = (k, s)
+    for (int kq = 0; kq < L.KQ; ++kq) {
+        const int k = kq / TQL, s = kq % TQL;
+        for (int nb = 0; nb < L.NBQ; ++nb)
+            o << "        DMMA(y" << nb << "_0, y" << nb << "_1, E" << s << "_" << k << ", Fc["
+              << (L.foff_q + static_cast<long long>(nb) * L.KQ + kq) * 32 << "]);\n";
     }
-    std::string nfexpr = "false";
-    for (const auto& g : L.groups)
-        for (size_t tt = 0; tt < g.terms.size(); ++tt) {
-            const std::string v = (g.vec ? "t" : "s") + S(g.space) + "_" + S(g.terms[tt]);
-            o << "          const double " << v << " = sm[" << g.offS << " + (" << tt * TQ << " + ql) * " << L.LDS
-              << " + c];\n";
-            nfexpr += " | NF(" + v + ")";
+    o << "      }\n";  // chunks
+    // ---- scatter from the accumulator fragments
+    o << "      if (cok) {\n";
+    for (int nb = 0; nb < L.NBQ; ++nb)
+        for (int i = 0; i < 2; ++i) {
+            const std::string v = "y" + S(nb) + "_" + S(i);
+            const bool partial = nb * 8 + 8 > sig.nW;
+            o << "        " << (partial ? "if (" + S(nb * 8 + i) + " + 2 * g < " + S(sig.nW) + ") " : "") << "{\n";
+            o << "          if (NF(" << v << ")) badc = min(badc, (unsigned long long)cell);\n";
+            o << "          atomicAdd(&P.y[__ldg(&P.tm[(" << nb * 8 + i << " + 2 * g) * STR + cell])], " << v << ");\n";
+            o << "        }\n";
         }
-    {
-        std::ostringstream m;
-        emit_map_nodes(m, sig, live, qdep, true, "__ldg(&P.tabg[" + S(sig.w_off) + " + q])");
-        o << m.str();
-    }
-    for (int k = 0; k < sig.Tw; ++k) {
-        o << "          sE[(" << k * TQ << " + ql) * " << L.LDU << " + c] = n" << sig.outputs[k] << ";\n";
-        nfexpr += " | NF(n" + S(sig.outputs[k]) + ")";
-    }
-    o << "          if ((" << nfexpr << ") && c0 + c < P.n_cells) atomicMin(P.bad, (unsigned long long)(c0 + c));\n";
-    o << "        } else {\n";
-    for (int k = 0; k < sig.Tw; ++k) o << "          sE[(" << k * TQ << " + ql) * " << L.LDU << " + c] = 0.0;\n";
-    o << "        }\n";
     o << "      }\n";
-    o << "      __syncthreads();\n";
-    // quadrature GEMM: persistent accumulators (fixed task set per warp across q tiles)
-    const long long ntq = static_cast<long long>((L.MBq + R - 1) / R) * NBS;
-    o << "      #pragma unroll\n      for (int j = 0; j < " << TPWq << "; ++j) {\n";
-    o << "        const int t = warp + j * " << NW << ";\n";
-    o << "        if (t < " << ntq << ") {\n";
-    o << "          const int mb0 = (t / " << NBS << ") * " << R << ", nb0 = (t % " << NBS << ") * " << SB << ";\n";
-    o << "          const double* Ab = Aq + (" << L.foff_q << " + mb0 * " << L.KSq << ") * 32;\n";
-    o << "          const double* Bb = sE + (lane & 3) * " << L.LDU << " + nb0 * 8 + (lane >> 2);\n";
-    o << "          #pragma unroll 4\n";
-    o << "          for (int ks = 0; ks < " << L.KSq << "; ++ks) {\n";
-    o << "            double a[" << R << "], b[" << SB << "];\n";
-    o << "            #pragma unroll\n            for (int r = 0; r < " << R << "; ++r) a[r] = (mb0 + r < " << L.MBq
-      << ") ? " << (smemA ? "Ab[(r * " + S(L.KSq) + " + ks) * 32]" : "__ldg(&Ab[(r * " + S(L.KSq) + " + ks) * 32])")
-      << " : 0.0;\n";
-    o << "            #pragma unroll\n            for (int s = 0; s < " << SB << "; ++s) b[s] = (nb0 + s < " << NB
-      << ") ? Bb[ks * " << 4 * L.LDU << " + s * 8] : 0.0;\n";
-    o << "            #pragma unroll\n            for (int r = 0; r < " << R
-      << "; ++r)\n              #pragma unroll\n              for (int s = 0; s < " << SB
-      << "; ++s) DMMA(yacc[j][r][s], a[r], b[s]);\n";
-    o << "          }\n";
-    o << "        }\n";
-    o << "      }\n";
-    o << "    }\n";  // q tiles
-    // scatter from the accumulator fragments
-    o << "    #pragma unroll\n    for (int j = 0; j < " << TPWq << "; ++j) {\n";
-    o << "      const int t = warp + j * " << NW << ";\n";
-    o << "      if (t < " << ntq << ") {\n";
-    o << "        const int mb0 = (t / " << NBS << ") * " << R << ", nb0 = (t % " << NBS << ") * " << SB << ";\n";
-    o << "        bool nf = false;\n";
-    o << "        int badc = 0x7fffffff;\n";
-    o << "        #pragma unroll\n        for (int r = 0; r < " << R << "; ++r) {\n";
-    o << "          const int jw = (mb0 + r) * 8 + (lane >> 2);\n";
-    o << "          if (jw < " << sig.nW << ") {\n";
-    o << "            #pragma unroll\n            for (int s = 0; s < " << SB << "; ++s)\n";
-    o << "              #pragma unroll\n              for (int i = 0; i < 2; ++i) {\n";
-    o << "                const int cell = c0 + (nb0 + s) * 8 + 2 * (lane & 3) + i;\n";
-    o << "                if (nb0 + s < " << NB << " && cell < P.n_cells) {\n";
-    o << "                  const double v = yacc[j][r][s][i];\n";
-    o << "                  if (NF(v)) { nf = true; badc = min(badc, cell); }\n";
-    o << "                  atomicAdd(&P.y[__ldg(&P.tm[(size_t)jw * STR + cell])], v);\n";
-    o << "                }\n";
-    o << "              }\n";
-    o << "          }\n";
-    o << "        }\n";
-    o << "        if (nf) atomicMin(P.bad, (unsigned long long)badc);\n";
-    o << "      }\n";
-    o << "    }\n";
-    o << "  }\n";  // tiles
+    o << "    }\n";  // m-blocks
+    if (sig.affine || nH > 0) o << "    __syncwarp();\n";
+    o << "  }\n";  // tasks
+    o << "  if (badc != ~0ULL) atomicMin(P.bad, badc);\n";
     o << "}\n";
 }
 

@@ -89,22 +89,20 @@ struct DmmaGroup {
     bool vec = false;
     int space = 0, comp = 0, n = 0;
     std::vector<int> terms;
-    int KS = 0, MB = 0;          // k-steps (n/4), m-blocks (terms*TQ/8)
-    long long foff = 0;          // first fragment within a q tile
-    long long offU = 0, offS = 0;  // shared-memory offsets (doubles)
+    int KS = 0, NB = 0;          // k-steps (n/4), n-blocks of 8 output slots per chunk
+    long long foff = 0;          // first fragment within a chunk
 };
 struct DmmaLayout {
-    int NC = 0, TQ = 0, NQT = 0;
-    long long LDU = 0, LDS = 0;  // row strides (doubles): B-operand tiles / accumulator tiles
+    int CW = 0, MB = 0;          // cells per warp task, m-blocks of 8 cells
+    int TQ = 0, TQL = 0, NCH = 0;  // quadrature points per chunk, per lane-group, chunks
     std::vector<DmmaGroup> groups;
-    int KSq = 0, MBq = 0;
-    long long foff_q = 0, FPT = 0;  // quadrature fragments; fragments per q tile
-    long long off_A = 0, off_E = 0, off_H = 0, smem_doubles = 0;
-    int nH_cap = 0;
+    int KQ = 0, NBQ = 0;         // quadrature k-steps (Tw*TQL) and n-blocks (nW/8) per chunk
+    long long foff_q = 0, FPC = 0, nfrag = 0;  // fragments: quadrature offset, per chunk, total
 };
 DmmaLayout dmma_layout(const Signature& sig, const KernelPlan& kp);
 std::vector<double> dmma_fragments(const Signature& sig, const DmmaLayout& L, const std::vector<double>& tab);
 size_t dmma_smem_bytes(const Signature& sig, const KernelPlan& kp);
+long long dmma_live_doubles(const Signature& sig, const DmmaLayout& L);
 void resolve_dmma(const Signature& sig, KernelPlan& kp, const femgpu_schedule* s);
 
 struct EmitResult {

@@ -444,44 +444,46 @@ double* Instance::dmma_fragments_for(const KernelPlan& kp) {
 // DMMA family schedule (FEMGPU_DMMA): defaults and feasibility.
 void resolve_dmma(const Signature& sig, KernelPlan& kp, const femgpu_schedule* s) {
     kp.family = Family::Dmma;
+    // cells per warp task: m-blocks of 8 cells, at most one geometry lane per cell
     kp.Nc = s->cells_per_group > 0 ? s->cells_per_group : 32;
-    if (kp.Nc % 8) fail(FEMGPU_E_INFEASIBLE, "dmma: cells per tile must be a multiple of 8");
-    const int lanes = s->lanes_per_cell > 0 ? s->lanes_per_cell : std::max(1, 256 / kp.Nc);
-    kp.Nwi = lanes;
-    kp.block = kp.Nc * lanes;
-    if (kp.block % 32 || kp.block > 1024)
-        fail(FEMGPU_E_INFEASIBLE, "dmma: threads per CTA (cells x lanes) must be a multiple of 32 and <= 1024");
-    kp.Ter = s->eval_row_tile > 0 ? s->eval_row_tile : 2;
-    kp.Tqr = s->quad_row_tile > 0 ? s->quad_row_tile : std::min(2, kp.Nc / 8);
+    if (kp.Nc % 8 || kp.Nc > 32) fail(FEMGPU_E_INFEASIBLE, "dmma: cells per warp task must be 8, 16, 24 or 32");
+    if (s->lanes_per_cell > 0 && s->lanes_per_cell != 4)
+        fail(FEMGPU_E_INFEASIBLE, "dmma: 4 lanes per cell (m8n8k4 fragment layout: 8 cells per warp m-block)");
+    kp.Nwi = 4;
+    kp.block = s->block_cells > 0 ? s->block_cells : 256;
+    if (kp.block % 32 || kp.block > 1024) fail(FEMGPU_E_INFEASIBLE, "dmma: threads per CTA must be a multiple of 32 and <= 1024");
     kp.min_blocks = s->reserved[2] > 0 ? s->reserved[2] : 1;
-    const long long smem_cap = 227 * 1024;
-    auto fits = [&](int TQ, int basis) {
-        KernelPlan t = kp;
-        t.TQ = TQ;
-        t.basis = basis;
-        return dmma_smem_bytes(sig, t) <= static_cast<size_t>(smem_cap);
-    };
-    int basis = s->basis == FEMGPU_BASIS_SMEM ? FEMGPU_BASIS_SMEM : kBasisGlobal;
+    const int q4 = (sig.Q + 3) / 4 * 4;
     if (s->quad_tile > 0) {
-        kp.TQ = std::min(s->quad_tile, sig.Q);
+        kp.TQ = std::min(q4, (s->quad_tile + 3) / 4 * 4);
     } else {
-        // largest quadrature tile whose per-CTA footprint leaves room for two CTAs per SM
-        kp.TQ = sig.Q;
-        while (kp.TQ > 1) {
+        // fewest padded DMMAs per m-block; among equals the smallest register footprint
+        long long best = -1, best_live = 0;
+        for (int tql = 1; tql * 4 <= q4; ++tql) {
             KernelPlan t = kp;
-            t.basis = basis;
-            if (dmma_smem_bytes(sig, t) <= 100 * 1024) break;
-            kp.TQ = (kp.TQ + 1) / 2;
+            t.TQ = 4 * tql;
+            const DmmaLayout L = dmma_layout(sig, t);
+            const long long live = dmma_live_doubles(sig, L);
+            if (live > 72 && best >= 0) continue;
+            const long long cost = L.nfrag;  // DMMAs per m-block = fragments (one B fragment per DMMA)
+            if (best < 0 || cost < best || (cost == best && live < best_live)) {
+                best = cost;
+                best_live = live;
+                kp.TQ = t.TQ;
+            }
         }
     }
-    if (s->basis == FEMGPU_BASIS_AUTO) {
+    const long long smem_cap = 227 * 1024;
+    int basis = s->basis;
+    if (basis == FEMGPU_BASIS_AUTO) {
         KernelPlan t = kp;
         t.basis = FEMGPU_BASIS_SMEM;
-        const DmmaLayout L = dmma_layout(sig, t);
-        if (L.NQT * L.FPT * 256 <= 48 * 1024 && dmma_smem_bytes(sig, t) <= 110 * 1024) basis = FEMGPU_BASIS_SMEM;
+        basis = dmma_smem_bytes(sig, t) <= 100 * 1024 ? FEMGPU_BASIS_SMEM : kBasisGlobal;
+    } else if (basis != FEMGPU_BASIS_SMEM) {
+        basis = kBasisGlobal;
     }
     kp.basis = basis;
-    if (!fits(kp.TQ, kp.basis))
+    if (dmma_smem_bytes(sig, kp) > static_cast<size_t>(smem_cap))
         fail(FEMGPU_E_INFEASIBLE, "dmma: " + std::to_string(dmma_smem_bytes(sig, kp)) +
                                       " bytes of shared memory per CTA exceed the 227 KB sm_100a limit");
 }
@@ -857,7 +859,7 @@ void run_action(Instance& I, const KernelPlan& kp, double* d_y, cudaStream_t str
     else if (kp.family == Family::Macro)
         grid = (I.macro_layout(kp.G).n_groups + kp.block - 1) / kp.block;
     else if (kp.family == Family::Dmma)
-        grid = std::min<long long>((static_cast<long long>(I.cells) + kp.Nc - 1) / kp.Nc,
+        grid = std::min<long long>(((static_cast<long long>(I.cells) + kp.Nc - 1) / kp.Nc + kp.block / 32 - 1) / (kp.block / 32),
                                    static_cast<long long>(mod->sms) * std::max(1, mod->occupancy));
     else
         grid = (static_cast<long long>(I.cells) + kp.block - 1) / kp.block;

@@ -1,4 +1,4 @@
-"""GPU parity of the cell-batched FP64 tensor-core family (FEMGPU_DMMA, emit_dmma.cpp).
+"""GPU parity of the warp-level FP64 tensor-core family (FEMGPU_DMMA, emit_dmma.cpp).
 
 Same bar as the other families: rel L2 <= 1e-12 (north star) and the reference's elementwise
 relative error <= 1e-10 (search.hpp:360-366) against the CPU oracle, over
@@ -26,11 +26,8 @@ def close(y, ref):
 
 def random_dmma(sig, rng):
     pick = lambda hi: 1 + rng.next_u64() % hi  # noqa: E731
-    nc = 8 * pick(8)
-    lanes = [l for l in (1, 2, 4, 8, 16, 32) if (nc * l) % 32 == 0 and nc * l <= 1024]
-    return fg.TilingParams.dmma(cells_per_group=nc, quad_tile=pick(sig.quad_points),
-                                lanes_per_cell=lanes[rng.next_u64() % len(lanes)], eval_row_tile=pick(3),
-                                quad_row_tile=pick(min(4, nc // 8)),
+    return fg.TilingParams.dmma(cells_per_group=8 * pick(4), quad_tile=pick(sig.quad_points),
+                                lanes_per_cell=(0, 4)[rng.next_u64() % 2], block_cells=32 * pick(8),
                                 basis=abi.BASIS_SMEM if rng.next_u64() % 2 else abi.BASIS_CONST)
 
 
@@ -90,3 +87,9 @@ def test_dmma_infeasible():
     p = preset_problem("mass", 2, 2, 6, 8, 3)
     with pytest.raises(fg.InfeasibleError):
         fg.gpu_action(p, fg.TilingParams.dmma(cells_per_group=12))
+
+
+def test_dmma_rejects_other_lane_counts():
+    p = preset_problem("mass", 2, 2, 6, 8, 3)
+    with pytest.raises(fg.InfeasibleError):
+        fg.gpu_action(p, fg.TilingParams.dmma(lanes_per_cell=2))

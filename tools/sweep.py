@@ -34,7 +34,7 @@ def sched(name):
             kw["block_cells"] = int(p)
     head = parts[0]
     if head == "dmma":
-        # dmma-c<NC>-q<TQ>-l<lanes>-R<r>-S<s>-smem|glob
+        # dmma-c<cells per warp task>-q<TQ>-b<CTA threads>-m<min CTAs/SM>-smem|glob
         d = {}
         for p in parts[1:]:
             if p.startswith("c"):
@@ -49,6 +49,8 @@ def sched(name):
                 d["quad_row_tile"] = int(p[1:])
             elif p.startswith("m"):
                 d["min_blocks"] = int(p[1:])
+            elif p.startswith("b"):
+                d["block_cells"] = int(p[1:])
             elif p == "smem":
                 d["basis"] = abi.BASIS_SMEM
             elif p == "glob":
