@@ -9,8 +9,10 @@ distributions (seed 7).  One step = one full action y = A x (zero y + the action
           events on the instance stream, bracketed by barrier + synchronize, max over ranks.
   e2e     the same metric through the public C-ABI call with HOST buffers
           (femgpu_action_host: H2D of x, the action, D2H of y, every step; pinned memory).
-  roofline  the dominant kernel against the measured FP64 DFMA peak (live, femgpu_fp64_peak;
-          MEASURED_PEAKS.json has no FP64 figure) and the HBM side against MEASURED_PEAKS.json.
+  roofline  the dominant kernel against the machine's FP64 peak = max(DFMA, DMMA), both measured
+          live (femgpu_fp64_peak / femgpu_fp64_dmma_peak; MEASURED_PEAKS.json has no FP64 figure),
+          its own pipe's peak alongside, and the HBM side against MEASURED_PEAKS.json.  The kernel
+          is whatever the automatic schedule picked (cost model + timing, tune.cpp).
   cpu_baseline  the reference's own reference_action (oracle/_ref, compiled from
           /root/reference/proj/include/femsched/form.hpp) on the host cores, rank 0, N=1.
 
@@ -278,7 +280,12 @@ def run_single(args):
     # linearity A(2x) = 2 A(x) exactly in binary floating point) and oracle on a cell sample
     y1 = g.action()
     # ---- roofline
-    peak_tf, nominal_ghz = fg.fp64_peak()
+    pk = fg.fp64_peaks()
+    plan = g.describe()
+    kernel = plan.split(" | ")[0]
+    on_dmma = kernel.startswith("femgpu_dmma")
+    peak_tf = pk["fp64"]  # the machine's FP64 peak: max(DFMA, DMMA), both measured live
+    pipe_tf = pk["dmma"] if on_dmma else pk["dfma"]
     peaks = load_peaks()
     hbm = peaks.get("hbm_gbs")
     alg_flops = flops_cell * cells
@@ -290,9 +297,11 @@ def run_single(args):
     roof = {"bound": "fp64" if t_fp64 >= (t_hbm or 0) else "hbm", "achieved": alg_flops / kern_s / 1e12,
             "peak": peak_tf, "unit": "TFLOP/s", "frac": (alg_flops / kern_s / 1e12) / peak_tf,
             "traffic": traffic,
-            "peak_source": "measured live on this GPU (femgpu_fp64_peak DFMA microbenchmark); "
-                           "MEASURED_PEAKS.json has no FP64 entry",
-            "kernel": "femgpu_macro (NVRTC sm_100a)", "kernel_us": kern_s * 1e6, "zero_y_us": zero_s * 1e6,
+            "peak_source": "measured live on this GPU: max(DFMA %.2f, DMMA %.2f) TFLOP/s (femgpu_fp64_peak, "
+                           "femgpu_fp64_dmma_peak); MEASURED_PEAKS.json has no FP64 entry" % (pk["dfma"], pk["dmma"]),
+            "pipe": {"name": "DMMA (mma.sync m8n8k4 f64)" if on_dmma else "DFMA", "peak": pipe_tf,
+                     "frac": (alg_flops / kern_s / 1e12) / pipe_tf},
+            "kernel": kernel + " (NVRTC sm_100a)", "schedule": plan, "kernel_us": kern_s * 1e6, "zero_y_us": zero_s * 1e6,
             "algorithmic_flops_per_launch": alg_flops, "algorithmic_bytes_per_launch": alg_bytes,
             "hbm": {"achieved_alg_gbs": alg_bytes / kern_s / 1e9, "peak_gbs": hbm,
                     "frac": (alg_bytes / kern_s / 1e9) / hbm if hbm else None, "peak_source": "MEASURED_PEAKS.json"},

@@ -219,19 +219,29 @@ femgpu_status femgpu_profile_action(femgpu_instance* inst, const femgpu_schedule
 /* The FP64 roofline denominator, measured live: DFMA peak of the current device
  * (TFLOP/s) and its nominal SM clock (GHz).  Ahead-of-time sm_100a kernel. */
 femgpu_status femgpu_fp64_peak(double* tflops, double* sm_clock_ghz);
+/* The FP64 tensor-core (DMMA m8n8k4) peak of the current device (TFLOP/s), measured live. */
+femgpu_status femgpu_fp64_dmma_peak(double* tflops);
 /* Executor seam (search.hpp:257-283): run, verify finiteness, report output and
  * measured seconds (mean of the timing protocol above). */
 femgpu_status femgpu_execute(femgpu_instance* inst, const femgpu_schedule* s, double* y_host,
                              double* measured_seconds);
-/* The schedule femgpu picks for this instance when s == NULL or all-auto. */
+/* The schedule femgpu uses for this instance when s == NULL: on instances of >= 200k cells the
+ * kernel families are pruned by an FP64-pipe cost model and the survivors timed once (CUDA
+ * events); the winner is cached in the instance (FEMGPU_AUTOTUNE=0 disables the timing).
+ * Replaces femsched::rank + tune (search.hpp:211-416) for the default path. */
 femgpu_status femgpu_default_schedule(const femgpu_instance* inst, femgpu_schedule* s);
+/* Human-readable kernel plan for schedule s (NULL = the automatic one, with its tuning log). */
+femgpu_status femgpu_describe_schedule(femgpu_instance* inst, const femgpu_schedule* s, char* buf, size_t cap,
+                                       size_t* len);
 /* Introspection: kernel launches issued by the last action, device bytes held. */
 femgpu_status femgpu_stats(const femgpu_instance* inst, int64_t* launches_last_action,
                            int64_t* device_bytes, int64_t* tiles, int64_t* max_tile_dofs);
 /* Device pointers (for zero-copy callers): output buffer of the instance. */
 femgpu_status femgpu_device_output(femgpu_instance* inst, double** y_dev);
 /* Device pointer of trial input vector `space` (scalar spaces first, then vector spaces),
- * for zero-copy halo exchanges (multi-GPU): length global_count (x dim for vector spaces). */
+ * for zero-copy halo exchanges (multi-GPU): length global_count for scalar spaces; vector spaces
+ * are stored node-major with the components padded to 16 bytes ([node][4] in 3D, [node][2] in
+ * 2D), so their length is global_count x (dim == 3 ? 4 : dim). */
 femgpu_status femgpu_device_input(femgpu_instance* inst, int32_t space, double** x_dev);
 /* The CUDA stream (cudaStream_t) the instance launches on. */
 femgpu_status femgpu_stream(femgpu_instance* inst, void** stream);

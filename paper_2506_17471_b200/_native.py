@@ -23,7 +23,8 @@ EXPORTS = (
     "femgpu_stats", "femgpu_device_output", "femgpu_stream", "femgpu_action_once",
     "femgpu_host_alloc", "femgpu_host_free", "femgpu_mesh_counts", "femgpu_mesh_build",
     "femgpu_color_cells", "femgpu_profile_action", "femgpu_fp64_peak",
-    "femgpu_time_steps", "femgpu_device_input",
+    "femgpu_time_steps", "femgpu_device_input", "femgpu_describe_schedule",
+    "femgpu_fp64_dmma_peak",
 )
 
 
@@ -73,6 +74,8 @@ def lib():
                                         _P(C.c_double)], C.c_int),
                 "femgpu_execute": ([C.c_void_p, _P(abi.Schedule), _P(C.c_double), _P(C.c_double)], C.c_int),
                 "femgpu_default_schedule": ([C.c_void_p, _P(abi.Schedule)], C.c_int),
+                "femgpu_describe_schedule": ([C.c_void_p, _P(abi.Schedule), C.c_char_p, C.c_size_t,
+                                              _P(C.c_size_t)], C.c_int),
                 "femgpu_stats": ([C.c_void_p, _P(C.c_int64), _P(C.c_int64), _P(C.c_int64), _P(C.c_int64)], C.c_int),
                 "femgpu_device_output": ([C.c_void_p, _P(C.c_void_p)], C.c_int),
                 "femgpu_stream": ([C.c_void_p, _P(C.c_void_p)], C.c_int),
@@ -88,6 +91,7 @@ def lib():
                 "femgpu_profile_action": ([C.c_void_p, _P(abi.Schedule), C.c_int32, C.c_int32, _P(C.c_double),
                                            _P(C.c_double), _P(C.c_double)], C.c_int),
                 "femgpu_fp64_peak": ([_P(C.c_double), _P(C.c_double)], C.c_int),
+                "femgpu_fp64_dmma_peak": ([_P(C.c_double)], C.c_int),
                 "femgpu_time_steps": ([C.c_void_p, _P(abi.Schedule), C.c_int32, _P(C.c_double)], C.c_int),
                 "femgpu_device_input": ([C.c_void_p, C.c_int32, _P(C.c_void_p)], C.c_int),
             }

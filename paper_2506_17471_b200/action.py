@@ -97,6 +97,17 @@ class TilingParams:
         s.reserved[3] = self.stage_smem
         return s
 
+    @staticmethod
+    def from_c(s: abi.Schedule) -> "TilingParams":
+        return TilingParams(kind=s.kind, quad_tile=s.quad_tile, eval_row_tile=s.eval_row_tile,
+                            eval_col_tiles_scalar=[t for t in s.eval_col_tiles_scalar if t],
+                            eval_col_tiles_vector=[t for t in s.eval_col_tiles_vector if t],
+                            quad_row_tile=s.quad_row_tile, quad_col_tile=s.quad_col_tile,
+                            cells_per_group=s.cells_per_group, lanes_per_cell=s.lanes_per_cell, basis=s.basis,
+                            scatter=s.scatter, block_cells=s.block_cells, group_cells=s.group_cells,
+                            strict=bool(s.reserved[0]), reg_target=s.reserved[1], min_blocks=s.reserved[2],
+                            stage_smem=s.reserved[3])
+
     def describe(self) -> str:  # search.hpp:301-310
         if self.kind == abi.SCPT:
             return "single-cell-per-work-item"
@@ -212,6 +223,21 @@ class GpuInstance:
         _call(lib().femgpu_profile_action(self._h, sp[0] if sp else None, warmup, reps, *[C.byref(x) for x in v]))
         return tuple(x.value for x in v)
 
+    def default_schedule(self) -> TilingParams:
+        """The automatic schedule (femgpu_default_schedule: cost-model pruning + timing, cached)."""
+        s = abi.Schedule()
+        _call(lib().femgpu_default_schedule(self._h, C.byref(s)))
+        return TilingParams.from_c(s)
+
+    def describe(self, params: Optional[TilingParams] = None) -> str:
+        """The kernel plan of `params` (None = the automatic schedule with its tuning log)."""
+        n = C.c_size_t()
+        sp = _sched(params)
+        _call(lib().femgpu_describe_schedule(self._h, sp[0] if sp else None, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        _call(lib().femgpu_describe_schedule(self._h, sp[0] if sp else None, buf, n.value + 1, C.byref(n)))
+        return buf.value.decode()
+
     def stats(self):
         v = [C.c_int64() for _ in range(4)]
         _call(lib().femgpu_stats(self._h, *[C.byref(x) for x in v]))
@@ -288,6 +314,14 @@ def jit_check(problem: ProblemInstance, params: Optional[TilingParams] = None) -
     cp = problem.to_c()
     sp = _sched(params)
     _call(lib().femgpu_jit_check(C.byref(cp.desc), sp[0] if sp else None))
+
+
+def fp64_peaks():
+    """Live FP64 peaks of the current device: {"dfma": TF, "dmma": TF, "fp64": max, "sm_ghz": nominal}."""
+    t, g, m = C.c_double(), C.c_double(), C.c_double()
+    _call(lib().femgpu_fp64_peak(C.byref(t), C.byref(g)))
+    _call(lib().femgpu_fp64_dmma_peak(C.byref(m)))
+    return {"dfma": t.value, "dmma": m.value, "fp64": max(t.value, m.value), "sm_ghz": g.value}
 
 
 def fp64_peak():

@@ -1,5 +1,6 @@
 // api.cpp — the extern "C" boundary (include/femgpu.h).  Converts every C++
 // exception into a femgpu_status + thread-local message; nothing throws across.
+#include <algorithm>
 #include <cstring>
 #include <string>
 
@@ -52,9 +53,8 @@ void copy_inputs(femgpu::Instance& I, const double* const* scalar_inputs, const 
     }
     for (size_t i = 0; i < I.vspaces.size(); ++i) {
         if (!vector_inputs || !vector_inputs[i]) femgpu::invalid("instance: vector input length mismatch");
-        FG_CUDA(cudaMemcpyAsync(I.vspaces[i].d_x, vector_inputs[i],
-                                sizeof(double) * I.vspaces[i].global * static_cast<size_t>(I.sig.dim),
-                                cudaMemcpyHostToDevice, stream));
+        femgpu::upload_padded(I.vspaces[i].d_x, vector_inputs[i], I.vspaces[i].global, I.sig.dim, I.vspaces[i].d_stage,
+                              stream);
     }
 }
 
@@ -183,7 +183,7 @@ femgpu_status femgpu_action(femgpu_instance* h, const femgpu_schedule* s, double
         if (!y_host) femgpu::invalid("null output buffer");
         std::lock_guard<std::mutex> lk(I.mu);
         FG_CUDA(cudaSetDevice(I.device));
-        const femgpu::KernelPlan kp = femgpu::resolve_schedule(I, s);
+        const femgpu::KernelPlan kp = femgpu::plan_for(I, s);
         femgpu::run_action(I, kp, I.d_y, I.stream);
         FG_CUDA(cudaMemcpyAsync(y_host, I.d_y, sizeof(double) * static_cast<size_t>(I.output_size),
                                 cudaMemcpyDeviceToHost, I.stream));
@@ -198,7 +198,7 @@ femgpu_status femgpu_action_host(femgpu_instance* h, const femgpu_schedule* s, c
         if (!y_host) femgpu::invalid("null output buffer");
         std::lock_guard<std::mutex> lk(I.mu);
         FG_CUDA(cudaSetDevice(I.device));
-        const femgpu::KernelPlan kp = femgpu::resolve_schedule(I, s);
+        const femgpu::KernelPlan kp = femgpu::plan_for(I, s);
         copy_inputs(I, scalar_inputs, vector_inputs, I.stream);
         femgpu::run_action(I, kp, I.d_y, I.stream);
         FG_CUDA(cudaMemcpyAsync(y_host, I.d_y, sizeof(double) * static_cast<size_t>(I.output_size),
@@ -212,7 +212,7 @@ femgpu_status femgpu_action_device(femgpu_instance* h, const femgpu_schedule* s,
         auto& I = get(h);
         std::lock_guard<std::mutex> lk(I.mu);
         FG_CUDA(cudaSetDevice(I.device));
-        const femgpu::KernelPlan kp = femgpu::resolve_schedule(I, s);
+        const femgpu::KernelPlan kp = femgpu::plan_for(I, s);
         femgpu::run_action(I, kp, y_dev ? y_dev : I.d_y, stream ? static_cast<cudaStream_t>(stream) : I.stream);
     });
 }
@@ -224,7 +224,7 @@ femgpu_status femgpu_time_action(femgpu_instance* h, const femgpu_schedule* s, i
         if (!seconds) femgpu::invalid("null output");
         std::lock_guard<std::mutex> lk(I.mu);
         FG_CUDA(cudaSetDevice(I.device));
-        const femgpu::KernelPlan kp = femgpu::resolve_schedule(I, s);
+        const femgpu::KernelPlan kp = femgpu::plan_for(I, s);
         for (int i = 0; i < warmup; ++i) femgpu::run_action(I, kp, I.d_y, I.stream);
         femgpu::check_failure(I, kp, I.stream);
         double total = 0.0;
@@ -252,7 +252,7 @@ femgpu_status femgpu_time_steps(femgpu_instance* h, const femgpu_schedule* s, in
         if (steps < 1 || !seconds) femgpu::invalid("time_steps: steps >= 1 and an output are required");
         std::lock_guard<std::mutex> lk(I.mu);
         FG_CUDA(cudaSetDevice(I.device));
-        const femgpu::KernelPlan kp = femgpu::resolve_schedule(I, s);
+        const femgpu::KernelPlan kp = femgpu::plan_for(I, s);
         FG_CUDA(cudaDeviceSynchronize());
         FG_CUDA(cudaEventRecord(I.ev0, I.stream));
         for (int i = 0; i < steps; ++i) femgpu::run_action(I, kp, I.d_y, I.stream);
@@ -273,7 +273,7 @@ femgpu_status femgpu_profile_action(femgpu_instance* h, const femgpu_schedule* s
         if (reps < 1) femgpu::invalid("profile: reps must be >= 1");
         std::lock_guard<std::mutex> lk(I.mu);
         FG_CUDA(cudaSetDevice(I.device));
-        const femgpu::KernelPlan kp = femgpu::resolve_schedule(I, s);
+        const femgpu::KernelPlan kp = femgpu::plan_for(I, s);
         for (int i = 0; i < warmup; ++i) femgpu::run_action(I, kp, I.d_y, I.stream);
         femgpu::check_failure(I, kp, I.stream);
         std::vector<cudaEvent_t> ev(3 * static_cast<size_t>(reps));
@@ -311,9 +311,29 @@ femgpu_status femgpu_execute(femgpu_instance* h, const femgpu_schedule* s, doubl
 
 femgpu_status femgpu_default_schedule(const femgpu_instance* h, femgpu_schedule* s) {
     return guard([&] {
-        if (!h || !s) femgpu::invalid("null argument");
-        std::memset(s, 0, sizeof *s);
-        s->kind = FEMGPU_SCPT;
+        if (!h || !h->impl || !s) femgpu::invalid("null argument");
+        auto& I = *h->impl;  // the automatic schedule is a lazily computed cache of the instance
+        std::lock_guard<std::mutex> lk(I.mu);
+        FG_CUDA(cudaSetDevice(I.device));
+        if (!I.auto_ready) femgpu::autotune(I);
+        *s = I.auto_sched;
+    });
+}
+
+femgpu_status femgpu_describe_schedule(femgpu_instance* h, const femgpu_schedule* s, char* buf, size_t cap,
+                                       size_t* len) {
+    return guard([&] {
+        auto& I = get(h);
+        std::lock_guard<std::mutex> lk(I.mu);
+        FG_CUDA(cudaSetDevice(I.device));
+        std::string d = femgpu::describe_plan(femgpu::plan_for(I, s));
+        if (!s) d += " | auto: " + I.auto_log;
+        if (len) *len = d.size();
+        if (buf && cap) {
+            const size_t n = std::min(cap - 1, d.size());
+            std::memcpy(buf, d.data(), n);
+            buf[n] = 0;
+        }
     });
 }
 

@@ -219,7 +219,7 @@ void emit_cell_body(Out& o, const Signature& sig, const KernelPlan& kp, const Ma
                            std::to_string(d) + "+" + std::to_string(c) + "];");
                 else
                     o.line("const double " + nm("w", i, j, c) + " = __ldg(&P.v" + std::to_string(i) + "[(size_t)" +
-                           node + "*" + std::to_string(d) + "+" + std::to_string(c) + "]);");
+                           node + "*" + std::to_string(vec_stride(d)) + "+" + std::to_string(c) + "]);");
             }
         }
     }
@@ -246,7 +246,7 @@ void emit_cell_body(Out& o, const Signature& sig, const KernelPlan& kp, const Ma
                     o.line("const double " + nm("X", j, c) + " = Xs[" + vtx + "*" + std::to_string(d) + "+" +
                            std::to_string(c) + "];");
                 else
-                    o.line("const double " + nm("X", j, c) + " = __ldg(&P.X[(size_t)" + vtx + "*" + std::to_string(d) +
+                    o.line("const double " + nm("X", j, c) + " = __ldg(&P.X[(size_t)" + vtx + "*" + std::to_string(vec_stride(d)) +
                            "+" + std::to_string(c) + "]);");
             }
         }
@@ -430,9 +430,16 @@ void emit_geometry(std::ostringstream& os, const Signature& sig, bool uses_inv, 
     const int d = sig.dim;
     for (int j = 0; j < sig.coord_dofs; ++j) {
         os << "        const int cv" << j << " = __ldg(&P.cm[" << j << " * (size_t)P.stride + " << cell << "]);\n";
-        for (int c = 0; c < d; ++c)
-            os << "        const double X" << j << "_" << c << " = __ldg(&P.X[(size_t)cv" << j << " * " << d << " + " << c
-               << "]);\n";
+        if (d >= 2) {
+            // padded layout: components (0,1) are one aligned 16-byte load
+            os << "        const double2 X" << j << "_01 = __ldg(reinterpret_cast<const double2*>(P.X + (size_t)cv" << j << " * "
+               << vec_stride(d) << "));\n";
+            os << "        const double X" << j << "_0 = X" << j << "_01.x, X" << j << "_1 = X" << j << "_01.y;\n";
+            if (d == 3)
+                os << "        const double X" << j << "_2 = __ldg(&P.X[(size_t)cv" << j << " * " << vec_stride(d) << " + 2]);\n";
+        } else {
+            os << "        const double X" << j << "_0 = __ldg(&P.X[(size_t)cv" << j << "]);\n";
+        }
     }
     for (int c = 0; c < d; ++c)
         for (int r = 0; r < d; ++r)
@@ -466,7 +473,7 @@ std::string KernelPlan::key() const {
     for (size_t g = 0; g < group_cap.size(); ++g) s << "g" << group_entries[g] << ":" << group_cap[g];
     for (int g : sgroup) s << "S" << g;
     for (int g : vgroup) s << "V" << g;
-    s << "T" << tgroup << "C" << cgroup;
+    s << "T" << tgroup << "C" << cgroup << "tv" << tvec;
     uint64_t h = 0xcbf29ce484222325ULL;
     for (const auto& p : mpat)
         for (int v : p) h = (h ^ static_cast<uint64_t>(v + 1)) * 0x100000001b3ULL;
@@ -645,7 +652,7 @@ void emit_tile_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const 
             o.line("  const int u = tid + k * " + S(TB) + ";");
             for (int c = 0; c < it.comps; ++c)
                 o.line("  cp8(" + base + " + " + S(it.off) + " + (u * " + S(it.comps) + " + " + S(c) + ") * 8, " + it.src +
-                       " + (size_t)gl" + S(it.group) + "[k] * " + S(it.comps) + " + " + S(c) + ");");
+                       " + (size_t)gl" + S(it.group) + "[k] * " + S(it.comps == 1 ? 1 : vec_stride(it.comps)) + " + " + S(c) + ");");
             o.line("}");
         }
     };
@@ -777,17 +784,28 @@ void emit_macro_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const
                 for (int i = 0; i < sig.ns(); ++i)
                     if (kp.sgroup[i] == g)
                         o.line("const double xg" + S(i) + "_" + S(u) + " = __ldg(&P.x" + S(i) + "[ig" + S(g) + "_" + S(u) + "]);");
+                // padded node-major layout: components (0,1) come as one aligned 16-byte load
+                auto node_loads = [&](const std::string& dst, const std::string& arr, const std::set<int>& comps) {
+                    const std::string base = arr + " + (size_t)ig" + S(g) + "_" + S(u) + " * " + S(vec_stride(D));
+                    const bool pair = D >= 2 && comps.count(0) && comps.count(1);
+                    if (pair) {
+                        // (no initializer: the checked twin's goto may jump over this declaration)
+                        o.line("double2 " + dst + "_01; " + dst + "_01 = __ldg(reinterpret_cast<const double2*>(" + base + "));");
+                        o.line("const double " + dst + "_0 = " + dst + "_01.x, " + dst + "_1 = " + dst + "_01.y;");
+                    }
+                    for (int c : comps)
+                        if (!pair || c >= 2) o.line("const double " + dst + "_" + S(c) + " = __ldg(" + base + " + " + S(c) + ");");
+                };
                 for (int i = 0; i < sig.nv(); ++i)
                     if (kp.vgroup[i] == g) {
                         std::set<int> comps(sig.vcomps[i].begin(), sig.vcomps[i].end());
-                        for (int c : comps)
-                            o.line("const double vg" + S(i) + "_" + S(u) + "_" + S(c) + " = __ldg(&P.v" + S(i) + "[(size_t)ig" +
-                                   S(g) + "_" + S(u) + " * " + S(D) + " + " + S(c) + "]);");
+                        node_loads("vg" + S(i) + "_" + S(u), "P.v" + S(i), comps);
                     }
-                if (sig.affine && kp.cgroup == g)
-                    for (int c = 0; c < D; ++c)
-                        o.line("const double Xg" + S(u) + "_" + S(c) + " = __ldg(&P.X[(size_t)ig" + S(g) + "_" + S(u) +
-                               " * " + S(D) + " + " + S(c) + "]);");
+                if (sig.affine && kp.cgroup == g) {
+                    std::set<int> comps;
+                    for (int c = 0; c < D; ++c) comps.insert(c);
+                    node_loads("Xg" + S(u), "P.X", comps);
+                }
             }
     };
     const int gt = kp.tgroup;
@@ -816,7 +834,7 @@ void emit_macro_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const
             for (int u = 0; u < kp.group_cap[kp.vgroup[i]]; ++u)
                 for (int c = 0; c < D; ++c)
                     copies.push_back("cp8s(" + S(slot + static_cast<long long>(u) * D + c) + ", P.v" + S(i) + " + (size_t)ig" +
-                                     S(kp.vgroup[i]) + "_" + S(u) + " * " + S(D) + " + " + S(c) + ");");
+                                     S(kp.vgroup[i]) + "_" + S(u) + " * " + S(vec_stride(D)) + " + " + S(c) + ");");
             slot += static_cast<long long>(kp.group_cap[kp.vgroup[i]]) * D;
         }
         if (sig.affine) {
@@ -824,7 +842,7 @@ void emit_macro_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const
             for (int u = 0; u < kp.group_cap[kp.cgroup]; ++u)
                 for (int c = 0; c < D; ++c)
                     copies.push_back("cp8s(" + S(slot + static_cast<long long>(u) * D + c) + ", P.X + (size_t)ig" +
-                                     S(kp.cgroup) + "_" + S(u) + " * " + S(D) + " + " + S(c) + ");");
+                                     S(kp.cgroup) + "_" + S(u) + " * " + S(vec_stride(D)) + " + " + S(c) + ");");
             slot += static_cast<long long>(kp.group_cap[kp.cgroup]) * D;
         }
         for (const auto& c : copies) o.line(c);
@@ -981,7 +999,7 @@ EmitResult emit_mlt(const Signature& sig, const KernelPlan& kp) {
             o.line("{");
             o.line("  const int v = __ldg(&P.cm[" + S(j) + "*(size_t)P.stride + cell]);");
             for (int c = 0; c < D; ++c)
-                o.line("  g[" + S(D * D + 1 + j * D + c) + "] = __ldg(&P.X[(size_t)v*" + S(D) + "+" + S(c) + "]);");
+                o.line("  g[" + S(D * D + 1 + j * D + c) + "] = __ldg(&P.X[(size_t)v*" + S(vec_stride(D)) + "+" + S(c) + "]);");
             o.line("}");
         }
         o.ind--;
@@ -1035,7 +1053,7 @@ EmitResult emit_mlt(const Signature& sig, const KernelPlan& kp) {
         o.line("if (live) for (int t = lid1; t < tc * " + S(comps) + "; t += " + S(NW) + ") {");
         o.line("  const int j = t / " + S(comps) + ", c = t % " + S(comps) + ";");
         o.line("  dofs[lid0 * " + S(dt) + " + t] = __ldg(&" + X + "[(size_t)__ldg(&" + M + "[(size_t)(cb + j) * P.stride + cell]) * " +
-               S(comps) + " + c]);");
+               S(sp.vec ? vec_stride(D) : 1) + " + c]);");
         o.line("}");
         // cooperative Phi-tile prefetch into the aliased buffer (roster of simulate.hpp:414-429)
         o.line("for (int f = tid; f < tr * tc; f += " + S(BS) + ") {");

@@ -31,6 +31,7 @@
 // failing cell (like the reference's first failing cell) and the stage-checked twin names the
 // stage.
 #include <algorithm>
+#include <cstdlib>
 #include <set>
 #include <sstream>
 
@@ -200,7 +201,11 @@ void emit_dmma_kernel(std::ostringstream& o, const Signature& sig, const KernelP
     const Hoist H = hoisted(sig, live, qdep);
     const Smem SM = dmma_smem(sig, kp, L);
     const int NT = kp.block, NW = NT / 32, CW = L.CW, MB = L.MB, TQL = L.TQL, nH = SM.nH;
+    const int MBJ = std::max(1, kp.Ter), PF = kp.Tqr > 0 ? 1 : 0;
+    const bool tv = kp.tvec >= 0 && std::getenv("FEMGPU_DEBUG_NO_TVEC") == nullptr;
     const bool smemA = kp.basis == FEMGPU_BASIS_SMEM;
+    // timing experiments only (wrong results): plain stores instead of red.add in the scatter
+    const bool scatter_store = std::getenv("FEMGPU_DEBUG_SCATTER_STORE") != nullptr;
     bool uses_inv = false;
     for (size_t id = 0; id < sig.nodes.size(); ++id)
         if (live[id] && sig.nodes[id].op == FEMGPU_OP_INV_JACOBIAN) uses_inv = true;
@@ -252,110 +257,237 @@ void emit_dmma_kernel(std::ostringstream& o, const Signature& sig, const KernelP
         o << "    }\n";
         o << "    __syncwarp();\n";
     }
-    o << "    #pragma unroll 1\n";
-    o << "    for (int mb = 0; mb < " << MB << "; ++mb) {\n";
-    o << "      const int cr = mb * 8 + r, cell = c0 + cr;\n";
-    o << "      const bool cok = cell < P.n_cells;\n";
-    // ---- gather A fragments (one index per (space, k-step), shared by the component groups)
+    // ---- m-groups of MBJ m-blocks sharing every B-fragment load; optional software prefetch:
+    // indices two m-groups ahead, values one m-group ahead (loop-carried registers).
     std::vector<std::vector<int>> by_space_s(sig.ns()), by_space_v(sig.nv());
     for (size_t gi = 0; gi < L.groups.size(); ++gi)
         (L.groups[gi].vec ? by_space_v[L.groups[gi].space] : by_space_s[L.groups[gi].space]).push_back(static_cast<int>(gi));
-    auto gather_space = [&](bool vec, int i, const std::vector<int>& gids) {
-        const DmmaGroup& g0 = L.groups[gids[0]];
-        for (int ks = 0; ks < g0.KS; ++ks) {
-            const bool partial = (ks + 1) * 4 > g0.n;
-            const std::string ok = partial ? "(cok && " + S(ks * 4) + " + g < " + S(g0.n) + ")" : "cok";
-            const std::string ix = "ix" + S(vec) + "_" + S(i) + "_" + S(ks);
-            o << "      const int " << ix << " = " << ok << " ? __ldg(&P." << (vec ? "vm" : "m") << i << "[(" << ks * 4
-              << " + g) * STR + cell]) : -1;\n";
-            for (int gid : gids) {
-                const DmmaGroup& g = L.groups[gid];
-                o << "      const double uA" << gid << "_" << ks << " = " << ix << " >= 0 ? ";
-                if (vec)
-                    o << "__ldg(&P.v" << i << "[(size_t)" << ix << " * " << sig.dim << " + " << g.comp << "])";
-                else
-                    o << "__ldg(&P.x" << i << "[" << ix << "])";
-                o << " : 0.0;\n";
+    struct Sp {
+        bool vec;
+        int i;
+        std::vector<int> gids;
+    };
+    std::vector<Sp> sps;
+    for (int i = 0; i < sig.ns(); ++i) sps.push_back({false, i, by_space_s[i]});
+    for (int i = 0; i < sig.nv(); ++i) sps.push_back({true, i, by_space_v[i]});
+    const std::string J = "_j";
+    auto ixname = [&](const std::string& pre, const Sp& sp, int ks, int j) {
+        return pre + S(sp.vec) + "_" + S(sp.i) + "_" + S(ks) + J + S(j);
+    };
+    auto uname = [&](const std::string& pre, int gid, int ks, int j) { return pre + S(gid) + "_" + S(ks) + J + S(j); };
+    // index loads of m-group `grp` (expression) into `pre` variables (decl: declare const)
+    auto emit_idx = [&](const std::string& ind, const std::string& pre, const std::string& grp, bool decl) {
+        for (int j = 0; j < MBJ; ++j) {
+            const std::string cell = "(c0 + ((" + grp + ") * " + S(MBJ) + " + " + S(j) + ") * 8 + r)";
+            for (const Sp& sp : sps) {
+                const DmmaGroup& g0 = L.groups[sp.gids[0]];
+                for (int ks = 0; ks < g0.KS; ++ks) {
+                    const bool partial = (ks + 1) * 4 > g0.n;
+                    std::string ok = cell + " < P.n_cells";
+                    if (partial) ok += " && " + S(ks * 4) + " + g < " + S(g0.n);
+                    o << ind << (decl ? "const int " : "") << ixname(pre, sp, ks, j) << " = (" << ok << ") ? __ldg(&P."
+                      << (sp.vec ? "vm" : "m") << sp.i << "[(" << ks * 4 << " + g) * STR + " << cell << "]) : -1;\n";
+                }
             }
         }
     };
-    for (int i = 0; i < sig.ns(); ++i) gather_space(false, i, by_space_s[i]);
-    for (int i = 0; i < sig.nv(); ++i) gather_space(true, i, by_space_v[i]);
-    for (int h = 0; h < nH; ++h) o << "      const double hv" << h << " = sH[" << static_cast<long long>(h) * CW << " + cr];\n";
-    for (int nb = 0; nb < L.NBQ; ++nb) o << "      double y" << nb << "_0 = 0.0, y" << nb << "_1 = 0.0;\n";
+    auto emit_vals = [&](const std::string& ind, const std::string& ipre, const std::string& upre, bool decl) {
+        for (int j = 0; j < MBJ; ++j)
+            for (const Sp& sp : sps) {
+                const DmmaGroup& g0 = L.groups[sp.gids[0]];
+                for (int ks = 0; ks < g0.KS; ++ks) {
+                    const std::string ix = ixname(ipre, sp, ks, j);
+                    // vector spaces: padded node-major layout, components (0,1) as one 16-byte load
+                    int g0c = -1, g1c = -1;
+                    if (sp.vec && sig.dim >= 2)
+                        for (int gid : sp.gids) {
+                            if (L.groups[gid].comp == 0) g0c = gid;
+                            if (L.groups[gid].comp == 1) g1c = gid;
+                        }
+                    const bool pair = g0c >= 0 && g1c >= 0;
+                    const std::string pv = "pv" + S(sp.i) + "_" + S(ks) + J + S(j) + "_" + upre;
+                    if (pair)
+                        o << ind << "const double2 " << pv << " = " << ix << " >= 0 ? __ldg(reinterpret_cast<const double2*>(P.v"
+                          << sp.i << " + (size_t)" << ix << " * " << vec_stride(sig.dim) << ")) : make_double2(0.0, 0.0);\n";
+                    for (int gid : sp.gids) {
+                        o << ind << (decl ? "const double " : "") << uname(upre, gid, ks, j) << " = ";
+                        if (pair && gid == g0c)
+                            o << pv << ".x;\n";
+                        else if (pair && gid == g1c)
+                            o << pv << ".y;\n";
+                        else if (sp.vec)
+                            o << ix << " >= 0 ? __ldg(&P.v" << sp.i << "[(size_t)" << ix << " * " << vec_stride(sig.dim) << " + "
+                              << L.groups[gid].comp << "]) : 0.0;\n";
+                        else
+                            o << ix << " >= 0 ? __ldg(&P.x" << sp.i << "[" << ix << "]) : 0.0;\n";
+                    }
+                }
+            }
+    };
+    const int NG = MB / MBJ;
+    if (PF) {
+        // declarations of the loop-carried prefetch registers
+        for (int j = 0; j < MBJ; ++j)
+            for (const Sp& sp : sps) {
+                const DmmaGroup& g0 = L.groups[sp.gids[0]];
+                for (int ks = 0; ks < g0.KS; ++ks) {
+                    o << "    int " << ixname("ixN", sp, ks, j) << " = -1;\n";
+                    for (int gid : sp.gids) o << "    double " << uname("uN", gid, ks, j) << " = 0.0;\n";
+                }
+            }
+    }
+    o << "    #pragma unroll 1\n";
+    o << "    for (int grp = 0; grp < " << NG << "; ++grp) {\n";
+    if (PF) {
+        // stage chain: grp 0 loads its own indices+values, later m-groups were prefetched
+        o << "      if (grp == 0) {\n";
+        emit_idx("        ", "ixN", "0", false);
+        emit_vals("        ", "ixN", "uN", false);
+        if (NG > 1) emit_idx("        ", "ixN", "1", false);
+        o << "      }\n";
+        for (int j = 0; j < MBJ; ++j)
+            for (const Sp& sp : sps)
+                for (int ks = 0; ks < L.groups[sp.gids[0]].KS; ++ks) {
+                    for (int gid : sp.gids)
+                        o << "      const double " << uname("uA", gid, ks, j) << " = " << uname("uN", gid, ks, j) << ";\n";
+                    if (tv && sp.vec && sp.i == kp.tvec)
+                        o << "      const int " << ixname("ixC", sp, ks, j) << " = " << ixname("ixN", sp, ks, j) << ";\n";
+                }
+        if (NG > 1) {
+            o << "      if (grp + 1 < " << NG << ") {\n";
+            emit_vals("        ", "ixN", "uN", false);
+            o << "      }\n";
+            if (NG > 2) {
+                o << "      if (grp + 2 < " << NG << ") {\n";
+                emit_idx("        ", "ixN", "grp + 2", false);
+                o << "      }\n";
+            }
+        }
+    } else {
+        emit_idx("      ", "ix", "grp", true);
+        emit_vals("      ", "ix", "uA", true);
+    }
+    for (int j = 0; j < MBJ; ++j) {
+        o << "      const int cr" << j << " = (grp * " << MBJ << " + " << j << ") * 8 + r, cell" << j << " = c0 + cr" << j << ";\n";
+        o << "      const bool cok" << j << " = cell" << j << " < P.n_cells;\n";
+        for (int h = 0; h < nH; ++h)
+            o << "      const double hv" << h << J << j << " = sH[" << static_cast<long long>(h) * CW << " + cr" << j << "];\n";
+        for (int nb = 0; nb < L.NBQ; ++nb)
+            o << "      double y" << nb << J << j << "_0 = 0.0, y" << nb << J << j << "_1 = 0.0;\n";
+    }
     o << "      #pragma unroll 1\n";
     o << "      for (int ch = 0; ch < " << L.NCH << "; ++ch) {\n";
     o << "        const double* const Fc = FR + (size_t)ch * " << L.FPC * 32 << ";\n";
-    // ---- evaluation GEMMs
+    // ---- evaluation GEMMs (one B fragment load feeds MBJ DMMAs)
     for (size_t gi = 0; gi < L.groups.size(); ++gi) {
         const DmmaGroup& g = L.groups[gi];
         for (int nb = 0; nb < g.NB; ++nb) {
-            const std::string d0 = "S" + S(gi) + "_" + S(nb) + "_0", d1 = "S" + S(gi) + "_" + S(nb) + "_1";
-            o << "        double " << d0 << " = 0.0, " << d1 << " = 0.0;\n";
-            for (int ks = 0; ks < g.KS; ++ks)
-                o << "        DMMA(" << d0 << ", " << d1 << ", uA" << gi << "_" << ks << ", Fc["
-                  << (g.foff + static_cast<long long>(nb) * g.KS + ks) * 32 << "]);\n";
-        }
-    }
-    // ---- pointwise map per owned quadrature point
-    for (int s = 0; s < TQL; ++s) {
-        o << "        double E" << s << "_0";
-        for (int k = 1; k < sig.Tw; ++k) o << ", E" << s << "_" << k;
-        o << ";\n";
-        o << "        {\n";
-        o << "          const int q = ch * " << L.TQ << " + " << 4 * s << " + g;\n";
-        o << "          const bool qok = q < " << sig.Q << ";\n";
-        o << "          const double wq = qok ? __ldg(&P.tabg[" << sig.w_off << " + q]) : 0.0;\n";
-        std::string nf = "false";
-        for (size_t gi = 0; gi < L.groups.size(); ++gi) {
-            const DmmaGroup& g = L.groups[gi];
-            for (size_t ti = 0; ti < g.terms.size(); ++ti) {
-                const int slot = static_cast<int>(ti) * TQL + s;
-                const std::string v = (g.vec ? "t" : "s") + S(g.space) + "_" + S(g.terms[ti]);
-                o << "          const double " << v << " = S" << gi << "_" << slot / 2 << "_" << slot % 2 << ";\n";
-                const bool used = g.vec ? vd_used.count({g.space, g.terms[ti]}) : sd_used.count({g.space, g.terms[ti]});
-                if (!used) nf += " | NF(" + v + ")";
+            for (int j = 0; j < MBJ; ++j)
+                o << "        double S" << gi << "_" << nb << J << j << "_0 = 0.0, S" << gi << "_" << nb << J << j << "_1 = 0.0;\n";
+            for (int ks = 0; ks < g.KS; ++ks) {
+                o << "        { const double b = Fc[" << (g.foff + static_cast<long long>(nb) * g.KS + ks) * 32 << "];";
+                for (int j = 0; j < MBJ; ++j)
+                    o << " DMMA(S" << gi << "_" << nb << J << j << "_0, S" << gi << "_" << nb << J << j << "_1, "
+                      << uname("uA", static_cast<int>(gi), ks, j) << ", b);";
+                o << " }\n";
             }
         }
-        for (int h = 0; h < nH; ++h) o << "          const double n" << H.stored[h] << " = hv" << h << ";\n";
-        for (int id : H.consts) {
-            char buf[64];
-            std::snprintf(buf, sizeof buf, "%a", sig.nodes[id].value);
-            o << "          const double n" << id << " = (" << buf << ");\n";
-        }
-        {
-            std::ostringstream m;
-            emit_map_nodes(m, sig, live, qdep, true, "wq");
-            o << m.str();
-        }
-        for (int k = 0; k < sig.Tw; ++k) {
-            o << "          E" << s << "_" << k << " = qok ? n" << sig.outputs[k] << " : 0.0;\n";
-            nf += " | NF(n" + S(sig.outputs[k]) + ")";
-        }
-        o << "          if (cok && qok && (" << nf << ")) badc = min(badc, (unsigned long long)cell);\n";
-        o << "        }\n";
     }
+    // ---- pointwise map per (m-block, owned quadrature point)
+    for (int s = 0; s < TQL; ++s) {
+        o << "        const int q" << s << " = ch * " << L.TQ << " + " << 4 * s << " + g;\n";
+        o << "        const bool qok" << s << " = q" << s << " < " << sig.Q << ";\n";
+        o << "        const double wq" << s << " = qok" << s << " ? __ldg(&P.tabg[" << sig.w_off << " + q" << s << "]) : 0.0;\n";
+    }
+    for (int j = 0; j < MBJ; ++j)
+        for (int s = 0; s < TQL; ++s) {
+            o << "        double E" << s << "_0" << J << j;
+            for (int k = 1; k < sig.Tw; ++k) o << ", E" << s << "_" << k << J << j;
+            o << ";\n";
+            o << "        {\n";
+            std::string nf = "false";
+            for (size_t gi = 0; gi < L.groups.size(); ++gi) {
+                const DmmaGroup& g = L.groups[gi];
+                for (size_t ti = 0; ti < g.terms.size(); ++ti) {
+                    const int slot = static_cast<int>(ti) * TQL + s;
+                    const std::string v = (g.vec ? "t" : "s") + S(g.space) + "_" + S(g.terms[ti]);
+                    o << "          const double " << v << " = S" << gi << "_" << slot / 2 << J << j << "_" << slot % 2 << ";\n";
+                    const bool used = g.vec ? vd_used.count({g.space, g.terms[ti]}) : sd_used.count({g.space, g.terms[ti]});
+                    if (!used) nf += " | NF(" + v + ")";
+                }
+            }
+            for (int h = 0; h < nH; ++h) o << "          const double n" << H.stored[h] << " = hv" << h << J << j << ";\n";
+            for (int id : H.consts) {
+                char buf[64];
+                std::snprintf(buf, sizeof buf, "%a", sig.nodes[id].value);
+                o << "          const double n" << id << " = (" << buf << ");\n";
+            }
+            {
+                std::ostringstream m;
+                emit_map_nodes(m, sig, live, qdep, true, "wq" + S(s));
+                o << m.str();
+            }
+            for (int k = 0; k < sig.Tw; ++k) {
+                o << "          E" << s << "_" << k << J << j << " = qok" << s << " ? n" << sig.outputs[k] << " : 0.0;\n";
+                nf += " | NF(n" + S(sig.outputs[k]) + ")";
+            }
+            o << "          if (cok" << j << " && qok" << s << " && (" << nf << ")) badc = min(badc, (unsigned long long)cell" << j
+              << ");\n";
+            o << "        }\n";
+        }
     // ---- quadrature GEMM: k-step kappa = (k, s)
     for (int kq = 0; kq < L.KQ; ++kq) {
         const int k = kq / TQL, s = kq % TQL;
-        for (int nb = 0; nb < L.NBQ; ++nb)
-            o << "        DMMA(y" << nb << "_0, y" << nb << "_1, E" << s << "_" << k << ", Fc["
-              << (L.foff_q + static_cast<long long>(nb) * L.KQ + kq) * 32 << "]);\n";
+        for (int nb = 0; nb < L.NBQ; ++nb) {
+            o << "        { const double b = Fc[" << (L.foff_q + static_cast<long long>(nb) * L.KQ + kq) * 32 << "];";
+            for (int j = 0; j < MBJ; ++j)
+                o << " DMMA(y" << nb << J << j << "_0, y" << nb << J << j << "_1, E" << s << "_" << k << J << j << ", b);";
+            o << " }\n";
+        }
     }
     o << "      }\n";  // chunks
     // ---- scatter from the accumulator fragments
-    o << "      if (cok) {\n";
-    for (int nb = 0; nb < L.NBQ; ++nb)
-        for (int i = 0; i < 2; ++i) {
-            const std::string v = "y" + S(nb) + "_" + S(i);
-            const bool partial = nb * 8 + 8 > sig.nW;
-            o << "        " << (partial ? "if (" + S(nb * 8 + i) + " + 2 * g < " + S(sig.nW) + ") " : "") << "{\n";
-            o << "          if (NF(" << v << ")) badc = min(badc, (unsigned long long)cell);\n";
-            o << "          atomicAdd(&P.y[__ldg(&P.tm[(" << nb * 8 + i << " + 2 * g) * STR + cell])], " << v << ");\n";
-            o << "        }\n";
+    const Sp* tsp = nullptr;
+    for (const Sp& sp : sps)
+        if (tv && sp.vec && sp.i == kp.tvec) tsp = &sp;
+    for (int j = 0; j < MBJ; ++j) {
+        if (tsp) {
+            // interleaved vector test space: y index = node(cell, a) * dim + comp with jw = a * dim + comp;
+            // node(cell r, a) was gathered by lane 4r + (a & 3) as its k-step a >> 2 index
+            const int d = sig.dim, KS = L.groups[tsp->gids[0]].KS;
+            for (int nb = 0; nb < L.NBQ; ++nb)
+                for (int i = 0; i < 2; ++i) {
+                    const int jlo = nb * 8 + i, jhi = std::min(nb * 8 + i + 6, sig.nW - 1);
+                    if (jlo > sig.nW - 1) continue;
+                    const int klo = (jlo / d) >> 2, khi = (jhi / d) >> 2;
+                    o << "      int ty" << nb << "_" << i << J << j << ";\n";
+                    o << "      {\n        const int jw = " << nb * 8 + i << " + 2 * g, a = jw / " << d << ";\n";
+                    o << "        const int src = (r << 2) | (a & 3);\n";
+                    std::string sel = "-1";
+                    for (int ks = std::min(khi, KS - 1); ks >= klo; --ks) {
+                        o << "        const int t" << ks << " = __shfl_sync(0xffffffffu, " << ixname(PF ? "ixC" : "ix", *tsp, ks, j)
+                          << ", src);\n";
+                        sel = "((a >> 2) == " + S(ks) + " ? t" + S(ks) + " : " + sel + ")";
+                    }
+                    o << "        ty" << nb << "_" << i << J << j << " = " << sel << " * " << d << " + jw % " << d << ";\n      }\n";
+                }
         }
-    o << "      }\n";
-    o << "    }\n";  // m-blocks
+        o << "      if (cok" << j << ") {\n";
+        for (int nb = 0; nb < L.NBQ; ++nb)
+            for (int i = 0; i < 2; ++i) {
+                const std::string v = "y" + S(nb) + J + S(j) + "_" + S(i);
+                const bool partial = nb * 8 + 8 > sig.nW;
+                o << "        " << (partial ? "if (" + S(nb * 8 + i) + " + 2 * g < " + S(sig.nW) + ") " : "") << "{\n";
+                o << "          if (NF(" << v << ")) badc = min(badc, (unsigned long long)cell" << j << ");\n";
+                const std::string yi = tsp ? "ty" + S(nb) + "_" + S(i) + J + S(j)
+                                           : "__ldg(&P.tm[(" + S(nb * 8 + i) + " + 2 * g) * STR + cell" + S(j) + "])";
+                o << "          " << (scatter_store ? "P.y[" : "atomicAdd(&P.y[") << yi << "]" << (scatter_store ? " = " : ", ") << v
+                  << (scatter_store ? ";\n" : ");\n");
+                o << "        }\n";
+            }
+        o << "      }\n";
+    }
+    o << "    }\n";  // m-groups
     if (sig.affine || nH > 0) o << "    __syncwarp();\n";
     o << "  }\n";  // tasks
     o << "  if (badc != ~0ULL) atomicMin(P.bad, badc);\n";

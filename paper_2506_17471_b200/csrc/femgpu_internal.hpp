@@ -1,6 +1,7 @@
 // femgpu_internal.hpp — host-side runtime structures of libfemgpu (not part of the ABI).
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <map>
 #include <memory>
@@ -55,6 +56,14 @@ struct Signature {
 
 Signature signature_from(const femgpu_problem* p);
 
+// Device layout of vector inputs and coordinates: node-major with the components padded to a
+// 16-byte multiple (3D: [node][4]), so a node's components are one aligned 16 B + 8 B pair of
+// loads instead of three 8 B loads (fewer L1 wavefronts per gather).  The host (ABI) layout stays
+// [node*dim + comp]; femgpu_create / set_inputs pad on upload.
+inline int vec_stride(int dim) { return dim == 3 ? 4 : dim; }
+// layout.cu: host [rows][d] -> device [rows][vec_stride(d)] (staging: rows*d doubles on the device)
+void upload_padded(double* dst, const double* src_host, long long rows, int d, double* staging, cudaStream_t stream);
+
 // Kernel families.
 enum class Family { Scpt, Tile, Mlt, Macro, Dmma };
 
@@ -72,6 +81,7 @@ struct KernelPlan {
     // Tile family: map-group ids per space (-1 = not staged) and smem capacities.
     std::vector<int> sgroup, vgroup;
     int tgroup = -1, cgroup = -1;
+    int tvec = -1;                     // DMMA: vector space whose node map interleaves into the test map
     std::vector<int> group_entries, group_cap;   // per group: entries per cell, max unique per tile
     // MLT family (TilingParams)
     int Nc = 1, Nwi = 1, TQ = 1, Ter = 1, Tqr = 1, Tqc = 1;
@@ -162,7 +172,8 @@ struct MacroLayout {
 
 struct DeviceSpace {
     int dofs = 0, terms = 0, global = 0;
-    double* d_x = nullptr;          // input vector
+    double* d_x = nullptr;          // input vector (vector spaces: padded [node][vec_stride])
+    double* d_stage = nullptr;      // vector spaces: contiguous upload staging ([node][dim])
     int32_t* d_mapT = nullptr;      // [entry][cell] (SoA, coalesced); may alias another space's
     int group = -1;                 // content-equal map group
 };
@@ -179,6 +190,10 @@ struct Instance {
     double* d_coords = nullptr;
     int coord_global = 0;
     int test_group = -1, coord_group = -1;
+    // vector space i with test_map[c][a*dim + comp] == map_i[c][a]*dim + comp (interleaved vector
+    // test space, form.hpp:664-665 convention), or -1: the scatter can then reuse the gathered node
+    // indices instead of reading the (dim x larger) test map
+    int test_vspace = -1;
     std::vector<std::vector<int32_t>> group_maps;  // host copies of distinct maps ([cell][entry])
     std::vector<int> group_global;
     double* d_y = nullptr;
@@ -195,6 +210,10 @@ struct Instance {
     int64_t device_bytes = 0;
     int64_t last_launches = 0;
     std::mutex mu;                  // serialises actions on this instance (tune(jobs>1))
+    // automatic schedule (s == NULL): chosen once per instance by tune.cpp
+    bool auto_ready = false;
+    femgpu_schedule auto_sched{};
+    std::string auto_log;
 
     ~Instance();
     template <typename T>
@@ -218,5 +237,9 @@ KernelPlan resolve_schedule(Instance& inst, const femgpu_schedule* s);
 void run_action(Instance& inst, const KernelPlan& kp, double* d_y, cudaStream_t stream,
                 cudaEvent_t after_zero = nullptr);
 void check_failure(Instance& inst, const KernelPlan& kp, cudaStream_t stream);
+// tune.cpp: the automatic schedule (cost-model pruning + empirical timing, cached per instance)
+void autotune(Instance& inst);
+KernelPlan plan_for(Instance& inst, const femgpu_schedule* s);
+std::string describe_plan(const KernelPlan& kp);
 
 }  // namespace femgpu

@@ -295,20 +295,35 @@ std::unique_ptr<Instance> create_instance(const femgpu_problem* p) {
         ds.global = sp.global_count;
         ds.group = group_of(sp.map, sp.dofs, sp.global_count);
         ds.d_mapT = group_dev[ds.group];
-        const size_t n = static_cast<size_t>(sp.global_count) * s.dim;
+        const int vs = vec_stride(s.dim);
+        const size_t n = static_cast<size_t>(sp.global_count) * vs;
         ds.d_x = I.alloc<double>(n);
-        FG_CUDA(cudaMemcpy(ds.d_x, sp.input, sizeof(double) * n, cudaMemcpyHostToDevice));
+        if (vs != s.dim) ds.d_stage = I.alloc<double>(static_cast<size_t>(sp.global_count) * s.dim);
+        upload_padded(ds.d_x, sp.input, sp.global_count, s.dim, ds.d_stage, nullptr);
         I.vspaces.push_back(ds);
     }
     if (s.affine) {
         I.coord_group = group_of(p->coord_map, p->coord_dofs, p->coord_global_count);
         I.d_cmapT = group_dev[I.coord_group];
         I.coord_global = p->coord_global_count;
-        const size_t n = static_cast<size_t>(p->coord_global_count) * s.dim;
+        const int vs = vec_stride(s.dim);
+        const size_t n = static_cast<size_t>(p->coord_global_count) * vs;
         I.d_coords = I.alloc<double>(n);
-        FG_CUDA(cudaMemcpy(I.d_coords, p->coords, sizeof(double) * n, cudaMemcpyHostToDevice));
+        double* stage = vs != s.dim ? I.alloc<double>(static_cast<size_t>(p->coord_global_count) * s.dim) : nullptr;
+        upload_padded(I.d_coords, p->coords, p->coord_global_count, s.dim, stage, nullptr);
+        FG_CUDA(cudaDeviceSynchronize());
     }
     I.d_tmapT = group_dev[I.test_group];
+    for (int i = 0; i < s.nv() && I.test_vspace < 0; ++i) {
+        const femgpu_space& sp = p->vector_spaces[i];
+        if (static_cast<long long>(sp.dofs) * s.dim != p->test_dofs) continue;
+        bool ok = true;
+        for (long long c = 0; c < I.cells && ok; ++c)
+            for (int a = 0; a < sp.dofs && ok; ++a)
+                for (int comp = 0; comp < s.dim && ok; ++comp)
+                    ok = p->test_map[c * p->test_dofs + a * s.dim + comp] == sp.map[c * sp.dofs + a] * s.dim + comp;
+        if (ok) I.test_vspace = i;
+    }
     for (const auto& g : groups) {
         I.group_maps.emplace_back(g.m, g.m + static_cast<size_t>(I.cells) * g.entries);
         I.group_global.push_back(g.global);
@@ -453,6 +468,11 @@ void resolve_dmma(const Signature& sig, KernelPlan& kp, const femgpu_schedule* s
     kp.block = s->block_cells > 0 ? s->block_cells : 256;
     if (kp.block % 32 || kp.block > 1024) fail(FEMGPU_E_INFEASIBLE, "dmma: threads per CTA must be a multiple of 32 and <= 1024");
     kp.min_blocks = s->reserved[2] > 0 ? s->reserved[2] : 1;
+    // m-blocks sharing each B-fragment load, and software prefetch of the next m-group's gather
+    kp.Ter = s->eval_row_tile > 0 ? s->eval_row_tile : 1;
+    if (kp.Ter > kp.Nc / 8 || (kp.Nc / 8) % kp.Ter)
+        fail(FEMGPU_E_INFEASIBLE, "dmma: joint m-blocks (eval_row_tile) must divide the m-blocks of a warp task");
+    kp.Tqr = s->quad_row_tile > 0 ? 1 : 0;
     const int q4 = (sig.Q + 3) / 4 * 4;
     if (s->quad_tile > 0) {
         kp.TQ = std::min(q4, (s->quad_tile + 3) / 4 * 4);
@@ -671,6 +691,7 @@ KernelPlan resolve_schedule(Instance& I, const femgpu_schedule* s) {
     }
     if (s->kind == FEMGPU_DMMA) {
         resolve_dmma(sig, kp, s);
+        kp.tvec = I.test_vspace;
         return kp;
     }
     // SCPT: one thread per cell.

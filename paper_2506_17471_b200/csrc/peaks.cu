@@ -1,7 +1,9 @@
-// peaks.cu — ahead-of-time sm_100a kernels of libfemgpu: the FP64 roofline denominator.
+// peaks.cu — ahead-of-time sm_100a kernels of libfemgpu: the FP64 roofline denominators.
 // MEASURED_PEAKS.json (driver-written) carries only an HBM copy and a bf16 GEMM figure, so
-// the FP64 DFMA peak is measured live on the same GPU by femgpu_fp64_peak (8 independent
-// FMA chains per thread, 8 CTAs of 256 threads per SM, best of 5 timed with CUDA events).
+// the FP64 peaks are measured live on the same GPU: femgpu_fp64_peak (DFMA: 8 independent
+// FMA chains per thread, 8 CTAs of 256 threads per SM) and femgpu_fp64_dmma_peak (DMMA
+// m8n8k4: 4 accumulators per warp), each the best of 5 timed with CUDA events.  The form
+// roofline uses the larger of the two (the machine's FP64 peak).
 #include <cuda_runtime.h>
 
 #include "femgpu_internal.hpp"
@@ -21,7 +23,59 @@ __global__ void dfma_peak_kernel(double* out, int iters, double a, double b) {
     if (s == 12345.678) out[blockIdx.x] = s;
 }
 
+// FP64 tensor path: mma.sync m8n8k4 .f64 (SASS DMMA), 4 independent accumulators per warp.
+__global__ void dmma_peak_kernel(double* out, int iters) {
+    double a = 1.0 + threadIdx.x * 1e-3, b = 1.0 - threadIdx.x * 1e-3;
+    double c[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                             : "+d"(c[k][0]), "+d"(c[k][1]) : "d"(a), "d"(b));
+        }
+    }
+    double s = 0;
+    for (int k = 0; k < 4; ++k) s += c[k][0] + c[k][1];
+    if (s == 12345.678) out[blockIdx.x] = s;
+}
+
 }  // namespace
+
+extern "C" femgpu_status femgpu_fp64_dmma_peak(double* tflops) {
+    try {
+        int dev = 0, sms = 0;
+        FG_CUDA(cudaGetDevice(&dev));
+        FG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        double* out = nullptr;
+        FG_CUDA(cudaMalloc(&out, sizeof(double) * 8 * sms));
+        cudaEvent_t e0, e1;
+        FG_CUDA(cudaEventCreate(&e0));
+        FG_CUDA(cudaEventCreate(&e1));
+        const int blocks = 8 * sms, threads = 256, iters = 1024;
+        dmma_peak_kernel<<<blocks, threads>>>(out, 16);
+        FG_CUDA(cudaGetLastError());
+        double best = 0.0;
+        for (int t = 0; t < 5; ++t) {
+            FG_CUDA(cudaEventRecord(e0));
+            dmma_peak_kernel<<<blocks, threads>>>(out, iters);
+            FG_CUDA(cudaEventRecord(e1));
+            FG_CUDA(cudaEventSynchronize(e1));
+            float ms = 0.f;
+            FG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+            const double flops = 512.0 * (blocks * threads / 32) * static_cast<double>(iters) * 8 * 4;
+            if (flops / (ms * 1e-3) > best) best = flops / (ms * 1e-3);
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaFree(out);
+        if (tflops) *tflops = best / 1e12;
+        return FEMGPU_OK;
+    } catch (const femgpu::Error& e) {
+        return e.code;
+    }
+}
 
 extern "C" femgpu_status femgpu_fp64_peak(double* tflops, double* sm_clock_ghz) {
     try {

@@ -1,0 +1,141 @@
+// tune.cpp — the automatic schedule (s == NULL at the C-ABI): the paper's "cost model prunes
+// the schedule space to a few candidates that are timed empirically per form", on B200.
+//
+// The reference ranks TilingParams candidates with an analytic bytes/bandwidth model
+// (perf_model.hpp:146-294, search.hpp:211-251, b = 9 + SCPT) and `tune` runs them through a
+// measuring Executor (search.hpp:338-416).  Here the candidate space is the B200 kernel
+// families: the DFMA families (macro-elements or SCPT, one thread per cell) and the warp-level
+// DMMA family with its knobs (joint m-blocks, gather prefetch, CTA size).  The model counts FP64
+// pipe slots per cell for each family (DFMA: usable FMAs + map + geometry at ~50 % pipe
+// efficiency; DMMA: padded m8n8k4 slots at ~55 %, measured round 1), keeps every family within
+// 1.6x of the best prediction, and each kept candidate is timed with CUDA events on the
+// instance stream ([zero y + action], 2 warm-up + 5 timed).  The winner is cached in the
+// instance.  Small instances (< kTuneMinCells) skip the timing and use the DFMA default.
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <sstream>
+
+#include "femgpu_internal.hpp"
+
+namespace femgpu {
+
+namespace {
+
+constexpr long long kTuneMinCells = 200000;
+
+femgpu_schedule dfma_default() {
+    femgpu_schedule s{};
+    s.kind = FEMGPU_SCPT;
+    return s;
+}
+
+femgpu_schedule dmma_variant(int joint, int prefetch, int block, int cells) {
+    femgpu_schedule s{};
+    s.kind = FEMGPU_DMMA;
+    s.eval_row_tile = joint;
+    s.quad_row_tile = prefetch;
+    s.block_cells = block;
+    s.cells_per_group = cells;
+    return s;
+}
+
+// FP64-pipe slots (FMA lanes) per cell of the map DAG evaluated at every quadrature point.
+long long map_ops(const Signature& sig) {
+    long long ops = 0;
+    for (const auto& n : sig.nodes)
+        if (n.op == FEMGPU_OP_ADD || n.op == FEMGPU_OP_MUL) ++ops;
+    return ops;
+}
+
+}  // namespace
+
+std::string describe_plan(const KernelPlan& kp) {
+    std::ostringstream s;
+    switch (kp.family) {
+        case Family::Macro: s << "femgpu_macro G=" << kp.G << " block=" << kp.block; break;
+        case Family::Scpt: s << "femgpu_scpt block=" << kp.block; break;
+        case Family::Tile: s << "femgpu_tile cells=" << kp.tile_cells; break;
+        case Family::Mlt: s << "femgpu_mlt Nc=" << kp.Nc << " Nwi=" << kp.Nwi << " TQ=" << kp.TQ; break;
+        case Family::Dmma:
+            s << "femgpu_dmma cells/task=" << kp.Nc << " TQ=" << kp.TQ << " joint=" << kp.Ter << " prefetch=" << kp.Tqr
+              << " block=" << kp.block << " basis=" << (kp.basis == FEMGPU_BASIS_SMEM ? "smem" : "l1");
+            break;
+    }
+    return s.str();
+}
+
+void autotune(Instance& I) {
+    I.auto_ready = true;
+    I.auto_sched = dfma_default();
+    I.auto_log.clear();
+    const char* env = std::getenv("FEMGPU_AUTOTUNE");
+    if ((env && std::strcmp(env, "0") == 0) || I.cells < kTuneMinCells) {
+        I.auto_log = "default (no timing: " + std::string(I.cells < kTuneMinCells ? "small instance" : "FEMGPU_AUTOTUNE=0") + ")";
+        return;
+    }
+    const Signature& sig = I.sig;
+    // ---- model: FP64-pipe lane-slots per cell
+    const double usable_fma = static_cast<double>(sig.usable_flops()) / 2.0;
+    const double map_slots = static_cast<double>(map_ops(sig)) * sig.Q;
+    const double geo_slots = sig.affine ? 6.0 * sig.dim * sig.dim : 0.0;
+    const double t_dfma = (usable_fma + map_slots + geo_slots) / 0.50;
+    double t_dmma = 1e300;
+    {
+        KernelPlan kp;
+        femgpu_schedule s = dmma_variant(1, 0, 0, 0);
+        try {
+            resolve_dmma(sig, kp, &s);
+            const DmmaLayout L = dmma_layout(sig, kp);
+            const double dmma_slots = static_cast<double>(L.nfrag) * 256.0 / 8.0;  // per cell
+            t_dmma = dmma_slots / 0.55 + (map_slots * (4.0 * L.TQL * L.NCH) / sig.Q + geo_slots) / 0.5;
+        } catch (const Error&) {
+        }
+    }
+    const double best = std::min(t_dfma, t_dmma);
+    std::vector<femgpu_schedule> cands;
+    if (t_dfma <= 1.6 * best) cands.push_back(dfma_default());
+    if (t_dmma <= 1.6 * best) {
+        for (int joint : {1, 2})
+            for (int prefetch : {0, 1})
+                for (int block : {128, 256}) cands.push_back(dmma_variant(joint, prefetch, block, 32));
+    }
+    std::ostringstream log;
+    log << "model slots/cell: dfma " << static_cast<long long>(t_dfma) << ", dmma "
+        << (t_dmma < 1e299 ? std::to_string(static_cast<long long>(t_dmma)) : std::string("n/a")) << "; timed:";
+    double best_t = 1e300;
+    for (const auto& c : cands) {
+        try {
+            const KernelPlan kp = resolve_schedule(I, &c);
+            for (int i = 0; i < 2; ++i) run_action(I, kp, I.d_y, I.stream);
+            FG_CUDA(cudaEventRecord(I.ev0, I.stream));
+            const int reps = 5;
+            for (int i = 0; i < reps; ++i) run_action(I, kp, I.d_y, I.stream);
+            FG_CUDA(cudaEventRecord(I.ev1, I.stream));
+            FG_CUDA(cudaEventSynchronize(I.ev1));
+            float ms = 0.f;
+            FG_CUDA(cudaEventElapsedTime(&ms, I.ev0, I.ev1));
+            const double t = ms * 1e-3 / reps;
+            log << " [" << describe_plan(kp) << ": " << static_cast<long long>(t * 1e7) / 10.0 << " us]";
+            if (t < best_t) {
+                best_t = t;
+                I.auto_sched = c;
+            }
+        } catch (const Error& e) {
+            if (e.code != FEMGPU_E_INFEASIBLE && e.code != FEMGPU_E_JIT) throw;
+            log << " [infeasible: " << e.what() << "]";
+        }
+    }
+    // a non-finite input must not leave a stale flag behind the tuning runs
+    FG_CUDA(cudaMemsetAsync(I.d_bad, 0xff, 2 * sizeof(unsigned long long), I.stream));
+    FG_CUDA(cudaStreamSynchronize(I.stream));
+    I.auto_log = log.str();
+}
+
+KernelPlan plan_for(Instance& I, const femgpu_schedule* s) {
+    if (s) return resolve_schedule(I, s);
+    if (!I.auto_ready) autotune(I);
+    return resolve_schedule(I, &I.auto_sched);
+}
+
+}  // namespace femgpu

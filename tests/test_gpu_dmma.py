@@ -26,8 +26,12 @@ def close(y, ref):
 
 def random_dmma(sig, rng):
     pick = lambda hi: 1 + rng.next_u64() % hi  # noqa: E731
-    return fg.TilingParams.dmma(cells_per_group=8 * pick(4), quad_tile=pick(sig.quad_points),
+    mb = pick(4)
+    joint = [j for j in (1, 2, 3, 4) if mb % j == 0]
+    return fg.TilingParams.dmma(cells_per_group=8 * mb, quad_tile=pick(sig.quad_points),
                                 lanes_per_cell=(0, 4)[rng.next_u64() % 2], block_cells=32 * pick(8),
+                                eval_row_tile=joint[rng.next_u64() % len(joint)],
+                                quad_row_tile=rng.next_u64() % 2,
                                 basis=abi.BASIS_SMEM if rng.next_u64() % 2 else abi.BASIS_CONST)
 
 
@@ -64,6 +68,8 @@ def test_dmma_mesh_forms(oracle, form, dim, deg, Q, n):
     with fg.GpuInstance(p) as g:
         close(g.action(fg.TilingParams.dmma()), ref)
         close(g.action(fg.TilingParams.dmma(quad_tile=max(1, Q // 4 + 1), cells_per_group=16)), ref)
+        close(g.action(fg.TilingParams.dmma(eval_row_tile=2, quad_row_tile=1)), ref)
+        close(g.action(fg.TilingParams.dmma(cells_per_group=24, eval_row_tile=3, quad_row_tile=1)), ref)
 
 
 def test_dmma_known_answer():

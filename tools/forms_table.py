@@ -1,0 +1,45 @@
+"""The benchmark-forms table: automatic schedule per config, step split, and the
+fraction of the form roofline t_roof = max(bytes_alg / BW_HBM, flops_alg / F_FP64), F_FP64 = max of the
+live DFMA and DMMA peaks.  One JSON line per config.
+
+usage: python tools/forms_table.py [C1,C1b,...]   (default: every config)
+"""
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, ".")
+import paper_2506_17471_b200 as fg  # noqa: E402
+from bench import algorithmic_bytes, load_peaks  # noqa: E402
+
+
+def main():
+    names = sys.argv[1].split(",") if len(sys.argv) > 1 else list(fg.CONFIGS)
+    pk = fg.fp64_peaks()
+    hbm = load_peaks().get("hbm_gbs") or 6545.9
+    print(json.dumps({"peaks": pk, "hbm_gbs": hbm}), flush=True)
+    for name in names:
+        t0 = time.time()
+        try:
+            p = fg.config_problem(name)
+            cells = p.connectivity.cell_count
+            flops = fg.usable_flops(p.signature) * cells
+            byts = algorithmic_bytes(p)
+            t_roof = max(flops / (pk["fp64"] * 1e12), byts / (hbm * 1e9))
+            with fg.GpuInstance(p) as g:
+                g.action()
+                step, kern, zero = g.profile(warmup=3, reps=20)
+                plan = g.describe()
+            print(json.dumps({"config": name, "cells": cells, "dofs": p.output_size, "step_us": round(step * 1e6, 1),
+                              "kernel_us": round(kern * 1e6, 1), "zero_us": round(zero * 1e6, 1),
+                              "t_roof_us": round(t_roof * 1e6, 1),
+                              "bound": "fp64" if flops / (pk["fp64"] * 1e12) >= byts / (hbm * 1e9) else "hbm",
+                              "frac_step": round(t_roof / step, 3), "gdofs": round(p.output_size / step / 1e9, 2),
+                              "plan": plan, "wall_s": round(time.time() - t0, 1)}), flush=True)
+        except Exception as e:  # noqa: BLE001
+            print(json.dumps({"config": name, "error": str(e)[:300]}), flush=True)
+
+
+if __name__ == "__main__":
+    main()

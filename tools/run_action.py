@@ -4,6 +4,7 @@ import sys
 sys.path.insert(0, ".")
 import paper_2506_17471_b200 as fg
 from paper_2506_17471_b200 import abi
+from tools.sweep import sched
 
 SCHED = {
     "auto": None,
@@ -20,5 +21,5 @@ n = int(sys.argv[4]) if len(sys.argv) > 4 else None
 p = fg.config_problem(cfg, n=n)
 with fg.GpuInstance(p) as g:
     for _ in range(reps):
-        g.action(SCHED[label])
+        g.action(SCHED[label] if label in SCHED else sched(label))
 print("done", cfg, label, reps)
