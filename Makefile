@@ -6,7 +6,7 @@ PKG := paper_2506_17471_b200
 SRC := $(PKG)/csrc
 OBJDIR := build/obj
 LIB := $(PKG)/_lib/libfemgpu.so
-CXXSRC := $(SRC)/api.cpp $(SRC)/instance.cpp $(SRC)/emit.cpp $(SRC)/emit_dmma.cpp $(SRC)/jit.cpp $(SRC)/mesh.cpp $(SRC)/tune.cpp
+CXXSRC := $(SRC)/api.cpp $(SRC)/instance.cpp $(SRC)/emit.cpp $(SRC)/emit_dmma.cpp $(SRC)/jit.cpp $(SRC)/mesh.cpp $(SRC)/tune.cpp $(SRC)/io.cpp
 CUSRC := $(wildcard $(SRC)/*.cu)
 HDRS := include/femgpu.h $(SRC)/femgpu_internal.hpp
 NVFLAGS := -gencode arch=compute_100a,code=sm_100a -lineinfo -O3 -std=c++17 -Xcompiler -fPIC,-O2 --expt-relaxed-constexpr
@@ -22,9 +22,10 @@ $(OBJDIR)/%.cu.o: $(SRC)/%.cu $(HDRS)
 	@mkdir -p $(OBJDIR)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
-$(LIB): $(OBJS)
+$(LIB): $(OBJS) $(SRC)/femgpu.map
 	@mkdir -p $(dir $@)
-	$(NVCC) -shared -gencode arch=compute_100a,code=sm_100a -o $@ $(OBJS) -lnvrtc -cudart static -Xlinker -rpath,$(CUDA)/lib64
+	$(NVCC) -shared -gencode arch=compute_100a,code=sm_100a -o $@ $(OBJS) -lnvrtc -cudart static -Xlinker -rpath,$(CUDA)/lib64 \
+	  -Xlinker --version-script=$(SRC)/femgpu.map -Xlinker --exclude-libs,ALL
 
 oracle:
 	$(MAKE) -s -C oracle

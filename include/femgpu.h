@@ -253,6 +253,19 @@ femgpu_status femgpu_action_once(const femgpu_problem* p, double* y_host);
 femgpu_status femgpu_host_alloc(size_t bytes, void** ptr);
 femgpu_status femgpu_host_free(void* ptr);
 
+/* ---- instance / candidate files (femsched io.hpp, format_version 1) ------
+ * The reference's versioned structured-text format (io.hpp:197-391): doubles with 17
+ * significant digits, bit-exact round trip; femgpu_problem_save writes byte-identical text to
+ * femsched::save_instance.  A loaded problem owns its arrays; *view stays valid until
+ * femgpu_problem_free.  Schedule files follow save_candidate/load_candidate (io.hpp:407-460)
+ * for kinds scpt/mlt; the B200 kinds are written as extension kinds ("b200_dmma"). */
+typedef struct femgpu_owned_problem femgpu_owned_problem;
+femgpu_status femgpu_problem_load(const char* path, femgpu_owned_problem** out, const femgpu_problem** view);
+femgpu_status femgpu_problem_free(femgpu_owned_problem* p);
+femgpu_status femgpu_problem_save(const femgpu_problem* p, const char* path);
+femgpu_status femgpu_schedule_save(const femgpu_schedule* s, int32_t n_scalar, int32_t n_vector, const char* path);
+femgpu_status femgpu_schedule_load(const char* path, femgpu_schedule* s);
+
 /* ---- structured meshes (synthetic unit square / unit cube) -------------
  * Unit square: n x n squares, 2 triangles each; unit cube: n^3 cubes, 6 Kuhn
  * tetrahedra each.  P_degree nodes live on the degree-refined lattice and the

@@ -81,6 +81,9 @@ def ref():
         L.ref_time_threads.argtypes = [C.POINTER(abi.Problem), C.c_int, C.c_int, C.c_int, C.c_int,
                                        C.POINTER(C.c_double), C.c_char_p, C.c_int]
         L.ref_time_threads.restype = C.c_double
+        L.ref_save_instance.argtypes = [C.POINTER(abi.Problem), C.c_char_p, C.c_char_p, C.c_int]
+        L.ref_load_instance.argtypes = [C.c_char_p, C.c_char_p, C.c_int]
+        L.ref_load_instance.restype = C.c_void_p
         _ref = L
     return _ref
 
@@ -153,44 +156,29 @@ def ref_make_problem(op: str, dim: int, degree: int, quad_points: int, cells: in
     if not h:
         raise OracleError(1, err.value.decode())
     try:
-        d = L.ref_instance_desc(h).contents
-        Q = d.quad_points
-        sig = FormSignature(dim=d.dim, quad_points=Q, coord_dofs=d.coord_dofs,
-                            affine_geometry=bool(d.affine_geometry), coordinate_space=d.coordinate_space,
-                            word_bytes=d.word_bytes, test_dofs=d.test_dofs, test_deriv_terms=d.test_deriv_terms)
-        tab = Tabulations()
-        conn = MeshConnectivity(cell_count=d.cell_count)
-        sx, vx = [], []
-        for i in range(d.n_scalar):
-            s = d.scalar_spaces[i]
-            sig.scalar_spaces.append(ScalarSpace(s.dofs, s.deriv_terms))
-            tab.scalar_phi.append(_arr(s.phi, s.deriv_terms * Q * s.dofs, np.float64).reshape(s.deriv_terms, Q, s.dofs))
-            conn.scalar_maps.append(IndexMap(_arr(s.map, d.cell_count * s.dofs, np.int32).reshape(d.cell_count, s.dofs),
-                                             s.global_count))
-            sx.append(_arr(s.input, s.global_count, np.float64))
-        for i in range(d.n_vector):
-            s = d.vector_spaces[i]
-            comps = list(_arr(s.components, s.deriv_terms, np.int32))
-            sig.vector_spaces.append(VectorSpace(s.dofs, s.deriv_terms, [int(c) for c in comps]))
-            tab.vector_phi.append(_arr(s.phi, s.deriv_terms * Q * s.dofs, np.float64).reshape(s.deriv_terms, Q, s.dofs))
-            conn.vector_maps.append(IndexMap(_arr(s.map, d.cell_count * s.dofs, np.int32).reshape(d.cell_count, s.dofs),
-                                             s.global_count))
-            vx.append(_arr(s.input, s.global_count * d.dim, np.float64))
-        tab.psi = _arr(d.psi, d.test_deriv_terms * d.test_dofs * Q, np.float64).reshape(d.test_deriv_terms, d.test_dofs, Q)
-        tab.weights = _arr(d.weights, Q, np.float64)
-        conn.test_map = IndexMap(_arr(d.test_map, d.cell_count * d.test_dofs, np.int32).reshape(d.cell_count, d.test_dofs),
-                                 d.test_global_count)
-        if d.affine_geometry:
-            conn.coord_map = IndexMap(_arr(d.coord_map, d.cell_count * d.coord_dofs, np.int32)
-                                      .reshape(d.cell_count, d.coord_dofs), d.coord_global_count)
-            conn.coord_global_count = d.coord_global_count
-            conn.coords = _arr(d.coords, d.coord_global_count * d.dim, np.float64).reshape(d.coord_global_count, d.dim)
-        m = PointwiseMap()
-        for i in range(d.n_map_nodes):
-            n = d.map_nodes[i]
-            m.nodes.append((int(n.op), float(n.value), int(n.a), int(n.b)))
-        m.outputs = [int(x) for x in _arr(d.map_outputs, d.n_map_outputs, np.int32)]
-        p = ProblemInstance(sig, m, tab, conn, sx, vx, d.output_size)
-        return p
+        from paper_2506_17471_b200.io import problem_from_desc
+        return problem_from_desc(L.ref_instance_desc(h).contents)
+    finally:
+        L.ref_free(h)
+
+
+def ref_save_instance(p, path) -> None:
+    """The reference's own femsched::save_instance_file (io.hpp:381-385)."""
+    err = C.create_string_buffer(512)
+    cp = _desc(p)
+    if ref().ref_save_instance(C.byref(cp.desc), str(path).encode(), err, 512):
+        raise OracleError(1, err.value.decode())
+
+
+def ref_load_instance(path) -> ProblemInstance:
+    """The reference's own femsched::load_instance_file (io.hpp:387-391)."""
+    from paper_2506_17471_b200.io import problem_from_desc
+    L = ref()
+    err = C.create_string_buffer(512)
+    h = L.ref_load_instance(str(path).encode(), err, 512)
+    if not h:
+        raise OracleError(1, err.value.decode())
+    try:
+        return problem_from_desc(L.ref_instance_desc(h).contents)
     finally:
         L.ref_free(h)

@@ -14,6 +14,7 @@
 //
 // Build recipe: oracle/Makefile (outputs only into oracle/_ref/).
 #include <femsched/form.hpp>
+#include <femsched/io.hpp>  // needs boost/rational.hpp: third_party/boost shim (qoi.hpp)
 
 #include <algorithm>
 #include <chrono>
@@ -354,6 +355,29 @@ double ref_time_threads(const femgpu_problem* d, int cell_begin, int cell_end, i
     } catch (const std::exception& e) {
         set_err(err, len, e.what());
         return -1.0;
+    }
+}
+
+// femsched::save_instance_file / load_instance_file (io.hpp:381-391), for the io parity tests.
+int ref_save_instance(const femgpu_problem* d, const char* path, char* err, int len) {
+    try {
+        femsched::save_instance_file(path, from_desc(d, 0, d->cell_count));
+        return 0;
+    } catch (const std::exception& e) {
+        set_err(err, len, e.what());
+        return 1;
+    }
+}
+
+void* ref_load_instance(const char* path, char* err, int len) {
+    try {
+        auto h = std::make_unique<Held>();
+        h->p = femsched::load_instance_file(path);
+        flatten(*h);
+        return h.release();
+    } catch (const std::exception& e) {
+        set_err(err, len, e.what());
+        return nullptr;
     }
 }
 

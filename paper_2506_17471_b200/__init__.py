@@ -4,3 +4,4 @@ from .action import (ExecutionOutcome, GpuInstance, TilingParams, device_count, 
                      gpu_action, gpu_executor, jit_check)
 from . import abi  # noqa: F401
 from .mesh import CONFIGS, color_cells, config_problem, mesh_problem, unit_mesh  # noqa: F401
+from .io import load_instance, load_schedule, save_instance, save_schedule  # noqa: F401,E402

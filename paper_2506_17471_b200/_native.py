@@ -24,7 +24,8 @@ EXPORTS = (
     "femgpu_host_alloc", "femgpu_host_free", "femgpu_mesh_counts", "femgpu_mesh_build",
     "femgpu_color_cells", "femgpu_profile_action", "femgpu_fp64_peak",
     "femgpu_time_steps", "femgpu_device_input", "femgpu_describe_schedule",
-    "femgpu_fp64_dmma_peak",
+    "femgpu_fp64_dmma_peak", "femgpu_problem_load", "femgpu_problem_free", "femgpu_problem_save",
+    "femgpu_schedule_save", "femgpu_schedule_load",
 )
 
 
@@ -92,6 +93,11 @@ def lib():
                                            _P(C.c_double), _P(C.c_double)], C.c_int),
                 "femgpu_fp64_peak": ([_P(C.c_double), _P(C.c_double)], C.c_int),
                 "femgpu_fp64_dmma_peak": ([_P(C.c_double)], C.c_int),
+                "femgpu_problem_load": ([C.c_char_p, _P(C.c_void_p), _P(_P(abi.Problem))], C.c_int),
+                "femgpu_problem_free": ([C.c_void_p], C.c_int),
+                "femgpu_problem_save": ([_P(abi.Problem), C.c_char_p], C.c_int),
+                "femgpu_schedule_save": ([_P(abi.Schedule), C.c_int32, C.c_int32, C.c_char_p], C.c_int),
+                "femgpu_schedule_load": ([C.c_char_p, _P(abi.Schedule)], C.c_int),
                 "femgpu_time_steps": ([C.c_void_p, _P(abi.Schedule), C.c_int32, _P(C.c_double)], C.c_int),
                 "femgpu_device_input": ([C.c_void_p, C.c_int32, _P(C.c_void_p)], C.c_int),
             }

@@ -2,6 +2,7 @@
 // exception into a femgpu_status + thread-local message; nothing throws across.
 #include <algorithm>
 #include <cstring>
+#include <fstream>
 #include <string>
 
 #include "femgpu_internal.hpp"
@@ -103,6 +104,10 @@ femgpu_status femgpu_emit_source(const femgpu_problem* p, const femgpu_schedule*
         femgpu::KernelPlan kp;
         if (s && s->kind == FEMGPU_DMMA) {
             femgpu::resolve_dmma(sig, kp, s);
+            // emitter checks without an instance: assume an interleaved vector test space when
+            // the shapes allow it (the instance decides from the actual maps)
+            for (int i = 0; i < sig.nv() && kp.tvec < 0; ++i)
+                if (sig.vdofs[i] * sig.dim == sig.nW) kp.tvec = i;
         } else if (s && s->kind == FEMGPU_MLT) {
             kp.family = femgpu::Family::Mlt;
             kp.TQ = s->quad_tile;
@@ -380,6 +385,51 @@ femgpu_status femgpu_action_once(const femgpu_problem* p, double* y_host) {
     femgpu_destroy(h);
     g_last_error = err;
     return st;
+}
+
+femgpu_status femgpu_problem_load(const char* path, femgpu_owned_problem** out, const femgpu_problem** view) {
+    return guard([&] {
+        if (!path || !out || !view) femgpu::invalid("null argument");
+        std::ifstream is(path, std::ios::binary);
+        if (!is) femgpu::invalid(std::string("cannot open: ") + path);
+        femgpu_owned_problem* p = femgpu::load_problem(is);
+        *out = p;
+        *view = femgpu_owned_view(p);
+    });
+}
+
+femgpu_status femgpu_problem_free(femgpu_owned_problem* p) {
+    return guard([&] { femgpu_owned_delete(p); });
+}
+
+femgpu_status femgpu_problem_save(const femgpu_problem* p, const char* path) {
+    return guard([&] {
+        if (!p || !path) femgpu::invalid("null argument");
+        std::ofstream os(path, std::ios::binary);
+        if (!os) femgpu::invalid(std::string("cannot open for writing: ") + path);
+        femgpu::save_problem(os, p);
+        if (!os) femgpu::invalid(std::string("write failed: ") + path);
+    });
+}
+
+femgpu_status femgpu_schedule_save(const femgpu_schedule* s, int32_t n_scalar, int32_t n_vector, const char* path) {
+    return guard([&] {
+        if (!s || !path) femgpu::invalid("null argument");
+        if (n_scalar < 0 || n_vector < 0 || n_scalar > FEMGPU_MAX_SPACES || n_vector > FEMGPU_MAX_SPACES)
+            femgpu::invalid("candidate file: bad space counts");
+        std::ofstream os(path, std::ios::binary);
+        if (!os) femgpu::invalid(std::string("cannot open for writing: ") + path);
+        femgpu::save_schedule(os, s, n_scalar, n_vector);
+    });
+}
+
+femgpu_status femgpu_schedule_load(const char* path, femgpu_schedule* s) {
+    return guard([&] {
+        if (!path || !s) femgpu::invalid("null argument");
+        std::ifstream is(path, std::ios::binary);
+        if (!is) femgpu::invalid(std::string("cannot open: ") + path);
+        *s = femgpu::load_schedule(is);
+    });
 }
 
 femgpu_status femgpu_host_alloc(size_t bytes, void** ptr) {

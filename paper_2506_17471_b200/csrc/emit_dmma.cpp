@@ -325,17 +325,29 @@ void emit_dmma_kernel(std::ostringstream& o, const Signature& sig, const KernelP
             }
     };
     const int NG = MB / MBJ;
+    // interleaved vector test space: its node indices feed the scatter too
+    const Sp* tsp = nullptr;
+    for (const Sp& sp : sps)
+        if (tv && sp.vec && sp.i == kp.tvec) tsp = &sp;
     if (PF) {
-        // declarations of the loop-carried prefetch registers
+        // loop-carried prefetch registers: ixN = indices of m-group grp+1, uN = values of grp,
+        // ixK = indices of grp (only the test-space indices are kept)
         for (int j = 0; j < MBJ; ++j)
             for (const Sp& sp : sps) {
                 const DmmaGroup& g0 = L.groups[sp.gids[0]];
                 for (int ks = 0; ks < g0.KS; ++ks) {
                     o << "    int " << ixname("ixN", sp, ks, j) << " = -1;\n";
+                    if (&sp == tsp) o << "    int " << ixname("ixK", sp, ks, j) << " = -1;\n";
                     for (int gid : sp.gids) o << "    double " << uname("uN", gid, ks, j) << " = 0.0;\n";
                 }
             }
     }
+    auto copy_tidx = [&](const std::string& ind, const std::string& dst, const std::string& src) {
+        if (!tsp) return;
+        for (int j = 0; j < MBJ; ++j)
+            for (int ks = 0; ks < L.groups[tsp->gids[0]].KS; ++ks)
+                o << ind << ixname(dst, *tsp, ks, j) << " = " << ixname(src, *tsp, ks, j) << ";\n";
+    };
     o << "    #pragma unroll 1\n";
     o << "    for (int grp = 0; grp < " << NG << "; ++grp) {\n";
     if (PF) {
@@ -343,6 +355,7 @@ void emit_dmma_kernel(std::ostringstream& o, const Signature& sig, const KernelP
         o << "      if (grp == 0) {\n";
         emit_idx("        ", "ixN", "0", false);
         emit_vals("        ", "ixN", "uN", false);
+        copy_tidx("        ", "ixK", "ixN");
         if (NG > 1) emit_idx("        ", "ixN", "1", false);
         o << "      }\n";
         for (int j = 0; j < MBJ; ++j)
@@ -350,12 +363,13 @@ void emit_dmma_kernel(std::ostringstream& o, const Signature& sig, const KernelP
                 for (int ks = 0; ks < L.groups[sp.gids[0]].KS; ++ks) {
                     for (int gid : sp.gids)
                         o << "      const double " << uname("uA", gid, ks, j) << " = " << uname("uN", gid, ks, j) << ";\n";
-                    if (tv && sp.vec && sp.i == kp.tvec)
-                        o << "      const int " << ixname("ixC", sp, ks, j) << " = " << ixname("ixN", sp, ks, j) << ";\n";
+                    if (&sp == tsp)
+                        o << "      const int " << ixname("ixC", sp, ks, j) << " = " << ixname("ixK", sp, ks, j) << ";\n";
                 }
         if (NG > 1) {
             o << "      if (grp + 1 < " << NG << ") {\n";
             emit_vals("        ", "ixN", "uN", false);
+            copy_tidx("        ", "ixK", "ixN");
             o << "      }\n";
             if (NG > 2) {
                 o << "      if (grp + 2 < " << NG << ") {\n";
@@ -447,9 +461,6 @@ void emit_dmma_kernel(std::ostringstream& o, const Signature& sig, const KernelP
     }
     o << "      }\n";  // chunks
     // ---- scatter from the accumulator fragments
-    const Sp* tsp = nullptr;
-    for (const Sp& sp : sps)
-        if (tv && sp.vec && sp.i == kp.tvec) tsp = &sp;
     for (int j = 0; j < MBJ; ++j) {
         if (tsp) {
             // interleaved vector test space: y index = node(cell, a) * dim + comp with jw = a * dim + comp;
@@ -476,6 +487,7 @@ void emit_dmma_kernel(std::ostringstream& o, const Signature& sig, const KernelP
         for (int nb = 0; nb < L.NBQ; ++nb)
             for (int i = 0; i < 2; ++i) {
                 const std::string v = "y" + S(nb) + J + S(j) + "_" + S(i);
+                if (nb * 8 + i >= sig.nW) continue;  // no lane holds a test DOF in this slot
                 const bool partial = nb * 8 + 8 > sig.nW;
                 o << "        " << (partial ? "if (" + S(nb * 8 + i) + " + 2 * g < " + S(sig.nW) + ") " : "") << "{\n";
                 o << "          if (NF(" << v << ")) badc = min(badc, (unsigned long long)cell" << j << ");\n";

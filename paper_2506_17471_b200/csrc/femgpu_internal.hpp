@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <iosfwd>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -237,6 +238,15 @@ KernelPlan resolve_schedule(Instance& inst, const femgpu_schedule* s);
 void run_action(Instance& inst, const KernelPlan& kp, double* d_y, cudaStream_t stream,
                 cudaEvent_t after_zero = nullptr);
 void check_failure(Instance& inst, const KernelPlan& kp, cudaStream_t stream);
+}  // namespace femgpu
+const femgpu_problem* femgpu_owned_view(const femgpu_owned_problem* p);
+void femgpu_owned_delete(femgpu_owned_problem* p);
+namespace femgpu {
+// io.cpp: the reference's structured-text instance / candidate files (io.hpp)
+void save_problem(std::ostream& os, const femgpu_problem* p);
+femgpu_owned_problem* load_problem(std::istream& is);
+void save_schedule(std::ostream& os, const femgpu_schedule* s, int n_scalar, int n_vector);
+femgpu_schedule load_schedule(std::istream& is);
 // tune.cpp: the automatic schedule (cost-model pruning + empirical timing, cached per instance)
 void autotune(Instance& inst);
 KernelPlan plan_for(Instance& inst, const femgpu_schedule* s);

@@ -1,0 +1,521 @@
+// io.cpp — the reference's versioned structured-text instance and candidate files
+// (femsched io.hpp: save_instance/load_instance :197-391, save_candidate/load_candidate
+// :407-460), restated for the flat femgpu_problem descriptor so fixtures written by the
+// reference (or by the CPU oracle) load on a GPU box without the reference, and instances
+// built here can be handed to the reference's CLI (`femsched ... --instance`).
+//
+// Format (format_version 1): "key: value" lines, '#' comments skipped; doubles with 17
+// significant digits (%.17g == iostream setprecision(17)), so a round trip is bit-exact; the
+// writer reproduces the reference writer byte for byte.  Error texts follow the reference's
+// std::runtime_error messages ("instance file: ...").  One extension: map op 9 (J^-1, not in
+// the reference language) is written/read as "node: ijac a b".
+#include <cerrno>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "femgpu_internal.hpp"
+
+struct femgpu_owned_problem {
+    femgpu_problem desc{};
+    std::vector<femgpu_space> sspaces, vspaces;
+    std::vector<std::vector<int32_t>> smaps, vmaps, comps;
+    std::vector<std::vector<double>> sphi, vphi, sin, vin;
+    std::vector<double> psi, weights, coords;
+    std::vector<int32_t> test_map, coord_map, outputs;
+    std::vector<femgpu_map_node> nodes;
+};
+
+const femgpu_problem* femgpu_owned_view(const femgpu_owned_problem* p) { return &p->desc; }
+void femgpu_owned_delete(femgpu_owned_problem* p) { delete p; }
+
+namespace femgpu {
+
+namespace {
+
+constexpr int kFormatVersion = 1;
+
+[[noreturn]] void ferr(const std::string& m) { fail(FEMGPU_E_INVALID, m); }
+
+std::string fmt17(double v) {
+    char buf[40];
+    std::snprintf(buf, sizeof buf, "%.17g", v);
+    return buf;
+}
+
+struct LineReader {
+    std::istream& is;
+    int line_no = 0;
+    std::string next() {
+        std::string line;
+        while (std::getline(is, line)) {
+            ++line_no;
+            if (!line.empty() && line[0] != '#') return line;
+        }
+        ferr("instance file: unexpected end of input at line " + std::to_string(line_no));
+    }
+    std::string expect(const std::string& key) {
+        const std::string line = next();
+        const auto colon = line.find(':');
+        if (colon == std::string::npos || line.substr(0, colon) != key)
+            ferr("instance file: expected '" + key + "' at line " + std::to_string(line_no) + ", got '" + line + "'");
+        auto rest = line.substr(colon + 1);
+        const auto start = rest.find_first_not_of(' ');
+        return start == std::string::npos ? std::string() : rest.substr(start);
+    }
+    long long expect_int(const std::string& key) {
+        const std::string v = expect(key);
+        errno = 0;
+        char* end = nullptr;
+        const long long r = std::strtoll(v.c_str(), &end, 10);
+        if (end == v.c_str() || errno) ferr("instance file: bad integer for '" + key + "' at line " + std::to_string(line_no));
+        return r;
+    }
+};
+
+std::vector<double> parse_doubles(const std::string& line, size_t expected, int line_no) {
+    std::vector<double> out;
+    out.reserve(expected);
+    const char* p = line.c_str();
+    for (;;) {
+        while (*p == ' ' || *p == '\t' || *p == '\r') ++p;
+        if (!*p) break;
+        char* end = nullptr;
+        const double v = std::strtod(p, &end);
+        if (end == p) break;
+        out.push_back(v);
+        p = end;
+    }
+    if (out.size() != expected)
+        ferr("instance file: expected " + std::to_string(expected) + " values at line " + std::to_string(line_no) +
+             ", got " + std::to_string(out.size()));
+    return out;
+}
+
+void write_doubles(std::ostream& os, const double* v, size_t n) {
+    for (size_t i = 0; i < n; ++i) os << (i ? " " : "") << fmt17(v[i]);
+    os << "\n";
+}
+
+// rows x cols row-major block, one row per line
+void write_matrix(std::ostream& os, const double* m, int rows, int cols) {
+    for (int r = 0; r < rows; ++r) {
+        for (int c = 0; c < cols; ++c) os << (c ? " " : "") << fmt17(m[static_cast<size_t>(r) * cols + c]);
+        os << "\n";
+    }
+}
+
+void read_matrix(LineReader& r, int rows, int cols, std::vector<double>& dst) {
+    for (int i = 0; i < rows; ++i) {
+        const auto row = parse_doubles(r.next(), static_cast<size_t>(cols), r.line_no);
+        dst.insert(dst.end(), row.begin(), row.end());
+    }
+}
+
+void write_index_map(std::ostream& os, const char* key, const int32_t* m, int cells, int entries, int global) {
+    os << key << ": " << cells << " " << entries << " " << global << "\n";
+    for (int c = 0; c < cells; ++c) {
+        for (int j = 0; j < entries; ++j) os << (j ? " " : "") << m[static_cast<size_t>(c) * entries + j];
+        os << "\n";
+    }
+}
+
+void read_index_map(LineReader& r, const std::string& key, std::vector<int32_t>& m, int& cells, int& entries,
+                    int& global) {
+    std::istringstream head(r.expect(key));
+    head >> cells >> entries >> global;
+    if (head.fail()) ferr("instance file: bad index map header for " + key);
+    if (cells < 0 || entries < 0) ferr("instance file: bad index map header for " + key);
+    m.resize(static_cast<size_t>(cells) * entries);
+    for (int c = 0; c < cells; ++c) {
+        const std::string line = r.next();
+        const char* p = line.c_str();
+        for (int j = 0; j < entries; ++j) {
+            char* end = nullptr;
+            const long v = std::strtol(p, &end, 10);
+            if (end == p) ferr("instance file: bad index row at line " + std::to_string(r.line_no));
+            m[static_cast<size_t>(c) * entries + j] = static_cast<int32_t>(v);
+            p = end;
+        }
+    }
+}
+
+const char* op_name(int op) {
+    switch (op) {
+        case FEMGPU_OP_CONSTANT: return "const";
+        case FEMGPU_OP_SCALAR_DERIV: return "sderiv";
+        case FEMGPU_OP_VECTOR_DERIV: return "vderiv";
+        case FEMGPU_OP_JACOBIAN: return "jac";
+        case FEMGPU_OP_DETERMINANT: return "det";
+        case FEMGPU_OP_WEIGHT: return "weight";
+        case FEMGPU_OP_COORD: return "coord";
+        case FEMGPU_OP_ADD: return "add";
+        case FEMGPU_OP_MUL: return "mul";
+        case FEMGPU_OP_INV_JACOBIAN: return "ijac";
+    }
+    return "?";
+}
+
+void write_signature_block(std::ostream& os, const femgpu_problem* p) {
+    os << "signature_begin:\n";
+    os << "dim: " << p->dim << "\n";
+    os << "quad_points: " << p->quad_points << "\n";
+    os << "coord_dofs: " << p->coord_dofs << "\n";
+    os << "test_dofs: " << p->test_dofs << "\n";
+    os << "test_deriv_terms: " << p->test_deriv_terms << "\n";
+    os << "word_bytes: " << p->word_bytes << "\n";
+    os << "affine_geometry: " << (p->affine_geometry ? 1 : 0) << "\n";
+    os << "coordinate_space: " << p->coordinate_space << "\n";
+    os << "scalar_spaces: " << p->n_scalar << "\n";
+    for (int i = 0; i < p->n_scalar; ++i)
+        os << "scalar_space: " << p->scalar_spaces[i].dofs << " " << p->scalar_spaces[i].deriv_terms << "\n";
+    os << "vector_spaces: " << p->n_vector << "\n";
+    for (int i = 0; i < p->n_vector; ++i) {
+        const femgpu_space& v = p->vector_spaces[i];
+        os << "vector_space: " << v.dofs << " " << v.deriv_terms;
+        for (int k = 0; k < v.deriv_terms; ++k) os << " " << v.components[k];
+        os << "\n";
+    }
+    os << "signature_end:\n";
+}
+
+}  // namespace
+
+// save_instance (io.hpp:197-264)
+void save_problem(std::ostream& os, const femgpu_problem* p) {
+    validate_problem(p);
+    os << "format_version: " << kFormatVersion << "\n";
+    write_signature_block(os, p);
+    os << "map_begin:\n";
+    for (int i = 0; i < p->n_map_nodes; ++i) {
+        const femgpu_map_node& n = p->map_nodes[i];
+        os << "node: " << op_name(n.op);
+        if (n.op == FEMGPU_OP_CONSTANT)
+            os << " " << fmt17(n.value);
+        else if (n.op != FEMGPU_OP_DETERMINANT && n.op != FEMGPU_OP_WEIGHT)
+            os << " " << n.a << " " << n.b;
+        os << "\n";
+    }
+    for (int i = 0; i < p->n_map_outputs; ++i) os << "output: " << p->map_outputs[i] << "\n";
+    os << "map_end:\n";
+    const int Q = p->quad_points;
+    os << "tabulations_begin:\n";
+    os << "weights:\n";
+    write_doubles(os, p->weights, static_cast<size_t>(Q));
+    for (int i = 0; i < p->n_scalar; ++i)
+        for (int k = 0; k < p->scalar_spaces[i].deriv_terms; ++k) {
+            os << "phi_scalar: " << i << " " << k << "\n";
+            const int n = p->scalar_spaces[i].dofs;
+            write_matrix(os, p->scalar_spaces[i].phi + static_cast<size_t>(k) * Q * n, Q, n);
+        }
+    for (int i = 0; i < p->n_vector; ++i)
+        for (int k = 0; k < p->vector_spaces[i].deriv_terms; ++k) {
+            os << "phi_vector: " << i << " " << k << "\n";
+            const int n = p->vector_spaces[i].dofs;
+            write_matrix(os, p->vector_spaces[i].phi + static_cast<size_t>(k) * Q * n, Q, n);
+        }
+    for (int k = 0; k < p->test_deriv_terms; ++k) {
+        os << "psi: " << k << "\n";
+        write_matrix(os, p->psi + static_cast<size_t>(k) * p->test_dofs * Q, p->test_dofs, Q);
+    }
+    os << "tabulations_end:\n";
+    os << "connectivity_begin:\n";
+    os << "cells: " << p->cell_count << "\n";
+    for (int i = 0; i < p->n_scalar; ++i)
+        write_index_map(os, "scalar_map", p->scalar_spaces[i].map, p->cell_count, p->scalar_spaces[i].dofs,
+                        p->scalar_spaces[i].global_count);
+    for (int i = 0; i < p->n_vector; ++i)
+        write_index_map(os, "vector_map", p->vector_spaces[i].map, p->cell_count, p->vector_spaces[i].dofs,
+                        p->vector_spaces[i].global_count);
+    write_index_map(os, "test_map", p->test_map, p->cell_count, p->test_dofs, p->test_global_count);
+    if (p->affine_geometry) {
+        write_index_map(os, "coord_map", p->coord_map, p->cell_count, p->coord_dofs, p->coord_global_count);
+        os << "coords: " << p->coord_global_count << "\n";
+        for (int i = 0; i < p->coord_global_count; ++i) {
+            for (int c = 0; c < p->dim; ++c) os << (c ? " " : "") << fmt17(p->coords[static_cast<size_t>(i) * p->dim + c]);
+            os << "\n";
+        }
+    }
+    os << "connectivity_end:\n";
+    os << "inputs_begin:\n";
+    for (int i = 0; i < p->n_scalar; ++i) {
+        os << "scalar_input:\n";
+        write_doubles(os, p->scalar_spaces[i].input, static_cast<size_t>(p->scalar_spaces[i].global_count));
+    }
+    for (int i = 0; i < p->n_vector; ++i) {
+        os << "vector_input:\n";
+        write_doubles(os, p->vector_spaces[i].input, static_cast<size_t>(p->vector_spaces[i].global_count) * p->dim);
+    }
+    os << "inputs_end:\n";
+    os << "output_size: " << p->output_size << "\n";
+}
+
+// load_instance (io.hpp:266-379)
+femgpu_owned_problem* load_problem(std::istream& is) {
+    auto P = std::make_unique<femgpu_owned_problem>();
+    femgpu_problem& d = P->desc;
+    LineReader r{is};
+    if (r.expect_int("format_version") != kFormatVersion) ferr("instance file: unsupported format version");
+    r.expect("signature_begin");
+    d.dim = static_cast<int>(r.expect_int("dim"));
+    d.quad_points = static_cast<int>(r.expect_int("quad_points"));
+    d.coord_dofs = static_cast<int>(r.expect_int("coord_dofs"));
+    d.test_dofs = static_cast<int>(r.expect_int("test_dofs"));
+    d.test_deriv_terms = static_cast<int>(r.expect_int("test_deriv_terms"));
+    d.word_bytes = static_cast<int>(r.expect_int("word_bytes"));
+    d.affine_geometry = r.expect_int("affine_geometry") != 0;
+    d.coordinate_space = static_cast<int>(r.expect_int("coordinate_space"));
+    const long long ns = r.expect_int("scalar_spaces");
+    if (ns < 0 || ns > FEMGPU_MAX_SPACES) ferr("instance file: bad scalar space count");
+    P->sspaces.resize(static_cast<size_t>(ns));
+    for (auto& s : P->sspaces) {
+        std::istringstream row(r.expect("scalar_space"));
+        row >> s.dofs >> s.deriv_terms;
+        if (row.fail()) ferr("instance file: bad scalar space line");
+    }
+    const long long nv = r.expect_int("vector_spaces");
+    if (nv < 0 || nv > FEMGPU_MAX_SPACES) ferr("instance file: bad vector space count");
+    P->vspaces.resize(static_cast<size_t>(nv));
+    P->comps.resize(static_cast<size_t>(nv));
+    for (long long i = 0; i < nv; ++i) {
+        std::istringstream row(r.expect("vector_space"));
+        femgpu_space& v = P->vspaces[i];
+        row >> v.dofs >> v.deriv_terms;
+        for (int k = 0; k < v.deriv_terms && !row.fail(); ++k) {
+            int c;
+            row >> c;
+            P->comps[i].push_back(c);
+        }
+        if (row.fail()) ferr("instance file: bad vector space line");
+    }
+    r.expect("signature_end");
+    // ---- map
+    r.expect("map_begin");
+    {
+        std::string line;
+        while ((line = r.next()).rfind("node:", 0) == 0) {
+            std::istringstream row(line.substr(5));
+            std::string op;
+            row >> op;
+            femgpu_map_node n{};
+            n.a = n.b = -1;  // operand-less nodes carry -1 like the reference builder (form.hpp:211-216)
+            if (op == "const") {
+                n.op = FEMGPU_OP_CONSTANT;
+                std::string v;
+                row >> v;
+                n.value = std::strtod(v.c_str(), nullptr);
+            } else if (op == "det") {
+                n.op = FEMGPU_OP_DETERMINANT;
+            } else if (op == "weight") {
+                n.op = FEMGPU_OP_WEIGHT;
+            } else {
+                row >> n.a >> n.b;
+                if (row.fail()) ferr("instance file: bad map node");
+                if (op == "sderiv") n.op = FEMGPU_OP_SCALAR_DERIV;
+                else if (op == "vderiv") n.op = FEMGPU_OP_VECTOR_DERIV;
+                else if (op == "jac") n.op = FEMGPU_OP_JACOBIAN;
+                else if (op == "coord") n.op = FEMGPU_OP_COORD;
+                else if (op == "add") n.op = FEMGPU_OP_ADD;
+                else if (op == "mul") n.op = FEMGPU_OP_MUL;
+                else if (op == "ijac") n.op = FEMGPU_OP_INV_JACOBIAN;
+                else ferr("instance file: unknown map node '" + op + "'");
+            }
+            P->nodes.push_back(n);
+        }
+        while (line.rfind("output:", 0) == 0) {
+            P->outputs.push_back(static_cast<int32_t>(std::atoi(line.c_str() + 7)));
+            line = r.next();
+        }
+        if (line.rfind("map_end", 0) != 0) ferr("instance file: expected map_end at line " + std::to_string(r.line_no));
+    }
+    // ---- tabulations
+    const int Q = d.quad_points;
+    if (Q < 1) ferr("instance file: quad_points must be >= 1");
+    r.expect("tabulations_begin");
+    r.expect("weights");
+    P->weights = parse_doubles(r.next(), static_cast<size_t>(Q), r.line_no);
+    P->sphi.resize(P->sspaces.size());
+    for (size_t i = 0; i < P->sspaces.size(); ++i)
+        for (int k = 0; k < P->sspaces[i].deriv_terms; ++k) {
+            r.expect("phi_scalar");
+            read_matrix(r, Q, P->sspaces[i].dofs, P->sphi[i]);
+        }
+    P->vphi.resize(P->vspaces.size());
+    for (size_t i = 0; i < P->vspaces.size(); ++i)
+        for (int k = 0; k < P->vspaces[i].deriv_terms; ++k) {
+            r.expect("phi_vector");
+            read_matrix(r, Q, P->vspaces[i].dofs, P->vphi[i]);
+        }
+    for (int k = 0; k < d.test_deriv_terms; ++k) {
+        r.expect("psi");
+        read_matrix(r, d.test_dofs, Q, P->psi);
+    }
+    r.expect("tabulations_end");
+    // ---- connectivity
+    r.expect("connectivity_begin");
+    d.cell_count = static_cast<int>(r.expect_int("cells"));
+    P->smaps.resize(P->sspaces.size());
+    P->vmaps.resize(P->vspaces.size());
+    int cells = 0, entries = 0, global = 0;
+    for (size_t i = 0; i < P->sspaces.size(); ++i) {
+        read_index_map(r, "scalar_map", P->smaps[i], cells, entries, global);
+        if (cells != d.cell_count || entries != P->sspaces[i].dofs) ferr("connectivity: bad shape for scalar map");
+        P->sspaces[i].global_count = global;
+    }
+    for (size_t i = 0; i < P->vspaces.size(); ++i) {
+        read_index_map(r, "vector_map", P->vmaps[i], cells, entries, global);
+        if (cells != d.cell_count || entries != P->vspaces[i].dofs) ferr("connectivity: bad shape for vector map");
+        P->vspaces[i].global_count = global;
+    }
+    read_index_map(r, "test_map", P->test_map, cells, entries, global);
+    if (cells != d.cell_count || entries != d.test_dofs) ferr("connectivity: bad shape for test map");
+    d.test_global_count = global;
+    if (d.affine_geometry) {
+        int cglobal = 0;
+        read_index_map(r, "coord_map", P->coord_map, cells, entries, cglobal);
+        if (cells != d.cell_count || entries != d.coord_dofs) ferr("connectivity: bad shape for coord map");
+        d.coord_global_count = static_cast<int>(r.expect_int("coords"));
+        if (cglobal != d.coord_global_count) ferr("connectivity: coordinate map bound mismatch");
+        for (int i = 0; i < d.coord_global_count; ++i) {
+            const auto row = parse_doubles(r.next(), static_cast<size_t>(d.dim), r.line_no);
+            P->coords.insert(P->coords.end(), row.begin(), row.end());
+        }
+    }
+    r.expect("connectivity_end");
+    // ---- inputs
+    r.expect("inputs_begin");
+    P->sin.resize(P->sspaces.size());
+    P->vin.resize(P->vspaces.size());
+    for (size_t i = 0; i < P->sspaces.size(); ++i) {
+        r.expect("scalar_input");
+        P->sin[i] = parse_doubles(r.next(), static_cast<size_t>(P->sspaces[i].global_count), r.line_no);
+    }
+    for (size_t i = 0; i < P->vspaces.size(); ++i) {
+        r.expect("vector_input");
+        P->vin[i] = parse_doubles(r.next(), static_cast<size_t>(P->vspaces[i].global_count) * d.dim, r.line_no);
+    }
+    r.expect("inputs_end");
+    d.output_size = static_cast<int>(r.expect_int("output_size"));
+    // ---- wire the descriptor to the owned storage
+    for (size_t i = 0; i < P->sspaces.size(); ++i) {
+        femgpu_space& s = P->sspaces[i];
+        s.components = nullptr;
+        s.phi = P->sphi[i].data();
+        s.map = P->smaps[i].data();
+        s.input = P->sin[i].data();
+    }
+    for (size_t i = 0; i < P->vspaces.size(); ++i) {
+        femgpu_space& v = P->vspaces[i];
+        v.components = P->comps[i].data();
+        v.phi = P->vphi[i].data();
+        v.map = P->vmaps[i].data();
+        v.input = P->vin[i].data();
+    }
+    d.n_scalar = static_cast<int>(P->sspaces.size());
+    d.n_vector = static_cast<int>(P->vspaces.size());
+    d.scalar_spaces = P->sspaces.empty() ? nullptr : P->sspaces.data();
+    d.vector_spaces = P->vspaces.empty() ? nullptr : P->vspaces.data();
+    d.psi = P->psi.data();
+    d.weights = P->weights.data();
+    d.test_map = P->test_map.data();
+    d.coord_map = d.affine_geometry ? P->coord_map.data() : nullptr;
+    d.coords = d.affine_geometry ? P->coords.data() : nullptr;
+    d.n_map_nodes = static_cast<int>(P->nodes.size());
+    d.map_nodes = P->nodes.data();
+    d.map_outputs = P->outputs.data();
+    d.n_map_outputs = static_cast<int>(P->outputs.size());
+    validate_problem(&d);
+    return P.release();
+}
+
+// save_candidate / load_candidate (io.hpp:407-460); B200 kinds and knobs as extra keys.
+void save_schedule(std::ostream& os, const femgpu_schedule* s, int n_scalar, int n_vector) {
+    os << "format_version: " << kFormatVersion << "\n";
+    if (s->kind == FEMGPU_SCPT && s->basis == 0 && s->scatter == 0 && s->block_cells == 0 && s->group_cells == 0) {
+        os << "kind: scpt\n";
+        return;
+    }
+    if (s->kind == FEMGPU_MLT) {
+        os << "kind: mlt\n";
+        os << "quad_tile: " << s->quad_tile << "\n";
+        os << "eval_row_tile: " << s->eval_row_tile << "\n";
+        os << "eval_col_tiles_scalar:";
+        for (int i = 0; i < n_scalar; ++i) os << " " << s->eval_col_tiles_scalar[i];
+        os << "\n";
+        os << "eval_col_tiles_vector:";
+        for (int i = 0; i < n_vector; ++i) os << " " << s->eval_col_tiles_vector[i];
+        os << "\n";
+        os << "quad_row_tile: " << s->quad_row_tile << "\n";
+        os << "quad_col_tile: " << s->quad_col_tile << "\n";
+        os << "cells_per_group: " << s->cells_per_group << "\n";
+        os << "lanes_per_cell: " << s->lanes_per_cell << "\n";
+        return;
+    }
+    // B200 extension kinds (not readable by the reference)
+    os << "kind: " << (s->kind == FEMGPU_DMMA ? "b200_dmma" : "b200_scpt") << "\n";
+    os << "quad_tile: " << s->quad_tile << "\n";
+    os << "eval_row_tile: " << s->eval_row_tile << "\n";
+    os << "quad_row_tile: " << s->quad_row_tile << "\n";
+    os << "cells_per_group: " << s->cells_per_group << "\n";
+    os << "lanes_per_cell: " << s->lanes_per_cell << "\n";
+    os << "basis: " << s->basis << "\n";
+    os << "scatter: " << s->scatter << "\n";
+    os << "block_cells: " << s->block_cells << "\n";
+    os << "group_cells: " << s->group_cells << "\n";
+    os << "reserved:";
+    for (int v : s->reserved) os << " " << v;
+    os << "\n";
+}
+
+femgpu_schedule load_schedule(std::istream& is) {
+    LineReader r{is};
+    femgpu_schedule s{};
+    if (r.expect_int("format_version") != kFormatVersion) ferr("candidate file: unsupported format version");
+    const std::string kind = r.expect("kind");
+    auto ints = [](const std::string& line) {
+        std::istringstream is2(line);
+        std::vector<int> out;
+        int v;
+        while (is2 >> v) out.push_back(v);
+        return out;
+    };
+    if (kind == "scpt") {
+        s.kind = FEMGPU_SCPT;  // TilingParams::scpt(): the SCPT family with automatic B200 knobs
+        return s;
+    }
+    if (kind == "mlt") {
+        s.kind = FEMGPU_MLT;
+        s.quad_tile = static_cast<int>(r.expect_int("quad_tile"));
+        s.eval_row_tile = static_cast<int>(r.expect_int("eval_row_tile"));
+        const auto ts = ints(r.expect("eval_col_tiles_scalar"));
+        const auto tv = ints(r.expect("eval_col_tiles_vector"));
+        if (ts.size() > FEMGPU_MAX_SPACES || tv.size() > FEMGPU_MAX_SPACES) ferr("candidate file: too many spaces");
+        for (size_t i = 0; i < ts.size(); ++i) s.eval_col_tiles_scalar[i] = ts[i];
+        for (size_t i = 0; i < tv.size(); ++i) s.eval_col_tiles_vector[i] = tv[i];
+        s.quad_row_tile = static_cast<int>(r.expect_int("quad_row_tile"));
+        s.quad_col_tile = static_cast<int>(r.expect_int("quad_col_tile"));
+        s.cells_per_group = static_cast<int>(r.expect_int("cells_per_group"));
+        s.lanes_per_cell = static_cast<int>(r.expect_int("lanes_per_cell"));
+        return s;
+    }
+    if (kind != "b200_dmma" && kind != "b200_scpt") ferr("candidate file: unknown kind '" + kind + "'");
+    s.kind = kind == "b200_dmma" ? FEMGPU_DMMA : FEMGPU_SCPT;
+    s.quad_tile = static_cast<int>(r.expect_int("quad_tile"));
+    s.eval_row_tile = static_cast<int>(r.expect_int("eval_row_tile"));
+    s.quad_row_tile = static_cast<int>(r.expect_int("quad_row_tile"));
+    s.cells_per_group = static_cast<int>(r.expect_int("cells_per_group"));
+    s.lanes_per_cell = static_cast<int>(r.expect_int("lanes_per_cell"));
+    s.basis = static_cast<int>(r.expect_int("basis"));
+    s.scatter = static_cast<int>(r.expect_int("scatter"));
+    s.block_cells = static_cast<int>(r.expect_int("block_cells"));
+    s.group_cells = static_cast<int>(r.expect_int("group_cells"));
+    const auto rv = ints(r.expect("reserved"));
+    for (size_t i = 0; i < rv.size() && i < 4; ++i) s.reserved[i] = rv[i];
+    return s;
+}
+
+}  // namespace femgpu

@@ -96,9 +96,36 @@ void autotune(Instance& I) {
     std::vector<femgpu_schedule> cands;
     if (t_dfma <= 1.6 * best) cands.push_back(dfma_default());
     if (t_dmma <= 1.6 * best) {
-        for (int joint : {1, 2})
-            for (int prefetch : {0, 1})
-                for (int block : {128, 256}) cands.push_back(dmma_variant(joint, prefetch, block, 32));
+        // quadrature chunk: the register-capped choice of resolve_dmma and, when different, the
+        // uncapped one with the fewest padded DMMAs (more registers, fewer tensor-pipe slots)
+        std::vector<int> tqs = {0};
+        {
+            long long bestf = -1;
+            int bestq = 0;
+            for (int tq = 4; tq <= (sig.Q + 3) / 4 * 4; tq += 4) {
+                KernelPlan kp;
+                femgpu_schedule s = dmma_variant(1, 0, 0, 0);
+                s.quad_tile = tq;
+                try {
+                    resolve_dmma(sig, kp, &s);
+                } catch (const Error&) {
+                    continue;
+                }
+                const long long f = dmma_layout(sig, kp).nfrag;
+                if (bestf < 0 || f < bestf) bestf = f, bestq = tq;
+            }
+            KernelPlan kp;
+            femgpu_schedule s = dmma_variant(1, 0, 0, 0);
+            resolve_dmma(sig, kp, &s);
+            if (bestq > 0 && bestq != kp.TQ) tqs.push_back(bestq);
+        }
+        for (int tq : tqs)
+            for (int joint : {1, 2})
+                for (int block : {128, 256}) {
+                    cands.push_back(dmma_variant(joint, 0, block, 32));
+                    cands.back().quad_tile = tq;
+                }
+        cands.push_back(dmma_variant(1, 1, 256, 32));  // gather prefetch
     }
     std::ostringstream log;
     log << "model slots/cell: dfma " << static_cast<long long>(t_dfma) << ", dmma "

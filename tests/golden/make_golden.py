@@ -54,6 +54,11 @@ def main():
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "reference_outputs.npz")
     np.savez_compressed(path, **out)
     print("wrote", path, len(CASES), "cases")
+    # an instance file written by the reference's own femsched::save_instance_file (io.hpp), so
+    # the io reader is pinned on a box without the reference (tests/test_io.py)
+    inst = os.path.join(os.path.dirname(os.path.abspath(__file__)), "instance_laplace_2d_p2.txt")
+    oracle.ref_save_instance(oracle.ref_make_problem("laplace", 2, 2, 6, 16, 7), inst)
+    print("wrote", inst)
 
 
 if __name__ == "__main__":
