@@ -126,6 +126,7 @@ femgpu_status femgpu_emit_source(const femgpu_problem* p, const femgpu_schedule*
             kp.block = (s && s->block_cells > 0) ? s->block_cells : 128;
             if (s && s->scatter == FEMGPU_SCATTER_TILE) femgpu::host_tile_plan(p, sig, kp, s);
             if (s && s->scatter == FEMGPU_SCATTER_MACRO) femgpu::host_macro_plan(p, sig, kp, s);
+            if (s && s->scatter == FEMGPU_SCATTER_ATOMIC && s->group_cells > 1) kp.G = s->group_cells;
         }
         kp.strict = s && s->reserved[0];
         femgpu::EmitResult em = femgpu::emit_kernel(sig, kp);

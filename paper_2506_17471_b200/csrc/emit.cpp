@@ -518,6 +518,184 @@ void emit_scpt_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const 
     o.line("}");
 }
 
+// SCPT with G independent cells per thread (cells c0 + k*blockDim, k < G, coalesced per k):
+// the per-cell statements are interleaved so that every tabulation operand (constant bank or
+// shared memory, one LDCU/LDS per DFMA in the one-cell kernel) is loaded once for G cells, and
+// the G cells give the scheduler independent DFMA chains.  No connectivity pattern is needed
+// (unlike the macro family); each cell keeps the reference's own operation order.
+void emit_scpt_multi_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const MapUse& use, bool unroll_q,
+                            const std::string& name, long long smem_tab_off) {
+    const int G = kp.G, d = sig.dim, Q = sig.Q;
+    auto TAB = [&](const std::string& idx) {
+        if (kp.basis == kBasisGlobal) return "__ldg(&P.tabg[" + idx + "])";
+        return kp.basis == FEMGPU_BASIS_CONST ? "P.tab[" + idx + "]" : "sT[" + idx + "]";
+    };
+    auto K = [](const std::string& v, int k) { return v + "_c" + std::to_string(k); };
+    // cell-invariant nodes the quadrature-point part reads (constants are re-emitted per cell)
+    std::set<int> need;
+    for (size_t id = 0; id < sig.nodes.size(); ++id) {
+        if (!use.live[id] || !use.qdep[id]) continue;
+        const MapNode& n = sig.nodes[id];
+        if (n.op == FEMGPU_OP_ADD || n.op == FEMGPU_OP_MUL) {
+            if (!use.qdep[n.a]) need.insert(n.a);
+            if (!use.qdep[n.b]) need.insert(n.b);
+        }
+    }
+    for (int out : sig.outputs)
+        if (!use.qdep[out]) need.insert(out);
+    o.line("");
+    o.line("extern \"C\" __global__ void __launch_bounds__(" + S(kp.block) + (kp.min_blocks > 1 ? ", " + S(kp.min_blocks) : "") +
+           ") " + name + "(const __grid_constant__ Params P) {");
+    o.ind++;
+    o.line("constexpr bool CHECKED = false;");
+    if (kp.basis == FEMGPU_BASIS_SMEM) {
+        o.line("extern __shared__ __align__(16) unsigned char smraw[];");
+        o.line("double* sT = reinterpret_cast<double*>(smraw + " + S(smem_tab_off) + ");");
+        o.line("for (int i = threadIdx.x; i < " + S(sig.tab_size) + "; i += blockDim.x) sT[i] = P.tabg[i];");
+        o.line("__syncthreads();");
+    }
+    o.line("const int cbase = blockIdx.x * " + S(G) + " * blockDim.x + threadIdx.x;");
+    o.line("if (cbase >= P.n_cells) return;");
+    for (int k = 0; k < G; ++k) {
+        o.line("const bool ok_c" + S(k) + " = cbase + " + S(k) + " * (int)blockDim.x < P.n_cells;");
+        o.line("const int cell_c" + S(k) + " = ok_c" + S(k) + " ? cbase + " + S(k) + " * (int)blockDim.x : cbase;");
+    }
+    // ---- per cell: gather, geometry, cell-invariant nodes (kept in hk<k>_<id>)
+    for (int k = 0; k < G; ++k) {
+        o.line("bool nf_c" + S(k) + " = false;");
+        for (int i = 0; i < sig.ns(); ++i)
+            for (int j = 0; j < sig.sdofs[i]; ++j)
+                o.line("const double " + K(nm("u", i, j), k) + " = __ldg(&P.x" + S(i) + "[__ldg(&P.m" + S(i) + "[" + S(j) +
+                       "*(size_t)P.stride + cell_c" + S(k) + "])]);");
+        for (int i = 0; i < sig.nv(); ++i) {
+            std::set<int> comps(sig.vcomps[i].begin(), sig.vcomps[i].end());
+            for (int j = 0; j < sig.vdofs[i]; ++j) {
+                const std::string node = K(nm("vn", i, j), k);
+                o.line("const int " + node + " = __ldg(&P.vm" + S(i) + "[" + S(j) + "*(size_t)P.stride + cell_c" + S(k) + "]);");
+                for (int c : comps)
+                    o.line("const double " + K(nm("w", i, j, c), k) + " = __ldg(&P.v" + S(i) + "[(size_t)" + node + "*" +
+                           S(vec_stride(d)) + "+" + S(c) + "]);");
+            }
+        }
+        for (int id : need) o.line("double " + K("hk" + S(id), k) + ";");
+        o.line("{");
+        o.ind++;
+        if (sig.affine) {
+            std::ostringstream g;
+            emit_geometry(g, sig, use.uses_inv, "cell_c" + S(k));
+            std::istringstream gl(g.str());
+            std::string line;
+            while (std::getline(gl, line)) o.line(line.substr(line.find_first_not_of(' ')));
+            o.line("nf_c" + S(k) + " = NF(det);");
+        }
+        emit_nodes(o, sig, use, false, "0", TAB);
+        for (int id : need) o.line(K("hk" + S(id), k) + " = n" + S(id) + ";");
+        o.ind--;
+        o.line("}");
+        {
+            std::string l = "double";
+            for (int jw = 0; jw < sig.nW; ++jw) l += std::string(jw ? "," : "") + " " + K("o" + S(jw), k) + " = 0.0";
+            o.line(l + ";");
+        }
+    }
+    auto body_q = [&](const std::string& qs) {
+        // evaluation: one tabulation load per (term, j) for all G cells
+        for (int i = 0; i < sig.ns(); ++i)
+            for (int t = 0; t < sig.sterms[i]; ++t) {
+                const long long base = sig.phi_off_s[i] + static_cast<long long>(t) * Q * sig.sdofs[i];
+                for (int k = 0; k < G; ++k) o.line("double " + K(nm("s", i, t), k) + ";");
+                for (int j = 0; j < sig.sdofs[i]; ++j) {
+                    std::string l = "{ const double tb = " + TAB(S(base + j) + "+(" + qs + ")*" + S(sig.sdofs[i])) + ";";
+                    for (int k = 0; k < G; ++k) {
+                        const std::string v = K(nm("s", i, t), k), u = K(nm("u", i, j), k);
+                        l += j == 0 ? " " + v + " = tb * " + u + ";" : " " + v + " = FMA(tb, " + u + ", " + v + ");";
+                    }
+                    o.line(l + " }");
+                }
+            }
+        for (int i = 0; i < sig.nv(); ++i)
+            for (int t = 0; t < sig.vterms[i]; ++t) {
+                const long long base = sig.phi_off_v[i] + static_cast<long long>(t) * Q * sig.vdofs[i];
+                const int comp = sig.vcomps[i][t];
+                for (int k = 0; k < G; ++k) o.line("double " + K(nm("t", i, t), k) + ";");
+                for (int j = 0; j < sig.vdofs[i]; ++j) {
+                    std::string l = "{ const double tb = " + TAB(S(base + j) + "+(" + qs + ")*" + S(sig.vdofs[i])) + ";";
+                    for (int k = 0; k < G; ++k) {
+                        const std::string v = K(nm("t", i, t), k), w = K(nm("w", i, j, comp), k);
+                        l += j == 0 ? " " + v + " = tb * " + w + ";" : " " + v + " = FMA(tb, " + w + ", " + v + ");";
+                    }
+                    o.line(l + " }");
+                }
+            }
+        // pointwise map per cell (same SSA as the one-cell kernel), outputs into e<kt>_c<k>
+        for (int k = 0; k < G; ++k) {
+            for (int kt = 0; kt < sig.Tw; ++kt) o.line("double " + K("e" + S(kt), k) + ";");
+            o.line("{");
+            o.ind++;
+            std::string unused;
+            for (int i = 0; i < sig.ns(); ++i)
+                for (int t = 0; t < sig.sterms[i]; ++t) {
+                    o.line("const double " + nm("s", i, t) + " = " + K(nm("s", i, t), k) + ";");
+                    if (!use.sd_used.count({i, t})) unused += " | NF(" + nm("s", i, t) + ")";
+                }
+            for (int i = 0; i < sig.nv(); ++i)
+                for (int t = 0; t < sig.vterms[i]; ++t) {
+                    o.line("const double " + nm("t", i, t) + " = " + K(nm("t", i, t), k) + ";");
+                    if (!use.vd_used.count({i, t})) unused += " | NF(" + nm("t", i, t) + ")";
+                }
+            if (!unused.empty()) o.line("nf_c" + S(k) + " = nf_c" + S(k) + unused + ";");
+            for (int id : need) {
+                if (sig.nodes[id].op == FEMGPU_OP_CONSTANT) o.line("const double n" + S(id) + " = " + lit(sig.nodes[id].value) + ";");
+                else o.line("const double n" + S(id) + " = " + K("hk" + S(id), k) + ";");
+            }
+            emit_nodes(o, sig, use, true, qs, TAB);
+            for (int kt = 0; kt < sig.Tw; ++kt) o.line(K("e" + S(kt), k) + " = n" + S(sig.outputs[kt]) + ";");
+            o.ind--;
+            o.line("}");
+        }
+        // quadrature: one Psi load per (jw, term) for all G cells, k inner as in the reference
+        for (int jw = 0; jw < sig.nW; ++jw)
+            for (int kt = 0; kt < sig.Tw; ++kt) {
+                const long long idx = sig.psi_off + (static_cast<long long>(kt) * sig.nW + jw) * Q;
+                std::string l = "{ const double tb = " + TAB(S(idx) + "+(" + qs + ")") + ";";
+                for (int k = 0; k < G; ++k)
+                    l += " " + K("o" + S(jw), k) + " = FMA(tb, " + K("e" + S(kt), k) + ", " + K("o" + S(jw), k) + ");";
+                o.line(l + " }");
+            }
+    };
+    if (unroll_q) {
+        for (int iq = 0; iq < Q; ++iq) {
+            o.line("{ // quadrature point " + S(iq));
+            o.ind++;
+            body_q(S(iq));
+            o.ind--;
+            o.line("}");
+        }
+    } else {
+        o.line("#pragma unroll 1");
+        o.line("for (int q = 0; q < " + S(Q) + "; ++q) {");
+        o.ind++;
+        body_q("q");
+        o.ind--;
+        o.line("}");
+    }
+    // ---- finiteness + scatter per cell
+    for (int k = 0; k < G; ++k) {
+        std::string chk;
+        for (int jw = 0; jw < sig.nW; ++jw) chk += " | NF(" + K("o" + S(jw), k) + ")";
+        o.line("if (ok_c" + S(k) + ") {");
+        o.ind++;
+        o.line("if (nf_c" + S(k) + chk + ") atomicMin(P.bad, (unsigned long long)cell_c" + S(k) + ");");
+        for (int jw = 0; jw < sig.nW; ++jw)
+            o.line("atomicAdd(&P.y[__ldg(&P.tm[" + S(jw) + "*(size_t)P.stride + cell_c" + S(k) + "])], " + K("o" + S(jw), k) + ");");
+        o.ind--;
+        o.line("}");
+    }
+    o.line("(void)CHECKED;");
+    o.ind--;
+    o.line("}");
+}
+
 // Shared-memory plan of the pipelined tile kernel (bytes, 16-byte aligned regions).
 struct TilePlan {
     struct Item {
@@ -930,7 +1108,10 @@ EmitResult emit_kernel(const Signature& sig, const KernelPlan& kp) {
         r.kernel = "femgpu_scpt";
         r.kernel_checked = "femgpu_scpt_checked";
         r.smem_bytes = kp.basis == FEMGPU_BASIS_SMEM ? static_cast<size_t>(sig.tab_size) * 8 : 0;
-        emit_scpt_kernel(o, sig, kp, use, unroll_q, false, r.kernel, 0);
+        if (kp.G > 1)
+            emit_scpt_multi_kernel(o, sig, kp, use, unroll_q && kp.G * fmas * sig.Q <= 12000, r.kernel, 0);
+        else
+            emit_scpt_kernel(o, sig, kp, use, unroll_q, false, r.kernel, 0);
         emit_scpt_kernel(o, sig, kp, use, unroll_q, true, r.kernel_checked, 0);
     }
     r.source = o.s.str();

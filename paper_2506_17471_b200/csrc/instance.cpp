@@ -787,6 +787,10 @@ KernelPlan resolve_schedule(Instance& I, const femgpu_schedule* s) {
     if (smem_tab > 227 * 1024)
         fail(FEMGPU_E_INFEASIBLE, "basis: tabulations exceed the shared-memory capacity of one CTA");
     kp.family = Family::Scpt;
+    // SCPT with G independent cells per thread (group_cells with atomic scatter): shared
+    // tabulation loads, more independent DFMA chains per thread
+    kp.G = scatter == FEMGPU_SCATTER_ATOMIC && s->group_cells > 1 ? s->group_cells : 1;
+    if (kp.G > 8) fail(FEMGPU_E_INFEASIBLE, "schedule: at most 8 cells per thread in the SCPT family");
     if (s->reserved[2] > 0) kp.min_blocks = s->reserved[2];
     (void)int_dim;
     return kp;
@@ -883,7 +887,8 @@ void run_action(Instance& I, const KernelPlan& kp, double* d_y, cudaStream_t str
         grid = std::min<long long>(((static_cast<long long>(I.cells) + kp.Nc - 1) / kp.Nc + kp.block / 32 - 1) / (kp.block / 32),
                                    static_cast<long long>(mod->sms) * std::max(1, mod->occupancy));
     else
-        grid = (static_cast<long long>(I.cells) + kp.block - 1) / kp.block;
+        grid = (static_cast<long long>(I.cells) + static_cast<long long>(kp.block) * std::max(1, kp.G) - 1) /
+               (static_cast<long long>(kp.block) * std::max(1, kp.G));
     if (grid > INT_MAX) fail(FEMGPU_E_INFEASIBLE, "launch: grid too large");
     FG_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(mod->fast), dim3(static_cast<unsigned>(grid)),
                              dim3(kp.block), args, mod->emitted.smem_bytes, stream));

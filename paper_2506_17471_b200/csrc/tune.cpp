@@ -54,7 +54,7 @@ std::string describe_plan(const KernelPlan& kp) {
     std::ostringstream s;
     switch (kp.family) {
         case Family::Macro: s << "femgpu_macro G=" << kp.G << " block=" << kp.block; break;
-        case Family::Scpt: s << "femgpu_scpt block=" << kp.block; break;
+        case Family::Scpt: s << "femgpu_scpt cells/thread=" << std::max(1, kp.G) << " block=" << kp.block; break;
         case Family::Tile: s << "femgpu_tile cells=" << kp.tile_cells; break;
         case Family::Mlt: s << "femgpu_mlt Nc=" << kp.Nc << " Nwi=" << kp.Nwi << " TQ=" << kp.TQ; break;
         case Family::Dmma:
@@ -94,7 +94,15 @@ void autotune(Instance& I) {
     }
     const double best = std::min(t_dfma, t_dmma);
     std::vector<femgpu_schedule> cands;
-    if (t_dfma <= 1.6 * best) cands.push_back(dfma_default());
+    if (t_dfma <= 1.6 * best) {
+        cands.push_back(dfma_default());
+        for (int G : {2}) {  // SCPT with G cells per thread (shared tabulation loads)
+            femgpu_schedule s = dfma_default();
+            s.scatter = FEMGPU_SCATTER_ATOMIC;
+            s.group_cells = G;
+            cands.push_back(s);
+        }
+    }
     if (t_dmma <= 1.6 * best) {
         // quadrature chunk: the register-capped choice of resolve_dmma and, when different, the
         // uncapped one with the fewest padded DMMAs (more registers, fewer tensor-pipe slots)

@@ -121,3 +121,43 @@ def test_cpp_adapter_drop_in():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+# ---- SCPT with G cells per thread (interleaved statements, shared tabulation loads)
+def scpt_g(G, basis=abi.BASIS_AUTO, block=0):
+    return fg.TilingParams.scpt(scatter=abi.SCATTER_ATOMIC, group_cells=G, basis=basis, block_cells=block)
+
+
+def test_scpt_multi_cell_random_signatures(oracle):
+    rng = fg.SynthRng(7781)
+    for _ in range(40):
+        sig = random_signature(rng)
+        cells = 1 + rng.next_u64() % 300  # partial last CTA and partial G-slices
+        p = fg.make_problem(sig, fg.generic_map(sig), cells, rng.next_u64())
+        ref = oracle.reference_action(p)
+        with fg.GpuInstance(p) as g:
+            G = 2 + rng.next_u64() % 3
+            basis = (abi.BASIS_CONST, abi.BASIS_SMEM)[rng.next_u64() % 2]
+            close(g.action(scpt_g(G, basis, 32 * (1 + rng.next_u64() % 4))), ref)
+
+
+@pytest.mark.parametrize("form,dim,deg,Q,n", [("laplace", 3, 2, 4, 3), ("advection", 3, 2, 14, 3),
+                                              ("helmholtz_coef", 2, 3, 12, 6), ("hyperelastic", 3, 1, 4, 3),
+                                              ("elasticity", 3, 2, 4, 2), ("mass", 2, 1, 3, 9)])
+def test_scpt_multi_cell_mesh_forms(oracle, form, dim, deg, Q, n):
+    p = fg.mesh_problem(form, dim, deg, Q, n)
+    ref = oracle.reference_action(p)
+    with fg.GpuInstance(p) as g:
+        for G in (2, 3):
+            close(g.action(scpt_g(G)), ref)
+
+
+def test_scpt_multi_cell_nonfinite_names_lowest_cell():
+    p = preset_problem("laplace", 2, 2, 6, 200, 7)
+    m = p.connectivity.scalar_maps[0].indices
+    bad = [150, 77]
+    for c in bad:
+        p.scalar_inputs[0][m[c, 0]] = np.nan
+    first = int(min(np.nonzero(np.any(np.isin(m, [m[c, 0] for c in bad]), axis=1))[0]))
+    with pytest.raises(RuntimeError, match="non-finite value at cell %d during" % first):
+        fg.gpu_action(p, scpt_g(3))

@@ -30,6 +30,8 @@ def sched(name):
             kw["min_blocks"] = int(p[1:])
         elif p.startswith("r"):
             kw["reg_target"] = int(p[1:])
+        elif p.startswith("g") and p[1:].isdigit():
+            kw["group_cells"] = int(p[1:])
         elif p.isdigit():
             kw["block_cells"] = int(p)
     head = parts[0]
