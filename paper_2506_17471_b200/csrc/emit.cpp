@@ -377,7 +377,9 @@ void emit_cell_body(Out& o, const Signature& sig, const KernelPlan& kp, const Ma
     o.ind++;
     for (int jw = 0; jw < sig.nW; ++jw) {
         std::string idx = std::to_string(jw) + "*(size_t)" + C + "+cell";
-        if (mc)
+        if (mc && kp.ysmem)
+            o.line("SY(" + std::to_string(pat(kp.tgroup, jw)) + ") += o" + std::to_string(jw) + ";");
+        else if (mc)
             o.line(nm("ya", pat(kp.tgroup, jw)) + " += o" + std::to_string(jw) + ";");
         else if (tile)
             o.line("st[" + std::to_string(jw * kp.tile_cells) + " + threadIdx.x] = o" + std::to_string(jw) + ";");
@@ -467,7 +469,7 @@ void emit_geometry(std::ostringstream& os, const Signature& sig, bool uses_inv, 
 std::string KernelPlan::key() const {
     std::ostringstream s;
     s << int(family) << "/" << basis << "/" << block << "/" << tile_cells << "/" << Nc << "x" << Nwi << "/" << TQ << "/"
-      << Ter << "/" << Tqr << "/" << Tqc << "/" << strict << "/" << min_blocks << "/G" << G << "/ms" << mstage;
+      << Ter << "/" << Tqr << "/" << Tqc << "/" << strict << "/" << min_blocks << "/G" << G << "/ms" << mstage << "/ys" << ysmem;
     for (int t : Tcs) s << "s" << t;
     for (int t : Tcv) s << "v" << t;
     for (size_t g = 0; g < group_cap.size(); ++g) s << "g" << group_entries[g] << ":" << group_cap[g];
@@ -908,7 +910,7 @@ void emit_tile_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const 
 // per-cell operation order of the reference, accumulates y per unique node in registers
 // (cells ascending), and issues one red.global.add.f64 per unique test DOF.
 void emit_macro_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const MapUse& use, bool unroll_q,
-                       const std::string& name, long long smem_tab_off) {
+                       const std::string& name, long long smem_tab_off, long long ysmem_off = 0) {
     const int D = sig.dim;
     o.line("");
     std::string bounds = "__launch_bounds__(" + S(kp.block) + (kp.min_blocks > 1 ? ", " + S(kp.min_blocks) : "") + ") ";
@@ -926,6 +928,10 @@ void emit_macro_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const
         o.line("volatile double* const sm_base = reinterpret_cast<volatile double*>(smraw + " + S(smem_tab_off + (kp.basis == FEMGPU_BASIS_SMEM ? al16(sig.tab_size * 8) : 0)) + ") + threadIdx.x;");
         o.line("#define SM(k) sm_base[(k) * " + S(kp.block) + "]");
         o.line("#define cp8s(k, src) cp8(const_cast<unsigned char*>(reinterpret_cast<volatile unsigned char*>(&SM(k))), (src))");
+    }
+    if (kp.ysmem) {
+        if (kp.basis != FEMGPU_BASIS_SMEM && !kp.mstage) o.line("extern __shared__ __align__(16) unsigned char smraw[];");
+        o.line("double* const sy_base = reinterpret_cast<double*>(smraw + " + S(ysmem_off) + ") + threadIdx.x;");
     }
     o.line("const int grp = blockIdx.x * " + S(kp.block) + " + threadIdx.x;");
     o.line("if (grp >= P.n_groups) return;");
@@ -992,7 +998,7 @@ void emit_macro_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const
             if (stream && last_use(gt, u) != s_now) continue;
             const std::string idx =
                 gathered.count(gt) ? "ig" + S(gt) + "_" + S(u) : "__ldg(&P.gidx" + S(gt) + "[" + S(u) + " * NG + grp])";
-            o.line("atomicAdd(&P.y[" + idx + "], ya" + S(u) + ");");
+            o.line("atomicAdd(&P.y[" + idx + "], " + (kp.ysmem ? "SY(" + S(u) + ")" : "ya" + S(u)) + ");");
         }
     };
     MacroCtx base{0, {}, {}, 0};
@@ -1027,7 +1033,11 @@ void emit_macro_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const
         o.line("cp_commit();");
         o.line("cp_wait_all();");
     }
-    {
+    if (kp.ysmem) {
+        // y accumulators in a thread-private shared-memory column (conflict-free), freeing registers
+        o.line("#define SY(k) sy_base[(k) * " + S(kp.block) + "]");
+        for (int u = 0; u < kp.group_cap[gt]; ++u) o.line("SY(" + S(u) + ") = 0.0;");
+    } else {
         std::string l = "double";
         for (int u = 0; u < kp.group_cap[gt]; ++u) l += std::string(u ? "," : "") + " ya" + S(u) + " = 0.0";
         o.line(l + ";");
@@ -1094,7 +1104,9 @@ EmitResult emit_kernel(const Signature& sig, const KernelPlan& kp) {
             if (sig.affine) slots += static_cast<long long>(kp.group_cap[kp.cgroup]) * sig.dim;
             r.smem_bytes += static_cast<size_t>(slots * 8 * kp.block);
         }
-        emit_macro_kernel(o, sig, kp, use, unroll_q, r.kernel, 0);
+        const long long ysmem_off = static_cast<long long>(r.smem_bytes);
+        if (kp.ysmem) r.smem_bytes += static_cast<size_t>(kp.group_cap[kp.tgroup]) * 8 * kp.block;
+        emit_macro_kernel(o, sig, kp, use, unroll_q, r.kernel, 0, ysmem_off);
         emit_scpt_kernel(o, sig, kp, use, unroll_q, true, r.kernel_checked, 0);
     } else if (tile) {
         o << kAsync;

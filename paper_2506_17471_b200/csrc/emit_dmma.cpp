@@ -413,8 +413,10 @@ void emit_dmma_kernel(std::ostringstream& o, const Signature& sig, const KernelP
         o << "        const bool qok" << s << " = q" << s << " < " << sig.Q << ";\n";
         o << "        const double wq" << s << " = qok" << s << " ? __ldg(&P.tabg[" << sig.w_off << " + q" << s << "]) : 0.0;\n";
     }
-    for (int j = 0; j < MBJ; ++j)
-        for (int s = 0; s < TQL; ++s) {
+    // map of owned point s for every m-block, then at once its quadrature k-steps kappa = (k, s):
+    // E values die right after their DMMAs (register pressure), sum order over kappa is s-major
+    for (int s = 0; s < TQL; ++s) {
+        for (int j = 0; j < MBJ; ++j) {
             o << "        double E" << s << "_0" << J << j;
             for (int k = 1; k < sig.Tw; ++k) o << ", E" << s << "_" << k << J << j;
             o << ";\n";
@@ -449,14 +451,15 @@ void emit_dmma_kernel(std::ostringstream& o, const Signature& sig, const KernelP
               << ");\n";
             o << "        }\n";
         }
-    // ---- quadrature GEMM: k-step kappa = (k, s)
-    for (int kq = 0; kq < L.KQ; ++kq) {
-        const int k = kq / TQL, s = kq % TQL;
-        for (int nb = 0; nb < L.NBQ; ++nb) {
-            o << "        { const double b = Fc[" << (L.foff_q + static_cast<long long>(nb) * L.KQ + kq) * 32 << "];";
-            for (int j = 0; j < MBJ; ++j)
-                o << " DMMA(y" << nb << J << j << "_0, y" << nb << J << j << "_1, E" << s << "_" << k << J << j << ", b);";
-            o << " }\n";
+        // ---- quadrature GEMM: k-steps kappa = (k, s) of this owned point
+        for (int k = 0; k < sig.Tw; ++k) {
+            const int kq = k * TQL + s;
+            for (int nb = 0; nb < L.NBQ; ++nb) {
+                o << "        { const double b = Fc[" << (L.foff_q + static_cast<long long>(nb) * L.KQ + kq) * 32 << "];";
+                for (int j = 0; j < MBJ; ++j)
+                    o << " DMMA(y" << nb << J << j << "_0, y" << nb << J << j << "_1, E" << s << "_" << k << J << j << ", b);";
+                o << " }\n";
+            }
         }
     }
     o << "      }\n";  // chunks

@@ -91,6 +91,7 @@ struct KernelPlan {
     // Macro family: G cells per thread sharing the compile-time local pattern mpat[group]
     int G = 0;
     int mstage = 0;                       // 0: gathered values in registers; 1: cp.async into smem
+    bool ysmem = false;                   // macro: y accumulators in thread-private smem columns (registers)
     std::vector<std::vector<int>> mpat;   // per map group: G*entries local indices
     std::string key() const;
 };

@@ -597,7 +597,8 @@ void host_macro_plan(const femgpu_problem* p, const Signature& sig, KernelPlan& 
     }
     kp.family = Family::Macro;
     kp.G = G;
-    kp.mstage = s->reserved[3];
+    kp.mstage = s->reserved[3] == 1 ? 1 : 0;
+    kp.ysmem = s->reserved[3] == 2;
     kp.block = s->block_cells > 0 ? s->block_cells : 64;
     const int reg_target = s->reserved[1] > 0 ? s->reserved[1] : 168;
     kp.min_blocks = std::max(1, std::min(16, 65536 / (kp.block * reg_target)));
@@ -723,7 +724,8 @@ KernelPlan resolve_schedule(Instance& I, const femgpu_schedule* s) {
             kp.family = Family::Macro;
             kp.basis = basis;
             kp.G = G;
-            kp.mstage = s->reserved[3];
+            kp.mstage = s->reserved[3] == 1 ? 1 : 0;
+            kp.ysmem = s->reserved[3] == 2;
             kp.block = s->block_cells > 0 ? s->block_cells : 64;
             const int reg_target = s->reserved[1] > 0 ? s->reserved[1] : 168;
             kp.min_blocks = std::max(1, std::min(16, 65536 / (kp.block * reg_target)));

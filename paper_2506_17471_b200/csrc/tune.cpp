@@ -126,6 +126,8 @@ void autotune(Instance& I) {
             femgpu_schedule s = dmma_variant(1, 0, 0, 0);
             resolve_dmma(sig, kp, &s);
             if (bestq > 0 && bestq != kp.TQ) tqs.push_back(bestq);
+            // two owned points per lane-group: measured best on several high-Q forms (hyp-P4)
+            if (sig.Q > 8 && kp.TQ != 8 && bestq != 8) tqs.push_back(8);
         }
         for (int tq : tqs)
             for (int joint : {1, 2})

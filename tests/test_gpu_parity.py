@@ -170,3 +170,14 @@ def test_executor_outcome(oracle):
     assert out.ok, out.error
     assert out.measured_seconds is not None and np.isfinite(out.measured_seconds) and out.measured_seconds > 0
     check(out.output, oracle.reference_action(p))
+
+
+def test_non_affine_instance_matches_oracle(oracle):
+    """The reference's non-affine instance (test_io.cpp:10-42, 65-96): coordinates as a vector trial
+    space, per-point metric from its derivative terms; no coord map, no affine J."""
+    from tests.test_io import non_affine_problem
+    p = non_affine_problem()
+    ref = oracle.reference_action(p)
+    for sched in (None, fg.TilingParams.scpt(scatter=abi.SCATTER_ATOMIC), fg.TilingParams.dmma()):
+        y = fg.gpu_action(p, sched)
+        assert rel_l2(y, ref) <= 1e-12 and max_rel(y, ref) <= 1e-10

@@ -161,3 +161,13 @@ def test_scpt_multi_cell_nonfinite_names_lowest_cell():
     first = int(min(np.nonzero(np.any(np.isin(m, [m[c, 0] for c in bad]), axis=1))[0]))
     with pytest.raises(RuntimeError, match="non-finite value at cell %d during" % first):
         fg.gpu_action(p, scpt_g(3))
+
+
+@pytest.mark.parametrize("form,dim,deg,Q,n", [("laplace", 3, 2, 4, 3), ("mass", 2, 1, 3, 9), ("advection", 3, 1, 4, 3)])
+def test_macro_y_accumulators_in_smem(oracle, form, dim, deg, Q, n):
+    """Macro family with the y accumulators in thread-private shared memory (stage_smem=2)."""
+    p = fg.mesh_problem(form, dim, deg, Q, n)
+    ref = oracle.reference_action(p)
+    with fg.GpuInstance(p) as g:
+        close(g.action(fg.TilingParams.scpt(scatter=abi.SCATTER_MACRO, stage_smem=2)), ref)
+        close(g.action(fg.TilingParams.scpt(scatter=abi.SCATTER_MACRO, stage_smem=2, block_cells=128)), ref)

@@ -20,6 +20,8 @@ def sched(name):
     for p in parts[1:] if parts[0] != "dmma" else []:
         if p == "ms":
             kw["stage_smem"] = 1
+        elif p == "ys":
+            kw["stage_smem"] = 2
         elif p == "smem":
             kw["basis"] = abi.BASIS_SMEM
         elif p == "const":
