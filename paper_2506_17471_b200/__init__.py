@@ -5,3 +5,4 @@ from .action import (ExecutionOutcome, GpuInstance, TilingParams, device_count, 
 from . import abi  # noqa: F401
 from .mesh import CONFIGS, color_cells, config_problem, mesh_problem, unit_mesh  # noqa: F401
 from .io import load_instance, load_schedule, save_instance, save_schedule  # noqa: F401,E402
+from .krylov import DeviceOperator, cg, symmetric_problem  # noqa: F401,E402

@@ -14,7 +14,9 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <fstream>
 #include <sstream>
+#include <sys/stat.h>
 
 #include "femgpu_internal.hpp"
 
@@ -48,6 +50,46 @@ long long map_ops(const Signature& sig) {
     return ops;
 }
 
+// Persisted decisions: the timing pass runs once per (form, map, cell count, device) and the winner is
+// written next to the JIT cache, so a later process on the same box (e.g. a profiler run, whose timings
+// would be distorted by the instrumentation) replays the same kernel.  FEMGPU_TUNE_CACHE=0 disables.
+std::string tune_key(const Instance& I) {
+    const Signature& sig = I.sig;
+    std::ostringstream k;
+    k << "v2|" << sig.dim << "|" << sig.Q << "|" << sig.nW << "|" << sig.Tw << "|" << I.cells << "|" << I.output_size;
+    for (size_t i = 0; i < sig.sdofs.size(); ++i) k << "|s" << sig.sdofs[i] << ":" << sig.sterms[i];
+    for (size_t i = 0; i < sig.vdofs.size(); ++i) {
+        k << "|v" << sig.vdofs[i] << ":" << sig.vterms[i];
+        for (int c : sig.vcomps[i]) k << "," << c;
+    }
+    for (const auto& n : sig.nodes) k << "|" << n.op << "," << n.a << "," << n.b << "," << n.value;
+    for (int o : sig.outputs) k << "|o" << o;
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceProp prop{};
+    cudaGetDeviceProperties(&prop, dev);
+    k << "|" << prop.name << "|" << sms;
+    uint64_t h = 0xcbf29ce484222325ULL;
+    for (unsigned char c : k.str()) h = (h ^ c) * 0x100000001b3ULL;
+    char hex[32];
+    std::snprintf(hex, sizeof hex, "%016llx", static_cast<unsigned long long>(h));
+    return hex;
+}
+
+std::string tune_path(const Instance& I) {
+    std::string dir;
+    if (const char* e = std::getenv("FEMGPU_CACHE")) dir = e;
+    else dir = std::string(std::getenv("HOME") ? std::getenv("HOME") : "/tmp") + "/.cache/femgpu";
+    ::mkdir(dir.c_str(), 0755);
+    return dir + "/tune_" + tune_key(I) + ".txt";
+}
+
+bool tune_cache_enabled() {
+    const char* e = std::getenv("FEMGPU_TUNE_CACHE");
+    return !(e && std::strcmp(e, "0") == 0);
+}
+
 }  // namespace
 
 std::string describe_plan(const KernelPlan& kp) {
@@ -73,6 +115,19 @@ void autotune(Instance& I) {
     if ((env && std::strcmp(env, "0") == 0) || I.cells < kTuneMinCells) {
         I.auto_log = "default (no timing: " + std::string(I.cells < kTuneMinCells ? "small instance" : "FEMGPU_AUTOTUNE=0") + ")";
         return;
+    }
+    if (tune_cache_enabled()) {
+        std::ifstream in(tune_path(I));
+        if (in) {
+            try {
+                I.auto_sched = load_schedule(in);
+                I.auto_log = "cached decision (" + tune_path(I) + ")";
+                resolve_schedule(I, &I.auto_sched);  // still feasible here
+                return;
+            } catch (const Error&) {
+                I.auto_sched = dfma_default();
+            }
+        }
     }
     const Signature& sig = I.sig;
     // ---- model: FP64-pipe lane-slots per cell
@@ -167,6 +222,10 @@ void autotune(Instance& I) {
     FG_CUDA(cudaMemsetAsync(I.d_bad, 0xff, 2 * sizeof(unsigned long long), I.stream));
     FG_CUDA(cudaStreamSynchronize(I.stream));
     I.auto_log = log.str();
+    if (tune_cache_enabled()) {
+        std::ofstream out(tune_path(I));
+        if (out) save_schedule(out, &I.auto_sched, sig.ns(), sig.nv());
+    }
 }
 
 KernelPlan plan_for(Instance& I, const femgpu_schedule* s) {

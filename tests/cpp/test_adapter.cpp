@@ -4,6 +4,9 @@
 // and the binary travels to the GPU box).  Exit code 0 = all checks passed; 77 = no GPU.
 #include <cmath>
 #include <cstdio>
+#include <fstream>
+#include <string>
+#include <unistd.h>
 
 #define FEMGPU_WITH_FEMSCHED_SEARCH 1
 #include <femgpu/femsched_adapter.hpp>
@@ -65,6 +68,38 @@ int main() {
         } catch (const std::exception& e) {
             std::printf("tune failed: %s\n", e.what());
             ++fails;
+        }
+    }
+    // the B200 DeviceSpec (devices/b200.device, measured on this GPU) feeding the
+    // reference's own rank (b = 9 + SCPT) and tune through the measuring executor, jobs = 1 and 2
+    // (search.hpp:396-403 calls the executor concurrently; results must not depend on jobs)
+    {
+        char exe[4096] = {0};
+        const ssize_t n = readlink("/proc/self/exe", exe, sizeof exe - 1);
+        std::string root = n > 0 ? std::string(exe, static_cast<size_t>(n)) : std::string();
+        for (int up = 0; up < 4 && !root.empty(); ++up) root = root.substr(0, root.find_last_of('/'));
+        std::ifstream is(root + "/devices/b200.device");
+        if (!is) {
+            std::printf("devices/b200.device missing\n");
+            ++fails;
+        } else {
+            const DeviceSpec dev = load_device(is);
+            const auto sig = preset_signature(Operator::elasticity, 3, 2, 4);
+            const auto inst = make_problem(sig, preset_map(Operator::elasticity, sig), 200, 11);
+            SearchConfig cfg;  // b = 9 (search.hpp defaults)
+            try {
+                auto r1 = tune(inst, dev, cfg, 1, femgpu::executor());
+                auto r2 = tune(inst, dev, cfg, 2, femgpu::executor());
+                std::printf("tune on %s: %zu candidates verified (jobs 1), %zu (jobs 2), winner %s\n", dev.name.c_str(),
+                            r1.records.size(), r2.records.size(), detail::describe(r1.winner.params).c_str());
+                if (r1.records.size() != r2.records.size()) ++fails;
+                for (const auto* res : {&r1, &r2})
+                    for (const auto& r : res->records)
+                        if (!r.output_ok || !std::isfinite(r.selection_seconds)) ++fails;
+            } catch (const std::exception& e) {
+                std::printf("tune (b200) failed: %s\n", e.what());
+                ++fails;
+            }
         }
     }
     std::printf(fails ? "FAIL (%d)\n" : "PASS\n", fails);

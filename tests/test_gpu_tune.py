@@ -14,7 +14,8 @@ pytestmark = pytest.mark.gpu
 
 @pytest.mark.parametrize("form,dim,deg,Q,n", [("laplace", 3, 2, 4, 33), ("elasticity", 3, 2, 4, 33),
                                               ("helmholtz_coef", 2, 3, 12, 330)])
-def test_auto_schedule_is_tuned_and_matches_oracle(oracle, form, dim, deg, Q, n):
+def test_auto_schedule_is_tuned_and_matches_oracle(oracle, monkeypatch, form, dim, deg, Q, n):
+    monkeypatch.setenv("FEMGPU_TUNE_CACHE", "0")
     p = fg.mesh_problem(form, dim, deg, Q, n)
     assert p.connectivity.cell_count >= 200000
     ref = oracle.reference_action(p)
@@ -44,3 +45,20 @@ def test_nonfinite_input_survives_tuning(oracle):
     with fg.GpuInstance(p) as g:
         with pytest.raises(RuntimeError, match="non-finite value at cell"):
             g.action()
+
+
+def test_tuning_decision_is_persisted(tmp_path, monkeypatch):
+    monkeypatch.setenv("FEMGPU_CACHE", str(tmp_path))
+    monkeypatch.delenv("FEMGPU_TUNE_CACHE", raising=False)
+    p = fg.mesh_problem("laplace", 3, 2, 4, 33)
+    with fg.GpuInstance(p) as g:
+        y1 = g.action()
+        assert "timed:" in g.describe()
+        s1 = g.default_schedule()
+    assert list(tmp_path.glob("tune_*.txt"))
+    with fg.GpuInstance(p) as g:
+        y2 = g.action()
+        assert "cached decision" in g.describe()
+        s2 = g.default_schedule()
+    assert (s1.kind, s1.eval_row_tile, s1.quad_tile, s1.block_cells) == (s2.kind, s2.eval_row_tile, s2.quad_tile, s2.block_cells)
+    assert rel_l2(y1, y2) <= 1e-12

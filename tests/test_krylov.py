@@ -1,0 +1,56 @@
+"""The CG caller (paper_2506_17471_b200/krylov.py).
+
+CPU: the CG algorithm on torch CPU tensors with the CPU oracle as the operator (symmetric Helmholtz
+instance, Psi = Phi^T) converges and its solution satisfies the oracle's A x = b.
+GPU: the device-resident loop (femgpu_action_device into torch tensors, no host copies per action)
+converges to the same tolerance, checked against the oracle's action."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2506_17471_b200 as fg
+
+
+def oracle_apply(oracle, p):
+    def apply(v, out):
+        p.scalar_inputs[0] = v.numpy().copy()
+        out.copy_(torch.from_numpy(oracle.reference_action(p)))
+    return apply
+
+
+def test_symmetric_problem_is_symmetric(oracle):
+    p = fg.symmetric_problem("helmholtz", 2, 2, 6, 3)
+    n = p.output_size
+    rng = np.random.default_rng(1)
+    u, v = rng.standard_normal(n), rng.standard_normal(n)
+    p.scalar_inputs[0] = u
+    au = oracle.reference_action(p)
+    p.scalar_inputs[0] = v
+    av = oracle.reference_action(p)
+    assert abs(np.dot(v, au) - np.dot(u, av)) <= 1e-12 * np.linalg.norm(au) * np.linalg.norm(v)
+
+
+def test_cg_converges_with_oracle_operator(oracle):
+    p = fg.symmetric_problem("helmholtz", 2, 2, 6, 4)
+    b = torch.from_numpy(np.random.default_rng(3).uniform(0.5, 1.5, p.output_size))
+    x, it, hist = fg.cg(oracle_apply(oracle, p), b, rtol=1e-10, maxiter=500)
+    assert hist[-1] <= 1e-10 * float(torch.linalg.norm(b)) and it < 500
+    p.scalar_inputs[0] = x.numpy().copy()
+    r = oracle.reference_action(p) - b.numpy()
+    assert np.linalg.norm(r) <= 1e-9 * np.linalg.norm(b.numpy())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("form,dim,deg,Q,n", [("helmholtz", 3, 2, 14, 4), ("mass", 3, 2, 14, 4)])
+def test_device_cg_converges(oracle, form, dim, deg, Q, n):
+    p = fg.symmetric_problem(form, dim, deg, Q, n)
+    dev = torch.device("cuda", 0)
+    b = torch.from_numpy(np.random.default_rng(5).uniform(0.5, 1.5, p.output_size)).to(dev)
+    with fg.GpuInstance(p) as g:
+        op = fg.DeviceOperator(g)
+        x, it, hist = fg.cg(op.apply, b, rtol=1e-10, maxiter=2000, check_every=5)
+        assert op.launches == it  # one device action per iteration, no extra launches
+    assert hist[-1] <= 1e-10 * float(torch.linalg.norm(b))
+    p.scalar_inputs[0] = x.cpu().numpy().copy()
+    r = oracle.reference_action(p) - b.cpu().numpy()
+    assert np.linalg.norm(r) <= 1e-8 * np.linalg.norm(b.cpu().numpy())
