@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="femgpu", choices=["femgpu", "reference"])
     ap.add_argument("--config", default=CONFIG)
-    ap.add_argument("--n", type=int, default=None, help="override mesh size (testing)")
+    ap.add_argument("--mesh-n", dest="n", type=int, default=None, help="override mesh size (testing)")
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()

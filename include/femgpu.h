@@ -198,7 +198,9 @@ femgpu_status femgpu_action_host(femgpu_instance* inst, const femgpu_schedule* s
                                  const double* const* scalar_inputs,
                                  const double* const* vector_inputs, double* y_host);
 /* Device-resident: y_dev is a device pointer of output_size doubles; stream is a
- * cudaStream_t (NULL = the instance stream).  Asynchronous, no host sync. */
+ * cudaStream_t (NULL = the instance stream, a non-blocking stream; pass cudaStreamLegacy to order
+ * after work on the legacy default stream, e.g. torch's default stream whose handle is 0).
+ * Asynchronous, no host sync. */
 femgpu_status femgpu_action_device(femgpu_instance* inst, const femgpu_schedule* s, double* y_dev,
                                    void* stream);
 /* Paper timing protocol: warmup launches, then at least

@@ -131,6 +131,13 @@ def exchange(plan_: RankPlan, buf, send: Dict[int, np.ndarray], recv: Dict[int, 
     """Point-to-point halo exchange on torch tensors (NCCL or gloo): send buf[send[q]] to q,
     receive into buf[recv[q]] (added in ascending rank order when add=True)."""
     import torch.distributed as dist
+    if buf.is_cuda and dist.get_backend() == "gloo":
+        # gloo moves host tensors only: stage through the host (tests run several ranks on one GPU)
+        host = buf.detach().cpu()
+        cpu = lambda d: {q: (v.cpu() if hasattr(v, "cpu") else v) for q, v in d.items()}  # noqa: E731
+        exchange(plan_, host, cpu(send), cpu(recv), add, xp)
+        buf.copy_(host.to(buf.device))
+        return buf
     ops, recvs = [], []
     for q in sorted(set(send) | set(recv)):
         if q in send:
@@ -174,25 +181,34 @@ def bench(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local_rank)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    lib().femgpu_set_device(local_rank)
+    device = local_rank % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(device)
+    backend = os.environ.get("FEMGPU_DIST_BACKEND", "nccl")  # gloo: functional tests with ranks sharing a GPU
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", device))
+    else:
+        dist.init_process_group(backend)
+    lib().femgpu_set_device(device)
     p = fg.config_problem(args.config, n=args.n)
     plans = plan(p, world)
     pl = plans[rank]
     g = fg.GpuInstance(pl.local)
-    dev = torch.device("cuda", local_rank)
+    dev = torch.device("cuda", device)
     ysend, yrecv, xsend, xrecv = _index_tensors(pl, dev)
     y = torch.zeros(pl.local.output_size, dtype=torch.float64, device=dev)
     import ctypes as C
-    xp = C.c_void_p()
-    lib().femgpu_device_input(g.handle, 0, C.byref(xp))
-    x = torch.as_tensor(_CudaArray(xp.value, pl.local.scalar_inputs[0].size), device=dev)
+    x = None
+    if pl.x_send or pl.x_recv:
+        # forward halo of trial space 0 (scalar, same numbering as the test space)
+        xp = C.c_void_p()
+        lib().femgpu_device_input(g.handle, 0, C.byref(xp))
+        x = torch.as_tensor(_CudaArray(xp.value, pl.local.scalar_inputs[0].size), device=dev)
     stream = torch.cuda.current_stream(dev)
 
     def step():
-        exchange(pl, x, xsend, xrecv, False, torch)
-        g.action_device(y_dev=y.data_ptr(), stream=stream.cuda_stream)
+        if x is not None:
+            exchange(pl, x, xsend, xrecv, False, torch)
+        g.action_device(y_dev=y.data_ptr(), stream=stream.cuda_stream or 1)
         exchange(pl, y, ysend, yrecv, True, torch)
 
     for _ in range(max(args.warmup, 3)):
@@ -206,18 +222,24 @@ def bench(args):
     e1.record(stream)
     torch.cuda.synchronize()
     dist.barrier()
-    t = torch.tensor([e0.elapsed_time(e1) * 1e-3 / args.steps], dtype=torch.float64, device=dev)
+    t = torch.tensor([e0.elapsed_time(e1) * 1e-3 / args.steps], dtype=torch.float64,
+                     device=dev if backend == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_step = float(t.item())
     # parity: gather owned y to rank 0 and compare with the single-instance GPU result
-    owned = y[torch.as_tensor(np.nonzero(pl.owned_mask)[0], device=dev)]
-    gids = torch.as_tensor(pl.test_global[pl.owned_mask], device=dev)
+    gdev = dev if backend == "nccl" else torch.device("cpu")  # gloo collectives on host tensors
+    owned = y[torch.as_tensor(np.nonzero(pl.owned_mask)[0], device=dev)].to(gdev)
+    gids = torch.as_tensor(pl.test_global[pl.owned_mask], device=gdev)
     sizes = [None] * world
     dist.all_gather_object(sizes, int(owned.numel()))
-    outs = [torch.empty(s, dtype=torch.float64, device=dev) for s in sizes]
-    ids = [torch.empty(s, dtype=torch.int64, device=dev) for s in sizes]
-    dist.all_gather(outs, owned)
-    dist.all_gather(ids, gids)
+    mx = max(sizes)
+    pad = lambda t: torch.cat([t, t.new_zeros(mx - t.numel())])  # noqa: E731  (all_gather needs equal sizes)
+    outs = [torch.empty(mx, dtype=torch.float64, device=gdev) for _ in sizes]
+    ids = [torch.empty(mx, dtype=torch.int64, device=gdev) for _ in sizes]
+    dist.all_gather(outs, pad(owned))
+    dist.all_gather(ids, pad(gids))
+    outs = [o[:s] for o, s in zip(outs, sizes)]
+    ids = [i[:s] for i, s in zip(ids, sizes)]
     if rank == 0:
         yfull = np.zeros(p.output_size)
         for o, i in zip(outs, ids):
@@ -227,14 +249,18 @@ def bench(args):
             "metric": "FP64 operator-action GDOF/s", "value": p.output_size / t_step / 1e9, "unit": "GDOF/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "%s cell-partitioned over %d GPUs (contiguous brick-major ranges), "
-                                   "forward x halo + action + reverse y halo over NCCL per step" % (args.config, world),
+            "config": {"workload": "%s cell-partitioned over %d GPUs (contiguous brick-major ranges), %s"
+                                   "action + reverse y halo over %s per step"
+                                   % (args.config, world, "forward x halo + " if x is not None else
+                                      "(x static: no forward halo planned for this trial space) + ", backend.upper()),
                        "cells": int(p.connectivity.cell_count), "dofs": int(p.output_size),
                        "rank0_halo_dofs": int(halo), "parallelism": "cells%d" % world},
             "gpu_launches": args.steps,
         }
-        ref = fg.GpuInstance(p).action()
+        with fg.GpuInstance(p) as gi:
+            ref = gi.action()
         out["parity_vs_1gpu_rel_l2"] = float(np.linalg.norm(yfull - ref) / np.linalg.norm(ref))
+        out["backend"] = backend
         print(json.dumps(out))
     dist.destroy_process_group()
     g.close()

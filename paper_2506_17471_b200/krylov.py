@@ -65,7 +65,7 @@ class DeviceOperator:
         """out = A v (both float64 device tensors); ordered on torch's current stream."""
         import torch
         self.x.copy_(v)
-        stream = torch.cuda.current_stream(self.dev).cuda_stream
+        stream = torch.cuda.current_stream(self.dev).cuda_stream or 1  # 0 = legacy default stream -> cudaStreamLegacy
         self.inst.action_device(self.params, y_dev=out.data_ptr(), stream=stream)
         self.launches += 1
 
@@ -103,3 +103,34 @@ def cg(apply: Callable, b, x0=None, rtol: float = 1e-10, maxiter: int = 1000,
             if hist[-1] <= rtol * bnorm:
                 return x, it, hist
     return x, maxiter, hist
+
+
+def dist_cg(plan_, local_apply: Callable, b_local, rtol: float = 1e-10, maxiter: int = 1000, check_every: int = 1):
+    """Distributed CG over the cell partition of dist.plan (one rank per GPU, persistent halos).
+
+    Vectors live in the rank's local test numbering (owned DOFs + ghosts).  Per iteration: forward halo
+    of the search direction (owners -> ghosts, dist.exchange), the local action `local_apply(v, out)`,
+    reverse halo of the partial products (ghost contributions -> owners, summed in ascending rank
+    order), and all-reduced dot products over owned DOFs.  Requires a scalar trial space numbered like
+    the test space (plan_.x_send / x_recv); the halo index tensors are built once (persistent)."""
+    import torch
+    import torch.distributed as dist
+
+    from .dist import exchange
+    dev = b_local.device
+    conv = lambda d: {q: torch.as_tensor(v, device=dev) for q, v in d.items()}  # noqa: E731
+    xs, xr, ys, yr = conv(plan_.x_send), conv(plan_.x_recv), conv(plan_.y_send), conv(plan_.y_recv)
+    owned = torch.as_tensor(plan_.owned_mask, device=dev)
+
+    def dot(a, c):
+        t = torch.sum(a[owned] * c[owned]).reshape(1)
+        dist.all_reduce(t)
+        return t[0]
+
+    def apply(v, out):
+        exchange(plan_, v, xs, xr, False, torch)   # ghosts of v <- owners
+        local_apply(v, out)
+        exchange(plan_, out, ys, yr, True, torch)  # owners += ghost partial products
+        out[~owned] = 0.0
+
+    return cg(apply, b_local, rtol=rtol, maxiter=maxiter, check_every=check_every, dot=dot)

@@ -54,3 +54,50 @@ def test_device_cg_converges(oracle, form, dim, deg, Q, n):
     p.scalar_inputs[0] = x.cpu().numpy().copy()
     r = oracle.reference_action(p) - b.cpu().numpy()
     assert np.linalg.norm(r) <= 1e-8 * np.linalg.norm(b.cpu().numpy())
+
+
+def _dist_worker(rank, world, port, out_dir):
+    import os
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import oracle
+    from paper_2506_17471_b200 import dist as fdist
+    p = fg.symmetric_problem("helmholtz", 2, 2, 6, 6)
+    b = np.random.default_rng(3).uniform(0.5, 1.5, p.output_size)
+    pl = fdist.plan(p, world, align=2)[rank]
+    loc = pl.local
+
+    def local_apply(v, out):
+        loc.scalar_inputs[0] = v.numpy().copy()
+        out.copy_(torch.from_numpy(oracle.reference_action(loc)))
+
+    b_loc = torch.from_numpy(b[pl.test_global] * pl.owned_mask)
+    x, it, hist = fg.krylov.dist_cg(pl, local_apply, b_loc, rtol=1e-10, maxiter=500)
+    np.savez(os.path.join(out_dir, "r%d.npz" % rank), gids=pl.test_global[pl.owned_mask],
+             xs=x.numpy()[pl.owned_mask], it=it)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_distributed_cg_matches_single_process(tmp_path, oracle, world):
+    import os
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    mp.spawn(_dist_worker, args=(world, port, str(tmp_path)), nprocs=world, join=True)
+    p = fg.symmetric_problem("helmholtz", 2, 2, 6, 6)
+    b = np.random.default_rng(3).uniform(0.5, 1.5, p.output_size)
+    x = np.full(p.output_size, np.nan)
+    for r in range(world):
+        d = np.load(os.path.join(tmp_path, "r%d.npz" % r))
+        x[d["gids"]] = d["xs"]
+    assert not np.any(np.isnan(x))
+    p.scalar_inputs[0] = x
+    res = oracle.reference_action(p) - b
+    assert np.linalg.norm(res) <= 1e-9 * np.linalg.norm(b)
