@@ -475,7 +475,7 @@ std::string KernelPlan::key() const {
     for (size_t g = 0; g < group_cap.size(); ++g) s << "g" << group_entries[g] << ":" << group_cap[g];
     for (int g : sgroup) s << "S" << g;
     for (int g : vgroup) s << "V" << g;
-    s << "T" << tgroup << "C" << cgroup << "tv" << tvec;
+    s << "T" << tgroup << "C" << cgroup << "tv" << tvec << "br" << breg;
     uint64_t h = 0xcbf29ce484222325ULL;
     for (const auto& p : mpat)
         for (int v : p) h = (h ^ static_cast<uint64_t>(v + 1)) * 0x100000001b3ULL;

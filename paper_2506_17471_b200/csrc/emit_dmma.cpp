@@ -203,6 +203,7 @@ void emit_dmma_kernel(std::ostringstream& o, const Signature& sig, const KernelP
     const int NT = kp.block, NW = NT / 32, CW = L.CW, MB = L.MB, TQL = L.TQL, nH = SM.nH;
     const int MBJ = std::max(1, kp.Ter), PF = kp.Tqr > 0 ? 1 : 0;
     const bool tv = kp.tvec >= 0 && std::getenv("FEMGPU_DEBUG_NO_TVEC") == nullptr;
+    const bool breg = kp.breg && L.NCH == 1;
     const bool smemA = kp.basis == FEMGPU_BASIS_SMEM;
     // timing experiments only (wrong results): plain stores instead of red.add in the scatter
     const bool scatter_store = std::getenv("FEMGPU_DEBUG_SCATTER_STORE") != nullptr;
@@ -232,6 +233,8 @@ void emit_dmma_kernel(std::ostringstream& o, const Signature& sig, const KernelP
         o << "  const double* const FR = P.afr + lane;\n";
     }
     o << "  double* const sH = sm + " << SM.off_H << " + warp * " << static_cast<long long>(nH) * CW << "; (void)sH;\n";
+    if (breg)  // single chunk: every B fragment of the form lives in registers for the whole kernel
+        for (long long f = 0; f < L.FPC; ++f) o << "  const double Bf" << f << " = FR[" << f * 32 << "];\n";
     o << "  const int n_tasks = (P.n_cells + " << CW - 1 << ") / " << CW << ";\n";
     o << "  unsigned long long badc = ~0ULL;\n";
     o << "  #pragma unroll 1\n";
@@ -391,7 +394,7 @@ void emit_dmma_kernel(std::ostringstream& o, const Signature& sig, const KernelP
     }
     o << "      #pragma unroll 1\n";
     o << "      for (int ch = 0; ch < " << L.NCH << "; ++ch) {\n";
-    o << "        const double* const Fc = FR + (size_t)ch * " << L.FPC * 32 << ";\n";
+    o << "        const double* const Fc = FR + (size_t)ch * " << L.FPC * 32 << "; (void)Fc;\n";
     // ---- evaluation GEMMs (one B fragment load feeds MBJ DMMAs)
     for (size_t gi = 0; gi < L.groups.size(); ++gi) {
         const DmmaGroup& g = L.groups[gi];
@@ -399,7 +402,8 @@ void emit_dmma_kernel(std::ostringstream& o, const Signature& sig, const KernelP
             for (int j = 0; j < MBJ; ++j)
                 o << "        double S" << gi << "_" << nb << J << j << "_0 = 0.0, S" << gi << "_" << nb << J << j << "_1 = 0.0;\n";
             for (int ks = 0; ks < g.KS; ++ks) {
-                o << "        { const double b = Fc[" << (g.foff + static_cast<long long>(nb) * g.KS + ks) * 32 << "];";
+                const long long f = g.foff + static_cast<long long>(nb) * g.KS + ks;
+                o << "        { const double b = " << (breg ? "Bf" + S(f) : "Fc[" + S(f * 32) + "]") << ";";
                 for (int j = 0; j < MBJ; ++j)
                     o << " DMMA(S" << gi << "_" << nb << J << j << "_0, S" << gi << "_" << nb << J << j << "_1, "
                       << uname("uA", static_cast<int>(gi), ks, j) << ", b);";
@@ -455,7 +459,8 @@ void emit_dmma_kernel(std::ostringstream& o, const Signature& sig, const KernelP
         for (int k = 0; k < sig.Tw; ++k) {
             const int kq = k * TQL + s;
             for (int nb = 0; nb < L.NBQ; ++nb) {
-                o << "        { const double b = Fc[" << (L.foff_q + static_cast<long long>(nb) * L.KQ + kq) * 32 << "];";
+                const long long f = L.foff_q + static_cast<long long>(nb) * L.KQ + kq;
+                o << "        { const double b = " << (breg ? "Bf" + S(f) : "Fc[" + S(f * 32) + "]") << ";";
                 for (int j = 0; j < MBJ; ++j)
                     o << " DMMA(y" << nb << J << j << "_0, y" << nb << J << j << "_1, E" << s << "_" << k << J << j << ", b);";
                 o << " }\n";

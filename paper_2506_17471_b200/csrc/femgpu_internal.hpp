@@ -83,6 +83,7 @@ struct KernelPlan {
     std::vector<int> sgroup, vgroup;
     int tgroup = -1, cgroup = -1;
     int tvec = -1;                     // DMMA: vector space whose node map interleaves into the test map
+    bool breg = false;                 // DMMA: B fragments in registers (single quadrature chunk)
     std::vector<int> group_entries, group_cap;   // per group: entries per cell, max unique per tile
     // MLT family (TilingParams)
     int Nc = 1, Nwi = 1, TQ = 1, Ter = 1, Tqr = 1, Tqc = 1;

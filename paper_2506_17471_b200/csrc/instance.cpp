@@ -473,6 +473,7 @@ void resolve_dmma(const Signature& sig, KernelPlan& kp, const femgpu_schedule* s
     if (kp.Ter > kp.Nc / 8 || (kp.Nc / 8) % kp.Ter)
         fail(FEMGPU_E_INFEASIBLE, "dmma: joint m-blocks (eval_row_tile) must divide the m-blocks of a warp task");
     kp.Tqr = s->quad_row_tile > 0 ? 1 : 0;
+    kp.breg = s->reserved[3] == 1;  // B fragments in registers (honoured for a single quadrature chunk)
     const int q4 = (sig.Q + 3) / 4 * 4;
     if (s->quad_tile > 0) {
         kp.TQ = std::min(q4, (s->quad_tile + 3) / 4 * 4);

@@ -31,7 +31,7 @@ def random_dmma(sig, rng):
     return fg.TilingParams.dmma(cells_per_group=8 * mb, quad_tile=pick(sig.quad_points),
                                 lanes_per_cell=(0, 4)[rng.next_u64() % 2], block_cells=32 * pick(8),
                                 eval_row_tile=joint[rng.next_u64() % len(joint)],
-                                quad_row_tile=rng.next_u64() % 2,
+                                quad_row_tile=rng.next_u64() % 2, stage_smem=rng.next_u64() % 2,
                                 basis=abi.BASIS_SMEM if rng.next_u64() % 2 else abi.BASIS_CONST)
 
 

@@ -53,6 +53,8 @@ def sched(name):
                 d["quad_row_tile"] = int(p[1:])
             elif p.startswith("m"):
                 d["min_blocks"] = int(p[1:])
+            elif p == "breg":
+                d["stage_smem"] = 1
             elif p.startswith("b"):
                 d["block_cells"] = int(p[1:])
             elif p == "smem":
