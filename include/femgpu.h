@@ -192,8 +192,10 @@ femgpu_status femgpu_set_inputs(femgpu_instance* inst, const double* const* scal
                                 const double* const* vector_inputs);
 /* y = A(u)·x into a host buffer of output_size doubles (H2D of nothing, D2H of y). */
 femgpu_status femgpu_action(femgpu_instance* inst, const femgpu_schedule* s, double* y_host);
-/* End to end: copy host inputs in (like set_inputs), run, copy y out; all on the
- * instance stream.  Host buffers should be pinned (femgpu_host_alloc) for speed. */
+/* End to end: copy host inputs in (like set_inputs), run, copy y out.  On instances with locality
+ * (>= 1M cells, node-ordered slabs) the H2D of x, the action (slab by slab over contiguous cell
+ * ranges) and the D2H of the finished part of y overlap on three streams (FEMGPU_PIPELINE=0
+ * disables).  Host buffers should be pinned (femgpu_host_alloc) for the overlap. */
 femgpu_status femgpu_action_host(femgpu_instance* inst, const femgpu_schedule* s,
                                  const double* const* scalar_inputs,
                                  const double* const* vector_inputs, double* y_host);

@@ -205,10 +205,13 @@ femgpu_status femgpu_action_host(femgpu_instance* h, const femgpu_schedule* s, c
         std::lock_guard<std::mutex> lk(I.mu);
         FG_CUDA(cudaSetDevice(I.device));
         const femgpu::KernelPlan kp = femgpu::plan_for(I, s);
-        copy_inputs(I, scalar_inputs, vector_inputs, I.stream);
-        femgpu::run_action(I, kp, I.d_y, I.stream);
-        FG_CUDA(cudaMemcpyAsync(y_host, I.d_y, sizeof(double) * static_cast<size_t>(I.output_size),
-                                cudaMemcpyDeviceToHost, I.stream));
+        // overlapped H2D / slabs / D2H when the instance has locality (pipeline.cpp), else sequential
+        if (!femgpu::pipelined_host_action(I, kp, scalar_inputs, vector_inputs, y_host)) {
+            copy_inputs(I, scalar_inputs, vector_inputs, I.stream);
+            femgpu::run_action(I, kp, I.d_y, I.stream);
+            FG_CUDA(cudaMemcpyAsync(y_host, I.d_y, sizeof(double) * static_cast<size_t>(I.output_size),
+                                    cudaMemcpyDeviceToHost, I.stream));
+        }
         femgpu::check_failure(I, kp, I.stream);
     });
 }

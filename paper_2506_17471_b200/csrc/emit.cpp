@@ -155,7 +155,9 @@ void emit_params(Out& o, const Signature& sig, const KernelPlan& kp, long long n
         o.line("  const int* goff" + std::to_string(g) + "; const int* gcnt" + std::to_string(g) + "; const int* glist" +
                std::to_string(g) + "; const unsigned short* gloc" + std::to_string(g) + ";");
     o.line("  const unsigned short* roff; const unsigned short* rpos;");
-    o.line("  int n_cells; int stride; int n_tiles; int lstride; int n_groups; int pad2_;");
+    // cell0 / n_cells: the cell range [cell0, n_cells) of this launch (pipelined host actions launch
+    // one slab at a time; macro: group range [cell0/G, n_cells/G)); stride / n_groups stay global
+    o.line("  int n_cells; int stride; int n_tiles; int lstride; int n_groups; int cell0;");
     if (nt_param > 0) o.line("  double tab[" + std::to_string(nt_param) + "];");
     o.line("};");
 }
@@ -506,7 +508,7 @@ void emit_scpt_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const 
         o.line("for (int i = threadIdx.x; i < " + S(sig.tab_size) + "; i += blockDim.x) sT[i] = P.tabg[i];");
         o.line("__syncthreads();");
     }
-    o.line("const int cell = blockIdx.x * blockDim.x + threadIdx.x;");
+    o.line("const int cell = P.cell0 + blockIdx.x * blockDim.x + threadIdx.x;");
     o.line("int stage = -1; (void)stage;");
     o.line("if (cell < P.n_cells) {");
     o.ind++;
@@ -556,7 +558,7 @@ void emit_scpt_multi_kernel(Out& o, const Signature& sig, const KernelPlan& kp, 
         o.line("for (int i = threadIdx.x; i < " + S(sig.tab_size) + "; i += blockDim.x) sT[i] = P.tabg[i];");
         o.line("__syncthreads();");
     }
-    o.line("const int cbase = blockIdx.x * " + S(G) + " * blockDim.x + threadIdx.x;");
+    o.line("const int cbase = P.cell0 + blockIdx.x * " + S(G) + " * blockDim.x + threadIdx.x;");
     o.line("if (cbase >= P.n_cells) return;");
     for (int k = 0; k < G; ++k) {
         o.line("const bool ok_c" + S(k) + " = cbase + " + S(k) + " * (int)blockDim.x < P.n_cells;");
@@ -933,8 +935,8 @@ void emit_macro_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const
         if (kp.basis != FEMGPU_BASIS_SMEM && !kp.mstage) o.line("extern __shared__ __align__(16) unsigned char smraw[];");
         o.line("double* const sy_base = reinterpret_cast<double*>(smraw + " + S(ysmem_off) + ") + threadIdx.x;");
     }
-    o.line("const int grp = blockIdx.x * " + S(kp.block) + " + threadIdx.x;");
-    o.line("if (grp >= P.n_groups) return;");
+    o.line("const int grp = P.cell0 / " + S(kp.G) + " + blockIdx.x * " + S(kp.block) + " + threadIdx.x;");
+    o.line("if (grp >= P.n_cells / " + S(kp.G) + ") return;");
     o.line("const size_t NG = (size_t)P.n_groups;");
     // gathers: unique global indices per group, then values
     std::set<int> gathered;

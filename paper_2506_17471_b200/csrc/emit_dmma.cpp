@@ -235,11 +235,11 @@ void emit_dmma_kernel(std::ostringstream& o, const Signature& sig, const KernelP
     o << "  double* const sH = sm + " << SM.off_H << " + warp * " << static_cast<long long>(nH) * CW << "; (void)sH;\n";
     if (breg)  // single chunk: every B fragment of the form lives in registers for the whole kernel
         for (long long f = 0; f < L.FPC; ++f) o << "  const double Bf" << f << " = FR[" << f * 32 << "];\n";
-    o << "  const int n_tasks = (P.n_cells + " << CW - 1 << ") / " << CW << ";\n";
+    o << "  const int n_tasks = (P.n_cells - P.cell0 + " << CW - 1 << ") / " << CW << ";\n";
     o << "  unsigned long long badc = ~0ULL;\n";
     o << "  #pragma unroll 1\n";
     o << "  for (int task = blockIdx.x * " << NW << " + warp; task < n_tasks; task += gridDim.x * " << NW << ") {\n";
-    o << "    const int c0 = task * " << CW << ";\n";
+    o << "    const int c0 = P.cell0 + task * " << CW << ";\n";
     // ---- geometry + cell-invariant nodes, one lane per cell
     if (sig.affine || nH > 0) {
         o << "    if (lane < " << CW << ") {\n";

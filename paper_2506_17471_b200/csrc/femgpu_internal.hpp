@@ -181,6 +181,16 @@ struct DeviceSpace {
     int group = -1;                 // content-equal map group
 };
 
+// Slab plan of the overlapped host-buffer action (pipeline.cpp).
+struct PipePlan {
+    int align = 1;
+    std::vector<int> cb;                      // slab k = cells [cb[k], cb[k+1])
+    std::vector<std::vector<long long>> up;   // per trial space: input rows resident before slab k
+    std::vector<long long> zero_hi;           // y rows zeroed before slab k
+    std::vector<long long> fin;               // y rows final (downloadable) after slab k
+    bool useful = false;
+};
+
 struct Instance {
     Signature sig;
     int device = 0;
@@ -214,6 +224,10 @@ struct Instance {
     int64_t last_launches = 0;
     std::mutex mu;                  // serialises actions on this instance (tune(jobs>1))
     // automatic schedule (s == NULL): chosen once per instance by tune.cpp
+    std::unique_ptr<PipePlan> pipe;
+    cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+    std::vector<cudaEvent_t> ev_pipe;
+    const PipePlan& pipe_plan(int align);
     bool auto_ready = false;
     femgpu_schedule auto_sched{};
     std::string auto_log;
@@ -239,6 +253,14 @@ std::unique_ptr<Instance> create_instance(const femgpu_problem* p);
 KernelPlan resolve_schedule(Instance& inst, const femgpu_schedule* s);
 void run_action(Instance& inst, const KernelPlan& kp, double* d_y, cudaStream_t stream,
                 cudaEvent_t after_zero = nullptr);
+// One launch over the cell range [c_begin, c_end) (Scpt, Macro (G-aligned) and Dmma families);
+// y is zeroed first only when zero_y.
+void run_action_range(Instance& inst, const KernelPlan& kp, double* d_y, cudaStream_t stream, int c_begin, int c_end,
+                      bool zero_y, cudaEvent_t after_zero = nullptr);
+bool supports_cell_range(const KernelPlan& kp);
+// pipeline.cpp: femgpu_action_host overlapped over H2D / compute / D2H streams; false = not applicable
+bool pipelined_host_action(Instance& inst, const KernelPlan& kp, const double* const* scalar_inputs,
+                           const double* const* vector_inputs, double* y_host);
 void check_failure(Instance& inst, const KernelPlan& kp, cudaStream_t stream);
 }  // namespace femgpu
 const femgpu_problem* femgpu_owned_view(const femgpu_owned_problem* p);

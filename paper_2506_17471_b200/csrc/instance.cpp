@@ -196,6 +196,12 @@ Instance::~Instance() {
     }
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
+    for (cudaStream_t s : {s_h2d, s_d2h})
+        if (s) {
+            cudaStreamSynchronize(s);
+            cudaStreamDestroy(s);
+        }
+    for (cudaEvent_t e : ev_pipe) cudaEventDestroy(e);
     for (void* p : allocations) cudaFree(p);
     cudaGetLastError();
 }
@@ -815,7 +821,8 @@ struct ParamBuf {
 };
 
 // Builds the kernel-parameter block in the exact layout of the emitted `struct Params`.
-ParamBuf build_params(Instance& I, const KernelPlan& kp, double* d_y, const TileLayout* L) {
+ParamBuf build_params(Instance& I, const KernelPlan& kp, double* d_y, const TileLayout* L, int c_begin = 0,
+                      int c_end = -1) {
     const Signature& sig = I.sig;
     ParamBuf P;
     for (const auto& sp : I.sspaces) {
@@ -845,12 +852,12 @@ ParamBuf build_params(Instance& I, const KernelPlan& kp, double* d_y, const Tile
     }
     P.put(static_cast<const void*>(L ? L->d_roff : nullptr));
     P.put(static_cast<const void*>(L ? L->d_rpos : nullptr));
-    P.put(static_cast<int32_t>(I.cells));
+    P.put(static_cast<int32_t>(c_end < 0 ? I.cells : c_end));  // end of the launched cell range
     P.put(static_cast<int32_t>(I.cells));  // stride of the [entry][cell] maps
     P.put(static_cast<int32_t>(L ? L->n_tiles : 0));
     P.put(static_cast<int32_t>(L ? L->n_tiles * L->tile_cells : 0));  // local-map row stride
     P.put(static_cast<int32_t>(M ? M->n_groups : 0));
-    P.put(static_cast<int32_t>(0));
+    P.put(static_cast<int32_t>(c_begin));  // cell0: first cell of the launched range
     if (kp.basis == FEMGPU_BASIS_CONST && kp.family != Family::Mlt)
         for (double v : I.tab) P.put(v);
     P.align(8);
@@ -869,28 +876,41 @@ std::shared_ptr<Module> Instance::module_for(const KernelPlan& kp) {
     return m;
 }
 
+bool supports_cell_range(const KernelPlan& kp) {
+    return kp.family == Family::Scpt || kp.family == Family::Macro || kp.family == Family::Dmma;
+}
+
 void run_action(Instance& I, const KernelPlan& kp, double* d_y, cudaStream_t stream, cudaEvent_t after_zero) {
+    run_action_range(I, kp, d_y, stream, 0, I.cells, true, after_zero);
+}
+
+void run_action_range(Instance& I, const KernelPlan& kp, double* d_y, cudaStream_t stream, int c_begin, int c_end,
+                      bool zero_y, cudaEvent_t after_zero) {
     auto mod = I.module_for(kp);
     if (mod->emitted.smem_bytes > 227 * 1024)
         fail(FEMGPU_E_INFEASIBLE, "schedule: " + std::to_string(mod->emitted.smem_bytes) +
                                       " bytes of shared memory per CTA exceed the 227 KB sm_100a limit");
+    if ((c_begin != 0 || c_end != I.cells) && !supports_cell_range(kp))
+        fail(FEMGPU_E_INTERNAL, "run_action_range: family does not support cell ranges");
     const TileLayout* L = kp.family == Family::Tile ? &I.tile_layout(kp.tile_cells) : nullptr;
-    ParamBuf P = build_params(I, kp, d_y, L);
+    ParamBuf P = build_params(I, kp, d_y, L, c_begin, c_end);
     void* args[] = {P.b.data()};
-    FG_CUDA(cudaMemsetAsync(d_y, 0, sizeof(double) * static_cast<size_t>(I.output_size), stream));
+    if (zero_y) FG_CUDA(cudaMemsetAsync(d_y, 0, sizeof(double) * static_cast<size_t>(I.output_size), stream));
     if (after_zero) FG_CUDA(cudaEventRecord(after_zero, stream));
+    const long long ncell = static_cast<long long>(c_end) - c_begin;
+    if (ncell <= 0) return;
     long long grid = 0;
     if (kp.family == Family::Mlt)
         grid = (static_cast<long long>(I.cells) + kp.Nc - 1) / kp.Nc;
     else if (kp.family == Family::Tile)
         grid = std::min<long long>(L->n_tiles, static_cast<long long>(mod->sms) * std::max(1, mod->occupancy));
     else if (kp.family == Family::Macro)
-        grid = (I.macro_layout(kp.G).n_groups + kp.block - 1) / kp.block;
+        grid = (ncell / kp.G + kp.block - 1) / kp.block;
     else if (kp.family == Family::Dmma)
-        grid = std::min<long long>(((static_cast<long long>(I.cells) + kp.Nc - 1) / kp.Nc + kp.block / 32 - 1) / (kp.block / 32),
+        grid = std::min<long long>(((ncell + kp.Nc - 1) / kp.Nc + kp.block / 32 - 1) / (kp.block / 32),
                                    static_cast<long long>(mod->sms) * std::max(1, mod->occupancy));
     else
-        grid = (static_cast<long long>(I.cells) + static_cast<long long>(kp.block) * std::max(1, kp.G) - 1) /
+        grid = (ncell + static_cast<long long>(kp.block) * std::max(1, kp.G) - 1) /
                (static_cast<long long>(kp.block) * std::max(1, kp.G));
     if (grid > INT_MAX) fail(FEMGPU_E_INFEASIBLE, "launch: grid too large");
     FG_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(mod->fast), dim3(static_cast<unsigned>(grid)),

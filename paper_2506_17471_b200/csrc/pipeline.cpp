@@ -1,0 +1,151 @@
+// pipeline.cpp — end-to-end action with host buffers (femgpu_action_host) overlapped across
+// three streams: the inputs are uploaded in node-ordered chunks, the action runs slab by slab
+// over contiguous cell ranges as soon as the nodes a slab reads are resident, and the finished
+// part of y is downloaded while later slabs still compute.  PCIe is full duplex, so the H2D of x
+// and the D2H of y overlap each other and the kernels: the host-buffer action approaches
+// max(H2D, D2H) instead of H2D + action + D2H.
+//
+// The slab plan comes from the instance's own maps (no mesh assumptions): for slab k and every
+// distinct map, the min/max index its cells touch.  Inputs of space i must be resident up to
+// max_k (prefix maximum); y rows below the smallest index any later slab touches are final after
+// slab k (suffix minimum) and are downloaded then; y rows are zeroed just before the first slab
+// that can write them.  Brick-major structured meshes give near-ideal overlap; for an instance
+// without locality the plan degenerates to the sequential order (and is then not used).
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <limits>
+
+#include "femgpu_internal.hpp"
+
+namespace femgpu {
+
+namespace {
+
+constexpr long long kPipeMinCells = 1000000;
+
+int slab_count() {
+    const char* e = std::getenv("FEMGPU_PIPE_SLABS");
+    const int k = e ? std::atoi(e) : 16;
+    return std::max(2, std::min(128, k));
+}
+
+}  // namespace
+
+const PipePlan& Instance::pipe_plan(int align) {
+    const int K = slab_count();
+    if (pipe && pipe->align == align && static_cast<int>(pipe->cb.size()) == K + 1) return *pipe;
+    auto P = std::make_unique<PipePlan>();
+    P->align = align;
+    const long long units = (static_cast<long long>(cells) + align - 1) / align;
+    for (int k = 0; k <= K; ++k) P->cb.push_back(static_cast<int>(std::min<long long>(cells, units * k / K * align)));
+    const size_t ng = group_maps.size();
+    std::vector<std::vector<long long>> lo(ng, std::vector<long long>(K)), hi(ng, std::vector<long long>(K));
+    for (size_t g = 0; g < ng; ++g) {
+        const std::vector<int32_t>& m = group_maps[g];
+        const long long E = static_cast<long long>(m.size() / cells);
+        for (int k = 0; k < K; ++k) {
+            long long a = std::numeric_limits<long long>::max(), b = -1;
+            for (long long i = static_cast<long long>(P->cb[k]) * E; i < static_cast<long long>(P->cb[k + 1]) * E; ++i) {
+                a = std::min<long long>(a, m[i]);
+                b = std::max<long long>(b, m[i]);
+            }
+            lo[g][k] = b < 0 ? group_global[g] : a;
+            hi[g][k] = b + 1;
+        }
+    }
+    auto prefix_max = [&](int g) {
+        std::vector<long long> v(K);
+        long long run = 0;
+        for (int k = 0; k < K; ++k) v[k] = run = std::max(run, hi[g][k]);
+        return v;
+    };
+    for (const auto& sp : sspaces) P->up.push_back(prefix_max(sp.group));
+    for (const auto& sp : vspaces) P->up.push_back(prefix_max(sp.group));
+    P->zero_hi = prefix_max(test_group);
+    P->zero_hi[K - 1] = output_size;  // rows no cell touches are zeros of the result too
+    P->fin.assign(K, output_size);
+    long long run = output_size;
+    for (int k = K - 1; k >= 0; --k) {
+        P->fin[k] = run;
+        run = std::min(run, lo[test_group][k]);
+    }
+    // useful when the first slab needs a small part of the inputs and y completes progressively
+    long long need0 = 0, total = 0;
+    for (size_t i = 0; i < P->up.size(); ++i) {
+        need0 += P->up[i][0];
+        total += P->up[i][K - 1];
+    }
+    P->useful = total > 0 && need0 * 10 <= total * 6 && P->fin[K / 2] * 10 >= static_cast<long long>(output_size) * 2;
+    pipe = std::move(P);
+    return *pipe;
+}
+
+bool pipelined_host_action(Instance& I, const KernelPlan& kp, const double* const* scalar_inputs,
+                           const double* const* vector_inputs, double* y_host) {
+    const char* env = std::getenv("FEMGPU_PIPELINE");
+    if ((env && std::strcmp(env, "0") == 0) || I.cells < kPipeMinCells || !supports_cell_range(kp)) return false;
+    const PipePlan& P = I.pipe_plan(kp.family == Family::Macro ? kp.G : 32);
+    if (!P.useful) return false;
+    const int K = static_cast<int>(P.cb.size()) - 1;
+    if (!I.s_h2d) {
+        FG_CUDA(cudaStreamCreateWithFlags(&I.s_h2d, cudaStreamNonBlocking));
+        FG_CUDA(cudaStreamCreateWithFlags(&I.s_d2h, cudaStreamNonBlocking));
+    }
+    while (static_cast<int>(I.ev_pipe.size()) < 2 * K + 1) {
+        cudaEvent_t e;
+        FG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        I.ev_pipe.push_back(e);
+    }
+    const int d = I.sig.dim;
+    // previous work on the instance stream (an earlier action) must finish before inputs change
+    FG_CUDA(cudaEventRecord(I.ev_pipe[2 * K], I.stream));
+    FG_CUDA(cudaStreamWaitEvent(I.s_h2d, I.ev_pipe[2 * K], 0));
+    std::vector<long long> done(P.up.size(), 0);
+    long long zeroed = 0, sent = 0;
+    for (int k = 0; k < K; ++k) {
+        // H2D: every trial space up to what slab k reads
+        for (size_t i = 0; i < I.sspaces.size(); ++i) {
+            const long long a = done[i], b = P.up[i][k];
+            if (b > a) {
+                if (!scalar_inputs || !scalar_inputs[i]) invalid("instance: scalar input length mismatch");
+                FG_CUDA(cudaMemcpyAsync(I.sspaces[i].d_x + a, scalar_inputs[i] + a, sizeof(double) * (b - a),
+                                        cudaMemcpyHostToDevice, I.s_h2d));
+                done[i] = b;
+            }
+        }
+        for (size_t i = 0; i < I.vspaces.size(); ++i) {
+            const size_t j = I.sspaces.size() + i;
+            const long long a = done[j], b = P.up[j][k];
+            if (b > a) {
+                if (!vector_inputs || !vector_inputs[i]) invalid("instance: vector input length mismatch");
+                const int vs = vec_stride(d);
+                upload_padded(I.vspaces[i].d_x + a * vs, vector_inputs[i] + a * d, b - a, d,
+                              I.vspaces[i].d_stage ? I.vspaces[i].d_stage + a * d : nullptr, I.s_h2d);
+                done[j] = b;
+            }
+        }
+        FG_CUDA(cudaEventRecord(I.ev_pipe[k], I.s_h2d));
+        // compute: zero the y rows slab k can newly reach, then the slab
+        FG_CUDA(cudaStreamWaitEvent(I.stream, I.ev_pipe[k], 0));
+        if (P.zero_hi[k] > zeroed) {
+            FG_CUDA(cudaMemsetAsync(I.d_y + zeroed, 0, sizeof(double) * (P.zero_hi[k] - zeroed), I.stream));
+            zeroed = P.zero_hi[k];
+        }
+        run_action_range(I, kp, I.d_y, I.stream, P.cb[k], P.cb[k + 1], false);
+        FG_CUDA(cudaEventRecord(I.ev_pipe[K + k], I.stream));
+        // D2H: the rows no later slab touches
+        FG_CUDA(cudaStreamWaitEvent(I.s_d2h, I.ev_pipe[K + k], 0));
+        if (P.fin[k] > sent) {
+            FG_CUDA(cudaMemcpyAsync(y_host + sent, I.d_y + sent, sizeof(double) * (P.fin[k] - sent),
+                                    cudaMemcpyDeviceToHost, I.s_d2h));
+            sent = P.fin[k];
+        }
+    }
+    FG_CUDA(cudaEventRecord(I.ev_pipe[2 * K], I.s_d2h));
+    FG_CUDA(cudaStreamWaitEvent(I.stream, I.ev_pipe[2 * K], 0));
+    I.last_launches = K;
+    return true;
+}
+
+}  // namespace femgpu
