@@ -29,6 +29,7 @@
 // instructions) or is staged once per CTA into shared memory.
 #include <cstdio>
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <set>
@@ -1093,7 +1094,9 @@ EmitResult emit_kernel(const Signature& sig, const KernelPlan& kp) {
     for (int i = 0; i < sig.ns(); ++i) fmas += static_cast<long long>(sig.sterms[i]) * sig.sdofs[i];
     for (int i = 0; i < sig.nv(); ++i) fmas += static_cast<long long>(sig.vterms[i]) * sig.vdofs[i];
     fmas += static_cast<long long>(sig.nW) * sig.Tw;
-    const bool unroll_q = fmas * sig.Q <= 6000;
+    // FEMGPU_DEBUG_UNROLL_Q=0/1 overrides the heuristic (I-cache experiments)
+    const char* uq = std::getenv("FEMGPU_DEBUG_UNROLL_Q");
+    const bool unroll_q = uq ? std::atoi(uq) != 0 : fmas * sig.Q <= 6000;
     if (kp.family == Family::Macro) {
         r.kernel = "femgpu_macro";
         r.kernel_checked = "femgpu_macro_checked";

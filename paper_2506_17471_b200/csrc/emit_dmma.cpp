@@ -240,7 +240,11 @@ void emit_dmma_kernel(std::ostringstream& o, const Signature& sig, const KernelP
     o << "  #pragma unroll 1\n";
     o << "  for (int task = blockIdx.x * " << NW << " + warp; task < n_tasks; task += gridDim.x * " << NW << ") {\n";
     o << "    const int c0 = P.cell0 + task * " << CW << ";\n";
-    // ---- geometry + cell-invariant nodes, one lane per cell
+    // ---- geometry + cell-invariant nodes, one lane per cell (emitted after the first m-group's
+    // gather has been issued, so its latency overlaps the geometry)
+    std::ostringstream geo;
+    {
+    std::ostringstream& o = geo;
     if (sig.affine || nH > 0) {
         o << "    if (lane < " << CW << ") {\n";
         o << "      const bool cok = c0 + lane < P.n_cells;\n";
@@ -259,6 +263,7 @@ void emit_dmma_kernel(std::ostringstream& o, const Signature& sig, const KernelP
         for (int h = 0; h < nH; ++h) o << "      sH[" << static_cast<long long>(h) * CW << " + lane] = n" << H.stored[h] << ";\n";
         o << "    }\n";
         o << "    __syncwarp();\n";
+    }
     }
     // ---- m-groups of MBJ m-blocks sharing every B-fragment load; optional software prefetch:
     // indices two m-groups ahead, values one m-group ahead (loop-carried registers).
@@ -351,16 +356,21 @@ void emit_dmma_kernel(std::ostringstream& o, const Signature& sig, const KernelP
             for (int ks = 0; ks < L.groups[tsp->gids[0]].KS; ++ks)
                 o << ind << ixname(dst, *tsp, ks, j) << " = " << ixname(src, *tsp, ks, j) << ";\n";
     };
+    if (PF) {
+        // stage chain: m-group 0 loads its own indices+values (before the geometry), later m-groups
+        // were prefetched one iteration ahead
+        emit_idx("    ", "ixN", "0", false);
+        emit_vals("    ", "ixN", "uN", false);
+        copy_tidx("    ", "ixK", "ixN");
+        if (NG > 1) emit_idx("    ", "ixN", "1", false);
+    } else {
+        emit_idx("    ", "ixP", "0", true);
+        emit_vals("    ", "ixP", "uP", true);
+    }
+    o << geo.str();
     o << "    #pragma unroll 1\n";
     o << "    for (int grp = 0; grp < " << NG << "; ++grp) {\n";
     if (PF) {
-        // stage chain: grp 0 loads its own indices+values, later m-groups were prefetched
-        o << "      if (grp == 0) {\n";
-        emit_idx("        ", "ixN", "0", false);
-        emit_vals("        ", "ixN", "uN", false);
-        copy_tidx("        ", "ixK", "ixN");
-        if (NG > 1) emit_idx("        ", "ixN", "1", false);
-        o << "      }\n";
         for (int j = 0; j < MBJ; ++j)
             for (const Sp& sp : sps)
                 for (int ks = 0; ks < L.groups[sp.gids[0]].KS; ++ks) {
@@ -381,8 +391,18 @@ void emit_dmma_kernel(std::ostringstream& o, const Signature& sig, const KernelP
             }
         }
     } else {
-        emit_idx("      ", "ix", "grp", true);
-        emit_vals("      ", "ix", "uA", true);
+        // m-group 0 was loaded before the geometry; later ones at the top of their iteration
+        for (int j = 0; j < MBJ; ++j)
+            for (const Sp& sp : sps)
+                for (int ks = 0; ks < L.groups[sp.gids[0]].KS; ++ks) {
+                    o << "      int " << ixname("ix", sp, ks, j) << " = " << ixname("ixP", sp, ks, j) << ";\n";
+                    for (int gid : sp.gids)
+                        o << "      double " << uname("uA", gid, ks, j) << " = " << uname("uP", gid, ks, j) << ";\n";
+                }
+        o << "      if (grp > 0) {\n";
+        emit_idx("        ", "ix", "grp", false);
+        emit_vals("        ", "ix", "uA", false);
+        o << "      }\n";
     }
     for (int j = 0; j < MBJ; ++j) {
         o << "      const int cr" << j << " = (grp * " << MBJ << " + " << j << ") * 8 + r, cell" << j << " = c0 + cr" << j << ";\n";
