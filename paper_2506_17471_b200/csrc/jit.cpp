@@ -10,6 +10,7 @@
 #include <fstream>
 #include <sstream>
 #include <sys/stat.h>
+#include <unistd.h>
 
 #include "femgpu_internal.hpp"
 
@@ -92,7 +93,8 @@ std::vector<char> jit_compile(const std::string& source, bool strict, std::strin
     nvrtcDestroyProgram(&prog);
     try {
         mkdirs(dir);
-        const std::string tmp = path + ".tmp" + std::to_string(reinterpret_cast<uintptr_t>(&bin));
+        // per-process temporary + rename: concurrent ranks compiling the same kernel never see a torn file
+        const std::string tmp = path + ".tmp" + std::to_string(static_cast<long long>(::getpid()));
         std::ofstream out(tmp, std::ios::binary);
         out.write(bin.data(), static_cast<std::streamsize>(bin.size()));
         out.close();

@@ -123,30 +123,35 @@ def form_map(form: str, sig: FormSignature) -> PointwiseMap:
             terms.append(m.mul(bc, m.scalar_deriv(0, c)))
         m.add_output(m.mul(w, m.sum(terms)))
     elif form == "hyperelastic":
+        # St. Venant-Kirchhoff tangent dP = dF S + F dS around F = I + grad(u0), written with the
+        # symmetry of C = F^T F and dE = (M + M^T)/2, M = dF^T F (the same form as the textbook
+        # E = (C - I)/2, S = 2 mu E + lam tr(E) I, dS = 2 mu dE + lam tr(dE) I, in ~30 % fewer map ops):
+        #   S = mu (C - I) + lam/2 (tr C - d) I,   dS = mu (M + M^T) + lam tr(M) I
         lam, mu = 1.25, 0.75
         wd = m.mul(m.weight(), m.determinant())
         dF = [[m.vector_deriv(0, a * d + c) for c in range(d)] for a in range(d)]          # grad(du)
         G0 = [[m.vector_deriv(1, a * d + c) for c in range(d)] for a in range(d)]          # grad(u0)
         F = [[m.add(m.constant(1.0), G0[a][c]) if a == c else G0[a][c] for c in range(d)] for a in range(d)]
-        half = m.constant(0.5)
-        # E = 1/2 (F^T F - I); dE = 1/2 (dF^T F + F^T dF)
-        FtF = [[m.sum([m.mul(F[k][a], F[k][c]) for k in range(d)]) for c in range(d)] for a in range(d)]
-        E = [[m.mul(half, m.add(FtF[a][c], m.constant(-1.0)) if a == c else FtF[a][c]) for c in range(d)]
-             for a in range(d)]
-        dE = [[m.mul(half, m.add(m.sum([m.mul(dF[k][a], F[k][c]) for k in range(d)]),
-                                 m.sum([m.mul(F[k][a], dF[k][c]) for k in range(d)]))) for c in range(d)]
-              for a in range(d)]
-        trE = m.sum([E[k][k] for k in range(d)])
-        trdE = m.sum([dE[k][k] for k in range(d)])
-        two_mu, lamc = m.constant(2.0 * mu), m.constant(lam)
-        S = [[m.add(m.mul(two_mu, E[a][c]), m.mul(lamc, trE)) if a == c else m.mul(two_mu, E[a][c])
-              for c in range(d)] for a in range(d)]
-        dS = [[m.add(m.mul(two_mu, dE[a][c]), m.mul(lamc, trdE)) if a == c else m.mul(two_mu, dE[a][c])
-               for c in range(d)] for a in range(d)]
+        C = {}
+        for a in range(d):
+            for c in range(a, d):
+                C[a, c] = C[c, a] = m.sum([m.mul(F[k][a], F[k][c]) for k in range(d)])
+        M = [[m.sum([m.mul(dF[k][a], F[k][c]) for k in range(d)]) for c in range(d)] for a in range(d)]
+        trC = m.sum([C[k, k] for k in range(d)])
+        trM = m.sum([M[k][k] for k in range(d)])
+        muc = m.constant(mu)
+        s0 = m.add(m.mul(m.constant(0.5 * lam), trC), m.constant(-mu - 0.5 * lam * d))
+        ltrM = m.mul(m.constant(lam), trM)
+        S, dS = {}, {}
+        for a in range(d):
+            for c in range(a, d):
+                S[a, c] = S[c, a] = m.add(m.mul(muc, C[a, c]), s0) if a == c else m.mul(muc, C[a, c])
+                dS[a, c] = dS[c, a] = (m.add(m.mul(m.constant(2.0 * mu), M[a][a]), ltrM) if a == c
+                                       else m.mul(muc, m.add(M[a][c], M[c][a])))
         for a in range(d):
             for c in range(d):
-                dP = m.add(m.sum([m.mul(dF[a][k], S[k][c]) for k in range(d)]),
-                           m.sum([m.mul(F[a][k], dS[k][c]) for k in range(d)]))
+                dP = m.add(m.sum([m.mul(dF[a][k], S[k, c]) for k in range(d)]),
+                           m.sum([m.mul(F[a][k], dS[k, c]) for k in range(d)]))
                 m.add_output(m.mul(wd, dP))
     else:
         raise ValueError("unknown form: " + form)
