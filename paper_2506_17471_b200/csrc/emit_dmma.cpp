@@ -363,9 +363,6 @@ void emit_dmma_kernel(std::ostringstream& o, const Signature& sig, const KernelP
         emit_vals("    ", "ixN", "uN", false);
         copy_tidx("    ", "ixK", "ixN");
         if (NG > 1) emit_idx("    ", "ixN", "1", false);
-    } else {
-        emit_idx("    ", "ixP", "0", true);
-        emit_vals("    ", "ixP", "uP", true);
     }
     o << geo.str();
     o << "    #pragma unroll 1\n";
@@ -391,18 +388,10 @@ void emit_dmma_kernel(std::ostringstream& o, const Signature& sig, const KernelP
             }
         }
     } else {
-        // m-group 0 was loaded before the geometry; later ones at the top of their iteration
-        for (int j = 0; j < MBJ; ++j)
-            for (const Sp& sp : sps)
-                for (int ks = 0; ks < L.groups[sp.gids[0]].KS; ++ks) {
-                    o << "      int " << ixname("ix", sp, ks, j) << " = " << ixname("ixP", sp, ks, j) << ";\n";
-                    for (int gid : sp.gids)
-                        o << "      double " << uname("uA", gid, ks, j) << " = " << uname("uP", gid, ks, j) << ";\n";
-                }
-        o << "      if (grp > 0) {\n";
-        emit_idx("        ", "ix", "grp", false);
-        emit_vals("        ", "ix", "uA", false);
-        o << "      }\n";
+        // (issuing m-group 0 before the geometry was measured neutral on C4 and 15 % slower on the
+        //  register-bound C5-hyp-P3/P4: the gathered values stay live across the geometry)
+        emit_idx("      ", "ix", "grp", true);
+        emit_vals("      ", "ix", "uA", true);
     }
     for (int j = 0; j < MBJ; ++j) {
         o << "      const int cr" << j << " = (grp * " << MBJ << " + " << j << ") * 8 + r, cell" << j << " = c0 + cr" << j << ";\n";
