@@ -216,10 +216,20 @@ void emit_cell_body(Out& o, const Signature& sig, const KernelPlan& kp, const Ma
                        std::to_string(j * kp.tile_cells) + " + threadIdx.x];");
             else
                 o.line("const int " + node + " = __ldg(&P.vm" + std::to_string(i) + "[" + idx + "]);");
+            // padded global layout: components (0,1) as one aligned 16-byte load (no initializer on the
+            // double2: the checked twin's goto may jump over it)
+            const bool pair = !(tile && kp.vgroup[i] >= 0) && d >= 2 && comps.count(0) && comps.count(1);
+            if (pair) {
+                const std::string pv = nm("wp", i, j);
+                o.line("double2 " + pv + "; " + pv + " = __ldg(reinterpret_cast<const double2*>(P.v" + std::to_string(i) +
+                       " + (size_t)" + node + "*" + std::to_string(vec_stride(d)) + "));");
+            }
             for (int c : comps) {
                 if (tile && kp.vgroup[i] >= 0)
                     o.line("const double " + nm("w", i, j, c) + " = vs" + std::to_string(i) + "[" + node + "*" +
                            std::to_string(d) + "+" + std::to_string(c) + "];");
+                else if (pair && c < 2)
+                    o.line("const double " + nm("w", i, j, c) + " = " + nm("wp", i, j) + (c == 0 ? ".x;" : ".y;"));
                 else
                     o.line("const double " + nm("w", i, j, c) + " = __ldg(&P.v" + std::to_string(i) + "[(size_t)" +
                            node + "*" + std::to_string(vec_stride(d)) + "+" + std::to_string(c) + "]);");
@@ -244,10 +254,16 @@ void emit_cell_body(Out& o, const Signature& sig, const KernelPlan& kp, const Ma
                        " + threadIdx.x];");
             else
                 o.line("const int " + vtx + " = __ldg(&P.cm[" + idx + "]);");
+            const bool xpair = !(tile && kp.cgroup >= 0) && d >= 2;
+            if (xpair)
+                o.line("double2 " + nm("Xp", j) + "; " + nm("Xp", j) + " = __ldg(reinterpret_cast<const double2*>(P.X + (size_t)" +
+                       vtx + "*" + std::to_string(vec_stride(d)) + "));");
             for (int c = 0; c < d; ++c) {
                 if (tile && kp.cgroup >= 0)
                     o.line("const double " + nm("X", j, c) + " = Xs[" + vtx + "*" + std::to_string(d) + "+" +
                            std::to_string(c) + "];");
+                else if (xpair && c < 2)
+                    o.line("const double " + nm("X", j, c) + " = " + nm("Xp", j) + (c == 0 ? ".x;" : ".y;"));
                 else
                     o.line("const double " + nm("X", j, c) + " = __ldg(&P.X[(size_t)" + vtx + "*" + std::to_string(vec_stride(d)) +
                            "+" + std::to_string(c) + "]);");
