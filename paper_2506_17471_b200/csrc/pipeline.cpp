@@ -37,8 +37,18 @@ const PipePlan& Instance::pipe_plan(int align) {
     if (pipe && pipe->align == align && static_cast<int>(pipe->cb.size()) == K + 1) return *pipe;
     auto P = std::make_unique<PipePlan>();
     P->align = align;
+    // slab sizes: equal by default; FEMGPU_PIPE_EDGE scales the first and last (fill / drain)
     const long long units = (static_cast<long long>(cells) + align - 1) / align;
-    for (int k = 0; k <= K; ++k) P->cb.push_back(static_cast<int>(std::min<long long>(cells, units * k / K * align)));
+    const char* edge_env = std::getenv("FEMGPU_PIPE_EDGE");
+    const double edge = edge_env ? std::atof(edge_env) : 1.0;  // measured: half-size edges do not help (PCIe-bound)
+    const double total_w = (K - 2) + 2 * edge;
+    double acc = 0.0;
+    P->cb.push_back(0);
+    for (int k = 0; k < K; ++k) {
+        acc += (k == 0 || k == K - 1) ? edge : 1.0;
+        const long long u = k == K - 1 ? units : static_cast<long long>(units * acc / total_w);
+        P->cb.push_back(static_cast<int>(std::min<long long>(cells, u * align)));
+    }
     const size_t ng = group_maps.size();
     std::vector<std::vector<long long>> lo(ng, std::vector<long long>(K)), hi(ng, std::vector<long long>(K));
     for (size_t g = 0; g < ng; ++g) {
