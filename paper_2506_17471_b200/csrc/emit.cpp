@@ -488,7 +488,8 @@ void emit_geometry(std::ostringstream& os, const Signature& sig, bool uses_inv, 
 std::string KernelPlan::key() const {
     std::ostringstream s;
     s << int(family) << "/" << basis << "/" << block << "/" << tile_cells << "/" << Nc << "x" << Nwi << "/" << TQ << "/"
-      << Ter << "/" << Tqr << "/" << Tqc << "/" << strict << "/" << min_blocks << "/G" << G << "/ms" << mstage << "/ys" << ysmem;
+      << Ter << "/" << Tqr << "/" << Tqc << "/" << strict << "/" << min_blocks << "/G" << G << "/ms" << mstage << "/ys" << ysmem
+      << "/qm" << qmajor;
     for (int t : Tcs) s << "s" << t;
     for (int t : Tcv) s << "v" << t;
     for (size_t g = 0; g < group_cap.size(); ++g) s << "g" << group_entries[g] << ":" << group_cap[g];
@@ -1082,6 +1083,217 @@ void emit_macro_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const
     o.line("}");
 }
 
+// Macro-elements, quadrature-point-major ("qmajor"): the G cells of a group are interleaved at
+// statement level inside each quadrature point, so every tabulation operand (LDCU from the
+// constant bank, or an LDS) is loaded once for the G cells instead of once per cell (the cell-major
+// macro kernel issues ~1 LDCU per 1.4 DFMA; sm_100a DFMA has no constant-bank operand form).  The
+// cell-invariant map nodes of each cell are parked in a thread-private shared-memory column
+// between the geometry pass and the quadrature loop, and the quadrature contributions go straight
+// into the group's y accumulators (one per unique test DOF; the sum order over (q, cell, k) is
+// reassociated, well inside the parity tolerance).  Non-finite values are detected on the
+// accumulators (plus the terms the map never reads and det); the stage-checked twin then names the
+// exact lowest cell and stage as usual.
+void emit_macro_qmajor_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const MapUse& use,
+                              const std::string& name, long long smem_tab_off, long long hsmem_off) {
+    const int D = sig.dim, G = kp.G, Q = sig.Q;
+    auto pat = [&](int g, int s, int j) { return kp.mpat[g][static_cast<size_t>(s) * kp.group_entries[g] + j]; };
+    auto TAB = [&](const std::string& idx) {
+        if (kp.basis == kBasisGlobal) return "__ldg(&P.tabg[" + idx + "])";
+        return kp.basis == FEMGPU_BASIS_CONST ? "P.tab[" + idx + "]" : "sT[" + idx + "]";
+    };
+    // cell-invariant nodes the quadrature part reads
+    std::vector<int> need;
+    {
+        std::set<int> nd;
+        for (size_t id = 0; id < sig.nodes.size(); ++id) {
+            if (!use.live[id] || !use.qdep[id]) continue;
+            const MapNode& n = sig.nodes[id];
+            if (n.op == FEMGPU_OP_ADD || n.op == FEMGPU_OP_MUL) {
+                if (!use.qdep[n.a]) nd.insert(n.a);
+                if (!use.qdep[n.b]) nd.insert(n.b);
+            }
+        }
+        for (int out : sig.outputs)
+            if (!use.qdep[out]) nd.insert(out);
+        need.assign(nd.begin(), nd.end());
+    }
+    std::vector<int> stored;
+    for (int id : need)
+        if (sig.nodes[id].op != FEMGPU_OP_CONSTANT) stored.push_back(id);
+    const int NH = static_cast<int>(stored.size());
+    o.line("");
+    o.line("extern \"C\" __global__ void __launch_bounds__(" + S(kp.block) + (kp.min_blocks > 1 ? ", " + S(kp.min_blocks) : "") +
+           ") " + name + "(const __grid_constant__ Params P) {");
+    o.ind++;
+    o.line("constexpr bool CHECKED = false;");
+    o.line("extern __shared__ __align__(16) unsigned char smraw[];");
+    if (kp.basis == FEMGPU_BASIS_SMEM) {
+        o.line("double* sT = reinterpret_cast<double*>(smraw + " + S(smem_tab_off) + ");");
+        o.line("for (int i = threadIdx.x; i < " + S(sig.tab_size) + "; i += blockDim.x) sT[i] = P.tabg[i];");
+        o.line("__syncthreads();");
+    }
+    o.line("double* const sh_base = reinterpret_cast<double*>(smraw + " + S(hsmem_off) + ") + threadIdx.x; (void)sh_base;");
+    o.line("#define SH(k) sh_base[(k) * " + S(kp.block) + "]");
+    o.line("const int grp = P.cell0 / " + S(G) + " + blockIdx.x * " + S(kp.block) + " + threadIdx.x;");
+    o.line("if (grp >= P.n_cells / " + S(G) + ") return;");
+    o.line("const size_t NG = (size_t)P.n_groups;");
+    std::set<int> gathered;
+    for (int i = 0; i < sig.ns(); ++i) gathered.insert(kp.sgroup[i]);
+    for (int i = 0; i < sig.nv(); ++i) gathered.insert(kp.vgroup[i]);
+    if (sig.affine) gathered.insert(kp.cgroup);
+    // ---- gathers: every unique node of the group once (16-byte loads of padded vector nodes)
+    for (int g : gathered)
+        for (int u = 0; u < kp.group_cap[g]; ++u) {
+            o.line("const int ig" + S(g) + "_" + S(u) + " = __ldg(&P.gidx" + S(g) + "[" + S(u) + " * NG + grp]);");
+            for (int i = 0; i < sig.ns(); ++i)
+                if (kp.sgroup[i] == g)
+                    o.line("const double xg" + S(i) + "_" + S(u) + " = __ldg(&P.x" + S(i) + "[ig" + S(g) + "_" + S(u) + "]);");
+            auto node_loads = [&](const std::string& dst, const std::string& arr, const std::set<int>& comps) {
+                const std::string base = arr + " + (size_t)ig" + S(g) + "_" + S(u) + " * " + S(vec_stride(D));
+                const bool pair = D >= 2 && comps.count(0) && comps.count(1);
+                if (pair) {
+                    o.line("const double2 " + dst + "_01 = __ldg(reinterpret_cast<const double2*>(" + base + "));");
+                    o.line("const double " + dst + "_0 = " + dst + "_01.x, " + dst + "_1 = " + dst + "_01.y;");
+                }
+                for (int c : comps)
+                    if (!pair || c >= 2) o.line("const double " + dst + "_" + S(c) + " = __ldg(" + base + " + " + S(c) + ");");
+            };
+            for (int i = 0; i < sig.nv(); ++i)
+                if (kp.vgroup[i] == g) node_loads("vg" + S(i) + "_" + S(u), "P.v" + S(i), std::set<int>(sig.vcomps[i].begin(), sig.vcomps[i].end()));
+            if (sig.affine && kp.cgroup == g) {
+                std::set<int> comps;
+                for (int c = 0; c < D; ++c) comps.insert(c);
+                node_loads("Xg" + S(u), "P.X", comps);
+            }
+        }
+    o.line("bool nf = false;");
+    // ---- per cell: geometry + cell-invariant nodes -> thread-private smem column
+    for (int sc = 0; sc < G; ++sc) {
+        o.line("{ // geometry of cell " + S(sc));
+        o.ind++;
+        if (sig.affine) {
+            for (int j = 0; j < sig.coord_dofs; ++j)
+                for (int c = 0; c < D; ++c)
+                    o.line("const double " + nm("X", j, c) + " = " + nm("Xg", pat(kp.cgroup, sc, j), c) + ";");
+            for (int c = 0; c < D; ++c)
+                for (int r = 0; r < D; ++r)
+                    o.line("const double " + nm("J", r, c) + " = " + nm("X", c + 1, r) + " - " + nm("X", 0, r) + ";");
+            if (D == 1) o.line("const double det = J0_0;");
+            if (D == 2) o.line("const double det = J0_0 * J1_1 - J0_1 * J1_0;");
+            if (D == 3)
+                o.line("const double det = J0_0 * (J1_1 * J2_2 - J1_2 * J2_1) - J0_1 * (J1_0 * J2_2 - J1_2 * J2_0) + "
+                       "J0_2 * (J1_0 * J2_1 - J1_1 * J2_0);");
+            if (use.uses_inv) {
+                std::ostringstream gi;
+                if (D == 1) gi << "const double Ji0_0 = 1.0 / det;";
+                if (D == 2) gi << "const double Ji0_0 = J1_1 / det, Ji0_1 = -J0_1 / det, Ji1_0 = -J1_0 / det, Ji1_1 = J0_0 / det;";
+                if (D == 3)
+                    gi << "const double Ji0_0 = (J1_1*J2_2 - J1_2*J2_1) / det, Ji0_1 = (J0_2*J2_1 - J0_1*J2_2) / det, "
+                          "Ji0_2 = (J0_1*J1_2 - J0_2*J1_1) / det, Ji1_0 = (J1_2*J2_0 - J1_0*J2_2) / det, "
+                          "Ji1_1 = (J0_0*J2_2 - J0_2*J2_0) / det, Ji1_2 = (J0_2*J1_0 - J0_0*J1_2) / det, "
+                          "Ji2_0 = (J1_0*J2_1 - J1_1*J2_0) / det, Ji2_1 = (J0_1*J2_0 - J0_0*J2_1) / det, "
+                          "Ji2_2 = (J0_0*J1_1 - J0_1*J1_0) / det;";
+                o.line(gi.str());
+            }
+            o.line("nf = nf | NF(det);");
+        }
+        emit_nodes(o, sig, use, false, "0", TAB);
+        for (int h = 0; h < NH; ++h) o.line("SH(" + S(sc * NH + h) + ") = n" + S(stored[h]) + ";");
+        o.ind--;
+        o.line("}");
+    }
+    {
+        std::string l = "double";
+        for (int u = 0; u < kp.group_cap[kp.tgroup]; ++u) l += std::string(u ? "," : "") + " ya" + S(u) + " = 0.0";
+        o.line(l + ";");
+    }
+    // ---- quadrature points: statements interleaved over the G cells
+    for (int q = 0; q < Q; ++q) {
+        o.line("{ // quadrature point " + S(q));
+        o.ind++;
+        // evaluation
+        for (int i = 0; i < sig.ns(); ++i)
+            for (int t = 0; t < sig.sterms[i]; ++t) {
+                const long long base = sig.phi_off_s[i] + static_cast<long long>(t) * Q * sig.sdofs[i] + static_cast<long long>(q) * sig.sdofs[i];
+                for (int sc = 0; sc < G; ++sc) o.line("double " + nm("s", i, t) + "_c" + S(sc) + ";");
+                for (int j = 0; j < sig.sdofs[i]; ++j) {
+                    std::string l = "{ const double tb = " + TAB(S(base + j)) + ";";
+                    for (int sc = 0; sc < G; ++sc) {
+                        const std::string v = nm("s", i, t) + "_c" + S(sc), u = nm("xg", i, pat(kp.sgroup[i], sc, j));
+                        l += j == 0 ? " " + v + " = tb * " + u + ";" : " " + v + " = FMA(tb, " + u + ", " + v + ");";
+                    }
+                    o.line(l + " }");
+                }
+            }
+        for (int i = 0; i < sig.nv(); ++i)
+            for (int t = 0; t < sig.vterms[i]; ++t) {
+                const long long base = sig.phi_off_v[i] + static_cast<long long>(t) * Q * sig.vdofs[i] + static_cast<long long>(q) * sig.vdofs[i];
+                const int comp = sig.vcomps[i][t];
+                for (int sc = 0; sc < G; ++sc) o.line("double " + nm("t", i, t) + "_c" + S(sc) + ";");
+                for (int j = 0; j < sig.vdofs[i]; ++j) {
+                    std::string l = "{ const double tb = " + TAB(S(base + j)) + ";";
+                    for (int sc = 0; sc < G; ++sc) {
+                        const std::string v = nm("t", i, t) + "_c" + S(sc), w = nm("vg", i, pat(kp.vgroup[i], sc, j), comp);
+                        l += j == 0 ? " " + v + " = tb * " + w + ";" : " " + v + " = FMA(tb, " + w + ", " + v + ");";
+                    }
+                    o.line(l + " }");
+                }
+            }
+        // map per cell
+        for (int sc = 0; sc < G; ++sc) {
+            for (int k = 0; k < sig.Tw; ++k) o.line("double e" + S(k) + "_c" + S(sc) + ";");
+            o.line("{");
+            o.ind++;
+            std::string unused;
+            for (int i = 0; i < sig.ns(); ++i)
+                for (int t = 0; t < sig.sterms[i]; ++t) {
+                    o.line("const double " + nm("s", i, t) + " = " + nm("s", i, t) + "_c" + S(sc) + ";");
+                    if (!use.sd_used.count({i, t})) unused += " | NF(" + nm("s", i, t) + ")";
+                }
+            for (int i = 0; i < sig.nv(); ++i)
+                for (int t = 0; t < sig.vterms[i]; ++t) {
+                    o.line("const double " + nm("t", i, t) + " = " + nm("t", i, t) + "_c" + S(sc) + ";");
+                    if (!use.vd_used.count({i, t})) unused += " | NF(" + nm("t", i, t) + ")";
+                }
+            if (!unused.empty()) o.line("nf = nf" + unused + ";");
+            for (int h = 0; h < NH; ++h) o.line("const double n" + S(stored[h]) + " = SH(" + S(sc * NH + h) + ");");
+            for (int id : need)
+                if (sig.nodes[id].op == FEMGPU_OP_CONSTANT) o.line("const double n" + S(id) + " = " + lit(sig.nodes[id].value) + ";");
+            emit_nodes(o, sig, use, true, S(q), TAB);
+            for (int k = 0; k < sig.Tw; ++k) o.line("e" + S(k) + "_c" + S(sc) + " = n" + S(sig.outputs[k]) + ";");
+            o.ind--;
+            o.line("}");
+        }
+        // quadrature straight into the group's y accumulators, one Psi load for the G cells
+        for (int jw = 0; jw < sig.nW; ++jw)
+            for (int k = 0; k < sig.Tw; ++k) {
+                const long long idx = sig.psi_off + (static_cast<long long>(k) * sig.nW + jw) * Q + q;
+                std::string l = "{ const double tb = " + TAB(S(idx)) + ";";
+                for (int sc = 0; sc < G; ++sc) {
+                    const std::string ya = "ya" + S(pat(kp.tgroup, sc, jw));
+                    l += " " + ya + " = FMA(tb, e" + S(k) + "_c" + S(sc) + ", " + ya + ");";
+                }
+                o.line(l + " }");
+            }
+        o.ind--;
+        o.line("}");
+    }
+    // ---- finiteness (any non-finite contribution reaches an accumulator) + scatter
+    {
+        std::string chk;
+        for (int u = 0; u < kp.group_cap[kp.tgroup]; ++u) chk += " | NF(ya" + S(u) + ")";
+        o.line("if (nf" + chk + ") atomicMin(P.bad, (unsigned long long)grp * " + S(G) + ");");
+    }
+    const int gt = kp.tgroup;
+    for (int u = 0; u < kp.group_cap[gt]; ++u) {
+        const std::string idx = gathered.count(gt) ? "ig" + S(gt) + "_" + S(u) : "__ldg(&P.gidx" + S(gt) + "[" + S(u) + " * NG + grp])";
+        o.line("atomicAdd(&P.y[" + idx + "], ya" + S(u) + ");");
+    }
+    o.line("(void)CHECKED;");
+    o.ind--;
+    o.line("}");
+}
+
 const char* kAsync = R"(
 __device__ __forceinline__ void cp16(unsigned char* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src) : "memory");
@@ -1127,7 +1339,26 @@ EmitResult emit_kernel(const Signature& sig, const KernelPlan& kp) {
         }
         const long long ysmem_off = static_cast<long long>(r.smem_bytes);
         if (kp.ysmem) r.smem_bytes += static_cast<size_t>(kp.group_cap[kp.tgroup]) * 8 * kp.block;
-        emit_macro_kernel(o, sig, kp, use, unroll_q, r.kernel, 0, ysmem_off);
+        if (kp.qmajor) {
+            // thread-private columns of the cell-invariant map nodes of the G cells
+            long long nh = 0;
+            for (size_t id = 0; id < sig.nodes.size(); ++id) {
+                if (!use.live[id] || use.qdep[id] || sig.nodes[id].op == FEMGPU_OP_CONSTANT) continue;
+                bool read = false;
+                for (size_t k = 0; k < sig.nodes.size() && !read; ++k) {
+                    const MapNode& n = sig.nodes[k];
+                    read = use.live[k] && use.qdep[k] && (n.op == FEMGPU_OP_ADD || n.op == FEMGPU_OP_MUL) &&
+                           (n.a == static_cast<int>(id) || n.b == static_cast<int>(id));
+                }
+                for (int out : sig.outputs) read = read || out == static_cast<int>(id);
+                if (read) ++nh;
+            }
+            const long long hoff = static_cast<long long>(al16(static_cast<long long>(r.smem_bytes)));
+            r.smem_bytes = static_cast<size_t>(hoff + nh * kp.G * 8 * kp.block);
+            emit_macro_qmajor_kernel(o, sig, kp, use, r.kernel, 0, hoff);
+        } else {
+            emit_macro_kernel(o, sig, kp, use, unroll_q, r.kernel, 0, ysmem_off);
+        }
         emit_scpt_kernel(o, sig, kp, use, unroll_q, true, r.kernel_checked, 0);
     } else if (tile) {
         o << kAsync;

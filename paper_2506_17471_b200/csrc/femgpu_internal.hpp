@@ -93,6 +93,7 @@ struct KernelPlan {
     int G = 0;
     int mstage = 0;                       // 0: gathered values in registers; 1: cp.async into smem
     bool ysmem = false;                   // macro: y accumulators in thread-private smem columns (registers)
+    bool qmajor = false;                  // macro: quadrature-point-major, statements interleaved over the G cells
     std::vector<std::vector<int>> mpat;   // per map group: G*entries local indices
     std::string key() const;
 };

@@ -606,6 +606,7 @@ void host_macro_plan(const femgpu_problem* p, const Signature& sig, KernelPlan& 
     kp.G = G;
     kp.mstage = s->reserved[3] == 1 ? 1 : 0;
     kp.ysmem = s->reserved[3] == 2;
+    kp.qmajor = s->reserved[3] == 3;
     kp.block = s->block_cells > 0 ? s->block_cells : 64;
     const int reg_target = s->reserved[1] > 0 ? s->reserved[1] : 168;
     kp.min_blocks = std::max(1, std::min(16, 65536 / (kp.block * reg_target)));
@@ -733,6 +734,7 @@ KernelPlan resolve_schedule(Instance& I, const femgpu_schedule* s) {
             kp.G = G;
             kp.mstage = s->reserved[3] == 1 ? 1 : 0;
             kp.ysmem = s->reserved[3] == 2;
+            kp.qmajor = s->reserved[3] == 3;
             kp.block = s->block_cells > 0 ? s->block_cells : 64;
             const int reg_target = s->reserved[1] > 0 ? s->reserved[1] : 168;
             kp.min_blocks = std::max(1, std::min(16, 65536 / (kp.block * reg_target)));

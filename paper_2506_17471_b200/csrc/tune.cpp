@@ -97,7 +97,9 @@ bool tune_cache_enabled() {
 std::string describe_plan(const KernelPlan& kp) {
     std::ostringstream s;
     switch (kp.family) {
-        case Family::Macro: s << "femgpu_macro G=" << kp.G << " block=" << kp.block; break;
+        case Family::Macro:
+            s << "femgpu_macro G=" << kp.G << " block=" << kp.block << (kp.qmajor ? " q-major" : "") << (kp.ysmem ? " y-smem" : "");
+            break;
         case Family::Scpt:
             s << "femgpu_scpt cells/thread=" << std::max(1, kp.G) << " block=" << kp.block << " minCTAs=" << kp.min_blocks;
             break;
@@ -159,6 +161,9 @@ void autotune(Instance& I) {
             femgpu_schedule s = dfma_default();
             s.scatter = FEMGPU_SCATTER_MACRO;
             s.block_cells = 32;
+            cands.push_back(s);
+            s.reserved[3] = 3;  // quadrature-point-major: one tabulation load for the group's cells
+            s.reserved[1] = 232;
             cands.push_back(s);
         }
         for (int mb : {3, 5}) {  // SCPT with a register cap (more resident warps to hide the gathers)

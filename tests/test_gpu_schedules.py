@@ -171,3 +171,24 @@ def test_macro_y_accumulators_in_smem(oracle, form, dim, deg, Q, n):
     with fg.GpuInstance(p) as g:
         close(g.action(fg.TilingParams.scpt(scatter=abi.SCATTER_MACRO, stage_smem=2)), ref)
         close(g.action(fg.TilingParams.scpt(scatter=abi.SCATTER_MACRO, stage_smem=2, block_cells=128)), ref)
+
+
+@pytest.mark.parametrize("form,dim,deg,Q,n", [("laplace", 3, 2, 4, 3), ("mass", 2, 1, 3, 9), ("advection", 3, 1, 4, 3),
+                                              ("helmholtz_coef", 2, 2, 6, 6)])
+def test_macro_quadrature_major(oracle, form, dim, deg, Q, n):
+    """Macro family, quadrature-point-major (stage_smem=3): statements interleaved over the group's
+    cells so every tabulation load serves all of them."""
+    p = fg.mesh_problem(form, dim, deg, Q, n)
+    ref = oracle.reference_action(p)
+    with fg.GpuInstance(p) as g:
+        close(g.action(fg.TilingParams.scpt(scatter=abi.SCATTER_MACRO, stage_smem=3)), ref)
+        close(g.action(fg.TilingParams.scpt(scatter=abi.SCATTER_MACRO, stage_smem=3, block_cells=32, reg_target=232)), ref)
+
+
+def test_macro_quadrature_major_nonfinite():
+    p = fg.mesh_problem("laplace", 3, 2, 4, 3)
+    m = p.connectivity.scalar_maps[0].indices
+    p.scalar_inputs[0][m[40, 3]] = np.inf
+    first = int(np.nonzero(np.any(m == m[40, 3], axis=1))[0].min())
+    with pytest.raises(RuntimeError, match="non-finite value at cell %d during" % first):
+        fg.gpu_action(p, fg.TilingParams.scpt(scatter=abi.SCATTER_MACRO, stage_smem=3))

@@ -22,6 +22,8 @@ def sched(name):
             kw["stage_smem"] = 1
         elif p == "ys":
             kw["stage_smem"] = 2
+        elif p == "qm":
+            kw["stage_smem"] = 3
         elif p == "smem":
             kw["basis"] = abi.BASIS_SMEM
         elif p == "const":
