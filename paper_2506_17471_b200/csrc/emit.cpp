@@ -489,7 +489,7 @@ std::string KernelPlan::key() const {
     std::ostringstream s;
     s << int(family) << "/" << basis << "/" << block << "/" << tile_cells << "/" << Nc << "x" << Nwi << "/" << TQ << "/"
       << Ter << "/" << Tqr << "/" << Tqc << "/" << strict << "/" << min_blocks << "/G" << G << "/ms" << mstage << "/ys" << ysmem
-      << "/qm" << qmajor;
+      << "/qm" << qmajor << "/ql" << qloop;
     for (int t : Tcs) s << "s" << t;
     for (int t : Tcv) s << "v" << t;
     for (size_t g = 0; g < group_cap.size(); ++g) s << "g" << group_entries[g] << ":" << group_cap[g];
@@ -1324,7 +1324,7 @@ EmitResult emit_kernel(const Signature& sig, const KernelPlan& kp) {
     fmas += static_cast<long long>(sig.nW) * sig.Tw;
     // FEMGPU_DEBUG_UNROLL_Q=0/1 overrides the heuristic (I-cache experiments)
     const char* uq = std::getenv("FEMGPU_DEBUG_UNROLL_Q");
-    const bool unroll_q = uq ? std::atoi(uq) != 0 : fmas * sig.Q <= 6000;
+    const bool unroll_q = uq ? std::atoi(uq) != 0 : (!kp.qloop && fmas * sig.Q <= 6000);
     if (kp.family == Family::Macro) {
         r.kernel = "femgpu_macro";
         r.kernel_checked = "femgpu_macro_checked";

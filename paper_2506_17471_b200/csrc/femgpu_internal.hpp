@@ -94,6 +94,7 @@ struct KernelPlan {
     int mstage = 0;                       // 0: gathered values in registers; 1: cp.async into smem
     bool ysmem = false;                   // macro: y accumulators in thread-private smem columns (registers)
     bool qmajor = false;                  // macro: quadrature-point-major, statements interleaved over the G cells
+    bool qloop = false;                   // scpt: keep the quadrature loop rolled (I-cache / registers)
     std::vector<std::vector<int>> mpat;   // per map group: G*entries local indices
     std::string key() const;
 };

@@ -801,6 +801,7 @@ KernelPlan resolve_schedule(Instance& I, const femgpu_schedule* s) {
     // SCPT with G independent cells per thread (group_cells with atomic scatter): shared
     // tabulation loads, more independent DFMA chains per thread
     kp.G = scatter == FEMGPU_SCATTER_ATOMIC && s->group_cells > 1 ? s->group_cells : 1;
+    kp.qloop = s->reserved[3] == 4;
     if (kp.G > 8) fail(FEMGPU_E_INFEASIBLE, "schedule: at most 8 cells per thread in the SCPT family");
     if (s->reserved[2] > 0) kp.min_blocks = s->reserved[2];
     (void)int_dim;

@@ -101,7 +101,8 @@ std::string describe_plan(const KernelPlan& kp) {
             s << "femgpu_macro G=" << kp.G << " block=" << kp.block << (kp.qmajor ? " q-major" : "") << (kp.ysmem ? " y-smem" : "");
             break;
         case Family::Scpt:
-            s << "femgpu_scpt cells/thread=" << std::max(1, kp.G) << " block=" << kp.block << " minCTAs=" << kp.min_blocks;
+            s << "femgpu_scpt cells/thread=" << std::max(1, kp.G) << " block=" << kp.block << " minCTAs=" << kp.min_blocks
+              << (kp.qloop ? " q-loop" : "");
             break;
         case Family::Tile: s << "femgpu_tile cells=" << kp.tile_cells; break;
         case Family::Mlt: s << "femgpu_mlt Nc=" << kp.Nc << " Nwi=" << kp.Nwi << " TQ=" << kp.TQ; break;
@@ -177,6 +178,8 @@ void autotune(Instance& I) {
             femgpu_schedule s = dfma_default();
             s.scatter = FEMGPU_SCATTER_ATOMIC;
             s.group_cells = G;
+            cands.push_back(s);
+            s.reserved[3] = 4;  // quadrature loop kept rolled (measured 7 % faster on C3a)
             cands.push_back(s);
         }
     }

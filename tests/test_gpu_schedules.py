@@ -192,3 +192,12 @@ def test_macro_quadrature_major_nonfinite():
     first = int(np.nonzero(np.any(m == m[40, 3], axis=1))[0].min())
     with pytest.raises(RuntimeError, match="non-finite value at cell %d during" % first):
         fg.gpu_action(p, fg.TilingParams.scpt(scatter=abi.SCATTER_MACRO, stage_smem=3))
+
+
+@pytest.mark.parametrize("form,dim,deg,Q,n", [("helmholtz_coef", 2, 3, 12, 6), ("advection", 3, 2, 14, 2)])
+def test_scpt_rolled_quadrature_loop(oracle, form, dim, deg, Q, n):
+    p = fg.mesh_problem(form, dim, deg, Q, n)
+    ref = oracle.reference_action(p)
+    with fg.GpuInstance(p) as g:
+        for G in (1, 2):
+            close(g.action(fg.TilingParams.scpt(scatter=abi.SCATTER_ATOMIC, group_cells=G, stage_smem=4)), ref)

@@ -24,6 +24,8 @@ def sched(name):
             kw["stage_smem"] = 2
         elif p == "qm":
             kw["stage_smem"] = 3
+        elif p == "ql":
+            kw["stage_smem"] = 4
         elif p == "smem":
             kw["basis"] = abi.BASIS_SMEM
         elif p == "const":
