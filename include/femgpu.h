@@ -138,8 +138,11 @@ typedef enum femgpu_scatter {
     FEMGPU_SCATTER_AUTO = 0,
     FEMGPU_SCATTER_ATOMIC = 1, /* red.global.add.f64 per (cell, test DOF) */
     FEMGPU_SCATTER_TILE = 2,   /* CTA-tile aggregation in smem; global atomics only on shared DOFs */
-    FEMGPU_SCATTER_MACRO = 3   /* macro-elements: G cells per thread with a common local pattern,
+    FEMGPU_SCATTER_MACRO = 3,  /* macro-elements: G cells per thread with a common local pattern,
                                   register accumulation, one atomic per unique DOF of the group */
+    FEMGPU_SCATTER_COLOR = 4   /* greedy cell colouring of the test map (femgpu_color_cells): one launch
+                                  per colour, plain read-modify-write of y (no two cells of a colour
+                                  share a DOF), so y is bitwise reproducible run to run */
 } femgpu_scatter;
 
 #define FEMGPU_MAX_SPACES 8

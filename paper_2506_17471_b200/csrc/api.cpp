@@ -128,6 +128,7 @@ femgpu_status femgpu_emit_source(const femgpu_problem* p, const femgpu_schedule*
             if (s && s->scatter == FEMGPU_SCATTER_MACRO) femgpu::host_macro_plan(p, sig, kp, s);
             if (s && s->scatter == FEMGPU_SCATTER_ATOMIC && s->group_cells > 1) kp.G = s->group_cells;
             if (s && s->reserved[3] == 4) kp.qloop = true;
+            if (s && s->scatter == FEMGPU_SCATTER_COLOR) kp.colour = true;
         }
         kp.strict = s && s->reserved[0];
         femgpu::EmitResult em = femgpu::emit_kernel(sig, kp);

@@ -149,6 +149,7 @@ void emit_params(Out& o, const Signature& sig, const KernelPlan& kp, long long n
     o.line("  const int* tm; const int* cm; const double* X;");
     o.line("  double* y; unsigned long long* bad; const double* tabg;");
     if (kp.family == Family::Dmma) o.line("  const double* afr;");
+    if (kp.colour) o.line("  const int* perm;");
     if (kp.family == Family::Macro)
         for (size_t g = 0; g < kp.group_entries.size(); ++g) o.line("  const int* gidx" + std::to_string(g) + ";");
     const int ngroups = kp.family == Family::Tile ? static_cast<int>(kp.group_entries.size()) : 0;
@@ -402,6 +403,8 @@ void emit_cell_body(Out& o, const Signature& sig, const KernelPlan& kp, const Ma
             o.line(nm("ya", pat(kp.tgroup, jw)) + " += o" + std::to_string(jw) + ";");
         else if (tile)
             o.line("st[" + std::to_string(jw * kp.tile_cells) + " + threadIdx.x] = o" + std::to_string(jw) + ";");
+        else if (kp.colour)  // no other cell of this launch (colour) touches the DOF
+            o.line("P.y[__ldg(&P.tm[" + idx + "])] += o" + std::to_string(jw) + ";");
         else
             o.line("atomicAdd(&P.y[__ldg(&P.tm[" + idx + "])], o" + std::to_string(jw) + ");");
     }
@@ -489,7 +492,7 @@ std::string KernelPlan::key() const {
     std::ostringstream s;
     s << int(family) << "/" << basis << "/" << block << "/" << tile_cells << "/" << Nc << "x" << Nwi << "/" << TQ << "/"
       << Ter << "/" << Tqr << "/" << Tqc << "/" << strict << "/" << min_blocks << "/G" << G << "/ms" << mstage << "/ys" << ysmem
-      << "/qm" << qmajor << "/ql" << qloop;
+      << "/qm" << qmajor << "/ql" << qloop << "/col" << colour;
     for (int t : Tcs) s << "s" << t;
     for (int t : Tcv) s << "v" << t;
     for (size_t g = 0; g < group_cap.size(); ++g) s << "g" << group_entries[g] << ":" << group_cap[g];
@@ -526,10 +529,19 @@ void emit_scpt_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const 
         o.line("for (int i = threadIdx.x; i < " + S(sig.tab_size) + "; i += blockDim.x) sT[i] = P.tabg[i];");
         o.line("__syncthreads();");
     }
-    o.line("const int cell = P.cell0 + blockIdx.x * blockDim.x + threadIdx.x;");
-    o.line("int stage = -1; (void)stage;");
-    o.line("if (cell < P.n_cells) {");
-    o.ind++;
+    if (kp.colour && !checked) {
+        // colour launch: positions [cell0, n_cells) of the colour-sorted permutation
+        o.line("const int ci = P.cell0 + blockIdx.x * blockDim.x + threadIdx.x;");
+        o.line("const int cell = ci < P.n_cells ? __ldg(&P.perm[ci]) : 0;");
+        o.line("int stage = -1; (void)stage;");
+        o.line("if (ci < P.n_cells) {");
+        o.ind++;
+    } else {
+        o.line("const int cell = P.cell0 + blockIdx.x * blockDim.x + threadIdx.x;");
+        o.line("int stage = -1; (void)stage;");
+        o.line("if (cell < P.n_cells) {");
+        o.ind++;
+    }
     emit_cell_body(o, sig, p, use, false, unroll_q);
     o.ind--;
     o.line("}");

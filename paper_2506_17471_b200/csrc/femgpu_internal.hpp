@@ -95,6 +95,7 @@ struct KernelPlan {
     bool ysmem = false;                   // macro: y accumulators in thread-private smem columns (registers)
     bool qmajor = false;                  // macro: quadrature-point-major, statements interleaved over the G cells
     bool qloop = false;                   // scpt: keep the quadrature loop rolled (I-cache / registers)
+    bool colour = false;                  // scpt: one launch per cell colour, plain y updates (deterministic)
     std::vector<std::vector<int>> mpat;   // per map group: G*entries local indices
     std::string key() const;
 };
@@ -175,6 +176,13 @@ struct MacroLayout {
     std::vector<int32_t*> d_gidx;            // per map group: [unique][n_groups] global indices
 };
 
+// Greedy colouring of the test map (femgpu_color_cells) with the cells sorted by colour.
+struct Colouring {
+    int n = 0;
+    std::vector<int> off;        // colour c = perm[off[c] .. off[c+1])
+    int32_t* d_perm = nullptr;   // cells ordered by (colour, cell)
+};
+
 struct DeviceSpace {
     int dofs = 0, terms = 0, global = 0;
     double* d_x = nullptr;          // input vector (vector spaces: padded [node][vec_stride])
@@ -227,6 +235,8 @@ struct Instance {
     std::mutex mu;                  // serialises actions on this instance (tune(jobs>1))
     // automatic schedule (s == NULL): chosen once per instance by tune.cpp
     std::unique_ptr<PipePlan> pipe;
+    std::unique_ptr<Colouring> colouring;
+    const Colouring& colour_plan();
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
     std::vector<cudaEvent_t> ev_pipe;
     const PipePlan& pipe_plan(int align);

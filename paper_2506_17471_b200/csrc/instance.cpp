@@ -755,6 +755,16 @@ KernelPlan resolve_schedule(Instance& I, const femgpu_schedule* s) {
         if (s->scatter == FEMGPU_SCATTER_MACRO)
             fail(FEMGPU_E_INFEASIBLE, "schedule: no macro-element pattern (cells per group) fits this instance");
     }
+    if (s->scatter == FEMGPU_SCATTER_COLOR) {
+        kp.family = Family::Scpt;
+        kp.colour = true;
+        kp.block = s->block_cells > 0 ? s->block_cells : 128;
+        if (kp.block > 1024) fail(FEMGPU_E_INFEASIBLE, "schedule: more than 1024 cells per CTA");
+        if (basis == FEMGPU_BASIS_SMEM && tab_bytes > 227 * 1024)
+            fail(FEMGPU_E_INFEASIBLE, "basis: tabulations exceed the shared-memory capacity of one CTA");
+        if (s->reserved[2] > 0) kp.min_blocks = s->reserved[2];
+        return kp;
+    }
     const int scatter = s->scatter == FEMGPU_SCATTER_AUTO ? FEMGPU_SCATTER_ATOMIC : s->scatter;
     int block = s->block_cells > 0 ? s->block_cells : (scatter == FEMGPU_SCATTER_TILE ? (sig.dim == 3 ? 384 : 256) : 128);
     if (block > 1024) fail(FEMGPU_E_INFEASIBLE, "schedule: more than 1024 cells per CTA");
@@ -843,6 +853,7 @@ ParamBuf build_params(Instance& I, const KernelPlan& kp, double* d_y, const Tile
     P.put(static_cast<void*>(I.d_bad));
     P.put(static_cast<const void*>(I.d_tab));
     if (kp.family == Family::Dmma) P.put(static_cast<const void*>(I.dmma_fragments_for(kp)));
+    if (kp.colour) P.put(static_cast<const void*>(I.colour_plan().d_perm));
     const int ngroups = kp.family == Family::Tile ? static_cast<int>(kp.group_entries.size()) : 0;
     const MacroLayout* M = kp.family == Family::Macro ? &I.macro_layout(kp.G) : nullptr;
     if (M)
@@ -880,10 +891,40 @@ std::shared_ptr<Module> Instance::module_for(const KernelPlan& kp) {
 }
 
 bool supports_cell_range(const KernelPlan& kp) {
-    return kp.family == Family::Scpt || kp.family == Family::Macro || kp.family == Family::Dmma;
+    return !kp.colour && (kp.family == Family::Scpt || kp.family == Family::Macro || kp.family == Family::Dmma);
+}
+
+const Colouring& Instance::colour_plan() {
+    if (colouring) return *colouring;
+    auto C = std::make_unique<Colouring>();
+    const std::vector<int32_t>& tmap = group_maps[test_group];
+    const int E = static_cast<int>(tmap.size() / cells);
+    std::vector<int32_t> col(static_cast<size_t>(cells));
+    int nc = 0;
+    if (femgpu_color_cells(tmap.data(), cells, E, group_global[test_group], col.data(), &nc) != FEMGPU_OK)
+        fail(FEMGPU_E_INTERNAL, "colouring failed");
+    C->n = nc;
+    C->off.assign(nc + 1, 0);
+    for (int c : col) ++C->off[c + 1];
+    for (int c = 0; c < nc; ++c) C->off[c + 1] += C->off[c];
+    std::vector<int32_t> perm(static_cast<size_t>(cells));
+    std::vector<int> fill(C->off.begin(), C->off.end() - 1);
+    for (int c = 0; c < cells; ++c) perm[fill[col[c]]++] = c;  // ascending cells within a colour
+    C->d_perm = alloc<int32_t>(perm.size());
+    FG_CUDA(cudaMemcpy(C->d_perm, perm.data(), perm.size() * 4, cudaMemcpyHostToDevice));
+    colouring = std::move(C);
+    return *colouring;
 }
 
 void run_action(Instance& I, const KernelPlan& kp, double* d_y, cudaStream_t stream, cudaEvent_t after_zero) {
+    if (kp.colour) {
+        // one launch per colour over its slice of the colour-sorted permutation, in colour order
+        const Colouring& C = I.colour_plan();
+        for (int c = 0; c < C.n; ++c)
+            run_action_range(I, kp, d_y, stream, C.off[c], C.off[c + 1], c == 0, c == 0 ? after_zero : nullptr);
+        I.last_launches = C.n;
+        return;
+    }
     run_action_range(I, kp, d_y, stream, 0, I.cells, true, after_zero);
 }
 
@@ -893,7 +934,7 @@ void run_action_range(Instance& I, const KernelPlan& kp, double* d_y, cudaStream
     if (mod->emitted.smem_bytes > 227 * 1024)
         fail(FEMGPU_E_INFEASIBLE, "schedule: " + std::to_string(mod->emitted.smem_bytes) +
                                       " bytes of shared memory per CTA exceed the 227 KB sm_100a limit");
-    if ((c_begin != 0 || c_end != I.cells) && !supports_cell_range(kp))
+    if ((c_begin != 0 || c_end != I.cells) && !supports_cell_range(kp) && !kp.colour)
         fail(FEMGPU_E_INTERNAL, "run_action_range: family does not support cell ranges");
     const TileLayout* L = kp.family == Family::Tile ? &I.tile_layout(kp.tile_cells) : nullptr;
     ParamBuf P = build_params(I, kp, d_y, L, c_begin, c_end);

@@ -181,3 +181,22 @@ def test_non_affine_instance_matches_oracle(oracle):
     for sched in (None, fg.TilingParams.scpt(scatter=abi.SCATTER_ATOMIC), fg.TilingParams.dmma()):
         y = fg.gpu_action(p, sched)
         assert rel_l2(y, ref) <= 1e-12 and max_rel(y, ref) <= 1e-10
+
+
+@pytest.mark.parametrize("form,dim,deg,Q,n", [("laplace", 3, 2, 4, 4), ("elasticity", 3, 2, 4, 3), ("mass", 2, 1, 3, 12),
+                                              ("advection", 3, 2, 14, 3)])
+def test_colour_scatter_is_deterministic(oracle, form, dim, deg, Q, n):
+    """SCATTER_COLOR: one launch per colour of the test-map colouring, plain y updates: matches the
+    oracle and is bitwise identical run to run and across instances."""
+    p = fg.mesh_problem(form, dim, deg, Q, n)
+    ref = oracle.reference_action(p)
+    sched = fg.TilingParams.scpt(scatter=abi.SCATTER_COLOR)
+    with fg.GpuInstance(p) as g:
+        y1 = g.action(sched)
+        y2 = g.action(sched)
+        assert g.stats()["launches_last_action"] > 1
+    with fg.GpuInstance(p) as g:
+        y3 = g.action(sched)
+    assert rel_l2(y1, ref) <= 1e-12 and max_rel(y1, ref) <= 1e-10
+    assert np.array_equal(y1.view(np.uint64), y2.view(np.uint64))
+    assert np.array_equal(y1.view(np.uint64), y3.view(np.uint64))

@@ -66,6 +66,8 @@ def sched(name):
             elif p == "glob":
                 d["basis"] = abi.BASIS_CONST
         return fg.TilingParams.dmma(**d)
+    if head == "colour":
+        return fg.TilingParams.scpt(scatter=abi.SCATTER_COLOR, **kw)
     if head == "scpt":
         return fg.TilingParams.scpt(scatter=abi.SCATTER_ATOMIC, **kw)
     if head.startswith("macro"):
