@@ -182,6 +182,14 @@ void autotune(Instance& I) {
             s.reserved[3] = 4;  // quadrature loop kept rolled (measured 7 % faster on C3a)
             cands.push_back(s);
         }
+        {  // 3 cells per thread, rolled quadrature loop, 64-thread CTAs (C3a: 181 us vs 205 us)
+            femgpu_schedule s = dfma_default();
+            s.scatter = FEMGPU_SCATTER_ATOMIC;
+            s.group_cells = 3;
+            s.block_cells = 64;
+            s.reserved[3] = 4;
+            cands.push_back(s);
+        }
     }
     if (t_dmma <= 1.6 * best) {
         // quadrature chunk: the register-capped choice of resolve_dmma and, when different, the
