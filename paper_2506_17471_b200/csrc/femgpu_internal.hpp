@@ -240,6 +240,12 @@ struct Instance {
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
     std::vector<cudaEvent_t> ev_pipe;
     const PipePlan& pipe_plan(int align);
+    // overlapped zeroing of y (pipeline.cpp): slab plan, high-priority zero stream, worker stream
+    std::unique_ptr<PipePlan> zplan;
+    const PipePlan& zero_plan(int align);
+    std::unique_ptr<PipePlan> slab_plan(int K, int align) const;
+    cudaStream_t s_zero = nullptr, s_work = nullptr;
+    std::vector<cudaEvent_t> ev_zero;
     bool auto_ready = false;
     femgpu_schedule auto_sched{};
     std::string auto_log;
@@ -270,6 +276,10 @@ void run_action(Instance& inst, const KernelPlan& kp, double* d_y, cudaStream_t 
 void run_action_range(Instance& inst, const KernelPlan& kp, double* d_y, cudaStream_t stream, int c_begin, int c_end,
                       bool zero_y, cudaEvent_t after_zero = nullptr);
 bool supports_cell_range(const KernelPlan& kp);
+int range_align(const KernelPlan& kp);
+// pipeline.cpp: y zeroing overlapped with slab-wise compute; false = not applicable
+bool overlapped_zero_action(Instance& inst, const KernelPlan& kp, double* d_y, cudaStream_t stream,
+                            cudaEvent_t after_zero);
 // pipeline.cpp: femgpu_action_host overlapped over H2D / compute / D2H streams; false = not applicable
 bool pipelined_host_action(Instance& inst, const KernelPlan& kp, const double* const* scalar_inputs,
                            const double* const* vector_inputs, double* y_host);

@@ -196,12 +196,13 @@ Instance::~Instance() {
     }
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
-    for (cudaStream_t s : {s_h2d, s_d2h})
+    for (cudaStream_t s : {s_h2d, s_d2h, s_zero, s_work})
         if (s) {
             cudaStreamSynchronize(s);
             cudaStreamDestroy(s);
         }
     for (cudaEvent_t e : ev_pipe) cudaEventDestroy(e);
+    for (cudaEvent_t e : ev_zero) cudaEventDestroy(e);
     for (void* p : allocations) cudaFree(p);
     cudaGetLastError();
 }
@@ -925,6 +926,7 @@ void run_action(Instance& I, const KernelPlan& kp, double* d_y, cudaStream_t str
         I.last_launches = C.n;
         return;
     }
+    if (overlapped_zero_action(I, kp, d_y, stream, after_zero)) return;
     run_action_range(I, kp, d_y, stream, 0, I.cells, true, after_zero);
 }
 

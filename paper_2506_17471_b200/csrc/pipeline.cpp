@@ -23,6 +23,8 @@ namespace femgpu {
 namespace {
 
 constexpr long long kPipeMinCells = 1000000;
+constexpr long long kZeroOverlapMinRows = 1 << 21;  // 16 MB of y: ~3 us of memset
+constexpr long long kZeroOverlapMinCells = 1 << 16;
 
 int slab_count() {
     const char* e = std::getenv("FEMGPU_PIPE_SLABS");
@@ -30,11 +32,29 @@ int slab_count() {
     return std::max(2, std::min(128, k));
 }
 
+int zero_slab_count() {
+    const char* e = std::getenv("FEMGPU_ZERO_SLABS");
+    const int k = e ? std::atoi(e) : 8;
+    return std::max(2, std::min(64, k));
+}
+
 }  // namespace
 
 const PipePlan& Instance::pipe_plan(int align) {
     const int K = slab_count();
     if (pipe && pipe->align == align && static_cast<int>(pipe->cb.size()) == K + 1) return *pipe;
+    pipe = slab_plan(K, align);
+    return *pipe;
+}
+
+const PipePlan& Instance::zero_plan(int align) {
+    const int K = zero_slab_count();
+    if (zplan && zplan->align == align && static_cast<int>(zplan->cb.size()) == K + 1) return *zplan;
+    zplan = slab_plan(K, align);
+    return *zplan;
+}
+
+std::unique_ptr<PipePlan> Instance::slab_plan(int K, int align) const {
     auto P = std::make_unique<PipePlan>();
     P->align = align;
     // slab sizes: equal by default; FEMGPU_PIPE_EDGE scales the first and last (fill / drain)
@@ -87,15 +107,76 @@ const PipePlan& Instance::pipe_plan(int align) {
         total += P->up[i][K - 1];
     }
     P->useful = total > 0 && need0 * 10 <= total * 6 && P->fin[K / 2] * 10 >= static_cast<long long>(output_size) * 2;
-    pipe = std::move(P);
-    return *pipe;
+    return P;
+}
+
+int range_align(const KernelPlan& kp) { return kp.family == Family::Macro ? kp.G : 32; }
+
+// Device action with the zeroing of y overlapped with the compute (opt-in, see below).  The y memset is an HBM-bound pass over the whole output (8 B/row at 6.5 TB/s,
+// 10 % of a P3 2D step) while the action kernels are FP64-bound, so it should run *beside* the
+// kernel, not before it.  The cells are split into K slabs (zero_plan: K = FEMGPU_ZERO_SLABS,
+// default 8); only the y rows slab 0 can reach are zeroed in front of it, the rows first reached
+// by slab k are zeroed on a high-priority side stream (its CTAs dispatch ahead of queued action
+// CTAs) and slab k waits only for its own chunk.  Slabs alternate between the caller's stream and
+// a second worker stream so that slab k+1's CTAs fill the SMs slab k's tail leaves idle (no wave
+// quantisation per slab); concurrent slabs only RED into y, which is order-independent up to the
+// usual floating-point reassociation, exactly as within one launch.
+bool overlapped_zero_action(Instance& I, const KernelPlan& kp, double* d_y, cudaStream_t stream,
+                            cudaEvent_t after_zero) {
+    // Opt-in (FEMGPU_ZERO_OVERLAP=1: DMMA family, =all: every cell-range family).  Measured
+    // (profiles/r01_zero_overlap.txt): beside the one-cell-per-thread DFMA kernels (Macro, SCPT:
+    // 4-16 resident CTAs at up to 255 registers) the memset CTAs take whole CTA slots and the step
+    // grows by more than the hidden memset (C3a 179 -> 196 us); the persistent DMMA kernels gain
+    // 0-2 % on large instances but lose up to 4 % when a slab holds too few warp tasks to fill the
+    // GPU (C5-hyp-P4), so the default is the one-launch path.
+    const char* env = std::getenv("FEMGPU_ZERO_OVERLAP");
+    const bool all = env && std::strcmp(env, "all") == 0;
+    if (!env || !(all || std::strcmp(env, "1") == 0) || !supports_cell_range(kp)) return false;
+    if (kp.family != Family::Dmma && !all) return false;
+    if (static_cast<long long>(I.output_size) < kZeroOverlapMinRows || I.cells < kZeroOverlapMinCells) return false;
+    const PipePlan& Z = I.zero_plan(range_align(kp));
+    const int K = static_cast<int>(Z.cb.size()) - 1;
+    if (Z.zero_hi[0] * 10 > static_cast<long long>(I.output_size) * 6) return false;  // no locality: nothing to overlap
+    if (!I.s_zero) {
+        int lo = 0, hi = 0;
+        FG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        FG_CUDA(cudaStreamCreateWithPriority(&I.s_zero, cudaStreamNonBlocking, hi));
+        FG_CUDA(cudaStreamCreateWithFlags(&I.s_work, cudaStreamNonBlocking));
+    }
+    while (static_cast<int>(I.ev_zero.size()) < K + 2) {
+        cudaEvent_t e;
+        FG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        I.ev_zero.push_back(e);
+    }
+    // ev_zero[0]: start (prior work on the stream done) and chunk 0 zeroed; [k]: chunk k zeroed;
+    // [K]: the worker stream's slabs done
+    FG_CUDA(cudaMemsetAsync(d_y, 0, sizeof(double) * static_cast<size_t>(Z.zero_hi[0]), stream));
+    if (after_zero) FG_CUDA(cudaEventRecord(after_zero, stream));
+    FG_CUDA(cudaEventRecord(I.ev_zero[0], stream));
+    FG_CUDA(cudaStreamWaitEvent(I.s_zero, I.ev_zero[0], 0));
+    FG_CUDA(cudaStreamWaitEvent(I.s_work, I.ev_zero[0], 0));
+    for (int k = 1; k < K; ++k) {
+        const long long a = Z.zero_hi[k - 1], b = Z.zero_hi[k];
+        if (b > a)
+            FG_CUDA(cudaMemsetAsync(d_y + a, 0, sizeof(double) * static_cast<size_t>(b - a), I.s_zero));
+        FG_CUDA(cudaEventRecord(I.ev_zero[k], I.s_zero));
+    }
+    for (int k = 0; k < K; ++k) {
+        cudaStream_t s = (k & 1) ? I.s_work : stream;
+        if (k > 0) FG_CUDA(cudaStreamWaitEvent(s, I.ev_zero[k], 0));
+        run_action_range(I, kp, d_y, s, Z.cb[k], Z.cb[k + 1], false);
+    }
+    FG_CUDA(cudaEventRecord(I.ev_zero[K], I.s_work));
+    FG_CUDA(cudaStreamWaitEvent(stream, I.ev_zero[K], 0));
+    I.last_launches = K;
+    return true;
 }
 
 bool pipelined_host_action(Instance& I, const KernelPlan& kp, const double* const* scalar_inputs,
                            const double* const* vector_inputs, double* y_host) {
     const char* env = std::getenv("FEMGPU_PIPELINE");
     if ((env && std::strcmp(env, "0") == 0) || I.cells < kPipeMinCells || !supports_cell_range(kp)) return false;
-    const PipePlan& P = I.pipe_plan(kp.family == Family::Macro ? kp.G : 32);
+    const PipePlan& P = I.pipe_plan(range_align(kp));
     if (!P.useful) return false;
     const int K = static_cast<int>(P.cb.size()) - 1;
     if (!I.s_h2d) {

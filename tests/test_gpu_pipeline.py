@@ -58,8 +58,39 @@ def test_pipelined_host_action_matches_oracle(oracle, monkeypatch, form, dim, de
         g.action_host(xs, vs, yh, scheds[0])
         assert rel_l2(yh, 2.0 * ref) <= 1e-12
         monkeypatch.setenv("FEMGPU_PIPELINE", "0")
+        monkeypatch.setenv("FEMGPU_ZERO_OVERLAP", "0")
         y2 = np.array(g.action_host(xs, vs, yh, scheds[0]))
         assert g.stats()["launches_last_action"] == 1
         assert rel_l2(y2, 2.0 * ref) <= 1e-12
     for ptr in keep:
         lib().femgpu_host_free(ptr)
+
+
+@pytest.mark.parametrize("form,dim,deg,Q,n,sched", [
+    ("laplace", 3, 2, 4, 64, None),
+    ("laplace", 3, 2, 4, 64, fg.TilingParams.dmma()),
+    ("laplace", 3, 2, 4, 64, fg.TilingParams.scpt(scatter=abi.SCATTER_ATOMIC)),
+    ("elasticity", 3, 2, 4, 48, fg.TilingParams.dmma()),
+    ("helmholtz_coef", 2, 3, 12, 600, None),
+])
+@pytest.mark.parametrize("slabs", ["4", "7"])
+def test_overlapped_zero_matches_sequential(monkeypatch, form, dim, deg, Q, n, sched, slabs):
+    """run_action's overlapped zeroing (pipeline.cpp overlapped_zero_action): slab k's y rows are
+    zeroed on a side stream while earlier slabs compute, slabs alternate between two streams.  Same
+    y as the one-launch path (rel L2 <= 1e-12; the kernels themselves are checked against the oracle
+    in test_gpu_parity), also across back-to-back actions, changed inputs and the device path."""
+    monkeypatch.setenv("FEMGPU_AUTOTUNE", "0")
+    monkeypatch.setenv("FEMGPU_ZERO_SLABS", slabs)
+    p = fg.mesh_problem(form, dim, deg, Q, n)
+    assert p.output_size >= 1 << 21
+    with fg.GpuInstance(p) as g:
+        monkeypatch.setenv("FEMGPU_ZERO_OVERLAP", "0")
+        ref = np.array(g.action(sched))
+        assert g.stats()["launches_last_action"] == 1
+        monkeypatch.setenv("FEMGPU_ZERO_OVERLAP", "all")  # opt-in; "1" = DMMA family only
+        for _ in range(3):
+            g.action_device(sched)
+        y = np.array(g.action(sched))
+        assert g.stats()["launches_last_action"] == int(slabs), "overlapped path not taken"
+        # every action re-zeroes all of y (a missed chunk would accumulate the previous result)
+        assert rel_l2(y, ref) <= 1e-12
