@@ -163,6 +163,9 @@ void autotune(Instance& I) {
             s.scatter = FEMGPU_SCATTER_MACRO;
             s.block_cells = 32;
             cands.push_back(s);
+            s.reserved[2] = 8;  // uncapped (255 registers, 8 warps/SM): C5-adv-P1 1448 us vs 1703 us
+            cands.push_back(s);
+            s.reserved[2] = 0;
             s.reserved[3] = 3;  // quadrature-point-major: one tabulation load for the group's cells
             s.reserved[1] = 232;
             cands.push_back(s);
@@ -223,7 +226,10 @@ void autotune(Instance& I) {
                     cands.push_back(dmma_variant(joint, 0, block, 32));
                     cands.back().quad_tile = tq;
                 }
-        cands.push_back(dmma_variant(1, 1, 256, 32));  // gather prefetch
+        for (int tq : tqs) {  // gather prefetch (C5-hyp-P2: T^Q=8 + prefetch 2226 us vs 2310 us)
+            cands.push_back(dmma_variant(1, 1, 256, 32));
+            cands.back().quad_tile = tq;
+        }
     }
     std::ostringstream log;
     log << "model slots/cell: dfma " << static_cast<long long>(t_dfma) << ", dmma "
