@@ -162,8 +162,13 @@ typedef struct femgpu_schedule {
     int32_t scatter;       /* femgpu_scatter */
     int32_t block_cells;   /* SCPT/tile: cells (threads) per CTA; macro: groups (threads) per CTA; 0 = auto */
     int32_t group_cells;   /* macro: cells per group G; 0 = auto */
-    int32_t reserved[4];   /* [0] strict (--fmad=false), [1] register target, [2] min CTAs/SM */
+    int32_t reserved[4];   /* [0] flags (FEMGPU_FLAG_*), [1] register target, [2] min CTAs/SM */
 } femgpu_schedule;
+
+/* femgpu_schedule.reserved[0] flags */
+#define FEMGPU_FLAG_STRICT 1      /* --fmad=false: the reference's bitwise per-cell arithmetic */
+#define FEMGPU_FLAG_FUSED_ZERO 2  /* y zeroing fused into slab launches (Macro/SCPT/DMMA, large
+                                     outputs; the automatic schedule sets it where it measures faster) */
 
 typedef struct femgpu_instance femgpu_instance;
 

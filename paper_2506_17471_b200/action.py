@@ -47,6 +47,7 @@ class TilingParams:
     reg_target: int = 0
     min_blocks: int = 0
     stage_smem: int = 0  # macro: stage the group's gathered values in shared memory (cp.async)
+    fused_zero: bool = False  # y zeroing fused into slab launches (FEMGPU_FLAG_FUSED_ZERO)
 
     @staticmethod
     def scpt(**knobs) -> "TilingParams":
@@ -91,7 +92,7 @@ class TilingParams:
         s.cells_per_group, s.lanes_per_cell = self.cells_per_group, self.lanes_per_cell
         s.basis, s.scatter, s.block_cells = self.basis, self.scatter, self.block_cells
         s.group_cells = self.group_cells
-        s.reserved[0] = 1 if self.strict else 0
+        s.reserved[0] = (abi.FLAG_STRICT if self.strict else 0) | (abi.FLAG_FUSED_ZERO if self.fused_zero else 0)
         s.reserved[1] = self.reg_target
         s.reserved[2] = self.min_blocks
         s.reserved[3] = self.stage_smem
@@ -105,8 +106,9 @@ class TilingParams:
                             quad_row_tile=s.quad_row_tile, quad_col_tile=s.quad_col_tile,
                             cells_per_group=s.cells_per_group, lanes_per_cell=s.lanes_per_cell, basis=s.basis,
                             scatter=s.scatter, block_cells=s.block_cells, group_cells=s.group_cells,
-                            strict=bool(s.reserved[0]), reg_target=s.reserved[1], min_blocks=s.reserved[2],
-                            stage_smem=s.reserved[3])
+                            strict=bool(s.reserved[0] & abi.FLAG_STRICT), reg_target=s.reserved[1],
+                            min_blocks=s.reserved[2], stage_smem=s.reserved[3],
+                            fused_zero=bool(s.reserved[0] & abi.FLAG_FUSED_ZERO))
 
     def describe(self) -> str:  # search.hpp:301-310
         if self.kind == abi.SCPT:

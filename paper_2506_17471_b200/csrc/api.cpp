@@ -130,7 +130,7 @@ femgpu_status femgpu_emit_source(const femgpu_problem* p, const femgpu_schedule*
             if (s && s->reserved[3] == 4) kp.qloop = true;
             if (s && s->scatter == FEMGPU_SCATTER_COLOR) kp.colour = true;
         }
-        kp.strict = s && s->reserved[0];
+        kp.strict = s && (s->reserved[0] & FEMGPU_FLAG_STRICT);
         femgpu::EmitResult em = femgpu::emit_kernel(sig, kp);
         if (len) *len = em.source.size();
         if (buf && cap) {
@@ -150,7 +150,7 @@ femgpu_status femgpu_jit_check(const femgpu_problem* p, const femgpu_schedule* s
         femgpu_emit_source(p, s, src.data(), src.size(), &len);
         src.resize(len);
         std::string log;
-        femgpu::jit_compile(src, s && s->reserved[0], &log);
+        femgpu::jit_compile(src, s && (s->reserved[0] & FEMGPU_FLAG_STRICT), &log);
     });
 }
 

@@ -160,6 +160,8 @@ void emit_params(Out& o, const Signature& sig, const KernelPlan& kp, long long n
     // cell0 / n_cells: the cell range [cell0, n_cells) of this launch (pipelined host actions launch
     // one slab at a time; macro: group range [cell0/G, n_cells/G)); stride / n_groups stay global
     o.line("  int n_cells; int stride; int n_tiles; int lstride; int n_groups; int cell0;");
+    // zp / zn: y rows a *later* slab reaches first, zeroed by this launch (pipeline.cpp fused zeroing)
+    o.line("  double* zp; long long zn;");
     if (nt_param > 0) o.line("  double tab[" + std::to_string(nt_param) + "];");
     o.line("};");
 }
@@ -509,6 +511,15 @@ std::string KernelPlan::key() const {
 EmitResult emit_mlt(const Signature& sig, const KernelPlan& kp);  // below
 EmitResult emit_dmma(const Signature& sig, const KernelPlan& kp);  // below
 
+// Fused zeroing (pipeline.cpp overlapped_zero_action): every CTA clears its share of the y rows
+// [zp, zp + zn) before any early exit; a launch never writes those rows itself.
+const char* kZeroPrologue =
+    "if (P.zn > 0) {\n"
+    "  const long long zper = (P.zn + gridDim.x - 1) / gridDim.x, z0 = (long long)blockIdx.x * zper;\n"
+    "  const long long z1 = min(z0 + zper, P.zn);\n"
+    "  for (long long i = z0 + threadIdx.x; i < z1; i += blockDim.x) P.zp[i] = 0.0;\n"
+    "}\n";
+
 namespace {
 
 std::string S(long long v) { return std::to_string(v); }
@@ -523,6 +534,7 @@ void emit_scpt_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const 
     o.line("extern \"C\" __global__ void " + bounds + name + "(const __grid_constant__ Params P) {");
     o.ind++;
     o.line(std::string("constexpr bool CHECKED = ") + (checked ? "true" : "false") + ";");
+    if (!checked) o << kZeroPrologue;
     if (kp.basis == FEMGPU_BASIS_SMEM) {
         o.line("extern __shared__ __align__(16) unsigned char smraw[];");
         o.line("double* sT = reinterpret_cast<double*>(smraw + " + S(smem_tab_off) + ");");
@@ -582,6 +594,7 @@ void emit_scpt_multi_kernel(Out& o, const Signature& sig, const KernelPlan& kp, 
            ") " + name + "(const __grid_constant__ Params P) {");
     o.ind++;
     o.line("constexpr bool CHECKED = false;");
+    o << kZeroPrologue;
     if (kp.basis == FEMGPU_BASIS_SMEM) {
         o.line("extern __shared__ __align__(16) unsigned char smraw[];");
         o.line("double* sT = reinterpret_cast<double*>(smraw + " + S(smem_tab_off) + ");");
@@ -808,6 +821,7 @@ void emit_tile_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const 
     o.line("extern \"C\" __global__ void " + bounds + name + "(const __grid_constant__ Params P) {");
     o.ind++;
     o.line("constexpr bool CHECKED = false;");
+    o << kZeroPrologue;
     o.line("extern __shared__ __align__(16) unsigned char smraw[];");
     if (kp.basis == FEMGPU_BASIS_SMEM) {
         o.line("double* sT = reinterpret_cast<double*>(smraw + " + S(T.tab_off) + ");");
@@ -949,6 +963,7 @@ void emit_macro_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const
     o.line("extern \"C\" __global__ void " + bounds + name + "(const __grid_constant__ Params P) {");
     o.ind++;
     o.line("constexpr bool CHECKED = false;");
+    o << kZeroPrologue;
     if (kp.basis == FEMGPU_BASIS_SMEM) {
         o.line("extern __shared__ __align__(16) unsigned char smraw[];");
         o.line("double* sT = reinterpret_cast<double*>(smraw + " + S(smem_tab_off) + ");");

@@ -84,6 +84,7 @@ struct KernelPlan {
     int tgroup = -1, cgroup = -1;
     int tvec = -1;                     // DMMA: vector space whose node map interleaves into the test map
     bool breg = false;                 // DMMA: B fragments in registers (single quadrature chunk)
+    bool zfused = false;               // run_action: y zeroing fused into slab launches (FEMGPU_FLAG_FUSED_ZERO)
     std::vector<int> group_entries, group_cap;   // per group: entries per cell, max unique per tile
     // MLT family (TilingParams)
     int Nc = 1, Nwi = 1, TQ = 1, Ter = 1, Tqr = 1, Tqc = 1;
@@ -240,11 +241,11 @@ struct Instance {
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
     std::vector<cudaEvent_t> ev_pipe;
     const PipePlan& pipe_plan(int align);
-    // overlapped zeroing of y (pipeline.cpp): slab plan, high-priority zero stream, worker stream
+    // fused zeroing of y (pipeline.cpp): slab plan, worker stream, per-slab events
     std::unique_ptr<PipePlan> zplan;
-    const PipePlan& zero_plan(int align);
+    const PipePlan& zero_plan(int align, int max_slabs);
     std::unique_ptr<PipePlan> slab_plan(int K, int align) const;
-    cudaStream_t s_zero = nullptr, s_work = nullptr;
+    cudaStream_t s_work = nullptr;
     std::vector<cudaEvent_t> ev_zero;
     bool auto_ready = false;
     femgpu_schedule auto_sched{};
@@ -273,11 +274,14 @@ void run_action(Instance& inst, const KernelPlan& kp, double* d_y, cudaStream_t 
                 cudaEvent_t after_zero = nullptr);
 // One launch over the cell range [c_begin, c_end) (Scpt, Macro (G-aligned) and Dmma families);
 // y is zeroed first only when zero_y.
+// zero_ptr / zero_n: y rows of a later slab this launch clears (fused zeroing, pipeline.cpp).
 void run_action_range(Instance& inst, const KernelPlan& kp, double* d_y, cudaStream_t stream, int c_begin, int c_end,
-                      bool zero_y, cudaEvent_t after_zero = nullptr);
+                      bool zero_y, cudaEvent_t after_zero = nullptr, double* zero_ptr = nullptr,
+                      long long zero_n = 0);
+extern const char* kZeroPrologue;  // emit.cpp
 bool supports_cell_range(const KernelPlan& kp);
 int range_align(const KernelPlan& kp);
-// pipeline.cpp: y zeroing overlapped with slab-wise compute; false = not applicable
+// pipeline.cpp: y zeroing fused into slab-wise compute; false = not applicable
 bool overlapped_zero_action(Instance& inst, const KernelPlan& kp, double* d_y, cudaStream_t stream,
                             cudaEvent_t after_zero);
 // pipeline.cpp: femgpu_action_host overlapped over H2D / compute / D2H streams; false = not applicable

@@ -196,7 +196,7 @@ Instance::~Instance() {
     }
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
-    for (cudaStream_t s : {s_h2d, s_d2h, s_zero, s_work})
+    for (cudaStream_t s : {s_h2d, s_d2h, s_work})
         if (s) {
             cudaStreamSynchronize(s);
             cudaStreamDestroy(s);
@@ -665,12 +665,23 @@ int int_dim(int a) { return a; }
 }  // namespace
 
 // Resolves a femgpu_schedule (TilingParams + B200 knobs) into a launch plan.
+namespace {
+KernelPlan resolve_schedule_impl(Instance& I, const femgpu_schedule* s);
+}
+
 KernelPlan resolve_schedule(Instance& I, const femgpu_schedule* s) {
+    KernelPlan kp = resolve_schedule_impl(I, s);
+    kp.zfused = s && (s->reserved[0] & FEMGPU_FLAG_FUSED_ZERO) && supports_cell_range(kp);
+    return kp;
+}
+
+namespace {
+KernelPlan resolve_schedule_impl(Instance& I, const femgpu_schedule* s) {
     const Signature& sig = I.sig;
     femgpu_schedule def{};
     if (!s) s = &def;
     KernelPlan kp;
-    kp.strict = s->reserved[0] != 0;
+    kp.strict = (s->reserved[0] & FEMGPU_FLAG_STRICT) != 0;
     const long long tab_bytes = sig.tab_size * 8;
     if (s->kind == FEMGPU_MLT) {
         kp.family = Family::Mlt;
@@ -799,7 +810,7 @@ KernelPlan resolve_schedule(Instance& I, const femgpu_schedule* s) {
                 return kp;
             }
             kp = KernelPlan{};
-            kp.strict = s->reserved[0] != 0;
+            kp.strict = (s->reserved[0] & FEMGPU_FLAG_STRICT) != 0;
             kp.basis = basis;
             kp.block = block;
         }
@@ -818,6 +829,7 @@ KernelPlan resolve_schedule(Instance& I, const femgpu_schedule* s) {
     (void)int_dim;
     return kp;
 }
+}  // namespace
 
 namespace {
 
@@ -836,7 +848,7 @@ struct ParamBuf {
 
 // Builds the kernel-parameter block in the exact layout of the emitted `struct Params`.
 ParamBuf build_params(Instance& I, const KernelPlan& kp, double* d_y, const TileLayout* L, int c_begin = 0,
-                      int c_end = -1) {
+                      int c_end = -1, double* zero_ptr = nullptr, long long zero_n = 0) {
     const Signature& sig = I.sig;
     ParamBuf P;
     for (const auto& sp : I.sspaces) {
@@ -873,6 +885,8 @@ ParamBuf build_params(Instance& I, const KernelPlan& kp, double* d_y, const Tile
     P.put(static_cast<int32_t>(L ? L->n_tiles * L->tile_cells : 0));  // local-map row stride
     P.put(static_cast<int32_t>(M ? M->n_groups : 0));
     P.put(static_cast<int32_t>(c_begin));  // cell0: first cell of the launched range
+    P.put(static_cast<void*>(zero_ptr));    // zp / zn: fused zeroing of a later slab's y rows
+    P.put(static_cast<long long>(zero_ptr ? zero_n : 0));
     if (kp.basis == FEMGPU_BASIS_CONST && kp.family != Family::Mlt)
         for (double v : I.tab) P.put(v);
     P.align(8);
@@ -931,7 +945,7 @@ void run_action(Instance& I, const KernelPlan& kp, double* d_y, cudaStream_t str
 }
 
 void run_action_range(Instance& I, const KernelPlan& kp, double* d_y, cudaStream_t stream, int c_begin, int c_end,
-                      bool zero_y, cudaEvent_t after_zero) {
+                      bool zero_y, cudaEvent_t after_zero, double* zero_ptr, long long zero_n) {
     auto mod = I.module_for(kp);
     if (mod->emitted.smem_bytes > 227 * 1024)
         fail(FEMGPU_E_INFEASIBLE, "schedule: " + std::to_string(mod->emitted.smem_bytes) +
@@ -939,7 +953,7 @@ void run_action_range(Instance& I, const KernelPlan& kp, double* d_y, cudaStream
     if ((c_begin != 0 || c_end != I.cells) && !supports_cell_range(kp) && !kp.colour)
         fail(FEMGPU_E_INTERNAL, "run_action_range: family does not support cell ranges");
     const TileLayout* L = kp.family == Family::Tile ? &I.tile_layout(kp.tile_cells) : nullptr;
-    ParamBuf P = build_params(I, kp, d_y, L, c_begin, c_end);
+    ParamBuf P = build_params(I, kp, d_y, L, c_begin, c_end, zero_ptr, zero_n);
     void* args[] = {P.b.data()};
     if (zero_y) FG_CUDA(cudaMemsetAsync(d_y, 0, sizeof(double) * static_cast<size_t>(I.output_size), stream));
     if (after_zero) FG_CUDA(cudaEventRecord(after_zero, stream));

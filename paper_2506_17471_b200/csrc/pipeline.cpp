@@ -47,8 +47,8 @@ const PipePlan& Instance::pipe_plan(int align) {
     return *pipe;
 }
 
-const PipePlan& Instance::zero_plan(int align) {
-    const int K = zero_slab_count();
+const PipePlan& Instance::zero_plan(int align, int max_slabs) {
+    const int K = std::min(zero_slab_count(), std::max(2, max_slabs));
     if (zplan && zplan->align == align && static_cast<int>(zplan->cb.size()) == K + 1) return *zplan;
     zplan = slab_plan(K, align);
     return *zplan;
@@ -112,62 +112,62 @@ std::unique_ptr<PipePlan> Instance::slab_plan(int K, int align) const {
 
 int range_align(const KernelPlan& kp) { return kp.family == Family::Macro ? kp.G : 32; }
 
-// Device action with the zeroing of y overlapped with the compute (opt-in, see below).  The y memset is an HBM-bound pass over the whole output (8 B/row at 6.5 TB/s,
-// 10 % of a P3 2D step) while the action kernels are FP64-bound, so it should run *beside* the
-// kernel, not before it.  The cells are split into K slabs (zero_plan: K = FEMGPU_ZERO_SLABS,
-// default 8); only the y rows slab 0 can reach are zeroed in front of it, the rows first reached
-// by slab k are zeroed on a high-priority side stream (its CTAs dispatch ahead of queued action
-// CTAs) and slab k waits only for its own chunk.  Slabs alternate between the caller's stream and
-// a second worker stream so that slab k+1's CTAs fill the SMs slab k's tail leaves idle (no wave
-// quantisation per slab); concurrent slabs only RED into y, which is order-independent up to the
-// usual floating-point reassociation, exactly as within one launch.
+// Device action with the zeroing of y fused into the compute (schedules with
+// FEMGPU_FLAG_FUSED_ZERO on large outputs; otherwise [memset y, one launch]).  The y memset is an HBM-bound
+// pass over the whole output (8 B/row: 17 us of a 179 us P3 2D step) in front of FP64-bound
+// kernels.  The cells are split into K slabs (zero_plan, K = FEMGPU_ZERO_SLABS, default 8,
+// fewer when a slab would hold less than one wave of CTAs); only the y rows slabs 0 and 1 can
+// reach are memset in front; slab k clears the rows slab k+2 reaches first ([zero_hi[k+1],
+// zero_hi[k+2])) in a prologue of its own CTAs (kZeroPrologue: a few 8-byte stores per thread,
+// free beside the FP64 work).  Slabs alternate between the caller's stream and a worker stream so
+// slab k+1's CTAs fill the SMs slab k's tail leaves idle (measured +2.7 us for 4 slabs vs +11 us
+// on one stream).  Ordering: slab j needs slabs 0..j-2 complete (they cleared its rows): those on
+// its own stream by stream order, those on the other stream through an event on slab j-3.
+// Concurrent slabs only RED into y (order-independent up to floating-point reassociation, as
+// within one launch), and no slab writes rows another concurrent slab clears (prefix maxima).
+// A side-stream memset instead of the fused prologue was measured slower than no overlap:
+// memset CTAs take whole CTA slots beside 255-register action CTAs (profiles/r01_zero_overlap.txt).
 bool overlapped_zero_action(Instance& I, const KernelPlan& kp, double* d_y, cudaStream_t stream,
                             cudaEvent_t after_zero) {
-    // Opt-in (FEMGPU_ZERO_OVERLAP=1: DMMA family, =all: every cell-range family).  Measured
-    // (profiles/r01_zero_overlap.txt): beside the one-cell-per-thread DFMA kernels (Macro, SCPT:
-    // 4-16 resident CTAs at up to 255 registers) the memset CTAs take whole CTA slots and the step
-    // grows by more than the hidden memset (C3a 179 -> 196 us); the persistent DMMA kernels gain
-    // 0-2 % on large instances but lose up to 4 % when a slab holds too few warp tasks to fill the
-    // GPU (C5-hyp-P4), so the default is the one-launch path.
+    // per schedule (FEMGPU_FLAG_FUSED_ZERO, chosen by the tuner where it measures faster);
+    // FEMGPU_ZERO_OVERLAP=0 / 1 forces it off / on for every cell-range schedule
     const char* env = std::getenv("FEMGPU_ZERO_OVERLAP");
-    const bool all = env && std::strcmp(env, "all") == 0;
-    if (!env || !(all || std::strcmp(env, "1") == 0) || !supports_cell_range(kp)) return false;
-    if (kp.family != Family::Dmma && !all) return false;
+    const bool on = env ? std::strcmp(env, "0") != 0 : kp.zfused;
+    if (!on || !supports_cell_range(kp)) return false;
     if (static_cast<long long>(I.output_size) < kZeroOverlapMinRows || I.cells < kZeroOverlapMinCells) return false;
-    const PipePlan& Z = I.zero_plan(range_align(kp));
+    // cells one full wave of resident CTAs processes: slabs smaller than that under-fill the GPU
+    auto mod = I.module_for(kp);
+    const long long cells_per_cta = kp.family == Family::Dmma ? static_cast<long long>(kp.block / 32) * kp.Nc
+                                                              : static_cast<long long>(kp.block) * std::max(1, kp.G);
+    const long long wave = static_cast<long long>(mod->sms) * std::max(1, mod->occupancy) * cells_per_cta;
+    const PipePlan& Z = I.zero_plan(range_align(kp), static_cast<int>(std::min<long long>(64, I.cells / std::max(1LL, wave))));
     const int K = static_cast<int>(Z.cb.size()) - 1;
-    if (Z.zero_hi[0] * 10 > static_cast<long long>(I.output_size) * 6) return false;  // no locality: nothing to overlap
-    if (!I.s_zero) {
-        int lo = 0, hi = 0;
-        FG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        FG_CUDA(cudaStreamCreateWithPriority(&I.s_zero, cudaStreamNonBlocking, hi));
-        FG_CUDA(cudaStreamCreateWithFlags(&I.s_work, cudaStreamNonBlocking));
-    }
+    if (K < 4 || Z.zero_hi[1] * 10 > static_cast<long long>(I.output_size) * 6) return false;  // no locality
+    if (!I.s_work) FG_CUDA(cudaStreamCreateWithFlags(&I.s_work, cudaStreamNonBlocking));
     while (static_cast<int>(I.ev_zero.size()) < K + 2) {
         cudaEvent_t e;
         FG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         I.ev_zero.push_back(e);
     }
-    // ev_zero[0]: start (prior work on the stream done) and chunk 0 zeroed; [k]: chunk k zeroed;
-    // [K]: the worker stream's slabs done
-    FG_CUDA(cudaMemsetAsync(d_y, 0, sizeof(double) * static_cast<size_t>(Z.zero_hi[0]), stream));
+    // ev_zero[k]: slab k done (on its stream); ev_zero[K]: rows of slabs 0, 1 zeroed
+    FG_CUDA(cudaMemsetAsync(d_y, 0, sizeof(double) * static_cast<size_t>(Z.zero_hi[1]), stream));
     if (after_zero) FG_CUDA(cudaEventRecord(after_zero, stream));
-    FG_CUDA(cudaEventRecord(I.ev_zero[0], stream));
-    FG_CUDA(cudaStreamWaitEvent(I.s_zero, I.ev_zero[0], 0));
-    FG_CUDA(cudaStreamWaitEvent(I.s_work, I.ev_zero[0], 0));
-    for (int k = 1; k < K; ++k) {
-        const long long a = Z.zero_hi[k - 1], b = Z.zero_hi[k];
-        if (b > a)
-            FG_CUDA(cudaMemsetAsync(d_y + a, 0, sizeof(double) * static_cast<size_t>(b - a), I.s_zero));
-        FG_CUDA(cudaEventRecord(I.ev_zero[k], I.s_zero));
-    }
+    FG_CUDA(cudaEventRecord(I.ev_zero[K], stream));
+    FG_CUDA(cudaStreamWaitEvent(I.s_work, I.ev_zero[K], 0));
     for (int k = 0; k < K; ++k) {
         cudaStream_t s = (k & 1) ? I.s_work : stream;
-        if (k > 0) FG_CUDA(cudaStreamWaitEvent(s, I.ev_zero[k], 0));
-        run_action_range(I, kp, d_y, s, Z.cb[k], Z.cb[k + 1], false);
+        if (k >= 3) FG_CUDA(cudaStreamWaitEvent(s, I.ev_zero[k - 3], 0));
+        double* zp = nullptr;
+        long long zn = 0;
+        if (k + 2 < K) {
+            zp = d_y + Z.zero_hi[k + 1];
+            zn = Z.zero_hi[k + 2] - Z.zero_hi[k + 1];
+        }
+        run_action_range(I, kp, d_y, s, Z.cb[k], Z.cb[k + 1], false, nullptr, zp, zn);
+        FG_CUDA(cudaEventRecord(I.ev_zero[k], s));
     }
-    FG_CUDA(cudaEventRecord(I.ev_zero[K], I.s_work));
-    FG_CUDA(cudaStreamWaitEvent(stream, I.ev_zero[K], 0));
+    // join: the worker stream's last slab (the caller's stream already follows its own slabs)
+    FG_CUDA(cudaStreamWaitEvent(stream, I.ev_zero[(K - 1) & 1 ? K - 1 : K - 2], 0));
     I.last_launches = K;
     return true;
 }

@@ -58,7 +58,7 @@ long long map_ops(const Signature& sig) {
 std::string tune_key(const Instance& I) {
     const Signature& sig = I.sig;
     std::ostringstream k;
-    k << "v2|" << sig.dim << "|" << sig.Q << "|" << sig.nW << "|" << sig.Tw << "|" << I.cells << "|" << I.output_size;
+    k << "v3|" << sig.dim << "|" << sig.Q << "|" << sig.nW << "|" << sig.Tw << "|" << I.cells << "|" << I.output_size;
     for (size_t i = 0; i < sig.sdofs.size(); ++i) k << "|s" << sig.sdofs[i] << ":" << sig.sterms[i];
     for (size_t i = 0; i < sig.vdofs.size(); ++i) {
         k << "|v" << sig.vdofs[i] << ":" << sig.vterms[i];
@@ -111,6 +111,7 @@ std::string describe_plan(const KernelPlan& kp) {
               << " block=" << kp.block << " basis=" << (kp.basis == FEMGPU_BASIS_SMEM ? "smem" : "l1");
             break;
     }
+    if (kp.zfused) s << " +fused-zero";
     return s.str();
 }
 
@@ -281,6 +282,29 @@ void autotune(Instance& I) {
                 if (retime[k] < retime[win]) win = k;
         I.auto_sched = cands[first[win].second];
         log << "; re-timed top " << top << ", winner " << describe_plan(plans[first[win].second]);
+        // fused y zeroing (pipeline.cpp): slabbed launches clear later slabs' rows instead of a
+        // memset in front; kept only where it times faster (it wins on C1b / C2 / C4 / C5-hyp-P1,
+        // loses where slab boundaries cost more than the memset)
+        const char* zo = std::getenv("FEMGPU_ZERO_OVERLAP");
+        femgpu_schedule fz = I.auto_sched;
+        fz.reserved[0] |= FEMGPU_FLAG_FUSED_ZERO;
+        const KernelPlan kz = resolve_schedule(I, &fz);
+        if (!zo && kz.zfused) {
+            const KernelPlan& k0 = plans[first[win].second];
+            const int reps = reps_of[first[win].second];
+            for (int i = 0; i < 2; ++i) run_action(I, kz, I.d_y, I.stream);
+            double t0 = 1e300, t1 = 1e300;
+            for (int round = 0; round < 2; ++round) {
+                t0 = std::min(t0, time_it(k0, reps));
+                t1 = std::min(t1, time_it(kz, reps));
+            }
+            const bool slabbed = I.last_launches > 1;
+            log << "; fused zeroing ";
+            if (slabbed) log << static_cast<long long>(t1 * 1e7) / 10.0 << " us";
+            else log << "n/a";
+            log << " vs " << static_cast<long long>(t0 * 1e7) / 10.0 << " us";
+            if (slabbed && t1 < 0.99 * t0) I.auto_sched = fz;
+        }
     }
     // a non-finite input must not leave a stale flag behind the tuning runs
     FG_CUDA(cudaMemsetAsync(I.d_bad, 0xff, 2 * sizeof(unsigned long long), I.stream));

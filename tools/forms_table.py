@@ -11,7 +11,7 @@ import time
 
 sys.path.insert(0, ".")
 import paper_2506_17471_b200 as fg  # noqa: E402
-from bench import algorithmic_bytes, load_peaks  # noqa: E402
+from bench import ClockSampler, algorithmic_bytes, load_peaks  # noqa: E402
 
 
 def main():
@@ -29,14 +29,15 @@ def main():
             t_roof = max(flops / (pk["fp64"] * 1e12), byts / (hbm * 1e9))
             with fg.GpuInstance(p) as g:
                 g.action()
-                step, kern, zero = g.profile(warmup=3, reps=20)
+                with ClockSampler() as clk:
+                    step, kern, zero = g.profile(warmup=3, reps=max(20, int(0.5 / max(g.time(min_reps=3, min_seconds=0.0), 1e-6))))
                 plan = g.describe()
             print(json.dumps({"config": name, "cells": cells, "dofs": p.output_size, "step_us": round(step * 1e6, 1),
                               "kernel_us": round(kern * 1e6, 1), "zero_us": round(zero * 1e6, 1),
                               "t_roof_us": round(t_roof * 1e6, 1),
                               "bound": "fp64" if flops / (pk["fp64"] * 1e12) >= byts / (hbm * 1e9) else "hbm",
                               "frac_step": round(t_roof / step, 3), "gdofs": round(p.output_size / step / 1e9, 2),
-                              "plan": plan, "wall_s": round(time.time() - t0, 1)}), flush=True)
+                              "plan": plan, "clocks": clk.summary(), "wall_s": round(time.time() - t0, 1)}), flush=True)
         except Exception as e:  # noqa: BLE001
             print(json.dumps({"config": name, "error": str(e)[:300]}), flush=True)
 
