@@ -318,8 +318,14 @@ def run_single(args):
     }
     if not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(p)
+    os.environ["FEMGPU_ZERO_OVERLAP"] = "0"  # the plain [memset y, one launch] path
+    y0 = g.action()
+    del os.environ["FEMGPU_ZERO_OVERLAP"]
     out["parity_check"] = {"finite": bool(np.all(np.isfinite(y1))), "repeatable_rel_l2":
-                           float(np.linalg.norm(y1 - y) / np.linalg.norm(y))}
+                           float(np.linalg.norm(y1 - y) / np.linalg.norm(y)),
+                           "vs_one_launch_rel_l2": float(np.linalg.norm(y1 - y0) / np.linalg.norm(y0))}
+    if not (out["parity_check"]["repeatable_rel_l2"] <= 1e-12 and out["parity_check"]["vs_one_launch_rel_l2"] <= 1e-12):
+        print("bench: timed path disagrees with the one-launch path: %s" % out["parity_check"], file=sys.stderr)
     g.close()
     print(json.dumps(out))
 

@@ -821,7 +821,6 @@ void emit_tile_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const 
     o.line("extern \"C\" __global__ void " + bounds + name + "(const __grid_constant__ Params P) {");
     o.ind++;
     o.line("constexpr bool CHECKED = false;");
-    o << kZeroPrologue;
     o.line("extern __shared__ __align__(16) unsigned char smraw[];");
     if (kp.basis == FEMGPU_BASIS_SMEM) {
         o.line("double* sT = reinterpret_cast<double*>(smraw + " + S(T.tab_off) + ");");
@@ -1153,6 +1152,7 @@ void emit_macro_qmajor_kernel(Out& o, const Signature& sig, const KernelPlan& kp
            ") " + name + "(const __grid_constant__ Params P) {");
     o.ind++;
     o.line("constexpr bool CHECKED = false;");
+    o << kZeroPrologue;
     o.line("extern __shared__ __align__(16) unsigned char smraw[];");
     if (kp.basis == FEMGPU_BASIS_SMEM) {
         o.line("double* sT = reinterpret_cast<double*>(smraw + " + S(smem_tab_off) + ");");

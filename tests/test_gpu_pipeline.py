@@ -95,3 +95,40 @@ def test_overlapped_zero_matches_sequential(monkeypatch, form, dim, deg, Q, n, s
         assert 4 <= g.stats()["launches_last_action"] <= int(slabs), "fused-zeroing path not taken"
         # every action re-zeroes all of y (a missed chunk would accumulate the previous result)
         assert rel_l2(y, ref) <= 1e-12
+
+
+FUSED_VARIANTS = {
+    "macro-b32": dict(scatter=abi.SCATTER_MACRO, block_cells=32),
+    "macro-b32-uncapped": dict(scatter=abi.SCATTER_MACRO, block_cells=32, min_blocks=8),
+    "macro-qmajor": dict(scatter=abi.SCATTER_MACRO, block_cells=32, stage_smem=3, reg_target=232),
+    "macro-ysmem": dict(scatter=abi.SCATTER_MACRO, stage_smem=2),
+    "macro-cp-async": dict(scatter=abi.SCATTER_MACRO, stage_smem=1),
+    "scpt-m5": dict(scatter=abi.SCATTER_ATOMIC, block_cells=128, min_blocks=5),
+    "scpt-g2": dict(scatter=abi.SCATTER_ATOMIC, group_cells=2),
+    "scpt-g2-qloop": dict(scatter=abi.SCATTER_ATOMIC, group_cells=2, stage_smem=4),
+    "scpt-g3-qloop-b64": dict(scatter=abi.SCATTER_ATOMIC, group_cells=3, block_cells=64, stage_smem=4),
+}
+
+
+@pytest.mark.parametrize("name", list(FUSED_VARIANTS) + ["dmma", "dmma-joint2", "dmma-prefetch", "dmma-breg"])
+def test_fused_zero_every_kernel_variant(monkeypatch, name):
+    """Every kernel variant the automatic schedule can pick carries the fused-zeroing prologue:
+    three back-to-back fused actions equal the one-launch result (a variant without the prologue
+    leaves rows uncleared and accumulates: rel L2 ~ 0.8, 1.6, 2.4, ...)."""
+    monkeypatch.setenv("FEMGPU_AUTOTUNE", "0")
+    monkeypatch.setenv("FEMGPU_ZERO_SLABS", "7")
+    if name.startswith("dmma"):
+        knobs = {"dmma": {}, "dmma-joint2": dict(eval_row_tile=2), "dmma-prefetch": dict(quad_row_tile=1, block_cells=256),
+                 "dmma-breg": dict(stage_smem=1)}[name]
+        s = fg.TilingParams.dmma(**knobs)
+    else:
+        s = fg.TilingParams.scpt(**FUSED_VARIANTS[name])
+    p = fg.mesh_problem("laplace", 3, 2, 4, 64)
+    with fg.GpuInstance(p) as g:
+        monkeypatch.setenv("FEMGPU_ZERO_OVERLAP", "0")
+        ref = np.array(g.action(s))
+        monkeypatch.setenv("FEMGPU_ZERO_OVERLAP", "1")
+        for i in range(3):
+            y = np.array(g.action(s))
+            assert g.stats()["launches_last_action"] >= 4, "fused-zeroing path not taken"
+            assert rel_l2(y, ref) <= 1e-12, (name, i, rel_l2(y, ref))
