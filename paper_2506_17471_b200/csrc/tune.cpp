@@ -283,7 +283,7 @@ void autotune(Instance& I) {
         I.auto_sched = cands[first[win].second];
         log << "; re-timed top " << top << ", winner " << describe_plan(plans[first[win].second]);
         // fused y zeroing (pipeline.cpp): slabbed launches clear later slabs' rows instead of a
-        // memset in front; kept only where it times faster (it wins on C1b / C2 / C4 / C5-hyp-P1,
+        // memset in front; kept only where it times faster (it wins on C5-hyp-P1 and C4,
         // loses where slab boundaries cost more than the memset)
         const char* zo = std::getenv("FEMGPU_ZERO_OVERLAP");
         femgpu_schedule fz = I.auto_sched;
