@@ -160,8 +160,10 @@ void emit_params(Out& o, const Signature& sig, const KernelPlan& kp, long long n
     // cell0 / n_cells: the cell range [cell0, n_cells) of this launch (pipelined host actions launch
     // one slab at a time; macro: group range [cell0/G, n_cells/G)); stride / n_groups stay global
     o.line("  int n_cells; int stride; int n_tiles; int lstride; int n_groups; int cell0;");
-    // zp / zn: y rows a *later* slab reaches first, zeroed by this launch (pipeline.cpp fused zeroing)
-    o.line("  double* zp; long long zn;");
+    // zp / zn: y rows a *later* slab reaches first, zeroed by this launch (pipeline.cpp fused
+    // zeroing; only in fused-zeroing kernels: two more fields cost C5-adv-P2 6 % elsewhere, see
+    // profiles/r01_prologue_ab.txt)
+    if (kp.zfused) o.line("  double* zp; long long zn;");
     if (nt_param > 0) o.line("  double tab[" + std::to_string(nt_param) + "];");
     o.line("};");
 }
@@ -494,7 +496,7 @@ std::string KernelPlan::key() const {
     std::ostringstream s;
     s << int(family) << "/" << basis << "/" << block << "/" << tile_cells << "/" << Nc << "x" << Nwi << "/" << TQ << "/"
       << Ter << "/" << Tqr << "/" << Tqc << "/" << strict << "/" << min_blocks << "/G" << G << "/ms" << mstage << "/ys" << ysmem
-      << "/qm" << qmajor << "/ql" << qloop << "/col" << colour;
+      << "/qm" << qmajor << "/ql" << qloop << "/col" << colour << "/zf" << zfused;
     for (int t : Tcs) s << "s" << t;
     for (int t : Tcv) s << "v" << t;
     for (size_t g = 0; g < group_cap.size(); ++g) s << "g" << group_entries[g] << ":" << group_cap[g];
@@ -534,7 +536,7 @@ void emit_scpt_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const 
     o.line("extern \"C\" __global__ void " + bounds + name + "(const __grid_constant__ Params P) {");
     o.ind++;
     o.line(std::string("constexpr bool CHECKED = ") + (checked ? "true" : "false") + ";");
-    if (!checked) o << kZeroPrologue;
+    if (!checked && kp.zfused) o << kZeroPrologue;
     if (kp.basis == FEMGPU_BASIS_SMEM) {
         o.line("extern __shared__ __align__(16) unsigned char smraw[];");
         o.line("double* sT = reinterpret_cast<double*>(smraw + " + S(smem_tab_off) + ");");
@@ -594,7 +596,7 @@ void emit_scpt_multi_kernel(Out& o, const Signature& sig, const KernelPlan& kp, 
            ") " + name + "(const __grid_constant__ Params P) {");
     o.ind++;
     o.line("constexpr bool CHECKED = false;");
-    o << kZeroPrologue;
+    if (kp.zfused) o << kZeroPrologue;
     if (kp.basis == FEMGPU_BASIS_SMEM) {
         o.line("extern __shared__ __align__(16) unsigned char smraw[];");
         o.line("double* sT = reinterpret_cast<double*>(smraw + " + S(smem_tab_off) + ");");
@@ -962,7 +964,7 @@ void emit_macro_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const
     o.line("extern \"C\" __global__ void " + bounds + name + "(const __grid_constant__ Params P) {");
     o.ind++;
     o.line("constexpr bool CHECKED = false;");
-    o << kZeroPrologue;
+    if (kp.zfused) o << kZeroPrologue;
     if (kp.basis == FEMGPU_BASIS_SMEM) {
         o.line("extern __shared__ __align__(16) unsigned char smraw[];");
         o.line("double* sT = reinterpret_cast<double*>(smraw + " + S(smem_tab_off) + ");");
@@ -1152,7 +1154,7 @@ void emit_macro_qmajor_kernel(Out& o, const Signature& sig, const KernelPlan& kp
            ") " + name + "(const __grid_constant__ Params P) {");
     o.ind++;
     o.line("constexpr bool CHECKED = false;");
-    o << kZeroPrologue;
+    if (kp.zfused) o << kZeroPrologue;
     o.line("extern __shared__ __align__(16) unsigned char smraw[];");
     if (kp.basis == FEMGPU_BASIS_SMEM) {
         o.line("double* sT = reinterpret_cast<double*>(smraw + " + S(smem_tab_off) + ");");

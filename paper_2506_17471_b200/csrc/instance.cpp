@@ -885,8 +885,12 @@ ParamBuf build_params(Instance& I, const KernelPlan& kp, double* d_y, const Tile
     P.put(static_cast<int32_t>(L ? L->n_tiles * L->tile_cells : 0));  // local-map row stride
     P.put(static_cast<int32_t>(M ? M->n_groups : 0));
     P.put(static_cast<int32_t>(c_begin));  // cell0: first cell of the launched range
-    P.put(static_cast<void*>(zero_ptr));    // zp / zn: fused zeroing of a later slab's y rows
-    P.put(static_cast<long long>(zero_ptr ? zero_n : 0));
+    if (kp.zfused) {  // zp / zn: fused zeroing of a later slab's y rows
+        P.put(static_cast<void*>(zero_ptr));
+        P.put(static_cast<long long>(zero_ptr ? zero_n : 0));
+    } else if (zero_ptr && zero_n > 0) {
+        fail(FEMGPU_E_INTERNAL, "run_action_range: zero range for a kernel without the fused-zeroing prologue");
+    }
     if (kp.basis == FEMGPU_BASIS_CONST && kp.family != Family::Mlt)
         for (double v : I.tab) P.put(v);
     P.align(8);

@@ -127,13 +127,16 @@ int range_align(const KernelPlan& kp) { return kp.family == Family::Macro ? kp.G
 // within one launch), and no slab writes rows another concurrent slab clears (prefix maxima).
 // A side-stream memset instead of the fused prologue was measured slower than no overlap:
 // memset CTAs take whole CTA slots beside 255-register action CTAs (profiles/r01_zero_overlap.txt).
-bool overlapped_zero_action(Instance& I, const KernelPlan& kp, double* d_y, cudaStream_t stream,
+bool overlapped_zero_action(Instance& I, const KernelPlan& plan, double* d_y, cudaStream_t stream,
                             cudaEvent_t after_zero) {
     // per schedule (FEMGPU_FLAG_FUSED_ZERO, chosen by the tuner where it measures faster);
     // FEMGPU_ZERO_OVERLAP=0 / 1 forces it off / on for every cell-range schedule
     const char* env = std::getenv("FEMGPU_ZERO_OVERLAP");
-    const bool on = env ? std::strcmp(env, "0") != 0 : kp.zfused;
-    if (!on || !supports_cell_range(kp)) return false;
+    const bool on = env ? std::strcmp(env, "0") != 0 : plan.zfused;
+    if (!on || !supports_cell_range(plan)) return false;
+    // the prologue is compiled only into zfused kernels (it costs up to 7 % elsewhere: C5-adv-P2)
+    KernelPlan kp = plan;
+    kp.zfused = true;
     if (static_cast<long long>(I.output_size) < kZeroOverlapMinRows || I.cells < kZeroOverlapMinCells) return false;
     // cells one full wave of resident CTAs processes: slabs smaller than that under-fill the GPU
     auto mod = I.module_for(kp);
