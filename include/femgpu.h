@@ -168,7 +168,8 @@ typedef struct femgpu_schedule {
 /* femgpu_schedule.reserved[0] flags */
 #define FEMGPU_FLAG_STRICT 1      /* --fmad=false: the reference's bitwise per-cell arithmetic */
 #define FEMGPU_FLAG_FUSED_ZERO 2  /* y zeroing fused into slab launches (Macro/SCPT/DMMA, large
-                                     outputs; the automatic schedule sets it where it measures faster) */
+                                     outputs; the automatic schedule sets it where it measures faster);
+                                     bits 8-15 of reserved[0]: slab count (0 = 8) */
 
 typedef struct femgpu_instance femgpu_instance;
 

@@ -48,6 +48,7 @@ class TilingParams:
     min_blocks: int = 0
     stage_smem: int = 0  # macro: stage the group's gathered values in shared memory (cp.async)
     fused_zero: bool = False  # y zeroing fused into slab launches (FEMGPU_FLAG_FUSED_ZERO)
+    zero_slabs: int = 0  # slabs for fused zeroing (0 = default 8)
 
     @staticmethod
     def scpt(**knobs) -> "TilingParams":
@@ -92,7 +93,8 @@ class TilingParams:
         s.cells_per_group, s.lanes_per_cell = self.cells_per_group, self.lanes_per_cell
         s.basis, s.scatter, s.block_cells = self.basis, self.scatter, self.block_cells
         s.group_cells = self.group_cells
-        s.reserved[0] = (abi.FLAG_STRICT if self.strict else 0) | (abi.FLAG_FUSED_ZERO if self.fused_zero else 0)
+        s.reserved[0] = ((abi.FLAG_STRICT if self.strict else 0) | (abi.FLAG_FUSED_ZERO if self.fused_zero else 0)
+                         | (self.zero_slabs & 0xff) << 8)
         s.reserved[1] = self.reg_target
         s.reserved[2] = self.min_blocks
         s.reserved[3] = self.stage_smem
@@ -108,7 +110,8 @@ class TilingParams:
                             scatter=s.scatter, block_cells=s.block_cells, group_cells=s.group_cells,
                             strict=bool(s.reserved[0] & abi.FLAG_STRICT), reg_target=s.reserved[1],
                             min_blocks=s.reserved[2], stage_smem=s.reserved[3],
-                            fused_zero=bool(s.reserved[0] & abi.FLAG_FUSED_ZERO))
+                            fused_zero=bool(s.reserved[0] & abi.FLAG_FUSED_ZERO),
+                            zero_slabs=(s.reserved[0] >> 8) & 0xff)
 
     def describe(self) -> str:  # search.hpp:301-310
         if self.kind == abi.SCPT:

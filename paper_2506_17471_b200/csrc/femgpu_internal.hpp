@@ -85,6 +85,7 @@ struct KernelPlan {
     int tvec = -1;                     // DMMA: vector space whose node map interleaves into the test map
     bool breg = false;                 // DMMA: B fragments in registers (single quadrature chunk)
     bool zfused = false;               // run_action: y zeroing fused into slab launches (FEMGPU_FLAG_FUSED_ZERO)
+    int zslabs = 0;                    // slabs for fused zeroing (reserved[0] >> 8; 0 = default)
     std::vector<int> group_entries, group_cap;   // per group: entries per cell, max unique per tile
     // MLT family (TilingParams)
     int Nc = 1, Nwi = 1, TQ = 1, Ter = 1, Tqr = 1, Tqc = 1;
@@ -242,8 +243,8 @@ struct Instance {
     std::vector<cudaEvent_t> ev_pipe;
     const PipePlan& pipe_plan(int align);
     // fused zeroing of y (pipeline.cpp): slab plan, worker stream, per-slab events
-    std::unique_ptr<PipePlan> zplan;
-    const PipePlan& zero_plan(int align, int max_slabs);
+    std::map<std::pair<int, int>, std::unique_ptr<PipePlan>> zplans;  // by (align, slabs): host scan of the maps
+    const PipePlan& zero_plan(int align, int slabs, int max_slabs);
     std::unique_ptr<PipePlan> slab_plan(int K, int align) const;
     cudaStream_t s_work = nullptr;
     std::vector<cudaEvent_t> ev_zero;

@@ -672,6 +672,7 @@ KernelPlan resolve_schedule_impl(Instance& I, const femgpu_schedule* s);
 KernelPlan resolve_schedule(Instance& I, const femgpu_schedule* s) {
     KernelPlan kp = resolve_schedule_impl(I, s);
     kp.zfused = s && (s->reserved[0] & FEMGPU_FLAG_FUSED_ZERO) && supports_cell_range(kp);
+    kp.zslabs = s ? (s->reserved[0] >> 8) & 0xff : 0;
     return kp;
 }
 

@@ -32,9 +32,10 @@ int slab_count() {
     return std::max(2, std::min(128, k));
 }
 
-int zero_slab_count() {
+// slabs for fused zeroing: FEMGPU_ZERO_SLABS, else the schedule's count (reserved[0] >> 8), else 8
+int zero_slab_count(int sched_slabs) {
     const char* e = std::getenv("FEMGPU_ZERO_SLABS");
-    const int k = e ? std::atoi(e) : 8;
+    const int k = e ? std::atoi(e) : (sched_slabs > 0 ? sched_slabs : 8);
     return std::max(2, std::min(64, k));
 }
 
@@ -47,11 +48,11 @@ const PipePlan& Instance::pipe_plan(int align) {
     return *pipe;
 }
 
-const PipePlan& Instance::zero_plan(int align, int max_slabs) {
-    const int K = std::min(zero_slab_count(), std::max(2, max_slabs));
-    if (zplan && zplan->align == align && static_cast<int>(zplan->cb.size()) == K + 1) return *zplan;
-    zplan = slab_plan(K, align);
-    return *zplan;
+const PipePlan& Instance::zero_plan(int align, int slabs, int max_slabs) {
+    const int K = std::min(zero_slab_count(slabs), std::max(2, max_slabs));
+    auto& z = zplans[{align, K}];
+    if (!z) z = slab_plan(K, align);
+    return *z;
 }
 
 std::unique_ptr<PipePlan> Instance::slab_plan(int K, int align) const {
@@ -115,7 +116,7 @@ int range_align(const KernelPlan& kp) { return kp.family == Family::Macro ? kp.G
 // Device action with the zeroing of y fused into the compute (schedules with
 // FEMGPU_FLAG_FUSED_ZERO on large outputs; otherwise [memset y, one launch]).  The y memset is an HBM-bound
 // pass over the whole output (8 B/row: 17 us of a 179 us P3 2D step) in front of FP64-bound
-// kernels.  The cells are split into K slabs (zero_plan, K = FEMGPU_ZERO_SLABS, default 8,
+// kernels.  The cells are split into K slabs (zero_plan: K from the schedule, default 8,
 // fewer when a slab would hold less than one wave of CTAs); only the y rows slabs 0 and 1 can
 // reach are memset in front; slab k clears the rows slab k+2 reaches first ([zero_hi[k+1],
 // zero_hi[k+2])) in a prologue of its own CTAs (kZeroPrologue: a few 8-byte stores per thread,
@@ -143,7 +144,8 @@ bool overlapped_zero_action(Instance& I, const KernelPlan& plan, double* d_y, cu
     const long long cells_per_cta = kp.family == Family::Dmma ? static_cast<long long>(kp.block / 32) * kp.Nc
                                                               : static_cast<long long>(kp.block) * std::max(1, kp.G);
     const long long wave = static_cast<long long>(mod->sms) * std::max(1, mod->occupancy) * cells_per_cta;
-    const PipePlan& Z = I.zero_plan(range_align(kp), static_cast<int>(std::min<long long>(64, I.cells / std::max(1LL, wave))));
+    const PipePlan& Z = I.zero_plan(range_align(kp), kp.zslabs,
+                                    static_cast<int>(std::min<long long>(64, I.cells / std::max(1LL, wave))));
     const int K = static_cast<int>(Z.cb.size()) - 1;
     if (K < 4 || Z.zero_hi[1] * 10 > static_cast<long long>(I.output_size) * 6) return false;  // no locality
     if (!I.s_work) FG_CUDA(cudaStreamCreateWithFlags(&I.s_work, cudaStreamNonBlocking));

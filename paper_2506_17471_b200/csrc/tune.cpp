@@ -111,7 +111,7 @@ std::string describe_plan(const KernelPlan& kp) {
               << " block=" << kp.block << " basis=" << (kp.basis == FEMGPU_BASIS_SMEM ? "smem" : "l1");
             break;
     }
-    if (kp.zfused) s << " +fused-zero";
+    if (kp.zfused) s << " +fused-zero" << (kp.zslabs > 0 ? "/" + std::to_string(kp.zslabs) : std::string());
     return s.str();
 }
 
@@ -286,24 +286,37 @@ void autotune(Instance& I) {
         // memset in front; kept only where it times faster (it wins on C5-hyp-P1 and C4,
         // loses where slab boundaries cost more than the memset)
         const char* zo = std::getenv("FEMGPU_ZERO_OVERLAP");
-        femgpu_schedule fz = I.auto_sched;
-        fz.reserved[0] |= FEMGPU_FLAG_FUSED_ZERO;
-        const KernelPlan kz = resolve_schedule(I, &fz);
-        if (!zo && kz.zfused) {
+        if (!zo) {
             const KernelPlan& k0 = plans[first[win].second];
             const int reps = reps_of[first[win].second];
-            for (int i = 0; i < 2; ++i) run_action(I, kz, I.d_y, I.stream);
-            double t0 = 1e300, t1 = 1e300;
-            for (int round = 0; round < 2; ++round) {
-                t0 = std::min(t0, time_it(k0, reps));
-                t1 = std::min(t1, time_it(kz, reps));
+            std::vector<femgpu_schedule> fzs;
+            std::vector<KernelPlan> kzs;
+            for (int slabs : {4, 8}) {  // fewer slabs: larger front memset, fewer slab boundaries
+                femgpu_schedule fz = I.auto_sched;
+                fz.reserved[0] |= FEMGPU_FLAG_FUSED_ZERO | (slabs << 8);
+                const KernelPlan kz = resolve_schedule(I, &fz);
+                if (!kz.zfused) continue;
+                for (int i = 0; i < 2; ++i) run_action(I, kz, I.d_y, I.stream);
+                if (I.last_launches <= 1) continue;  // not applicable here (size, locality)
+                fzs.push_back(fz);
+                kzs.push_back(kz);
             }
-            const bool slabbed = I.last_launches > 1;
-            log << "; fused zeroing ";
-            if (slabbed) log << static_cast<long long>(t1 * 1e7) / 10.0 << " us";
-            else log << "n/a";
-            log << " vs " << static_cast<long long>(t0 * 1e7) / 10.0 << " us";
-            if (slabbed && t1 < 0.99 * t0) I.auto_sched = fz;
+            double t0 = 1e300;
+            std::vector<double> tz(kzs.size(), 1e300);
+            for (int round = 0; round < 2 && !kzs.empty(); ++round) {
+                t0 = std::min(t0, time_it(k0, reps));
+                for (size_t i = 0; i < kzs.size(); ++i) tz[i] = std::min(tz[i], time_it(kzs[i], reps));
+            }
+            size_t best = 0;
+            for (size_t i = 1; i < tz.size(); ++i)
+                if (tz[i] < tz[best]) best = i;
+            if (!kzs.empty()) {
+                log << "; fused zeroing";
+                for (size_t i = 0; i < kzs.size(); ++i)
+                    log << " " << kzs[i].zslabs << " slabs " << static_cast<long long>(tz[i] * 1e7) / 10.0 << " us";
+                log << " vs one launch " << static_cast<long long>(t0 * 1e7) / 10.0 << " us";
+                if (tz[best] < 0.99 * t0) I.auto_sched = fzs[best];
+            }
         }
     }
     // a non-finite input must not leave a stale flag behind the tuning runs
