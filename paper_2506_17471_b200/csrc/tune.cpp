@@ -227,10 +227,11 @@ void autotune(Instance& I) {
                     cands.push_back(dmma_variant(joint, 0, block, 32));
                     cands.back().quad_tile = tq;
                 }
-        for (int tq : tqs) {  // gather prefetch (C5-hyp-P2: T^Q=8 + prefetch 2226 us vs 2310 us)
-            cands.push_back(dmma_variant(1, 1, 256, 32));
-            cands.back().quad_tile = tq;
-        }
+        for (int tq : tqs)  // gather prefetch (C5-hyp-P2: T^Q=8 + prefetch 2191-2226 us vs 2310 us)
+            for (int block : {128, 256}) {
+                cands.push_back(dmma_variant(1, 1, block, 32));
+                cands.back().quad_tile = tq;
+            }
     }
     std::ostringstream log;
     log << "model slots/cell: dfma " << static_cast<long long>(t_dfma) << ", dmma "
