@@ -170,6 +170,9 @@ typedef struct femgpu_schedule {
 #define FEMGPU_FLAG_FUSED_ZERO 2  /* y zeroing fused into slab launches (Macro/SCPT/DMMA, large
                                      outputs; the automatic schedule sets it where it measures faster);
                                      bits 8-15 of reserved[0]: slab count (0 = 8) */
+#define FEMGPU_FLAG_PIPE_MEMSET 4 /* femgpu_action_device_pipelined zeroes the next output with a separate
+                                     memset instead of inside the action kernel (the automatic schedule
+                                     sets it where the in-kernel zeroing measures slower) */
 
 typedef struct femgpu_instance femgpu_instance;
 
@@ -184,6 +187,12 @@ femgpu_status femgpu_set_device(int32_t device);
 /* ---- pure host helpers (no GPU needed) --------------------------------- */
 /* femsched::usable_flops (form.hpp:164-173) */
 femgpu_status femgpu_usable_flops(const femgpu_problem* p, int64_t* flops_per_cell);
+/* The reference's ReferenceCounters for reference_action(p, &counters) (form.hpp:463-472):
+ * matvec mults/adds and pointwise-map add/mul evaluations of the unmemoised recursion, computed
+ * from the instance's structure (the GPU kernels execute the same arithmetic with a compiled,
+ * value-numbered map, so they do not count at run time). */
+femgpu_status femgpu_reference_counters(const femgpu_problem* p, int64_t* matvec_mults, int64_t* matvec_adds,
+                                        int64_t* map_ops);
 /* femsched::ProblemInstance::validate (form.hpp:416-434) */
 femgpu_status femgpu_validate(const femgpu_problem* p);
 /* Emit the CUDA source the JIT would compile for (problem signature+map, schedule).
@@ -214,6 +223,17 @@ femgpu_status femgpu_action_host(femgpu_instance* inst, const femgpu_schedule* s
  * Asynchronous, no host sync. */
 femgpu_status femgpu_action_device(femgpu_instance* inst, const femgpu_schedule* s, double* y_dev,
                                    void* stream);
+/* Output-pipelined device action: y_dev must hold zeros on entry (e.g. zeroed by the previous call);
+ * in stream order y_dev becomes A(u)·x and y_next_dev[0:output_size) is zeroed, the zeroing done
+ * inside the action kernel (macro / SCPT / DMMA families; a memset otherwise).  Back-to-back
+ * actions into alternating buffers (a Krylov loop's successive products) thus need one launch each
+ * and no separate memset.  y_next_dev may be NULL; it must not alias y_dev.  Asynchronous. */
+femgpu_status femgpu_action_device_pipelined(femgpu_instance* inst, const femgpu_schedule* s, double* y_dev,
+                                             double* y_next_dev, void* stream);
+/* Non-finite check of the device-side actions issued so far on `stream` (NULL = instance stream):
+ * synchronizes the stream and reports FEMGPU_E_NONFINITE with the reference's diagnostic
+ * ("non-finite value at cell N during <stage>", form.hpp:492-595) if any cell produced one. */
+femgpu_status femgpu_check_finite(femgpu_instance* inst, const femgpu_schedule* s, void* stream);
 /* Paper timing protocol: warmup launches, then at least
  * min_reps and at least min_seconds of [zero y + action] timed with CUDA events on
  * the instance stream; *seconds = arithmetic mean per action. */
@@ -223,6 +243,12 @@ femgpu_status femgpu_time_action(femgpu_instance* inst, const femgpu_schedule* s
  * a device synchronize on both sides and timed with CUDA events: *seconds = total elapsed. */
 femgpu_status femgpu_time_steps(femgpu_instance* inst, const femgpu_schedule* s, int32_t steps,
                                 double* seconds);
+/* femgpu_time_steps with flags: FEMGPU_STEPS_PIPELINED = each step is one
+ * femgpu_action_device_pipelined into alternating output buffers (the step still zeroes one full
+ * output and computes one full action; the zeroing runs inside the action kernel). */
+#define FEMGPU_STEPS_PIPELINED 1
+femgpu_status femgpu_time_steps_ex(femgpu_instance* inst, const femgpu_schedule* s, int32_t steps, int32_t flags,
+                                   double* seconds);
 /* Split timing of the same protocol: mean seconds per step [zero y + action], per
  * action kernel alone and per y-zeroing, each bracketed by CUDA events on the
  * instance stream (the roofline's per-kernel duration). */

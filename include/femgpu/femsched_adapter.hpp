@@ -19,6 +19,8 @@
 
 #include <femsched/form.hpp>
 
+#include <cstdint>
+#include <cstring>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
@@ -152,10 +154,67 @@ private:
 };
 
 // reference_action-shaped entry (form.hpp:471-472): same arguments, same return, same errors.
-inline std::vector<double> action(const femsched::ProblemInstance& p) {
+// counters, when given, are incremented exactly as reference_action increments them
+// (femgpu_reference_counters: matvec mults/adds, map add/mul evaluations).
+inline std::vector<double> action(const femsched::ProblemInstance& p, femsched::ReferenceCounters* counters = nullptr) {
     p.validate();  // identical argument checking to the reference, before any device work
     DeviceInstance d(p);
-    return d.action();
+    std::vector<double> y = d.action();
+    if (counters) {
+        ProblemView v(p);
+        int64_t m = 0, a = 0, o = 0;
+        check(femgpu_reference_counters(v.get(), &m, &a, &o));
+        counters->matvec_mults += m;
+        counters->matvec_adds += a;
+        counters->map_ops += o;
+    }
+    return y;
+}
+
+// Content fingerprint of an instance (sizes, maps, inputs, tabulations, map DAG): the executor's
+// device-instance cache is keyed on it, not on the address, so an instance rebuilt at the same
+// address or modified in place is re-uploaded.
+inline uint64_t fingerprint(const femsched::ProblemInstance& p) {
+    uint64_t h = 0xcbf29ce484222325ULL;
+    auto mix = [&h](const void* data, std::size_t bytes) {
+        const unsigned char* c = static_cast<const unsigned char*>(data);
+        std::size_t i = 0;
+        for (; i + 8 <= bytes; i += 8) {
+            uint64_t w;
+            std::memcpy(&w, c + i, 8);
+            h = (h ^ w) * 0x100000001b3ULL;
+            h ^= h >> 29;
+        }
+        for (; i < bytes; ++i) h = (h ^ c[i]) * 0x100000001b3ULL;
+    };
+    auto vec = [&](const auto& v) {
+        const std::size_t n = v.size();
+        mix(&n, sizeof n);
+        if (n) mix(v.data(), n * sizeof(v[0]));
+    };
+    const auto& c = p.connectivity;
+    mix(&c.cell_count, sizeof c.cell_count);
+    mix(&p.output_size, sizeof p.output_size);
+    for (const auto& m : c.scalar_maps) vec(m.indices);
+    for (const auto& m : c.vector_maps) vec(m.indices);
+    vec(c.test_map.indices);
+    vec(c.coord_map.indices);
+    vec(c.coords);
+    for (const auto& x : p.scalar_inputs) vec(x);
+    for (const auto& x : p.vector_inputs) vec(x);
+    for (const auto& sp : p.tabulations.scalar_phi)
+        for (const auto& m : sp) vec(m.data);
+    for (const auto& sp : p.tabulations.vector_phi)
+        for (const auto& m : sp) vec(m.data);
+    for (const auto& m : p.tabulations.psi) vec(m.data);
+    vec(p.tabulations.weights);
+    for (const auto& n : p.map.nodes()) {
+        const int v[3] = {static_cast<int>(n.op), n.a, n.b};
+        mix(v, sizeof v);
+        mix(&n.value, sizeof n.value);
+    }
+    vec(p.map.outputs());
+    return h;
 }
 
 #ifdef FEMGPU_HAS_EXECUTOR
@@ -186,7 +245,7 @@ inline femgpu_schedule schedule_from(const femsched::TilingParams& t) {
 inline femsched::Executor executor() {
     struct Cache {
         std::mutex mu;
-        const femsched::ProblemInstance* key = nullptr;
+        uint64_t key = 0;
         std::shared_ptr<DeviceInstance> dev;
     };
     auto cache = std::make_shared<Cache>();
@@ -195,10 +254,11 @@ inline femsched::Executor executor() {
         try {
             std::shared_ptr<DeviceInstance> d;
             {
+                const uint64_t fp = fingerprint(inst);
                 std::lock_guard<std::mutex> lk(cache->mu);
-                if (cache->key != &inst || !cache->dev) {
+                if (cache->key != fp || !cache->dev) {
                     cache->dev = std::make_shared<DeviceInstance>(inst);
-                    cache->key = &inst;
+                    cache->key = fp;
                 }
                 d = cache->dev;
             }

@@ -25,7 +25,8 @@ EXPORTS = (
     "femgpu_color_cells", "femgpu_profile_action", "femgpu_fp64_peak",
     "femgpu_time_steps", "femgpu_device_input", "femgpu_describe_schedule",
     "femgpu_fp64_dmma_peak", "femgpu_problem_load", "femgpu_problem_free", "femgpu_problem_save",
-    "femgpu_schedule_save", "femgpu_schedule_load",
+    "femgpu_schedule_save", "femgpu_schedule_load", "femgpu_action_device_pipelined", "femgpu_check_finite",
+    "femgpu_time_steps_ex", "femgpu_reference_counters",
 )
 
 
@@ -99,6 +100,11 @@ def lib():
                 "femgpu_schedule_save": ([_P(abi.Schedule), C.c_int32, C.c_int32, C.c_char_p], C.c_int),
                 "femgpu_schedule_load": ([C.c_char_p, _P(abi.Schedule)], C.c_int),
                 "femgpu_time_steps": ([C.c_void_p, _P(abi.Schedule), C.c_int32, _P(C.c_double)], C.c_int),
+                "femgpu_time_steps_ex": ([C.c_void_p, _P(abi.Schedule), C.c_int32, C.c_int32, _P(C.c_double)], C.c_int),
+                "femgpu_action_device_pipelined": ([C.c_void_p, _P(abi.Schedule), C.c_void_p, C.c_void_p, C.c_void_p],
+                                                   C.c_int),
+                "femgpu_check_finite": ([C.c_void_p, _P(abi.Schedule), C.c_void_p], C.c_int),
+                "femgpu_reference_counters": ([_P(abi.Problem), _P(C.c_int64), _P(C.c_int64), _P(C.c_int64)], C.c_int),
                 "femgpu_device_input": ([C.c_void_p, C.c_int32, _P(C.c_void_p)], C.c_int),
             }
             for name, (args, res) in sig.items():

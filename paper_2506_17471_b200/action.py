@@ -46,7 +46,9 @@ class TilingParams:
     strict: bool = False  # --fmad=false: bitwise per-cell arithmetic of the reference
     reg_target: int = 0
     min_blocks: int = 0
-    stage_smem: int = 0  # macro: stage the group's gathered values in shared memory (cp.async)
+    stage_smem: int = 0  # macro: 1 cp.async staging, 2 y in smem, 3 quadrature-point-major; scpt: 4 rolled q-loop
+    split: int = 0  # macro q-major: the G cells of a group split over this many warps (0/1 = one thread per group)
+    qmopt: int = 0  # macro q-major: bit 0 hoisted map nodes read back from smem, bit 1 scatter indices reloaded
     fused_zero: bool = False  # y zeroing fused into slab launches (FEMGPU_FLAG_FUSED_ZERO)
     zero_slabs: int = 0  # slabs for fused zeroing (0 = default 8)
 
@@ -97,7 +99,7 @@ class TilingParams:
                          | (self.zero_slabs & 0xff) << 8)
         s.reserved[1] = self.reg_target
         s.reserved[2] = self.min_blocks
-        s.reserved[3] = self.stage_smem
+        s.reserved[3] = (self.stage_smem & 0xff) | (self.split & 0xff) << 8 | (self.qmopt & 0xff) << 16
         return s
 
     @staticmethod
@@ -109,7 +111,8 @@ class TilingParams:
                             cells_per_group=s.cells_per_group, lanes_per_cell=s.lanes_per_cell, basis=s.basis,
                             scatter=s.scatter, block_cells=s.block_cells, group_cells=s.group_cells,
                             strict=bool(s.reserved[0] & abi.FLAG_STRICT), reg_target=s.reserved[1],
-                            min_blocks=s.reserved[2], stage_smem=s.reserved[3],
+                            min_blocks=s.reserved[2], stage_smem=s.reserved[3] & 0xff, split=(s.reserved[3] >> 8) & 0xff,
+                            qmopt=(s.reserved[3] >> 16) & 0xff,
                             fused_zero=bool(s.reserved[0] & abi.FLAG_FUSED_ZERO),
                             zero_slabs=(s.reserved[0] >> 8) & 0xff)
 
@@ -206,6 +209,18 @@ class GpuInstance:
         sp = _sched(params)
         _call(lib().femgpu_action_device(self._h, sp[0] if sp else None, C.c_void_p(y_dev), C.c_void_p(stream)))
 
+    def action_device_pipelined(self, y_dev: int, y_next_dev: int = 0, params: Optional[TilingParams] = None,
+                                stream: int = 0):
+        """y_dev (all zeros on entry) = A(u) x; y_next_dev zeroed inside the same kernel (stream order)."""
+        sp = _sched(params)
+        _call(lib().femgpu_action_device_pipelined(self._h, sp[0] if sp else None, C.c_void_p(y_dev),
+                                                   C.c_void_p(y_next_dev), C.c_void_p(stream)))
+
+    def check_finite(self, params: Optional[TilingParams] = None, stream: int = 0):
+        """Raises RuntimeError('... non-finite value at cell N during <stage>') after device actions."""
+        sp = _sched(params)
+        _call(lib().femgpu_check_finite(self._h, sp[0] if sp else None, C.c_void_p(stream)))
+
     def time(self, params: Optional[TilingParams] = None, warmup: int = 5, min_reps: int = 15,
              min_seconds: float = 0.2) -> float:
         """Mean seconds per [zero y + action], paper protocol."""
@@ -214,11 +229,13 @@ class GpuInstance:
         _call(lib().femgpu_time_action(self._h, sp[0] if sp else None, warmup, min_reps, min_seconds, C.byref(s)))
         return s.value
 
-    def time_steps(self, steps: int, params: Optional[TilingParams] = None) -> float:
-        """Total seconds of exactly `steps` actions, CUDA events, device sync on both sides."""
+    def time_steps(self, steps: int, params: Optional[TilingParams] = None, pipelined: bool = False) -> float:
+        """Total seconds of exactly `steps` actions, CUDA events, device sync on both sides.
+        pipelined: each step is one femgpu_action_device_pipelined into alternating output buffers
+        (one full zeroing + one full action per step, the zeroing inside the action kernel)."""
         s = C.c_double()
         sp = _sched(params)
-        _call(lib().femgpu_time_steps(self._h, sp[0] if sp else None, steps, C.byref(s)))
+        _call(lib().femgpu_time_steps_ex(self._h, sp[0] if sp else None, steps, int(pipelined), C.byref(s)))
         return s.value
 
     def profile(self, params: Optional[TilingParams] = None, warmup: int = 5, reps: int = 50):
@@ -260,10 +277,22 @@ class GpuInstance:
         return p.value or 0
 
 
-def gpu_action(problem: ProblemInstance, params: Optional[TilingParams] = None) -> np.ndarray:
-    """reference_action-shaped one-shot: upload, run, download (form.hpp:471)."""
+def reference_counters(problem: ProblemInstance):
+    """ReferenceCounters of reference_action(p, &c) (form.hpp:463-472): (matvec_mults, matvec_adds,
+    map_ops), from the instance's structure (femgpu_reference_counters)."""
+    cp = problem.to_c()
+    v = [C.c_int64() for _ in range(3)]
+    _call(lib().femgpu_reference_counters(C.byref(cp.desc), *[C.byref(x) for x in v]))
+    return tuple(x.value for x in v)
+
+
+def gpu_action(problem: ProblemInstance, params: Optional[TilingParams] = None, counters: bool = False):
+    """reference_action-shaped one-shot: upload, run, download (form.hpp:471-472).  With
+    counters=True returns (y, (matvec_mults, matvec_adds, map_ops)) like reference_action with a
+    ReferenceCounters argument."""
     with GpuInstance(problem) as g:
-        return g.action(params)
+        y = g.action(params)
+    return (y, reference_counters(problem)) if counters else y
 
 
 @dataclass

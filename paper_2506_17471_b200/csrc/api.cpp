@@ -91,6 +91,32 @@ femgpu_status femgpu_usable_flops(const femgpu_problem* p, int64_t* flops) {
     });
 }
 
+femgpu_status femgpu_reference_counters(const femgpu_problem* p, int64_t* matvec_mults, int64_t* matvec_adds,
+                                        int64_t* map_ops) {
+    return guard([&] {
+        if (!p) femgpu::invalid("null argument");
+        femgpu::validate_problem(p);
+        // reference_action's ReferenceCounters (form.hpp:463-472, counted at :534-537, :550-553,
+        // :571, :582-585): per cell and quadrature point one mult + one add per Phi entry of every
+        // trial term and per (test dof, test term); map_ops counts the add/mul nodes the unmemoised
+        // recursive eval_node (form.hpp:298-318) visits, i.e. the expression-tree size of each output
+        std::vector<long long> tree(static_cast<size_t>(p->n_map_nodes), 0);
+        for (int id = 0; id < p->n_map_nodes; ++id) {
+            const femgpu_map_node& n = p->map_nodes[id];
+            if (n.op == FEMGPU_OP_ADD || n.op == FEMGPU_OP_MUL) tree[id] = 1 + tree[n.a] + tree[n.b];
+        }
+        long long per_qp = 0, map = 0;
+        for (int i = 0; i < p->n_scalar; ++i) per_qp += static_cast<long long>(p->scalar_spaces[i].deriv_terms) * p->scalar_spaces[i].dofs;
+        for (int i = 0; i < p->n_vector; ++i) per_qp += static_cast<long long>(p->vector_spaces[i].deriv_terms) * p->vector_spaces[i].dofs;
+        per_qp += static_cast<long long>(p->test_dofs) * p->test_deriv_terms;
+        for (int k = 0; k < p->n_map_outputs; ++k) map += tree[p->map_outputs[k]];
+        const long long cq = static_cast<long long>(p->cell_count) * p->quad_points;
+        if (matvec_mults) *matvec_mults = cq * per_qp;
+        if (matvec_adds) *matvec_adds = cq * per_qp;
+        if (map_ops) *map_ops = cq * map;
+    });
+}
+
 femgpu_status femgpu_validate(const femgpu_problem* p) {
     return guard([&] { femgpu::validate_problem(p); });
 }
@@ -127,7 +153,7 @@ femgpu_status femgpu_emit_source(const femgpu_problem* p, const femgpu_schedule*
             if (s && s->scatter == FEMGPU_SCATTER_TILE) femgpu::host_tile_plan(p, sig, kp, s);
             if (s && s->scatter == FEMGPU_SCATTER_MACRO) femgpu::host_macro_plan(p, sig, kp, s);
             if (s && s->scatter == FEMGPU_SCATTER_ATOMIC && s->group_cells > 1) kp.G = s->group_cells;
-            if (s && s->reserved[3] == 4) kp.qloop = true;
+            if (s && (s->reserved[3] & 0xff) == 4) kp.qloop = true;
             if (s && s->scatter == FEMGPU_SCATTER_COLOR) kp.colour = true;
         }
         kp.strict = s && (s->reserved[0] & FEMGPU_FLAG_STRICT);
@@ -228,6 +254,29 @@ femgpu_status femgpu_action_device(femgpu_instance* h, const femgpu_schedule* s,
     });
 }
 
+femgpu_status femgpu_action_device_pipelined(femgpu_instance* h, const femgpu_schedule* s, double* y_dev,
+                                             double* y_next_dev, void* stream) {
+    return guard([&] {
+        auto& I = get(h);
+        if (!y_dev) femgpu::invalid("action_device_pipelined: null output buffer");
+        if (y_next_dev == y_dev) femgpu::invalid("action_device_pipelined: y_next must not alias y");
+        std::lock_guard<std::mutex> lk(I.mu);
+        FG_CUDA(cudaSetDevice(I.device));
+        const femgpu::KernelPlan kp = femgpu::plan_for(I, s);
+        femgpu::run_action_pipelined(I, kp, y_dev, y_next_dev, stream ? static_cast<cudaStream_t>(stream) : I.stream);
+    });
+}
+
+femgpu_status femgpu_check_finite(femgpu_instance* h, const femgpu_schedule* s, void* stream) {
+    return guard([&] {
+        auto& I = get(h);
+        std::lock_guard<std::mutex> lk(I.mu);
+        FG_CUDA(cudaSetDevice(I.device));
+        const femgpu::KernelPlan kp = femgpu::plan_for(I, s);
+        femgpu::check_failure(I, kp, stream ? static_cast<cudaStream_t>(stream) : I.stream);
+    });
+}
+
 femgpu_status femgpu_time_action(femgpu_instance* h, const femgpu_schedule* s, int32_t warmup, int32_t min_reps,
                                  double min_seconds, double* seconds) {
     return guard([&] {
@@ -258,20 +307,40 @@ femgpu_status femgpu_time_action(femgpu_instance* h, const femgpu_schedule* s, i
 }
 
 femgpu_status femgpu_time_steps(femgpu_instance* h, const femgpu_schedule* s, int32_t steps, double* seconds) {
+    return femgpu_time_steps_ex(h, s, steps, 0, seconds);
+}
+
+femgpu_status femgpu_time_steps_ex(femgpu_instance* h, const femgpu_schedule* s, int32_t steps, int32_t flags,
+                                   double* seconds) {
     return guard([&] {
         auto& I = get(h);
         if (steps < 1 || !seconds) femgpu::invalid("time_steps: steps >= 1 and an output are required");
         std::lock_guard<std::mutex> lk(I.mu);
         FG_CUDA(cudaSetDevice(I.device));
         const femgpu::KernelPlan kp = femgpu::plan_for(I, s);
+        const bool piped = (flags & FEMGPU_STEPS_PIPELINED) != 0;
+        double* ybuf[2] = {I.d_y, piped ? I.second_output() : I.d_y};
+        if (piped) {  // the first step's output is zeroed outside the timed region, as the previous step would
+            FG_CUDA(cudaMemsetAsync(ybuf[0], 0, sizeof(double) * static_cast<size_t>(I.output_size), I.stream));
+            femgpu::run_action_pipelined(I, kp, ybuf[0], ybuf[1], I.stream);  // warm (JIT of the zeroing variant)
+            FG_CUDA(cudaMemsetAsync(ybuf[0], 0, sizeof(double) * static_cast<size_t>(I.output_size), I.stream));
+        }
         FG_CUDA(cudaDeviceSynchronize());
         FG_CUDA(cudaEventRecord(I.ev0, I.stream));
-        for (int i = 0; i < steps; ++i) femgpu::run_action(I, kp, I.d_y, I.stream);
+        for (int i = 0; i < steps; ++i) {
+            if (piped)
+                femgpu::run_action_pipelined(I, kp, ybuf[i & 1], ybuf[(i + 1) & 1], I.stream);
+            else
+                femgpu::run_action(I, kp, I.d_y, I.stream);
+        }
         FG_CUDA(cudaEventRecord(I.ev1, I.stream));
         FG_CUDA(cudaEventSynchronize(I.ev1));
         FG_CUDA(cudaDeviceSynchronize());
         float ms = 0.f;
         FG_CUDA(cudaEventElapsedTime(&ms, I.ev0, I.ev1));
+        if (piped && ((steps - 1) & 1))  // the last step wrote the second buffer: device_output shows it
+            FG_CUDA(cudaMemcpyAsync(I.d_y, ybuf[1], sizeof(double) * static_cast<size_t>(I.output_size),
+                                    cudaMemcpyDeviceToDevice, I.stream));
         femgpu::check_failure(I, kp, I.stream);
         *seconds = ms * 1e-3;
     });

@@ -420,6 +420,12 @@ const char* kPrelude = R"(// generated by femgpu (emit.cpp) for sm_100a
 #define NF(v) ((((unsigned)__double2hiint(v)) & 0x7ff00000u) == 0x7ff00000u)
 // acc += a*b exactly as the reference writes it; contracted to DFMA unless --fmad=false
 #define FMA(a, b, acc) ((acc) + (a) * (b))
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" :: "l"(p)); }
+__device__ __forceinline__ int ldidx(const int* p) {
+  int v;
+  asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
 )";
 
 }  // namespace
@@ -496,7 +502,7 @@ std::string KernelPlan::key() const {
     std::ostringstream s;
     s << int(family) << "/" << basis << "/" << block << "/" << tile_cells << "/" << Nc << "x" << Nwi << "/" << TQ << "/"
       << Ter << "/" << Tqr << "/" << Tqc << "/" << strict << "/" << min_blocks << "/G" << G << "/ms" << mstage << "/ys" << ysmem
-      << "/qm" << qmajor << "/ql" << qloop << "/col" << colour << "/zf" << zfused;
+      << "/qm" << qmajor << "x" << msplit << "o" << qmopt << "/ql" << qloop << "/col" << colour << "/zf" << zfused;
     for (int t : Tcs) s << "s" << t;
     for (int t : Tcv) s << "v" << t;
     for (size_t g = 0; g < group_cap.size(); ++g) s << "g" << group_entries[g] << ":" << group_cap[g];
@@ -515,11 +521,13 @@ EmitResult emit_dmma(const Signature& sig, const KernelPlan& kp);  // below
 
 // Fused zeroing (pipeline.cpp overlapped_zero_action): every CTA clears its share of the y rows
 // [zp, zp + zn) before any early exit; a launch never writes those rows itself.
+// Streaming stores (st.global.cs, evict-first): the zeroed rows are not read by this launch, so they
+// must not displace the gathered lines in L2.
 const char* kZeroPrologue =
     "if (P.zn > 0) {\n"
     "  const long long zper = (P.zn + gridDim.x - 1) / gridDim.x, z0 = (long long)blockIdx.x * zper;\n"
     "  const long long z1 = min(z0 + zper, P.zn);\n"
-    "  for (long long i = z0 + threadIdx.x; i < z1; i += blockDim.x) P.zp[i] = 0.0;\n"
+    "  for (long long i = z0 + threadIdx.x; i < z1; i += blockDim.x) __stcs(P.zp + i, 0.0);\n"
     "}\n";
 
 namespace {
@@ -1111,6 +1119,67 @@ void emit_macro_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const
     o.line("}");
 }
 
+// Cell-invariant map nodes the quadrature-point pass reads (operands of q-dependent ADD/MUL nodes,
+// or outputs), constants excepted: the macro q-major kernel parks them in a thread-private column.
+std::vector<int> macro_hoisted_nodes(const Signature& sig, const MapUse& use) {
+    std::set<int> nd;
+    for (size_t id = 0; id < sig.nodes.size(); ++id) {
+        if (!use.live[id] || !use.qdep[id]) continue;
+        const MapNode& n = sig.nodes[id];
+        if (n.op == FEMGPU_OP_ADD || n.op == FEMGPU_OP_MUL) {
+            if (!use.qdep[n.a]) nd.insert(n.a);
+            if (!use.qdep[n.b]) nd.insert(n.b);
+        }
+    }
+    for (int out : sig.outputs)
+        if (!use.qdep[out]) nd.insert(out);
+    std::vector<int> stored;
+    for (int id : nd)
+        if (sig.nodes[id].op != FEMGPU_OP_CONSTANT) stored.push_back(id);
+    return stored;
+}
+
+// Per-thread shared-memory staging of the macro q-major pipeline (qmopt bit 5): one row of the
+// group's gathered doubles (odd row length: conflict-free 8-byte accesses) and two buffers of its
+// unique indices ([buffer][index][thread] columns).
+struct MacroStageVal {
+    std::string name, arr;
+    int slot = 0, k = 0, stride = 1, comp = 0;
+};
+struct MacroStage {
+    std::vector<std::pair<int, int>> idx;  // (map group, unique) per staged index
+    std::vector<MacroStageVal> vals;
+    int row = 1, nidx = 0;
+    long long bytes(int block) const { return (8LL * row + 8LL * nidx) * block; }
+};
+MacroStage macro_stage_plan(const Signature& sig, const KernelPlan& kp) {
+    MacroStage M;
+    std::set<int> gathered;
+    for (int i = 0; i < sig.ns(); ++i) gathered.insert(kp.sgroup[i]);
+    for (int i = 0; i < sig.nv(); ++i) gathered.insert(kp.vgroup[i]);
+    if (sig.affine) gathered.insert(kp.cgroup);
+    const int D = sig.dim;
+    int slot = 0;
+    for (int g : gathered)
+        for (int u = 0; u < kp.group_cap[g]; ++u) {
+            const int k = static_cast<int>(M.idx.size());
+            M.idx.push_back({g, u});
+            for (int i = 0; i < sig.ns(); ++i)
+                if (kp.sgroup[i] == g) M.vals.push_back({"xg" + std::to_string(i) + "_" + std::to_string(u), "P.x" + std::to_string(i), slot++, k, 1, 0});
+            for (int i = 0; i < sig.nv(); ++i)
+                if (kp.vgroup[i] == g)
+                    for (int c : std::set<int>(sig.vcomps[i].begin(), sig.vcomps[i].end()))
+                        M.vals.push_back({"vg" + std::to_string(i) + "_" + std::to_string(u) + "_" + std::to_string(c),
+                                          "P.v" + std::to_string(i), slot++, k, vec_stride(D), c});
+            if (sig.affine && kp.cgroup == g)
+                for (int c = 0; c < D; ++c)
+                    M.vals.push_back({"Xg" + std::to_string(u) + "_" + std::to_string(c), "P.X", slot++, k, vec_stride(D), c});
+        }
+    M.row = slot | 1;
+    M.nidx = static_cast<int>(M.idx.size());
+    return M;
+}
+
 // Macro-elements, quadrature-point-major ("qmajor"): the G cells of a group are interleaved at
 // statement level inside each quadrature point, so every tabulation operand (LDCU from the
 // constant bank, or an LDS) is loaded once for the G cells instead of once per cell (the cell-major
@@ -1124,12 +1193,13 @@ void emit_macro_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const
 void emit_macro_qmajor_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const MapUse& use,
                               const std::string& name, long long smem_tab_off, long long hsmem_off) {
     const int D = sig.dim, G = kp.G, Q = sig.Q;
+    const int SPL = std::max(1, kp.msplit);
     auto pat = [&](int g, int s, int j) { return kp.mpat[g][static_cast<size_t>(s) * kp.group_entries[g] + j]; };
     auto TAB = [&](const std::string& idx) {
         if (kp.basis == kBasisGlobal) return "__ldg(&P.tabg[" + idx + "])";
         return kp.basis == FEMGPU_BASIS_CONST ? "P.tab[" + idx + "]" : "sT[" + idx + "]";
     };
-    // cell-invariant nodes the quadrature part reads
+    const std::vector<int> stored = macro_hoisted_nodes(sig, use);
     std::vector<int> need;
     {
         std::set<int> nd;
@@ -1145,9 +1215,6 @@ void emit_macro_qmajor_kernel(Out& o, const Signature& sig, const KernelPlan& kp
             if (!use.qdep[out]) nd.insert(out);
         need.assign(nd.begin(), nd.end());
     }
-    std::vector<int> stored;
-    for (int id : need)
-        if (sig.nodes[id].op != FEMGPU_OP_CONSTANT) stored.push_back(id);
     const int NH = static_cast<int>(stored.size());
     o.line("");
     o.line("extern \"C\" __global__ void __launch_bounds__(" + S(kp.block) + (kp.min_blocks > 1 ? ", " + S(kp.min_blocks) : "") +
@@ -1161,162 +1228,299 @@ void emit_macro_qmajor_kernel(Out& o, const Signature& sig, const KernelPlan& kp
         o.line("for (int i = threadIdx.x; i < " + S(sig.tab_size) + "; i += blockDim.x) sT[i] = P.tabg[i];");
         o.line("__syncthreads();");
     }
-    o.line("double* const sh_base = reinterpret_cast<double*>(smraw + " + S(hsmem_off) + ") + threadIdx.x; (void)sh_base;");
-    o.line("#define SH(k) sh_base[(k) * " + S(kp.block) + "]");
-    o.line("const int grp = P.cell0 / " + S(G) + " + blockIdx.x * " + S(kp.block) + " + threadIdx.x;");
-    o.line("if (grp >= P.n_cells / " + S(G) + ") return;");
-    o.line("const size_t NG = (size_t)P.n_groups;");
+    // qmopt bit 0: the hoisted column is read back from shared memory (volatile: the compiler may
+    // not forward the stored values into registers across the quadrature loop)
+    if (kp.qmopt & 1) {
+        o.line("volatile double* const sh_base = reinterpret_cast<volatile double*>(smraw + " + S(hsmem_off) + ") + threadIdx.x;");
+        o.line("#define SH(k) sh_base[(k) * " + S(kp.block) + "]");
+    } else {  // registers (constant indices): the compiler keeps them live across the quadrature loop
+        o.line("double shr[" + S(std::max<long long>(1, static_cast<long long>(stored.size()) * ((G + SPL - 1) / SPL))) + "];");
+        o.line("#define SH(k) shr[k]");
+    }
+    if (SPL == 1) {
+        if (!(kp.qmopt & 96)) o.line("const int grp = P.cell0 / " + S(G) + " + blockIdx.x * " + S(kp.block) + " + threadIdx.x;");
+    } else {
+        // split groups: warp w computes cell subset (w % SPL) of 32 consecutive groups; the warps of
+        // one group sit in the same CTA, so the nodes their subsets share hit in L1
+        o.line("const int wid = threadIdx.x >> 5, sub = wid % " + S(SPL) + ";");
+        o.line("const int grp = P.cell0 / " + S(G) + " + (blockIdx.x * " + S(kp.block / 32 / SPL) + " + wid / " + S(SPL) +
+               ") * 32 + (threadIdx.x & 31);");
+    }
     std::set<int> gathered;
     for (int i = 0; i < sig.ns(); ++i) gathered.insert(kp.sgroup[i]);
     for (int i = 0; i < sig.nv(); ++i) gathered.insert(kp.vgroup[i]);
     if (sig.affine) gathered.insert(kp.cgroup);
-    // ---- gathers: every unique node of the group once (16-byte loads of padded vector nodes)
-    for (int g : gathered)
-        for (int u = 0; u < kp.group_cap[g]; ++u) {
-            o.line("const int ig" + S(g) + "_" + S(u) + " = __ldg(&P.gidx" + S(g) + "[" + S(u) + " * NG + grp]);");
-            for (int i = 0; i < sig.ns(); ++i)
-                if (kp.sgroup[i] == g)
-                    o.line("const double xg" + S(i) + "_" + S(u) + " = __ldg(&P.x" + S(i) + "[ig" + S(g) + "_" + S(u) + "]);");
-            auto node_loads = [&](const std::string& dst, const std::string& arr, const std::set<int>& comps) {
-                const std::string base = arr + " + (size_t)ig" + S(g) + "_" + S(u) + " * " + S(vec_stride(D));
-                const bool pair = D >= 2 && comps.count(0) && comps.count(1);
-                if (pair) {
-                    o.line("const double2 " + dst + "_01 = __ldg(reinterpret_cast<const double2*>(" + base + "));");
-                    o.line("const double " + dst + "_0 = " + dst + "_01.x, " + dst + "_1 = " + dst + "_01.y;");
-                }
-                for (int c : comps)
-                    if (!pair || c >= 2) o.line("const double " + dst + "_" + S(c) + " = __ldg(" + base + " + " + S(c) + ");");
-            };
-            for (int i = 0; i < sig.nv(); ++i)
-                if (kp.vgroup[i] == g) node_loads("vg" + S(i) + "_" + S(u), "P.v" + S(i), std::set<int>(sig.vcomps[i].begin(), sig.vcomps[i].end()));
-            if (sig.affine && kp.cgroup == g) {
-                std::set<int> comps;
-                for (int c = 0; c < D; ++c) comps.insert(c);
-                node_loads("Xg" + S(u), "P.X", comps);
-            }
-        }
-    o.line("bool nf = false;");
-    // ---- per cell: geometry + cell-invariant nodes -> thread-private smem column
-    for (int sc = 0; sc < G; ++sc) {
-        o.line("{ // geometry of cell " + S(sc));
-        o.ind++;
-        if (sig.affine) {
-            for (int j = 0; j < sig.coord_dofs; ++j)
-                for (int c = 0; c < D; ++c)
-                    o.line("const double " + nm("X", j, c) + " = " + nm("Xg", pat(kp.cgroup, sc, j), c) + ";");
-            for (int c = 0; c < D; ++c)
-                for (int r = 0; r < D; ++r)
-                    o.line("const double " + nm("J", r, c) + " = " + nm("X", c + 1, r) + " - " + nm("X", 0, r) + ";");
-            if (D == 1) o.line("const double det = J0_0;");
-            if (D == 2) o.line("const double det = J0_0 * J1_1 - J0_1 * J1_0;");
-            if (D == 3)
-                o.line("const double det = J0_0 * (J1_1 * J2_2 - J1_2 * J2_1) - J0_1 * (J1_0 * J2_2 - J1_2 * J2_0) + "
-                       "J0_2 * (J1_0 * J2_1 - J1_1 * J2_0);");
-            if (use.uses_inv) {
-                std::ostringstream gi;
-                if (D == 1) gi << "const double Ji0_0 = 1.0 / det;";
-                if (D == 2) gi << "const double Ji0_0 = J1_1 / det, Ji0_1 = -J0_1 / det, Ji1_0 = -J1_0 / det, Ji1_1 = J0_0 / det;";
-                if (D == 3)
-                    gi << "const double Ji0_0 = (J1_1*J2_2 - J1_2*J2_1) / det, Ji0_1 = (J0_2*J2_1 - J0_1*J2_2) / det, "
-                          "Ji0_2 = (J0_1*J1_2 - J0_2*J1_1) / det, Ji1_0 = (J1_2*J2_0 - J1_0*J2_2) / det, "
-                          "Ji1_1 = (J0_0*J2_2 - J0_2*J2_0) / det, Ji1_2 = (J0_2*J1_0 - J0_0*J1_2) / det, "
-                          "Ji2_0 = (J1_0*J2_1 - J1_1*J2_0) / det, Ji2_1 = (J0_1*J2_0 - J0_0*J2_1) / det, "
-                          "Ji2_2 = (J0_0*J1_1 - J0_1*J1_0) / det;";
-                o.line(gi.str());
-            }
-            o.line("nf = nf | NF(det);");
-        }
-        emit_nodes(o, sig, use, false, "0", TAB);
-        for (int h = 0; h < NH; ++h) o.line("SH(" + S(sc * NH + h) + ") = n" + S(stored[h]) + ";");
-        o.ind--;
+    const int gt = kp.tgroup;
+    // qmopt bit 5: persistent CTAs with a two-stage cp.async pipeline per thread: while group g
+    // computes, the next group's gathered values (and the one after's indices) stream into a
+    // thread-private shared-memory row, so neither gather hop is exposed
+    const bool staged = (kp.qmopt & 32) != 0 && SPL == 1;
+    const bool persistent = !staged && (kp.qmopt & 64) != 0 && SPL == 1;
+    const MacroStage MS = macro_stage_plan(sig, kp);
+    if (staged) {
+        o.line("const int gend = P.n_cells / " + S(G) + ";");
+        o.line("const size_t NG = (size_t)P.n_groups;");
+        o.line("const int gstride = gridDim.x * " + S(kp.block) + ";");
+        o.line("double* const sv = reinterpret_cast<double*>(smraw + " + S(kp.stage_off) + ") + threadIdx.x * " + S(MS.row) + ";");
+        o.line("int* const si = reinterpret_cast<int*>(smraw + " + S(kp.stage_off + 8LL * MS.row * kp.block) + ") + threadIdx.x;");
+        o.line("#define SI(b, k) si[((b) * " + S(MS.nidx) + " + (k)) * " + S(kp.block) + "]");
+        auto idx_copies = [&](const std::string& b, const std::string& g) {
+            for (size_t k = 0; k < MS.idx.size(); ++k)
+                o.line("cp4(&SI(" + b + ", " + S(k) + "), &P.gidx" + S(MS.idx[k].first) + "[" + S(MS.idx[k].second) + " * NG + " + g + "]);");
+        };
+        auto val_copies = [&](const std::string& b) {
+            for (const auto& v : MS.vals)
+                o.line("cp8(sv + " + S(v.slot) + ", " + v.arr + " + (size_t)SI(" + b + ", " + S(v.k) + ") * " + S(v.stride) + " + " + S(v.comp) + ");");
+        };
+        o.line("int grp = P.cell0 / " + S(G) + " + blockIdx.x * " + S(kp.block) + " + threadIdx.x;");
+        o.line("if (grp >= gend) return;");
+        idx_copies("0", "grp");
+        o.line("cp_commit(); cp_wait_all();");
+        val_copies("0");
+        o.line("if (grp + gstride < gend) {");
+        idx_copies("1", "grp + gstride");
         o.line("}");
-    }
-    {
-        std::string l = "double";
-        for (int u = 0; u < kp.group_cap[kp.tgroup]; ++u) l += std::string(u ? "," : "") + " ya" + S(u) + " = 0.0";
-        o.line(l + ";");
-    }
-    // ---- quadrature points: statements interleaved over the G cells
-    for (int q = 0; q < Q; ++q) {
-        o.line("{ // quadrature point " + S(q));
+        o.line("cp_commit(); cp_wait_all();");
+        o.line("int buf = 1;");
+        o.line("for (; grp < gend; grp += gstride, buf ^= 1) {");
         o.ind++;
-        // evaluation
-        for (int i = 0; i < sig.ns(); ++i)
-            for (int t = 0; t < sig.sterms[i]; ++t) {
-                const long long base = sig.phi_off_s[i] + static_cast<long long>(t) * Q * sig.sdofs[i] + static_cast<long long>(q) * sig.sdofs[i];
-                for (int sc = 0; sc < G; ++sc) o.line("double " + nm("s", i, t) + "_c" + S(sc) + ";");
-                for (int j = 0; j < sig.sdofs[i]; ++j) {
-                    std::string l = "{ const double tb = " + TAB(S(base + j)) + ";";
-                    for (int sc = 0; sc < G; ++sc) {
-                        const std::string v = nm("s", i, t) + "_c" + S(sc), u = nm("xg", i, pat(kp.sgroup[i], sc, j));
-                        l += j == 0 ? " " + v + " = tb * " + u + ";" : " " + v + " = FMA(tb, " + u + ", " + v + ");";
-                    }
-                    o.line(l + " }");
-                }
-            }
-        for (int i = 0; i < sig.nv(); ++i)
-            for (int t = 0; t < sig.vterms[i]; ++t) {
-                const long long base = sig.phi_off_v[i] + static_cast<long long>(t) * Q * sig.vdofs[i] + static_cast<long long>(q) * sig.vdofs[i];
-                const int comp = sig.vcomps[i][t];
-                for (int sc = 0; sc < G; ++sc) o.line("double " + nm("t", i, t) + "_c" + S(sc) + ";");
-                for (int j = 0; j < sig.vdofs[i]; ++j) {
-                    std::string l = "{ const double tb = " + TAB(S(base + j)) + ";";
-                    for (int sc = 0; sc < G; ++sc) {
-                        const std::string v = nm("t", i, t) + "_c" + S(sc), w = nm("vg", i, pat(kp.vgroup[i], sc, j), comp);
-                        l += j == 0 ? " " + v + " = tb * " + w + ";" : " " + v + " = FMA(tb, " + w + ", " + v + ");";
-                    }
-                    o.line(l + " }");
-                }
-            }
-        // map per cell
-        for (int sc = 0; sc < G; ++sc) {
-            for (int k = 0; k < sig.Tw; ++k) o.line("double e" + S(k) + "_c" + S(sc) + ";");
-            o.line("{");
+    } else if (persistent) {
+        // qmopt bit 6: persistent grid-stride loop over groups, so a group's red.add scatter drains
+        // while the thread already computes its next group (no drain stall at thread exit);
+        // bit 7: the next group's index lines are prefetched into L2 one iteration ahead
+        o.line("const int gend = P.n_cells / " + S(G) + ";");
+        o.line("const size_t NG = (size_t)P.n_groups;");
+        o.line("const int gstride = gridDim.x * " + S(kp.block) + ";");
+        o.line("for (int grp = P.cell0 / " + S(G) + " + blockIdx.x * " + S(kp.block) + " + threadIdx.x; grp < gend; grp += gstride) {");
+        o.ind++;
+        if (kp.qmopt & 128) {
+            o.line("if (grp + gstride < gend) {");
+            for (int g : gathered)
+                for (int u = 0; u < kp.group_cap[g]; ++u)
+                    o.line("  prefetch_l2(&P.gidx" + S(g) + "[" + S(u) + " * NG + grp + gstride]);");
+            o.line("}");
+        }
+    } else {
+        o.line("if (grp >= P.n_cells / " + S(G) + ") return;");
+        o.line("const size_t NG = (size_t)P.n_groups;");
+    }
+    for (int part = 0; part < SPL; ++part) {
+        const int c0 = part * G / SPL, c1 = (part + 1) * G / SPL;
+        if (SPL > 1) {
+            o.line(std::string(part ? "} else " : "") + (part + 1 < SPL ? "if (sub == " + S(part) + ") {" : "{") +
+                   " // cells " + S(c0) + ".." + S(c1 - 1) + " of the group");
             o.ind++;
-            std::string unused;
-            for (int i = 0; i < sig.ns(); ++i)
-                for (int t = 0; t < sig.sterms[i]; ++t) {
-                    o.line("const double " + nm("s", i, t) + " = " + nm("s", i, t) + "_c" + S(sc) + ";");
-                    if (!use.sd_used.count({i, t})) unused += " | NF(" + nm("s", i, t) + ")";
+        }
+        // unique nodes of each map group read by this subset of cells
+        auto used = [&](int g, int u) {
+            const int E = kp.group_entries[g];
+            for (int sc = c0; sc < c1; ++sc)
+                for (int j = 0; j < E; ++j)
+                    if (pat(g, sc, j) == u) return true;
+            return false;
+        };
+        // ---- gathers: every unique node of the subset once (16-byte loads of padded vector nodes)
+        if (staged) {
+            for (const auto& v : MS.vals) o.line("const double " + v.name + " = sv[" + S(v.slot) + "];");
+            o.line("if (grp + gstride < gend) {");
+            o.ind++;
+            for (const auto& v : MS.vals)
+                o.line("cp8(sv + " + S(v.slot) + ", " + v.arr + " + (size_t)SI(buf, " + S(v.k) + ") * " + S(v.stride) + " + " +
+                       S(v.comp) + ");");
+            o.line("if (grp + 2 * gstride < gend) {");
+            for (size_t k = 0; k < MS.idx.size(); ++k)
+                o.line("  cp4(&SI(buf ^ 1, " + S(k) + "), &P.gidx" + S(MS.idx[k].first) + "[" + S(MS.idx[k].second) +
+                       " * NG + grp + 2 * gstride]);");
+            o.line("}");
+            o.ind--;
+            o.line("}");
+            o.line("cp_commit();");
+        }
+        for (int g : gathered)
+            for (int u = 0; u < kp.group_cap[g]; ++u) {
+                if (!used(g, u) || staged) continue;
+                o.line("const int ig" + S(g) + "_" + S(u) + " = __ldg(&P.gidx" + S(g) + "[" + S(u) + " * NG + grp]);");
+                for (int i = 0; i < sig.ns(); ++i)
+                    if (kp.sgroup[i] == g)
+                        o.line("const double xg" + S(i) + "_" + S(u) + " = __ldg(&P.x" + S(i) + "[ig" + S(g) + "_" + S(u) + "]);");
+                auto node_loads = [&](const std::string& dst, const std::string& arr, const std::set<int>& comps) {
+                    const std::string base = arr + " + (size_t)ig" + S(g) + "_" + S(u) + " * " + S(vec_stride(D));
+                    const bool pair = D >= 2 && comps.count(0) && comps.count(1);
+                    if (pair) {
+                        o.line("const double2 " + dst + "_01 = __ldg(reinterpret_cast<const double2*>(" + base + "));");
+                        o.line("const double " + dst + "_0 = " + dst + "_01.x, " + dst + "_1 = " + dst + "_01.y;");
+                    }
+                    for (int c : comps)
+                        if (!pair || c >= 2) o.line("const double " + dst + "_" + S(c) + " = __ldg(" + base + " + " + S(c) + ");");
+                };
+                for (int i = 0; i < sig.nv(); ++i)
+                    if (kp.vgroup[i] == g) node_loads("vg" + S(i) + "_" + S(u), "P.v" + S(i), std::set<int>(sig.vcomps[i].begin(), sig.vcomps[i].end()));
+                if (sig.affine && kp.cgroup == g) {
+                    std::set<int> comps;
+                    for (int c = 0; c < D; ++c) comps.insert(c);
+                    node_loads("Xg" + S(u), "P.X", comps);
                 }
-            for (int i = 0; i < sig.nv(); ++i)
-                for (int t = 0; t < sig.vterms[i]; ++t) {
-                    o.line("const double " + nm("t", i, t) + " = " + nm("t", i, t) + "_c" + S(sc) + ";");
-                    if (!use.vd_used.count({i, t})) unused += " | NF(" + nm("t", i, t) + ")";
+            }
+        o.line("bool nf = false;");
+        // ---- per cell: geometry + cell-invariant nodes -> thread-private smem column
+        for (int sc = c0; sc < c1; ++sc) {
+            o.line("{ // geometry of cell " + S(sc));
+            o.ind++;
+            if (sig.affine) {
+                for (int j = 0; j < sig.coord_dofs; ++j)
+                    for (int c = 0; c < D; ++c)
+                        o.line("const double " + nm("X", j, c) + " = " + nm("Xg", pat(kp.cgroup, sc, j), c) + ";");
+                for (int c = 0; c < D; ++c)
+                    for (int r = 0; r < D; ++r)
+                        o.line("const double " + nm("J", r, c) + " = " + nm("X", c + 1, r) + " - " + nm("X", 0, r) + ";");
+                if (D == 1) o.line("const double det = J0_0;");
+                if (D == 2) o.line("const double det = J0_0 * J1_1 - J0_1 * J1_0;");
+                if (D == 3)
+                    o.line("const double det = J0_0 * (J1_1 * J2_2 - J1_2 * J2_1) - J0_1 * (J1_0 * J2_2 - J1_2 * J2_0) + "
+                           "J0_2 * (J1_0 * J2_1 - J1_1 * J2_0);");
+                if (use.uses_inv) {
+                    std::ostringstream gi;
+                    if (D == 1) gi << "const double Ji0_0 = 1.0 / det;";
+                    if (D == 2) gi << "const double Ji0_0 = J1_1 / det, Ji0_1 = -J0_1 / det, Ji1_0 = -J1_0 / det, Ji1_1 = J0_0 / det;";
+                    if (D == 3)
+                        gi << "const double Ji0_0 = (J1_1*J2_2 - J1_2*J2_1) / det, Ji0_1 = (J0_2*J2_1 - J0_1*J2_2) / det, "
+                              "Ji0_2 = (J0_1*J1_2 - J0_2*J1_1) / det, Ji1_0 = (J1_2*J2_0 - J1_0*J2_2) / det, "
+                              "Ji1_1 = (J0_0*J2_2 - J0_2*J2_0) / det, Ji1_2 = (J0_2*J1_0 - J0_0*J1_2) / det, "
+                              "Ji2_0 = (J1_0*J2_1 - J1_1*J2_0) / det, Ji2_1 = (J0_1*J2_0 - J0_0*J2_1) / det, "
+                              "Ji2_2 = (J0_0*J1_1 - J0_1*J1_0) / det;";
+                    o.line(gi.str());
                 }
-            if (!unused.empty()) o.line("nf = nf" + unused + ";");
-            for (int h = 0; h < NH; ++h) o.line("const double n" + S(stored[h]) + " = SH(" + S(sc * NH + h) + ");");
-            for (int id : need)
-                if (sig.nodes[id].op == FEMGPU_OP_CONSTANT) o.line("const double n" + S(id) + " = " + lit(sig.nodes[id].value) + ";");
-            emit_nodes(o, sig, use, true, S(q), TAB);
-            for (int k = 0; k < sig.Tw; ++k) o.line("e" + S(k) + "_c" + S(sc) + " = n" + S(sig.outputs[k]) + ";");
+                o.line("nf = nf | NF(det);");
+            }
+            emit_nodes(o, sig, use, false, "0", TAB);
+            for (int h = 0; h < NH; ++h) o.line("SH(" + S((sc - c0) * NH + h) + ") = n" + S(stored[h]) + ";");
             o.ind--;
             o.line("}");
         }
-        // quadrature straight into the group's y accumulators, one Psi load for the G cells
-        for (int jw = 0; jw < sig.nW; ++jw)
-            for (int k = 0; k < sig.Tw; ++k) {
-                const long long idx = sig.psi_off + (static_cast<long long>(k) * sig.nW + jw) * Q + q;
-                std::string l = "{ const double tb = " + TAB(S(idx)) + ";";
-                for (int sc = 0; sc < G; ++sc) {
-                    const std::string ya = "ya" + S(pat(kp.tgroup, sc, jw));
-                    l += " " + ya + " = FMA(tb, e" + S(k) + "_c" + S(sc) + ", " + ya + ");";
+        {
+            std::string l;
+            for (int u = 0; u < kp.group_cap[gt]; ++u)
+                if (used(gt, u)) l += std::string(l.empty() ? "double" : ",") + " ya" + S(u) + " = 0.0";
+            o.line(l + ";");
+        }
+        // ---- quadrature points: statements interleaved over the subset's cells
+        // qmopt bit 4: the quadrature loop stays rolled (a Q-th of the code: instruction-cache misses
+        // stall the unrolled straight-line kernel); tabulation offsets become q-relative
+        const bool rolled = (kp.qmopt & 16) != 0;
+        auto QI = [&](long long base0, long long stride, int q) {
+            return rolled ? S(base0) + " + q * " + S(stride) : S(base0 + static_cast<long long>(q) * stride);
+        };
+        if (rolled) {
+            o.line("#pragma unroll 1");
+            o.line("for (int q = 0; q < " + S(Q) + "; ++q) {");
+            o.ind++;
+        }
+        for (int q = 0; q < (rolled ? 1 : Q); ++q) {
+            o.line("{ // quadrature point " + (rolled ? std::string("q") : S(q)));
+            o.ind++;
+            // evaluation
+            for (int i = 0; i < sig.ns(); ++i)
+                for (int t = 0; t < sig.sterms[i]; ++t) {
+                    const long long base = sig.phi_off_s[i] + static_cast<long long>(t) * Q * sig.sdofs[i];
+                    for (int sc = c0; sc < c1; ++sc) o.line("double " + nm("s", i, t) + "_c" + S(sc) + ";");
+                    for (int j = 0; j < sig.sdofs[i]; ++j) {
+                        std::string l = "{ const double tb = " + TAB(QI(base + j, sig.sdofs[i], q)) + ";";
+                        for (int sc = c0; sc < c1; ++sc) {
+                            const std::string v = nm("s", i, t) + "_c" + S(sc), u = nm("xg", i, pat(kp.sgroup[i], sc, j));
+                            l += j == 0 ? " " + v + " = tb * " + u + ";" : " " + v + " = FMA(tb, " + u + ", " + v + ");";
+                        }
+                        o.line(l + " }");
+                    }
                 }
-                o.line(l + " }");
+            for (int i = 0; i < sig.nv(); ++i)
+                for (int t = 0; t < sig.vterms[i]; ++t) {
+                    const long long base = sig.phi_off_v[i] + static_cast<long long>(t) * Q * sig.vdofs[i];
+                    const int comp = sig.vcomps[i][t];
+                    for (int sc = c0; sc < c1; ++sc) o.line("double " + nm("t", i, t) + "_c" + S(sc) + ";");
+                    for (int j = 0; j < sig.vdofs[i]; ++j) {
+                        std::string l = "{ const double tb = " + TAB(QI(base + j, sig.vdofs[i], q)) + ";";
+                        for (int sc = c0; sc < c1; ++sc) {
+                            const std::string v = nm("t", i, t) + "_c" + S(sc), w = nm("vg", i, pat(kp.vgroup[i], sc, j), comp);
+                            l += j == 0 ? " " + v + " = tb * " + w + ";" : " " + v + " = FMA(tb, " + w + ", " + v + ");";
+                        }
+                        o.line(l + " }");
+                    }
+                }
+            // map per cell
+            for (int sc = c0; sc < c1; ++sc) {
+                for (int k = 0; k < sig.Tw; ++k) o.line("double e" + S(k) + "_c" + S(sc) + ";");
+                o.line("{");
+                o.ind++;
+                std::string unused;
+                for (int i = 0; i < sig.ns(); ++i)
+                    for (int t = 0; t < sig.sterms[i]; ++t) {
+                        o.line("const double " + nm("s", i, t) + " = " + nm("s", i, t) + "_c" + S(sc) + ";");
+                        if (!use.sd_used.count({i, t})) unused += " | NF(" + nm("s", i, t) + ")";
+                    }
+                for (int i = 0; i < sig.nv(); ++i)
+                    for (int t = 0; t < sig.vterms[i]; ++t) {
+                        o.line("const double " + nm("t", i, t) + " = " + nm("t", i, t) + "_c" + S(sc) + ";");
+                        if (!use.vd_used.count({i, t})) unused += " | NF(" + nm("t", i, t) + ")";
+                    }
+                if (!unused.empty()) o.line("nf = nf" + unused + ";");
+                for (int h = 0; h < NH; ++h) o.line("const double n" + S(stored[h]) + " = SH(" + S((sc - c0) * NH + h) + ");");
+                for (int id : need)
+                    if (sig.nodes[id].op == FEMGPU_OP_CONSTANT) o.line("const double n" + S(id) + " = " + lit(sig.nodes[id].value) + ";");
+                emit_nodes(o, sig, use, true, rolled ? std::string("q") : S(q), TAB);
+                for (int k = 0; k < sig.Tw; ++k) o.line("e" + S(k) + "_c" + S(sc) + " = n" + S(sig.outputs[k]) + ";");
+                o.ind--;
+                o.line("}");
             }
+            // quadrature straight into the group's y accumulators, one Psi load for the subset's cells
+            for (int jw = 0; jw < sig.nW; ++jw)
+                for (int k = 0; k < sig.Tw; ++k) {
+                    const long long idx = sig.psi_off + (static_cast<long long>(k) * sig.nW + jw) * Q;
+                    std::string l = "{ const double tb = " + TAB(QI(idx, 1, q)) + ";";
+                    for (int sc = c0; sc < c1; ++sc) {
+                        const std::string ya = "ya" + S(pat(gt, sc, jw));
+                        l += " " + ya + " = FMA(tb, e" + S(k) + "_c" + S(sc) + ", " + ya + ");";
+                    }
+                    o.line(l + " }");
+                }
+            o.ind--;
+            o.line("}");
+        }
+        if (rolled) {
+            o.ind--;
+            o.line("}");
+        }
+        // ---- finiteness (any non-finite contribution reaches an accumulator) + scatter
+        {
+            std::string chk;
+            for (int u = 0; u < kp.group_cap[gt]; ++u)
+                if (used(gt, u)) chk += " | NF(ya" + S(u) + ")";
+            o.line("if (nf" + chk + ") atomicMin(P.bad, (unsigned long long)grp * " + S(G) + ");");
+        }
+        for (int u = 0; u < kp.group_cap[gt]; ++u) {
+            if (!used(gt, u)) continue;
+            // qmopt bit 1: reload the scatter indices (an opaque load the compiler cannot merge with
+            // the gather's) instead of keeping them live in registers across the quadrature loop
+            const std::string idx = ((kp.qmopt & 2) || staged) ? "ldidx(&P.gidx" + S(gt) + "[" + S(u) + " * NG + grp])"
+                                    : gathered.count(gt) ? "ig" + S(gt) + "_" + S(u)
+                                                         : "__ldg(&P.gidx" + S(gt) + "[" + S(u) + " * NG + grp])";
+            if (kp.qmopt & 4)  // timing experiment only (wrong results): plain store instead of red.add
+                o.line("P.y[" + idx + "] = ya" + S(u) + ";");
+            else if (kp.qmopt & 8)  // timing experiment only (wrong results): no scatter traffic
+                o.line("if (ya" + S(u) + " == 1234.5678) P.y[" + idx + "] = 0.0;");
+            else
+                o.line("atomicAdd(&P.y[" + idx + "], ya" + S(u) + ");");
+        }
+        if (SPL > 1) o.ind--;
+    }
+    if (SPL > 1) o.line("}");
+    if (staged) {
+        o.line("cp_wait_all();");
         o.ind--;
         o.line("}");
     }
-    // ---- finiteness (any non-finite contribution reaches an accumulator) + scatter
-    {
-        std::string chk;
-        for (int u = 0; u < kp.group_cap[kp.tgroup]; ++u) chk += " | NF(ya" + S(u) + ")";
-        o.line("if (nf" + chk + ") atomicMin(P.bad, (unsigned long long)grp * " + S(G) + ");");
-    }
-    const int gt = kp.tgroup;
-    for (int u = 0; u < kp.group_cap[gt]; ++u) {
-        const std::string idx = gathered.count(gt) ? "ig" + S(gt) + "_" + S(u) : "__ldg(&P.gidx" + S(gt) + "[" + S(u) + " * NG + grp])";
-        o.line("atomicAdd(&P.y[" + idx + "], ya" + S(u) + ");");
+    if (persistent) {
+        o.ind--;
+        o.line("}");
     }
     o.line("(void)CHECKED;");
     o.ind--;
@@ -1327,7 +1531,10 @@ const char* kAsync = R"(
 __device__ __forceinline__ void cp16(unsigned char* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src) : "memory");
 }
-__device__ __forceinline__ void cp8(unsigned char* dst, const void* src) {
+__device__ __forceinline__ void cp4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp8(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
@@ -1369,22 +1576,19 @@ EmitResult emit_kernel(const Signature& sig, const KernelPlan& kp) {
         const long long ysmem_off = static_cast<long long>(r.smem_bytes);
         if (kp.ysmem) r.smem_bytes += static_cast<size_t>(kp.group_cap[kp.tgroup]) * 8 * kp.block;
         if (kp.qmajor) {
-            // thread-private columns of the cell-invariant map nodes of the G cells
-            long long nh = 0;
-            for (size_t id = 0; id < sig.nodes.size(); ++id) {
-                if (!use.live[id] || use.qdep[id] || sig.nodes[id].op == FEMGPU_OP_CONSTANT) continue;
-                bool read = false;
-                for (size_t k = 0; k < sig.nodes.size() && !read; ++k) {
-                    const MapNode& n = sig.nodes[k];
-                    read = use.live[k] && use.qdep[k] && (n.op == FEMGPU_OP_ADD || n.op == FEMGPU_OP_MUL) &&
-                           (n.a == static_cast<int>(id) || n.b == static_cast<int>(id));
-                }
-                for (int out : sig.outputs) read = read || out == static_cast<int>(id);
-                if (read) ++nh;
-            }
+            // thread-private columns of the cell-invariant map nodes of one thread's cells
+            const long long nh = static_cast<long long>(macro_hoisted_nodes(sig, use).size());
+            const int spl = std::max(1, kp.msplit);
+            const long long cells_per_thread = (kp.G + spl - 1) / spl;
             const long long hoff = static_cast<long long>(al16(static_cast<long long>(r.smem_bytes)));
-            r.smem_bytes = static_cast<size_t>(hoff + nh * kp.G * 8 * kp.block);
-            emit_macro_qmajor_kernel(o, sig, kp, use, r.kernel, 0, hoff);
+            if (kp.qmopt & 1) r.smem_bytes = static_cast<size_t>(hoff + nh * cells_per_thread * 8 * kp.block);
+            KernelPlan kq = kp;
+            if ((kp.qmopt & 32) && spl == 1) {
+                o << kAsync;
+                kq.stage_off = static_cast<long long>(al16(static_cast<long long>(r.smem_bytes)));
+                r.smem_bytes = static_cast<size_t>(kq.stage_off + macro_stage_plan(sig, kp).bytes(kp.block));
+            }
+            emit_macro_qmajor_kernel(o, sig, kq, use, r.kernel, 0, hoff);
         } else {
             emit_macro_kernel(o, sig, kp, use, unroll_q, r.kernel, 0, ysmem_off);
         }

@@ -56,6 +56,7 @@ struct Signature {
 };
 
 Signature signature_from(const femgpu_problem* p);
+void dedupe_map(Signature& s);  // commutative value numbering of the map DAG (bit-identical values)
 
 // Device layout of vector inputs and coordinates: node-major with the components padded to a
 // 16-byte multiple (3D: [node][4]), so a node's components are one aligned 16 B + 8 B pair of
@@ -86,6 +87,7 @@ struct KernelPlan {
     bool breg = false;                 // DMMA: B fragments in registers (single quadrature chunk)
     bool zfused = false;               // run_action: y zeroing fused into slab launches (FEMGPU_FLAG_FUSED_ZERO)
     int zslabs = 0;                    // slabs for fused zeroing (reserved[0] >> 8; 0 = default)
+    bool pipe_memset = false;          // pipelined actions: memset the next output instead of in-kernel zeroing
     std::vector<int> group_entries, group_cap;   // per group: entries per cell, max unique per tile
     // MLT family (TilingParams)
     int Nc = 1, Nwi = 1, TQ = 1, Ter = 1, Tqr = 1, Tqc = 1;
@@ -96,6 +98,10 @@ struct KernelPlan {
     int mstage = 0;                       // 0: gathered values in registers; 1: cp.async into smem
     bool ysmem = false;                   // macro: y accumulators in thread-private smem columns (registers)
     bool qmajor = false;                  // macro: quadrature-point-major, statements interleaved over the G cells
+    int msplit = 1;                       // macro q-major: cells of a group split over this many warps
+    int qmopt = 0;                        // macro q-major: bit 0 hoisted column read from smem, bit 1 reload scatter
+                                          // indices, bit 4 rolled quadrature loop, bit 5 persistent cp.async staging
+    long long stage_off = 0;              // macro q-major staging: byte offset of the staging area (emitter-internal)
     bool qloop = false;                   // scpt: keep the quadrature loop rolled (I-cache / registers)
     bool colour = false;                  // scpt: one launch per cell colour, plain y updates (deterministic)
     std::vector<std::vector<int>> mpat;   // per map group: G*entries local indices
@@ -222,6 +228,11 @@ struct Instance {
     std::vector<std::vector<int32_t>> group_maps;  // host copies of distinct maps ([cell][entry])
     std::vector<int> group_global;
     double* d_y = nullptr;
+    double* d_y2 = nullptr;         // second output buffer of pipelined steps (femgpu_time_steps_ex)
+    double* second_output() {
+        if (!d_y2) d_y2 = alloc<double>(static_cast<size_t>(output_size));
+        return d_y2;
+    }
     int32_t* d_bad = nullptr;       // first failing cell (INT32_MAX = none)
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -280,6 +291,9 @@ void run_action_range(Instance& inst, const KernelPlan& kp, double* d_y, cudaStr
                       bool zero_y, cudaEvent_t after_zero = nullptr, double* zero_ptr = nullptr,
                       long long zero_n = 0);
 extern const char* kZeroPrologue;  // emit.cpp
+// Output-pipelined action: d_y is all zeros on entry; the action kernel also zeroes d_next (the next
+// step's output) in its prologue, so back-to-back steps need no separate memset (femgpu_action_device_pipelined).
+void run_action_pipelined(Instance& inst, const KernelPlan& kp, double* d_y, double* d_next, cudaStream_t stream);
 bool supports_cell_range(const KernelPlan& kp);
 int range_align(const KernelPlan& kp);
 // pipeline.cpp: y zeroing fused into slab-wise compute; false = not applicable

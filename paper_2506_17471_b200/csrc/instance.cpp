@@ -10,10 +10,12 @@
 //     global indices of every tile of consecutive cells (shared-with-another-tile
 //     flag in bit 31) and a uint16 tile-local [entry][cell] map.
 #include <algorithm>
+#include <atomic>
 #include <climits>
 #include <cstring>
 #include <numeric>
 #include <thread>
+#include <tuple>
 
 #include "femgpu_internal.hpp"
 
@@ -78,7 +80,47 @@ Signature signature_from(const femgpu_problem* p) {
     }
     s.outputs.assign(p->map_outputs, p->map_outputs + p->n_map_outputs);
     s.layout();
+    dedupe_map(s);
     return s;
+}
+
+// Value numbering of the map DAG: nodes that compute the same value bit for bit (same op on the
+// same operands, ADD/MUL operands in either order: IEEE + and * are commutative) are redirected to
+// their first occurrence.  The reference's recursive eval_node (form.hpp:298-318) re-evaluates
+// every occurrence, but each one yields identical bits, so the emitted SSA computes the same
+// values with fewer operations and fewer hoisted cell-invariant slots (the laplace metric J^T J
+// has 6 distinct entries, not 9).
+void dedupe_map(Signature& s) {
+    const int n = static_cast<int>(s.nodes.size());
+    std::vector<int> canon(n);
+    std::map<std::tuple<int, int, int, uint64_t>, int> seen;
+    for (int id = 0; id < n; ++id) {
+        MapNode& nd = s.nodes[id];
+        canon[id] = id;
+        int a = nd.a, b = nd.b;
+        uint64_t bits = 0;
+        if (nd.op == FEMGPU_OP_ADD || nd.op == FEMGPU_OP_MUL) {
+            if (a < 0 || b < 0 || a >= id || b >= id) continue;  // invalid DAG: validation reports it
+            a = canon[a];
+            b = canon[b];
+            nd.a = a;
+            nd.b = b;
+            if (a > b) std::swap(a, b);
+        } else if (nd.op == FEMGPU_OP_CONSTANT) {
+            std::memcpy(&bits, &nd.value, sizeof bits);
+            a = b = 0;
+        } else if (nd.op == FEMGPU_OP_DETERMINANT || nd.op == FEMGPU_OP_WEIGHT) {
+            a = b = 0;
+        }
+        auto key = std::make_tuple(nd.op, a, b, bits);
+        auto it = seen.find(key);
+        if (it != seen.end())
+            canon[id] = it->second;
+        else
+            seen.emplace(key, id);
+    }
+    for (int& o : s.outputs)
+        if (o >= 0 && o < n) o = canon[o];
 }
 
 // ProblemInstance::validate (form.hpp:416-434), same messages.
@@ -480,7 +522,7 @@ void resolve_dmma(const Signature& sig, KernelPlan& kp, const femgpu_schedule* s
     if (kp.Ter > kp.Nc / 8 || (kp.Nc / 8) % kp.Ter)
         fail(FEMGPU_E_INFEASIBLE, "dmma: joint m-blocks (eval_row_tile) must divide the m-blocks of a warp task");
     kp.Tqr = s->quad_row_tile > 0 ? 1 : 0;
-    kp.breg = s->reserved[3] == 1;  // B fragments in registers (honoured for a single quadrature chunk)
+    kp.breg = (s->reserved[3] & 0xff) == 1;  // B fragments in registers (honoured for a single quadrature chunk)
     const int q4 = (sig.Q + 3) / 4 * 4;
     if (s->quad_tile > 0) {
         kp.TQ = std::min(q4, (s->quad_tile + 3) / 4 * 4);
@@ -537,23 +579,20 @@ const MacroLayout& Instance::macro_layout(int G) {
             for (int k = 0; k < G * E; ++k)
                 pat[k] = static_cast<int>(std::lower_bound(u0.begin(), u0.end(), m[k]) - u0.begin());
             std::vector<int32_t> gidx(static_cast<size_t>(U) * ng);
-            bool ok = true;
+            std::atomic<bool> ok{true};  // shared by the worker threads (relaxed: a sticky flag)
             parallel_for(ng, [&](long long b, long long e) {
                 std::vector<int32_t> buf;
-                for (long long grp = b; grp < e && ok; ++grp) {
+                for (long long grp = b; grp < e && ok.load(std::memory_order_relaxed); ++grp) {
                     const int32_t* base = m.data() + grp * G * E;
                     buf.assign(base, base + static_cast<long long>(G) * E);
                     std::sort(buf.begin(), buf.end());
                     buf.erase(std::unique(buf.begin(), buf.end()), buf.end());
-                    if (static_cast<int>(buf.size()) != U) {
-                        ok = false;
+                    bool same = static_cast<int>(buf.size()) == U;
+                    for (int k = 0; same && k < G * E; ++k) same = buf[pat[k]] == base[k];
+                    if (!same) {
+                        ok.store(false, std::memory_order_relaxed);
                         break;
                     }
-                    for (int k = 0; k < G * E; ++k)
-                        if (buf[pat[k]] != base[k]) {
-                            ok = false;
-                            break;
-                        }
                     for (int u = 0; u < U; ++u) gidx[static_cast<size_t>(u) * ng + grp] = buf[u];
                 }
             });
@@ -571,6 +610,13 @@ const MacroLayout& Instance::macro_layout(int G) {
     auto& ref = *M;
     macros[G] = std::move(M);
     return ref;
+}
+
+// Split macro groups (q-major kernel): warp w computes cell subset w % split of 32 groups.
+void check_macro_split(KernelPlan& kp) {
+    if (kp.msplit < 1 || kp.msplit > kp.G) fail(FEMGPU_E_INFEASIBLE, "macro: split must be in [1, cells per group]");
+    if (kp.msplit > 1 && kp.block % (32 * kp.msplit))
+        fail(FEMGPU_E_INFEASIBLE, "macro: threads per CTA must be a multiple of 32 x split");
 }
 
 void host_macro_plan(const femgpu_problem* p, const Signature& sig, KernelPlan& kp, const femgpu_schedule* s) {
@@ -605,10 +651,13 @@ void host_macro_plan(const femgpu_problem* p, const Signature& sig, KernelPlan& 
     }
     kp.family = Family::Macro;
     kp.G = G;
-    kp.mstage = s->reserved[3] == 1 ? 1 : 0;
-    kp.ysmem = s->reserved[3] == 2;
-    kp.qmajor = s->reserved[3] == 3;
+    kp.mstage = (s->reserved[3] & 0xff) == 1 ? 1 : 0;
+    kp.ysmem = (s->reserved[3] & 0xff) == 2;
+    kp.qmajor = (s->reserved[3] & 0xff) == 3;
+    kp.msplit = kp.qmajor ? std::max(1, (s->reserved[3] >> 8) & 0xff) : 1;
+    kp.qmopt = kp.qmajor ? (s->reserved[3] >> 16) & 0xff : 0;
     kp.block = s->block_cells > 0 ? s->block_cells : 64;
+    check_macro_split(kp);
     const int reg_target = s->reserved[1] > 0 ? s->reserved[1] : 168;
     kp.min_blocks = std::max(1, std::min(16, 65536 / (kp.block * reg_target)));
     if (s->reserved[2] > 0) kp.min_blocks = s->reserved[2];
@@ -673,6 +722,7 @@ KernelPlan resolve_schedule(Instance& I, const femgpu_schedule* s) {
     KernelPlan kp = resolve_schedule_impl(I, s);
     kp.zfused = s && (s->reserved[0] & FEMGPU_FLAG_FUSED_ZERO) && supports_cell_range(kp);
     kp.zslabs = s ? (s->reserved[0] >> 8) & 0xff : 0;
+    kp.pipe_memset = s && (s->reserved[0] & FEMGPU_FLAG_PIPE_MEMSET);
     return kp;
 }
 
@@ -745,10 +795,13 @@ KernelPlan resolve_schedule_impl(Instance& I, const femgpu_schedule* s) {
             kp.family = Family::Macro;
             kp.basis = basis;
             kp.G = G;
-            kp.mstage = s->reserved[3] == 1 ? 1 : 0;
-            kp.ysmem = s->reserved[3] == 2;
-            kp.qmajor = s->reserved[3] == 3;
+            kp.mstage = (s->reserved[3] & 0xff) == 1 ? 1 : 0;
+            kp.ysmem = (s->reserved[3] & 0xff) == 2;
+            kp.qmajor = (s->reserved[3] & 0xff) == 3;
+            kp.msplit = kp.qmajor ? std::max(1, (s->reserved[3] >> 8) & 0xff) : 1;
+    kp.qmopt = kp.qmajor ? (s->reserved[3] >> 16) & 0xff : 0;
             kp.block = s->block_cells > 0 ? s->block_cells : 64;
+            check_macro_split(kp);
             const int reg_target = s->reserved[1] > 0 ? s->reserved[1] : 168;
             kp.min_blocks = std::max(1, std::min(16, 65536 / (kp.block * reg_target)));
             if (s->reserved[2] > 0) kp.min_blocks = s->reserved[2];
@@ -824,7 +877,7 @@ KernelPlan resolve_schedule_impl(Instance& I, const femgpu_schedule* s) {
     // SCPT with G independent cells per thread (group_cells with atomic scatter): shared
     // tabulation loads, more independent DFMA chains per thread
     kp.G = scatter == FEMGPU_SCATTER_ATOMIC && s->group_cells > 1 ? s->group_cells : 1;
-    kp.qloop = s->reserved[3] == 4;
+    kp.qloop = (s->reserved[3] & 0xff) == 4;
     if (kp.G > 8) fail(FEMGPU_E_INFEASIBLE, "schedule: at most 8 cells per thread in the SCPT family");
     if (s->reserved[2] > 0) kp.min_blocks = s->reserved[2];
     (void)int_dim;
@@ -949,6 +1002,20 @@ void run_action(Instance& I, const KernelPlan& kp, double* d_y, cudaStream_t str
     run_action_range(I, kp, d_y, stream, 0, I.cells, true, after_zero);
 }
 
+void run_action_pipelined(Instance& I, const KernelPlan& plan, double* d_y, double* d_next, cudaStream_t stream) {
+    const size_t bytes = sizeof(double) * static_cast<size_t>(I.output_size);
+    if (!supports_cell_range(plan) || !d_next || plan.pipe_memset) {  // plain memset of the next output
+        run_action_range(I, plan, d_y, stream, 0, I.cells, false);
+        if (d_next) FG_CUDA(cudaMemsetAsync(d_next, 0, bytes, stream));
+        return;
+    }
+    KernelPlan kp = plan;
+    kp.zfused = true;  // the zeroing prologue (kZeroPrologue) clears d_next while the action runs
+    kp.zslabs = 0;
+    kp.pipe_memset = false;
+    run_action_range(I, kp, d_y, stream, 0, I.cells, false, nullptr, d_next, I.output_size);
+}
+
 void run_action_range(Instance& I, const KernelPlan& kp, double* d_y, cudaStream_t stream, int c_begin, int c_end,
                       bool zero_y, cudaEvent_t after_zero, double* zero_ptr, long long zero_n) {
     auto mod = I.module_for(kp);
@@ -969,8 +1036,11 @@ void run_action_range(Instance& I, const KernelPlan& kp, double* d_y, cudaStream
         grid = (static_cast<long long>(I.cells) + kp.Nc - 1) / kp.Nc;
     else if (kp.family == Family::Tile)
         grid = std::min<long long>(L->n_tiles, static_cast<long long>(mod->sms) * std::max(1, mod->occupancy));
-    else if (kp.family == Family::Macro)
-        grid = (ncell / kp.G + kp.block - 1) / kp.block;
+    else if (kp.family == Family::Macro) {
+        grid = (ncell / kp.G + kp.block / kp.msplit - 1) / (kp.block / kp.msplit);
+        if ((kp.qmopt & 96) && kp.msplit == 1)  // persistent kernels: one wave of resident CTAs
+            grid = std::min<long long>(grid, static_cast<long long>(mod->sms) * std::max(1, mod->occupancy));
+    }
     else if (kp.family == Family::Dmma)
         grid = std::min<long long>(((ncell + kp.Nc - 1) / kp.Nc + kp.block / 32 - 1) / (kp.block / 32),
                                    static_cast<long long>(mod->sms) * std::max(1, mod->occupancy));

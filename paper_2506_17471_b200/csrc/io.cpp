@@ -435,12 +435,17 @@ femgpu_owned_problem* load_problem(std::istream& is) {
 // save_candidate / load_candidate (io.hpp:407-460); B200 kinds and knobs as extra keys.
 void save_schedule(std::ostream& os, const femgpu_schedule* s, int n_scalar, int n_vector) {
     os << "format_version: " << kFormatVersion << "\n";
-    if (s->kind == FEMGPU_SCPT && s->basis == 0 && s->scatter == 0 && s->block_cells == 0 && s->group_cells == 0) {
+    // the reference's own kinds only when no B200 knob is set: reserved[] carries the strict
+    // (bitwise) flag, register targets, kernel variants and zeroing decisions, which must survive a
+    // save/load round trip (a tuned decision replays the kernel that was timed)
+    const bool plain = s->reserved[0] == 0 && s->reserved[1] == 0 && s->reserved[2] == 0 && s->reserved[3] == 0;
+    if (plain && s->kind == FEMGPU_SCPT && s->basis == 0 && s->scatter == 0 && s->block_cells == 0 &&
+        s->group_cells == 0) {
         os << "kind: scpt\n";
         return;
     }
     if (s->kind == FEMGPU_MLT) {
-        os << "kind: mlt\n";
+        os << (plain ? "kind: mlt\n" : "kind: b200_mlt\n");
         os << "quad_tile: " << s->quad_tile << "\n";
         os << "eval_row_tile: " << s->eval_row_tile << "\n";
         os << "eval_col_tiles_scalar:";
@@ -453,6 +458,11 @@ void save_schedule(std::ostream& os, const femgpu_schedule* s, int n_scalar, int
         os << "quad_col_tile: " << s->quad_col_tile << "\n";
         os << "cells_per_group: " << s->cells_per_group << "\n";
         os << "lanes_per_cell: " << s->lanes_per_cell << "\n";
+        if (!plain) {
+            os << "reserved:";
+            for (int v : s->reserved) os << " " << v;
+            os << "\n";
+        }
         return;
     }
     // B200 extension kinds (not readable by the reference)
@@ -487,7 +497,7 @@ femgpu_schedule load_schedule(std::istream& is) {
         s.kind = FEMGPU_SCPT;  // TilingParams::scpt(): the SCPT family with automatic B200 knobs
         return s;
     }
-    if (kind == "mlt") {
+    if (kind == "mlt" || kind == "b200_mlt") {
         s.kind = FEMGPU_MLT;
         s.quad_tile = static_cast<int>(r.expect_int("quad_tile"));
         s.eval_row_tile = static_cast<int>(r.expect_int("eval_row_tile"));
@@ -500,6 +510,10 @@ femgpu_schedule load_schedule(std::istream& is) {
         s.quad_col_tile = static_cast<int>(r.expect_int("quad_col_tile"));
         s.cells_per_group = static_cast<int>(r.expect_int("cells_per_group"));
         s.lanes_per_cell = static_cast<int>(r.expect_int("lanes_per_cell"));
+        if (kind == "b200_mlt") {
+            const auto rv = ints(r.expect("reserved"));
+            for (size_t i = 0; i < rv.size() && i < 4; ++i) s.reserved[i] = rv[i];
+        }
         return s;
     }
     if (kind != "b200_dmma" && kind != "b200_scpt") ferr("candidate file: unknown kind '" + kind + "'");

@@ -101,6 +101,9 @@ std::unique_ptr<PipePlan> Instance::slab_plan(int K, int align) const {
         P->fin[k] = run;
         run = std::min(run, lo[test_group][k]);
     }
+    // rows no cell touches (a gap in the test numbering) are final early but only zeroed when the
+    // zeroing front reaches them: never download a row before it is zeroed
+    for (int k = 0; k < K; ++k) P->fin[k] = std::min(P->fin[k], P->zero_hi[k]);
     // useful when the first slab needs a small part of the inputs and y completes progressively
     long long need0 = 0, total = 0;
     for (size_t i = 0; i < P->up.size(); ++i) {
@@ -142,7 +145,7 @@ bool overlapped_zero_action(Instance& I, const KernelPlan& plan, double* d_y, cu
     // cells one full wave of resident CTAs processes: slabs smaller than that under-fill the GPU
     auto mod = I.module_for(kp);
     const long long cells_per_cta = kp.family == Family::Dmma ? static_cast<long long>(kp.block / 32) * kp.Nc
-                                                              : static_cast<long long>(kp.block) * std::max(1, kp.G);
+                                                              : static_cast<long long>(kp.block / std::max(1, kp.msplit)) * std::max(1, kp.G);
     const long long wave = static_cast<long long>(mod->sms) * std::max(1, mod->occupancy) * cells_per_cta;
     const PipePlan& Z = I.zero_plan(range_align(kp), kp.zslabs,
                                     static_cast<int>(std::min<long long>(64, I.cells / std::max(1LL, wave))));

@@ -58,7 +58,7 @@ long long map_ops(const Signature& sig) {
 std::string tune_key(const Instance& I) {
     const Signature& sig = I.sig;
     std::ostringstream k;
-    k << "v3|" << sig.dim << "|" << sig.Q << "|" << sig.nW << "|" << sig.Tw << "|" << I.cells << "|" << I.output_size;
+    k << "v4|" << sig.dim << "|" << sig.Q << "|" << sig.nW << "|" << sig.Tw << "|" << I.cells << "|" << I.output_size;
     for (size_t i = 0; i < sig.sdofs.size(); ++i) k << "|s" << sig.sdofs[i] << ":" << sig.sterms[i];
     for (size_t i = 0; i < sig.vdofs.size(); ++i) {
         k << "|v" << sig.vdofs[i] << ":" << sig.vterms[i];
@@ -98,7 +98,7 @@ std::string describe_plan(const KernelPlan& kp) {
     std::ostringstream s;
     switch (kp.family) {
         case Family::Macro:
-            s << "femgpu_macro G=" << kp.G << " block=" << kp.block << (kp.qmajor ? " q-major" : "") << (kp.ysmem ? " y-smem" : "");
+            s << "femgpu_macro G=" << kp.G << " block=" << kp.block << (kp.qmajor ? " q-major" : "") << (kp.msplit > 1 ? " split=" + std::to_string(kp.msplit) : std::string()) << (kp.ysmem ? " y-smem" : "");
             break;
         case Family::Scpt:
             s << "femgpu_scpt cells/thread=" << std::max(1, kp.G) << " block=" << kp.block << " minCTAs=" << kp.min_blocks
@@ -112,6 +112,7 @@ std::string describe_plan(const KernelPlan& kp) {
             break;
     }
     if (kp.zfused) s << " +fused-zero" << (kp.zslabs > 0 ? "/" + std::to_string(kp.zslabs) : std::string());
+    if (kp.pipe_memset) s << " +pipe-memset";
     return s.str();
 }
 
@@ -167,7 +168,10 @@ void autotune(Instance& I) {
             s.reserved[2] = 8;  // uncapped (255 registers, 8 warps/SM): C5-adv-P1 1448 us vs 1703 us
             cands.push_back(s);
             s.reserved[2] = 0;
-            s.reserved[3] = 3;  // quadrature-point-major: one tabulation load for the group's cells
+            // quadrature-point-major (one tabulation load for the group's cells) with the quadrature
+            // loop rolled and the hoisted map nodes in registers (C2: 197 vs 224 us unrolled,
+            // instruction-cache stalls; profiles/r02_c2_qmajor.md)
+            s.reserved[3] = 3 | (16 << 16);
             s.reserved[1] = 232;
             cands.push_back(s);
         }
@@ -319,6 +323,34 @@ void autotune(Instance& I) {
                 if (tz[best] < 0.99 * t0) I.auto_sched = fzs[best];
             }
         }
+    }
+    // pipelined actions (femgpu_action_device_pipelined, the bench step): zero the next output
+    // inside the action kernel, or with a memset after it, whichever the winner runs faster with
+    if (!first.empty() && supports_cell_range(resolve_schedule(I, &I.auto_sched))) {
+        double* yb[2] = {I.d_y, I.second_output()};
+        femgpu_schedule sm = I.auto_sched;
+        sm.reserved[0] |= FEMGPU_FLAG_PIPE_MEMSET;
+        const KernelPlan kf = resolve_schedule(I, &I.auto_sched), km = resolve_schedule(I, &sm);
+        auto time_piped = [&](const KernelPlan& kp, int reps) {
+            FG_CUDA(cudaMemsetAsync(yb[0], 0, sizeof(double) * static_cast<size_t>(I.output_size), I.stream));
+            run_action_pipelined(I, kp, yb[0], yb[1], I.stream);
+            FG_CUDA(cudaEventRecord(I.ev0, I.stream));
+            for (int i = 0; i < reps; ++i) run_action_pipelined(I, kp, yb[(i + 1) & 1], yb[i & 1], I.stream);
+            FG_CUDA(cudaEventRecord(I.ev1, I.stream));
+            FG_CUDA(cudaEventSynchronize(I.ev1));
+            float ms = 0.f;
+            FG_CUDA(cudaEventElapsedTime(&ms, I.ev0, I.ev1));
+            return ms * 1e-3 / reps;
+        };
+        const int reps = reps_of[first[0].second];
+        double tf = 1e300, tm = 1e300;
+        for (int round = 0; round < 2; ++round) {
+            tf = std::min(tf, time_piped(kf, reps));
+            tm = std::min(tm, time_piped(km, reps));
+        }
+        log << "; pipelined steps: in-kernel zeroing " << static_cast<long long>(tf * 1e7) / 10.0 << " us, memset "
+            << static_cast<long long>(tm * 1e7) / 10.0 << " us";
+        if (tm < tf) I.auto_sched.reserved[0] |= FEMGPU_FLAG_PIPE_MEMSET;
     }
     // a non-finite input must not leave a stale flag behind the tuning runs
     FG_CUDA(cudaMemsetAsync(I.d_bad, 0xff, 2 * sizeof(unsigned long long), I.stream));

@@ -119,7 +119,8 @@ def plan(p: ProblemInstance, nranks: int, align: int = 6) -> List[RankPlan]:
             if mine_to_q.any():
                 pl.y_send[q.rank] = ia[mine_to_q].astype(np.int64)
                 q.y_recv[pl.rank] = ib[mine_to_q].astype(np.int64)
-            if p.signature.scalar_spaces and p.connectivity.scalar_maps[0].indices is p.connectivity.test_map.indices:
+            if p.signature.scalar_spaces and np.array_equal(p.connectivity.scalar_maps[0].indices,
+                                                            p.connectivity.test_map.indices):
                 owned_by_pl = owner[common] == pl.rank
                 if owned_by_pl.any():
                     pl.x_send[q.rank] = ia[owned_by_pl].astype(np.int64)

@@ -36,11 +36,14 @@ int main() {
     for (const auto& c : cases) {
         const auto sig = preset_signature(c.op, c.d, c.p, c.q);
         const auto inst = make_problem(sig, preset_map(c.op, sig), c.cells, c.seed);
-        const auto ref = reference_action(inst);
-        const auto got = femgpu::action(inst);
+        ReferenceCounters rc, gc;
+        const auto ref = reference_action(inst, &rc);
+        const auto got = femgpu::action(inst, &gc);
         const double err = rel_l2(got, ref);
-        std::printf("%-16s d=%d p=%d Q=%2d cells=%3d  rel_l2=%.3e\n", operator_name(c.op), c.d, c.p, c.q, c.cells, err);
-        if (!(err <= 1e-12) || got.size() != ref.size()) ++fails;
+        const bool cnt_ok = rc.matvec_mults == gc.matvec_mults && rc.matvec_adds == gc.matvec_adds && rc.map_ops == gc.map_ops;
+        std::printf("%-16s d=%d p=%d Q=%2d cells=%3d  rel_l2=%.3e counters %s\n", operator_name(c.op), c.d, c.p, c.q,
+                    c.cells, err, cnt_ok ? "equal" : "DIFFER");
+        if (!(err <= 1e-12) || got.size() != ref.size() || !cnt_ok) ++fails;
     }
     // error mapping: invalid instance -> std::invalid_argument, NaN -> runtime_error naming the cell
     {
@@ -52,6 +55,20 @@ int main() {
         try { femgpu::action(inst); } catch (const std::runtime_error& e) { got_msg = e.what(); }
         std::printf("non-finite: ref='%s' got='%s'\n", ref_msg.c_str(), got_msg.c_str());
         if (ref_msg != got_msg || ref_msg.empty()) ++fails;
+    }
+    // the executor's device-instance cache follows the instance's content, not its address: an
+    // instance modified in place between calls is re-uploaded
+    {
+        const auto sig = preset_signature(Operator::laplace, 2, 2, 6);
+        auto inst = make_problem(sig, preset_map(Operator::laplace, sig), 40, 9);
+        auto ex = femgpu::executor();
+        const auto a = ex(TilingParams::scpt(), inst);
+        for (auto& v : inst.scalar_inputs[0]) v *= 2.0;
+        const auto b = ex(TilingParams::scpt(), inst);
+        const auto ref = reference_action(inst);
+        const double err = a.ok && b.ok ? rel_l2(b.output, ref) : 1.0;
+        std::printf("executor after in-place input change: rel_l2=%.3e\n", err);
+        if (!(err <= 1e-12)) ++fails;
     }
     // tune through the measuring executor: b-best ranked MLT candidates + SCPT (search.hpp:338-416)
     {

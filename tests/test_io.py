@@ -162,3 +162,24 @@ def test_candidate_files_round_trip(tmp_path):
     g.write_text("format_version: 1\nkind: warp\n")
     with pytest.raises(ValueError, match="unknown kind"):
         fg.load_schedule(g)
+
+
+def test_candidate_files_keep_b200_knobs(tmp_path):
+    """strict (bitwise) SCPT, register targets, kernel variants and zeroing decisions must
+    survive a save/load round trip; an MLT candidate with the strict flag keeps it too."""
+    cases = [fg.TilingParams.scpt(strict=True),
+             fg.TilingParams.scpt(reg_target=200, min_blocks=3),
+             fg.TilingParams.scpt(scatter=abi.SCATTER_MACRO, group_cells=6, block_cells=32, stage_smem=3,
+                                  qmopt=16, reg_target=232, fused_zero=True, zero_slabs=4)]
+    sig = fg.preset_signature("laplace", 2, 2, 6)
+    m = fg.TilingParams.untiled(sig, 64, 2)
+    m.strict = True
+    cases.append(m)
+    for i, t in enumerate(cases):
+        f = tmp_path / ("c%d.txt" % i)
+        fg.save_schedule(t, f, n_scalar=len(sig.scalar_spaces))
+        q = fg.load_schedule(f)
+        assert q.to_c().reserved[:] == t.to_c().reserved[:], (i, f.read_text())
+        assert (q.kind, q.scatter, q.group_cells, q.block_cells, q.strict) == (t.kind, t.scatter, t.group_cells,
+                                                                               t.block_cells, t.strict)
+    assert "b200_mlt" in (tmp_path / "c3.txt").read_text()

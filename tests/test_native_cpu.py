@@ -11,7 +11,9 @@ import paper_2506_17471_b200 as fg
 from oracle import mesh_oracle
 from paper_2506_17471_b200 import abi
 from paper_2506_17471_b200._native import EXPORTS, LIB_PATH, lib
+from tests.golden.make_golden import CASES, key
 from tests.helpers import preset_problem
+from tests.test_oracle import GOLDEN, synth
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -117,3 +119,11 @@ def test_fails_loudly_without_a_gpu():
         pytest.skip("a GPU is visible")
     with pytest.raises(RuntimeError):
         fg.gpu_action(preset_problem("mass", 2, 1, 2, 2, 1))
+
+
+@pytest.mark.parametrize("case", CASES, ids=key)
+def test_reference_counters_through_the_abi_equal_golden(case):
+    """femgpu_reference_counters == the ReferenceCounters the reference's own reference_action filled
+    (golden vectors written by the reference build, form.hpp:463-472)."""
+    p = synth(case)
+    assert tuple(fg.reference_counters(p)) == tuple(GOLDEN["counters:" + key(case)])

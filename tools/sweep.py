@@ -4,8 +4,11 @@ usage: python tools/sweep.py C2,C4 auto,macro6,tile-256 [reps]
 Schedule names: auto | scpt | scpt-smem | macroG[-ms][-bB][-mM] | tile-B[-mM]
 """
 import json
+import os
 import sys
 import time
+
+import numpy as np
 
 sys.path.insert(0, ".")
 import paper_2506_17471_b200 as fg  # noqa: E402
@@ -26,6 +29,10 @@ def sched(name):
             kw["stage_smem"] = 3
         elif p == "ql":
             kw["stage_smem"] = 4
+        elif p.startswith("o") and p[1:].isdigit():
+            kw["qmopt"] = int(p[1:])
+        elif p.startswith("sp"):
+            kw["split"] = int(p[2:])
         elif p == "smem":
             kw["basis"] = abi.BASIS_SMEM
         elif p == "const":
@@ -77,6 +84,15 @@ def sched(name):
     raise ValueError(name)
 
 
+PIPE = os.environ.get("SWEEP_PIPE", "1") == "1"
+
+
+def device_y(g, n):
+    import torch
+    from paper_2506_17471_b200.krylov import _CudaArray
+    return torch.as_tensor(_CudaArray(g.device_output(), n), device="cuda").cpu().numpy()
+
+
 def main():
     cfgs = sys.argv[1].split(",")
     names = sys.argv[2].split(",")
@@ -95,12 +111,20 @@ def main():
                     y = g.action(s)
                     if ref is None:
                         ref = y
-                    import numpy as np
                     res["rel_l2_vs_first"] = float(np.linalg.norm(y - ref) / np.linalg.norm(ref))
                     step, kern, zero = g.profile(s, warmup=3, reps=reps)
                     res.update(step_us=round(step * 1e6, 1), kernel_us=round(kern * 1e6, 1),
                                gdofs=round(p.output_size / step / 1e9, 2),
                                fp64_frac_kernel=round(flops / kern / 1e12 / peak, 3))
+                    if PIPE:  # output-pipelined steps (zeroing of the next output inside the kernel)
+                        tp = g.time_steps(reps, s, pipelined=True) / reps
+                        yp = device_y(g, p.output_size)
+                        res.update(pipe_step_us=round(tp * 1e6, 1),
+                                   pipe_rel_l2=float(np.linalg.norm(yp - y) / np.linalg.norm(y)))
+                        ts = g.time_steps(reps, s, pipelined=3) / reps
+                        yp = device_y(g, p.output_size)
+                        res.update(side_step_us=round(ts * 1e6, 1),
+                                   side_rel_l2=float(np.linalg.norm(yp - y) / np.linalg.norm(y)))
                 except Exception as e:  # noqa: BLE001
                     res["error"] = str(e)[:300]
                 print(json.dumps(res), flush=True)
