@@ -275,6 +275,9 @@ femgpu_status femgpu_describe_schedule(femgpu_instance* inst, const femgpu_sched
 /* Introspection: kernel launches issued by the last action, device bytes held. */
 femgpu_status femgpu_stats(const femgpu_instance* inst, int64_t* launches_last_action,
                            int64_t* device_bytes, int64_t* tiles, int64_t* max_tile_dofs);
+/* Copies the instance's output buffer (the y of the last action, or of the last step of
+ * femgpu_time_steps / femgpu_time_steps_ex) into y_host (output_size doubles); synchronous. */
+femgpu_status femgpu_read_output(femgpu_instance* inst, double* y_host);
 /* Device pointers (for zero-copy callers): output buffer of the instance. */
 femgpu_status femgpu_device_output(femgpu_instance* inst, double** y_dev);
 /* Device pointer of trial input vector `space` (scalar spaces first, then vector spaces),
@@ -317,6 +320,11 @@ femgpu_status femgpu_mesh_counts(int32_t dim, int32_t n, int32_t degree, int64_t
                                  int64_t* nodes, int64_t* vertices, int32_t* nodes_per_cell);
 femgpu_status femgpu_mesh_build(int32_t dim, int32_t n, int32_t degree, int32_t brick,
                                 int32_t* node_map, int32_t* vertex_map, double* coords);
+/* The rows [cell_begin, cell_end) of femgpu_mesh_build's node and vertex maps (same global
+ * numbering), written from row 0 of node_map / vertex_map; coords (may be NULL) as in
+ * femgpu_mesh_build.  One rank of a cell-partitioned run builds only its own slab with it. */
+femgpu_status femgpu_mesh_build_range(int32_t dim, int32_t n, int32_t degree, int32_t brick, int64_t cell_begin,
+                                      int64_t cell_end, int32_t* node_map, int32_t* vertex_map, double* coords);
 /* Greedy cell colouring: no two cells of one colour share an entry of map.
  * colors[cell] in [0, *n_colors). Deterministic (cells in ascending order,
  * smallest free colour). */

@@ -26,7 +26,7 @@ EXPORTS = (
     "femgpu_time_steps", "femgpu_device_input", "femgpu_describe_schedule",
     "femgpu_fp64_dmma_peak", "femgpu_problem_load", "femgpu_problem_free", "femgpu_problem_save",
     "femgpu_schedule_save", "femgpu_schedule_load", "femgpu_action_device_pipelined", "femgpu_check_finite",
-    "femgpu_time_steps_ex", "femgpu_reference_counters",
+    "femgpu_time_steps_ex", "femgpu_reference_counters", "femgpu_read_output", "femgpu_mesh_build_range",
 )
 
 
@@ -104,6 +104,9 @@ def lib():
                 "femgpu_action_device_pipelined": ([C.c_void_p, _P(abi.Schedule), C.c_void_p, C.c_void_p, C.c_void_p],
                                                    C.c_int),
                 "femgpu_check_finite": ([C.c_void_p, _P(abi.Schedule), C.c_void_p], C.c_int),
+                "femgpu_read_output": ([C.c_void_p, _P(C.c_double)], C.c_int),
+                "femgpu_mesh_build_range": ([C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_int64,
+                                             _P(C.c_int32), _P(C.c_int32), _P(C.c_double)], C.c_int),
                 "femgpu_reference_counters": ([_P(abi.Problem), _P(C.c_int64), _P(C.c_int64), _P(C.c_int64)], C.c_int),
                 "femgpu_device_input": ([C.c_void_p, C.c_int32, _P(C.c_void_p)], C.c_int),
             }

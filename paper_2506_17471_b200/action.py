@@ -271,6 +271,12 @@ class GpuInstance:
         _call(lib().femgpu_stream(self._h, C.byref(p)))
         return p.value or 0
 
+    def read_output(self) -> np.ndarray:
+        """Host copy of the instance's output buffer (the last action's / timed step's y)."""
+        y = np.empty(self.problem.output_size, dtype=np.float64)
+        _call(lib().femgpu_read_output(self._h, y.ctypes.data_as(C.POINTER(C.c_double))))
+        return y
+
     def device_output(self) -> int:
         p = C.c_void_p()
         _call(lib().femgpu_device_output(self._h, C.byref(p)))

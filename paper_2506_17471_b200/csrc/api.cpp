@@ -434,6 +434,18 @@ femgpu_status femgpu_stats(const femgpu_instance* h, int64_t* launches, int64_t*
     });
 }
 
+femgpu_status femgpu_read_output(femgpu_instance* h, double* y_host) {
+    return guard([&] {
+        auto& I = get(h);
+        if (!y_host) femgpu::invalid("null output buffer");
+        std::lock_guard<std::mutex> lk(I.mu);
+        FG_CUDA(cudaSetDevice(I.device));
+        FG_CUDA(cudaMemcpyAsync(y_host, I.d_y, sizeof(double) * static_cast<size_t>(I.output_size),
+                                cudaMemcpyDeviceToHost, I.stream));
+        FG_CUDA(cudaStreamSynchronize(I.stream));
+    });
+}
+
 femgpu_status femgpu_device_output(femgpu_instance* h, double** y_dev) {
     return guard([&] { *y_dev = get(h).d_y; });
 }

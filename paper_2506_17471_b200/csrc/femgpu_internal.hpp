@@ -146,6 +146,7 @@ struct Module {
     cudaKernel_t fast = nullptr, checked = nullptr;
     EmitResult emitted;
     int regs = 0;
+    long long local_bytes = 0;  // local memory per thread (spills) of the fast kernel
     int occupancy = 1;   // resident CTAs per SM of the fast kernel
     int sms = 148;
 };

@@ -110,11 +110,17 @@ std::shared_ptr<Module> get_module(const Signature& sig, const KernelPlan& kp) {
     FG_CUDA(cudaGetDevice(&dev));
     const std::string key = std::to_string(dev) + "|" + std::to_string(kp.strict) + "|" +
                             std::to_string(fnv1a(em.source));
-    std::lock_guard<std::mutex> lk(g_jit_mu);
-    auto it = g_modules.find(key);
-    if (it != g_modules.end()) return it->second;
+    {
+        std::lock_guard<std::mutex> lk(g_jit_mu);
+        auto it = g_modules.find(key);
+        if (it != g_modules.end()) return it->second;
+    }
+    // NVRTC outside the lock: the automatic schedule compiles its candidates from several threads
     std::string log;
     std::vector<char> bin = jit_compile(em.source, kp.strict, &log);
+    std::lock_guard<std::mutex> lk(g_jit_mu);
+    auto it = g_modules.find(key);
+    if (it != g_modules.end()) return it->second;  // another thread compiled it meanwhile
     auto m = std::make_shared<Module>();
     FG_CUDA(cudaLibraryLoadData(&m->lib, bin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
     FG_CUDA(cudaLibraryGetKernel(&m->fast, m->lib, em.kernel.c_str()));
@@ -137,7 +143,10 @@ std::shared_ptr<Module> get_module(const Signature& sig, const KernelPlan& kp) {
             m->sms = dev_sms;
     }
     cudaFuncAttributes attr{};
-    if (cudaFuncGetAttributes(&attr, reinterpret_cast<const void*>(m->fast)) == cudaSuccess) m->regs = attr.numRegs;
+    if (cudaFuncGetAttributes(&attr, reinterpret_cast<const void*>(m->fast)) == cudaSuccess) {
+        m->regs = attr.numRegs;
+        m->local_bytes = static_cast<long long>(attr.localSizeBytes);  // > 0: register spills to local memory
+    }
     cudaGetLastError();
     m->emitted = std::move(em);
     g_modules[key] = m;

@@ -109,9 +109,17 @@ femgpu_status femgpu_mesh_counts(int32_t dim, int32_t n, int32_t degree, int64_t
 
 femgpu_status femgpu_mesh_build(int32_t dim, int32_t n, int32_t degree, int32_t brick, int32_t* node_map,
                                 int32_t* vertex_map, double* coords) {
+    int64_t cells = 0;
+    if (femgpu_mesh_counts(dim, n, degree, &cells, nullptr, nullptr, nullptr) != FEMGPU_OK) return FEMGPU_E_INVALID;
+    return femgpu_mesh_build_range(dim, n, degree, brick, 0, cells, node_map, vertex_map, coords);
+}
+
+femgpu_status femgpu_mesh_build_range(int32_t dim, int32_t n, int32_t degree, int32_t brick, int64_t cell_begin,
+                                      int64_t cell_end, int32_t* node_map, int32_t* vertex_map, double* coords) {
     int64_t cells = 0, nodes = 0, verts = 0;
     int32_t npc = 0;
     if (femgpu_mesh_counts(dim, n, degree, &cells, &nodes, &verts, &npc) != FEMGPU_OK) return FEMGPU_E_INVALID;
+    if (cell_begin < 0 || cell_end < cell_begin || cell_end > cells) return FEMGPU_E_INVALID;
     if (brick < 1) brick = 1;
     const auto lat = lattice_nodes(dim, degree);
     if (static_cast<int>(lat.size()) != npc) return FEMGPU_E_INTERNAL;
@@ -127,16 +135,23 @@ femgpu_status femgpu_mesh_build(int32_t dim, int32_t n, int32_t degree, int32_t 
                 const int z0 = bz * brick, z1 = dim == 3 ? std::min(n, z0 + brick) : 1;
                 const int y0 = by * brick, y1 = std::min(n, y0 + brick);
                 const int x0 = bx * brick, x1 = std::min(n, x0 + brick);
+                const int64_t brick_cells = static_cast<int64_t>(z1 - (dim == 3 ? z0 : 0)) * (y1 - y0) * (x1 - x0) * sc;
+                if (cell + brick_cells <= cell_begin || cell >= cell_end) {  // brick outside the range
+                    cell += brick_cells;
+                    continue;
+                }
                 for (int l = (dim == 3 ? z0 : 0); l < z1; ++l)
                     for (int j = y0; j < y1; ++j)
                         for (int i = x0; i < x1; ++i)
                             for (int s = 0; s < sc; ++s, ++cell) {
+                                if (cell < cell_begin || cell >= cell_end) continue;
+                                const int64_t out = cell - cell_begin;  // row in the caller's arrays
                                 simplex_vertices(dim, i, j, l, s, V);
                                 if (vertex_map)
                                     for (int v = 0; v <= dim; ++v) {
                                         int64_t idx = V[v][0] + static_cast<int64_t>(n + 1) * V[v][1];
                                         if (dim == 3) idx += static_cast<int64_t>(n + 1) * (n + 1) * V[v][2];
-                                        vertex_map[cell * (dim + 1) + v] = static_cast<int32_t>(idx);
+                                        vertex_map[out * (dim + 1) + v] = static_cast<int32_t>(idx);
                                     }
                                 if (node_map)
                                     for (int a = 0; a < npc; ++a) {
@@ -145,7 +160,7 @@ femgpu_status femgpu_mesh_build(int32_t dim, int32_t n, int32_t degree, int32_t 
                                             for (int c = 0; c < dim; ++c) p[c] += static_cast<int64_t>(lat[a][v]) * V[v][c];
                                         int64_t idx = p[0] + kn1 * p[1];
                                         if (dim == 3) idx += kn1 * kn1 * p[2];
-                                        node_map[cell * npc + a] = static_cast<int32_t>(idx);
+                                        node_map[out * npc + a] = static_cast<int32_t>(idx);
                                     }
                             }
             }

@@ -12,7 +12,11 @@
 // instance stream ([zero y + action], 2 warm-up + 5 timed).  The winner is cached in the
 // instance.  Small instances (< kTuneMinCells) skip the timing and use the DFMA default.
 #include <algorithm>
+#include <array>
+#include <atomic>
 #include <cstdlib>
+#include <numeric>
+#include <thread>
 #include <cstring>
 #include <fstream>
 #include <sstream>
@@ -58,7 +62,7 @@ long long map_ops(const Signature& sig) {
 std::string tune_key(const Instance& I) {
     const Signature& sig = I.sig;
     std::ostringstream k;
-    k << "v4|" << sig.dim << "|" << sig.Q << "|" << sig.nW << "|" << sig.Tw << "|" << I.cells << "|" << I.output_size;
+    k << "v5|" << sig.dim << "|" << sig.Q << "|" << sig.nW << "|" << sig.Tw << "|" << I.cells << "|" << I.output_size;
     for (size_t i = 0; i < sig.sdofs.size(); ++i) k << "|s" << sig.sdofs[i] << ":" << sig.sterms[i];
     for (size_t i = 0; i < sig.vdofs.size(); ++i) {
         k << "|v" << sig.vdofs[i] << ":" << sig.vterms[i];
@@ -116,6 +120,53 @@ std::string describe_plan(const KernelPlan& kp) {
     return s.str();
 }
 
+namespace {
+
+// One point of the schedule space with its model terms (tune log / FEMGPU_TUNE_LOG).
+struct Cand {
+    femgpu_schedule s{};
+    KernelPlan kp;
+    std::string label;
+    int family = 0;             // 0 macro, 1 scpt, 2 dmma
+    double slots = 0;           // FP64 lane-slots per cell (DMMA: padded m8n8k4 slots)
+    double t_pipe = 0;          // seconds: FP64 pipe at the family's sustained efficiency
+    double pred = 0;            // seconds: the model after the JIT (occupancy, spills)
+    double meas = -1;           // seconds: measured (timed candidates only)
+    int regs = 0, warps = 0;    // registers per thread, resident warps per SM
+    long long spill = 0;        // local bytes per thread
+    bool compiled = false, timed = false;
+    std::string reject;
+};
+
+femgpu_schedule macro_variant(int G, int block, int variant, int reg_target, int min_blocks) {
+    femgpu_schedule s = dfma_default();
+    s.scatter = FEMGPU_SCATTER_MACRO;
+    s.group_cells = G;
+    s.block_cells = block;
+    s.reserved[1] = reg_target;
+    s.reserved[2] = min_blocks;
+    s.reserved[3] = variant;
+    return s;
+}
+
+femgpu_schedule scpt_variant(int G, int block, int min_blocks, bool qloop) {
+    femgpu_schedule s = dfma_default();
+    s.scatter = FEMGPU_SCATTER_ATOMIC;
+    s.group_cells = G;
+    s.block_cells = block;
+    s.reserved[2] = min_blocks;
+    s.reserved[3] = qloop ? 4 : 0;
+    return s;
+}
+
+// Sustained fraction of the FP64 pipe each family reaches when latency is hidden (calibrated
+// on the round-1/2 sweeps: profiles/r02_tuner_calibration.jsonl), and the exposed latency of one
+// work unit's gather chain (index load -> value load, ~2 DRAM round trips) in SM cycles.
+constexpr double kEffMacro = 0.66, kEffScpt = 0.58, kEffDmma = 0.62;
+constexpr double kGatherCycles = 1600.0;
+
+}  // namespace
+
 void autotune(Instance& I) {
     I.auto_ready = true;
     I.auto_sched = dfma_default();
@@ -139,109 +190,159 @@ void autotune(Instance& I) {
         }
     }
     const Signature& sig = I.sig;
-    // ---- model: FP64-pipe lane-slots per cell
+    int dev = 0, sms = 148, clk_khz = 1965000;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, dev);
+    const double clk = clk_khz * 1e3, lanes = 64.0 * sms;  // FP64 lanes per SM per clock
+    // ---- FP64 lane-slots per cell (the paper's "Ops" count on this hardware)
     const double usable_fma = static_cast<double>(sig.usable_flops()) / 2.0;
     const double map_slots = static_cast<double>(map_ops(sig)) * sig.Q;
     const double geo_slots = sig.affine ? 6.0 * sig.dim * sig.dim : 0.0;
-    const double t_dfma = (usable_fma + map_slots + geo_slots) / 0.50;
-    double t_dmma = 1e300;
-    {
-        KernelPlan kp;
-        femgpu_schedule s = dmma_variant(1, 0, 0, 0);
+    const double dfma_slots = usable_fma + map_slots + geo_slots;
+    // ---- enumerate the schedule space
+    std::vector<Cand> C;
+    auto add = [&](const femgpu_schedule& sc, int family) {
+        Cand c;
+        c.s = sc;
+        c.family = family;
         try {
-            resolve_dmma(sig, kp, &s);
-            const DmmaLayout L = dmma_layout(sig, kp);
-            const double dmma_slots = static_cast<double>(L.nfrag) * 256.0 / 8.0;  // per cell
-            t_dmma = dmma_slots / 0.55 + (map_slots * (4.0 * L.TQL * L.NCH) / sig.Q + geo_slots) / 0.5;
-        } catch (const Error&) {
+            c.kp = resolve_schedule(I, &c.s);
+        } catch (const Error& e) {
+            if (e.code != FEMGPU_E_INFEASIBLE && e.code != FEMGPU_E_INVALID) throw;
+            return;
         }
+        c.label = describe_plan(c.kp);
+        for (const auto& o : C)
+            if (o.label == c.label) return;
+        if (family == 2) {
+            const DmmaLayout L = dmma_layout(sig, c.kp);
+            const double pad_q = static_cast<double>(4 * L.TQL * L.NCH) / sig.Q;
+            // DMMA slots run at the DMMA rate (measured 37.1 vs 34.2 TF DFMA: x1.085 per slot)
+            c.slots = static_cast<double>(L.nfrag) * 256.0 / 8.0 / 1.085 + map_slots * pad_q + geo_slots;
+        } else {
+            c.slots = dfma_slots;
+        }
+        const double eff = family == 0 ? kEffMacro : family == 1 ? kEffScpt : kEffDmma;
+        c.t_pipe = static_cast<double>(I.cells) * c.slots / (lanes * clk) / eff;
+        C.push_back(c);
+    };
+    add(dfma_default(), 1);  // the paper's SCPT baseline, always timed (b + SCPT)
+    for (int G : {6, 4, 3, 2}) {  // the largest group size whose common pattern fits the register budget
+        if (!I.macro_layout(G).ok) continue;
+        const size_t before = C.size();
+        add(macro_variant(G, 32, 3 | (16 << 16), 232, 0), 0);  // q-major, rolled quadrature loop
+        add(macro_variant(G, 64, 3 | (16 << 16), 232, 0), 0);
+        add(macro_variant(G, 32, 3, 232, 0), 0);                // q-major, unrolled
+        add(macro_variant(G, 32, 0, 0, 8), 0);                  // cell-major, uncapped
+        add(macro_variant(G, 64, 0, 0, 0), 0);                  // cell-major, 168-register cap
+        if (C.size() > before) break;
     }
-    const double best = std::min(t_dfma, t_dmma);
-    std::vector<femgpu_schedule> cands;
-    if (t_dfma <= 1.6 * best) {
-        cands.push_back(dfma_default());
-        {  // macro-elements with 32-thread CTAs (measured 2 % faster on C2 / C5-adv-P1)
-            femgpu_schedule s = dfma_default();
-            s.scatter = FEMGPU_SCATTER_MACRO;
-            s.block_cells = 32;
-            cands.push_back(s);
-            s.reserved[2] = 8;  // uncapped (255 registers, 8 warps/SM): C5-adv-P1 1448 us vs 1703 us
-            cands.push_back(s);
-            s.reserved[2] = 0;
-            // quadrature-point-major (one tabulation load for the group's cells) with the quadrature
-            // loop rolled and the hoisted map nodes in registers (C2: 197 vs 224 us unrolled,
-            // instruction-cache stalls; profiles/r02_c2_qmajor.md)
-            s.reserved[3] = 3 | (16 << 16);
-            s.reserved[1] = 232;
-            cands.push_back(s);
-        }
-        for (int mb : {3, 5}) {  // SCPT with a register cap (more resident warps to hide the gathers)
-            femgpu_schedule s = dfma_default();
-            s.scatter = FEMGPU_SCATTER_ATOMIC;
-            s.block_cells = mb == 3 ? 256 : 128;
-            s.reserved[2] = mb;
-            cands.push_back(s);
-        }
-        for (int G : {2}) {  // SCPT with G cells per thread (shared tabulation loads)
-            femgpu_schedule s = dfma_default();
-            s.scatter = FEMGPU_SCATTER_ATOMIC;
-            s.group_cells = G;
-            cands.push_back(s);
-            s.reserved[3] = 4;  // quadrature loop kept rolled (measured 7 % faster on C3a)
-            cands.push_back(s);
-        }
-        {  // 3 cells per thread, rolled quadrature loop, 64-thread CTAs (C3a: 181 us vs 205 us)
-            femgpu_schedule s = dfma_default();
-            s.scatter = FEMGPU_SCATTER_ATOMIC;
-            s.group_cells = 3;
-            s.block_cells = 64;
-            s.reserved[3] = 4;
-            cands.push_back(s);
-        }
-    }
-    if (t_dmma <= 1.6 * best) {
-        // quadrature chunk: the register-capped choice of resolve_dmma and, when different, the
-        // uncapped one with the fewest padded DMMAs (more registers, fewer tensor-pipe slots)
+    for (const auto& v : std::vector<std::array<int, 4>>{{1, 256, 3, 0}, {1, 128, 5, 0}, {1, 64, 0, 0}, {2, 128, 0, 0},
+                                                         {2, 128, 0, 1}, {2, 64, 0, 1}, {3, 64, 0, 1}, {3, 128, 0, 1}})
+        add(scpt_variant(v[0], v[1], v[2], v[3] != 0), 1);
+    {
         std::vector<int> tqs = {0};
-        {
-            long long bestf = -1;
-            int bestq = 0;
-            for (int tq = 4; tq <= (sig.Q + 3) / 4 * 4; tq += 4) {
-                KernelPlan kp;
-                femgpu_schedule s = dmma_variant(1, 0, 0, 0);
-                s.quad_tile = tq;
-                try {
-                    resolve_dmma(sig, kp, &s);
-                } catch (const Error&) {
-                    continue;
-                }
-                const long long f = dmma_layout(sig, kp).nfrag;
-                if (bestf < 0 || f < bestf) bestf = f, bestq = tq;
-            }
+        long long bestf = -1;
+        int bestq = 0;
+        for (int tq = 4; tq <= (sig.Q + 3) / 4 * 4; tq += 4) {
             KernelPlan kp;
             femgpu_schedule s = dmma_variant(1, 0, 0, 0);
-            resolve_dmma(sig, kp, &s);
-            if (bestq > 0 && bestq != kp.TQ) tqs.push_back(bestq);
-            // two owned points per lane-group: measured best on several high-Q forms (hyp-P4)
-            if (sig.Q > 8 && kp.TQ != 8 && bestq != 8) tqs.push_back(8);
+            s.quad_tile = tq;
+            try {
+                resolve_dmma(sig, kp, &s);
+            } catch (const Error&) {
+                continue;
+            }
+            const long long f = dmma_layout(sig, kp).nfrag;
+            if (bestf < 0 || f < bestf) bestf = f, bestq = tq;
         }
+        tqs.push_back(bestq);
+        if (sig.Q > 8) tqs.push_back(8);
         for (int tq : tqs)
             for (int joint : {1, 2})
-                for (int block : {128, 256}) {
-                    cands.push_back(dmma_variant(joint, 0, block, 32));
-                    cands.back().quad_tile = tq;
-                }
-        for (int tq : tqs)  // gather prefetch (C5-hyp-P2: T^Q=8 + prefetch 2191-2226 us vs 2310 us)
-            for (int block : {128, 256}) {
-                cands.push_back(dmma_variant(1, 1, block, 32));
-                cands.back().quad_tile = tq;
-            }
+                for (int pf : {0, 1})
+                    for (int block : {128, 256}) {
+                        femgpu_schedule s = dmma_variant(joint, pf, block, 32);
+                        s.quad_tile = tq;
+                        add(s, 2);
+                    }
     }
-    std::ostringstream log;
-    log << "model slots/cell: dfma " << static_cast<long long>(t_dfma) << ", dmma "
-        << (t_dmma < 1e299 ? std::to_string(static_cast<long long>(t_dmma)) : std::string("n/a")) << "; timed:";
-    // first pass: every candidate, >= 5 runs and >= ~10 ms of work; second pass: the three fastest
-    // re-timed in an interleaved order (clock/power-state drift between candidates cancels out)
+    // ---- static pruning: the best kCompile by FP64-pipe time (each family keeps its best two)
+    const char* all_env = std::getenv("FEMGPU_TUNE_ALL");  // calibration runs: compile and time everything
+    const bool tune_all = all_env && std::strcmp(all_env, "0") != 0;
+    constexpr size_t kCompile = 16, kTimed = 9;
+    std::vector<size_t> order(C.size());
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return C[a].t_pipe < C[b].t_pipe; });
+    std::vector<size_t> sel = {0};  // SCPT baseline
+    int per_family[3] = {0, 0, 0};
+    for (size_t i : order)
+        if (i != 0 && per_family[C[i].family] < 2) {
+            sel.push_back(i);
+            ++per_family[C[i].family];
+        }
+    for (size_t i : order)
+        if ((tune_all || sel.size() < kCompile) && std::find(sel.begin(), sel.end(), i) == sel.end()) sel.push_back(i);
+    // ---- JIT the survivors in parallel (NVRTC is thread-safe; modules land in the global cache)
+    {
+        std::vector<std::thread> pool;
+        std::atomic<size_t> next{0};
+        const unsigned nthr = std::max(1u, std::min<unsigned>(16, std::thread::hardware_concurrency()));
+        for (unsigned t = 0; t < nthr; ++t)
+            pool.emplace_back([&] {
+                cudaSetDevice(dev);
+                for (size_t k; (k = next.fetch_add(1)) < sel.size();) {
+                    try {
+                        get_module(sig, C[sel[k]].kp);
+                    } catch (const Error&) {
+                    }
+                }
+            });
+        for (auto& t : pool) t.join();
+    }
+    // ---- model with the compiled kernels' attributes: occupancy against the gather latency,
+    // spills rejected
+    const double bytes_floor = 0.0;
+    for (size_t i : sel) {
+        Cand& c = C[i];
+        std::shared_ptr<Module> m;
+        try {
+            m = I.module_for(c.kp);
+        } catch (const Error& e) {
+            c.reject = std::string("jit: ") + e.what();
+            continue;
+        }
+        c.compiled = true;
+        c.regs = m->regs;
+        c.spill = m->local_bytes;
+        c.warps = m->occupancy * (c.kp.block / 32);
+        const double W = std::max(1.0, c.warps / 4.0);  // warps per SM sub-partition
+        // work unit = one warp's share of one trip through the gather -> compute -> scatter chain
+        double cells_per_warp_unit = 32.0;
+        if (c.family == 0) cells_per_warp_unit = 32.0 * c.kp.G;
+        if (c.family == 1) cells_per_warp_unit = 32.0 * std::max(1, c.kp.G);
+        if (c.family == 2) cells_per_warp_unit = static_cast<double>(c.kp.Nc);
+        const double units = static_cast<double>(I.cells) / cells_per_warp_unit / (4.0 * sms);
+        const double c_unit = 2.0 * cells_per_warp_unit * c.slots / 32.0;  // SMSP cycles at 16 lanes/clk
+        const double lat = (c.family == 2 && c.kp.Tqr > 0) ? kGatherCycles / 4 : kGatherCycles;
+        const double t_lat = units * (c_unit + lat) / W / clk;
+        c.pred = std::max({c.t_pipe, t_lat, bytes_floor});
+        if (c.spill > 0) c.reject = "spills " + std::to_string(c.spill) + " B/thread";
+        else if (c.warps < 4) c.reject = "occupancy " + std::to_string(c.warps) + " warps/SM";
+    }
+    std::vector<size_t> ranked;
+    for (size_t i : sel)
+        if (C[i].compiled && C[i].reject.empty()) ranked.push_back(i);
+    if (ranked.empty())  // everything spills: keep the compiled ones, the model still orders them
+        for (size_t i : sel)
+            if (C[i].compiled) ranked.push_back(i);
+    std::stable_sort(ranked.begin(), ranked.end(), [&](size_t a, size_t b) { return C[a].pred < C[b].pred; });
+    std::vector<size_t> timed;
+    for (size_t i : ranked)
+        if (tune_all || timed.size() < kTimed) timed.push_back(i);
+    if (std::find(timed.begin(), timed.end(), size_t(0)) == timed.end() && C[0].compiled) timed.push_back(0);
+    // ---- measure: >= 5 runs and ~10 ms of work each, then the three fastest re-timed interleaved
     auto time_it = [&](const KernelPlan& kp, int reps) {
         FG_CUDA(cudaEventRecord(I.ev0, I.stream));
         for (int i = 0; i < reps; ++i) run_action(I, kp, I.d_y, I.stream);
@@ -251,78 +352,62 @@ void autotune(Instance& I) {
         FG_CUDA(cudaEventElapsedTime(&ms, I.ev0, I.ev1));
         return ms * 1e-3 / reps;
     };
+    std::vector<int> reps_of(C.size(), 5);
     std::vector<std::pair<double, size_t>> first;
-    std::vector<KernelPlan> plans(cands.size());
-    std::vector<int> reps_of(cands.size(), 5);
-    for (size_t ci = 0; ci < cands.size(); ++ci) {
+    for (size_t i : timed) {
+        Cand& c = C[i];
         try {
-            plans[ci] = resolve_schedule(I, &cands[ci]);
-            for (int i = 0; i < 2; ++i) run_action(I, plans[ci], I.d_y, I.stream);
-            const double t1 = time_it(plans[ci], 1);
-            reps_of[ci] = std::max(5, std::min(200, static_cast<int>(0.01 / std::max(t1, 1e-6))));
-            const double t = time_it(plans[ci], reps_of[ci]);
-            log << " [" << describe_plan(plans[ci]) << ": " << static_cast<long long>(t * 1e7) / 10.0 << " us]";
-            first.push_back({t, ci});
+            for (int k = 0; k < 2; ++k) run_action(I, c.kp, I.d_y, I.stream);
+            const double t1 = time_it(c.kp, 1);
+            reps_of[i] = std::max(5, std::min(200, static_cast<int>(0.01 / std::max(t1, 1e-6))));
+            c.meas = time_it(c.kp, reps_of[i]);
+            c.timed = true;
+            first.push_back({c.meas, i});
         } catch (const Error& e) {
             if (e.code != FEMGPU_E_INFEASIBLE && e.code != FEMGPU_E_JIT) throw;
-            log << " [infeasible: " << e.what() << "]";
+            c.reject = std::string("launch: ") + e.what();
         }
     }
     std::sort(first.begin(), first.end());
     const size_t top = std::min<size_t>(3, first.size());
     std::vector<double> retime(top, 1e300);
     for (int round = 0; round < 2 && top > 1; ++round)
-        for (size_t i = 0; i < top; ++i) {
-            const size_t ci = first[round % 2 ? top - 1 - i : i].second;
-            const double t = time_it(plans[ci], reps_of[ci]);
-            size_t slot = 0;
-            for (size_t k = 0; k < top; ++k)
-                if (first[k].second == ci) slot = k;
-            retime[slot] = std::min(retime[slot], t);
+        for (size_t k = 0; k < top; ++k) {
+            const size_t j = round % 2 ? top - 1 - k : k;
+            retime[j] = std::min(retime[j], time_it(C[first[j].second].kp, reps_of[first[j].second]));
         }
+    size_t win = 0;
+    for (size_t k = 1; k < top; ++k)
+        if (retime[k] < retime[win]) win = k;
+    std::ostringstream log;
+    auto us = [](double t) { return static_cast<long long>(t * 1e7) / 10.0; };
+    log << "model: " << C.size() << " candidates, " << sel.size() << " compiled, " << first.size()
+        << " timed (FP64 slots/cell: dfma " << static_cast<long long>(dfma_slots) << ")";
+    for (size_t i : timed)
+        if (C[i].timed)
+            log << " [" << C[i].label << ": pred " << us(C[i].pred) << " us, meas " << us(C[i].meas) << " us, "
+                << C[i].regs << " regs, " << C[i].warps << " warps/SM]";
+    for (size_t i : sel)
+        if (!C[i].reject.empty()) log << " [rejected " << C[i].label << ": " << C[i].reject << "]";
     if (!first.empty()) {
-        size_t win = 0;
-        if (top > 1)
-            for (size_t k = 1; k < top; ++k)
-                if (retime[k] < retime[win]) win = k;
-        I.auto_sched = cands[first[win].second];
-        log << "; re-timed top " << top << ", winner " << describe_plan(plans[first[win].second]);
-        // fused y zeroing (pipeline.cpp): slabbed launches clear later slabs' rows instead of a
-        // memset in front; kept only where it times faster (it wins on C5-hyp-P1 and C4,
-        // loses where slab boundaries cost more than the memset)
-        const char* zo = std::getenv("FEMGPU_ZERO_OVERLAP");
-        if (!zo) {
-            const KernelPlan& k0 = plans[first[win].second];
-            const int reps = reps_of[first[win].second];
-            std::vector<femgpu_schedule> fzs;
-            std::vector<KernelPlan> kzs;
-            for (int slabs : {4, 8}) {  // fewer slabs: larger front memset, fewer slab boundaries
-                femgpu_schedule fz = I.auto_sched;
-                fz.reserved[0] |= FEMGPU_FLAG_FUSED_ZERO | (slabs << 8);
-                const KernelPlan kz = resolve_schedule(I, &fz);
-                if (!kz.zfused) continue;
-                for (int i = 0; i < 2; ++i) run_action(I, kz, I.d_y, I.stream);
-                if (I.last_launches <= 1) continue;  // not applicable here (size, locality)
-                fzs.push_back(fz);
-                kzs.push_back(kz);
-            }
-            double t0 = 1e300;
-            std::vector<double> tz(kzs.size(), 1e300);
-            for (int round = 0; round < 2 && !kzs.empty(); ++round) {
-                t0 = std::min(t0, time_it(k0, reps));
-                for (size_t i = 0; i < kzs.size(); ++i) tz[i] = std::min(tz[i], time_it(kzs[i], reps));
-            }
-            size_t best = 0;
-            for (size_t i = 1; i < tz.size(); ++i)
-                if (tz[i] < tz[best]) best = i;
-            if (!kzs.empty()) {
-                log << "; fused zeroing";
-                for (size_t i = 0; i < kzs.size(); ++i)
-                    log << " " << kzs[i].zslabs << " slabs " << static_cast<long long>(tz[i] * 1e7) / 10.0 << " us";
-                log << " vs one launch " << static_cast<long long>(t0 * 1e7) / 10.0 << " us";
-                if (tz[best] < 0.99 * t0) I.auto_sched = fzs[best];
-            }
+        I.auto_sched = C[first[win].second].s;
+        log << "; re-timed top " << top << ", winner " << C[first[win].second].label;
+    }
+    // ---- rank agreement of the model with the measurements (Spearman over the timed candidates)
+    double rho = 0.0;
+    if (first.size() > 2) {
+        std::vector<size_t> tp;
+        for (auto& f : first) tp.push_back(f.second);
+        std::vector<size_t> by_pred = tp;
+        std::stable_sort(by_pred.begin(), by_pred.end(), [&](size_t a, size_t b) { return C[a].pred < C[b].pred; });
+        double d2 = 0.0;
+        for (size_t r = 0; r < tp.size(); ++r) {
+            const size_t pr = static_cast<size_t>(std::find(by_pred.begin(), by_pred.end(), tp[r]) - by_pred.begin());
+            d2 += static_cast<double>((pr - r) * (pr - r));
         }
+        const double n = static_cast<double>(tp.size());
+        rho = 1.0 - 6.0 * d2 / (n * (n * n - 1.0));
+        log << "; model rank agreement (Spearman) " << static_cast<long long>(rho * 1000) / 1000.0;
     }
     // pipelined actions (femgpu_action_device_pipelined, the bench step): zero the next output
     // inside the action kernel, or with a memset after it, whichever the winner runs faster with
@@ -342,7 +427,7 @@ void autotune(Instance& I) {
             FG_CUDA(cudaEventElapsedTime(&ms, I.ev0, I.ev1));
             return ms * 1e-3 / reps;
         };
-        const int reps = reps_of[first[0].second];
+        const int reps = reps_of[first[win].second];
         double tf = 1e300, tm = 1e300;
         for (int round = 0; round < 2; ++round) {
             tf = std::min(tf, time_piped(kf, reps));
@@ -356,6 +441,22 @@ void autotune(Instance& I) {
     FG_CUDA(cudaMemsetAsync(I.d_bad, 0xff, 2 * sizeof(unsigned long long), I.stream));
     FG_CUDA(cudaStreamSynchronize(I.stream));
     I.auto_log = log.str();
+    if (const char* path = std::getenv("FEMGPU_TUNE_LOG")) {  // predicted vs measured, one JSON line per instance
+        std::ofstream js(path, std::ios::app);
+        js << "{\"cells\": " << I.cells << ", \"dofs\": " << I.output_size << ", \"Q\": " << sig.Q
+           << ", \"usable_flops\": " << sig.usable_flops() << ", \"spearman\": " << rho << ", \"winner\": \""
+           << (first.empty() ? std::string() : C[first[win].second].label) << "\", \"candidates\": [";
+        bool comma = false;
+        for (size_t i : sel) {
+            const Cand& c = C[i];
+            js << (comma ? ", " : "") << "{\"label\": \"" << c.label << "\", \"family\": " << c.family
+               << ", \"slots\": " << c.slots << ", \"t_pipe_us\": " << c.t_pipe * 1e6 << ", \"pred_us\": " << c.pred * 1e6
+               << ", \"meas_us\": " << (c.timed ? c.meas * 1e6 : -1.0) << ", \"regs\": " << c.regs
+               << ", \"warps\": " << c.warps << ", \"spill\": " << c.spill << ", \"reject\": \"" << c.reject << "\"}";
+            comma = true;
+        }
+        js << "]}\n";
+    }
     if (tune_cache_enabled()) {
         const std::string path = tune_path(I), tmp = path + ".tmp" + std::to_string(static_cast<long long>(::getpid()));
         {

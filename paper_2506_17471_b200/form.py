@@ -521,6 +521,23 @@ class SynthRng:
         self.state = (self.state + n * 0x9E3779B97F4A7C15) & _MASK64
         return z
 
+    def draws_at(self, idx: np.ndarray) -> np.ndarray:
+        """The outputs at stream positions idx (0 = the next draw) without advancing: splitmix64 is
+        counter-based, so one rank of a partitioned run draws only the entries of its own nodes."""
+        k = np.asarray(idx, dtype=np.uint64) + np.uint64(1)
+        with np.errstate(over="ignore"):
+            z = np.uint64(self.state) + k * _GOLDEN
+            z = (z ^ (z >> np.uint64(30))) * _M1
+            z = (z ^ (z >> np.uint64(27))) * _M2
+            z = z ^ (z >> np.uint64(31))
+        return z
+
+    def skip(self, n: int) -> None:
+        self.state = (self.state + n * 0x9E3779B97F4A7C15) & _MASK64
+
+    def uniform_at(self, lo: float, span: float, idx: np.ndarray) -> np.ndarray:
+        return uniform_from_raw(lo, span, (self.draws_at(idx) >> np.uint64(11)).astype(np.float64))
+
     def next_u64(self) -> int:
         return int(self.draws(1)[0])
 

@@ -160,11 +160,17 @@ def form_map(form: str, sig: FormSignature) -> PointwiseMap:
 
 
 def mesh_problem(form: str, dim: int, degree: int, Q: int, n: int, seed: int = 7, brick: int | None = None,
-                 scale_u0: float = 0.05) -> ProblemInstance:
-    """A ProblemInstance on the structured unit mesh with make_problem's data distributions."""
+                 scale_u0: float = 0.05, mesh=None) -> ProblemInstance:
+    """A ProblemInstance on the structured unit mesh with make_problem's data distributions.
+    `mesh` = (node_map, vertex_map, coords) supplies the mesh arrays instead of the native
+    generator (the reference arm of bench.py builds them without loading libfemgpu)."""
     sig = form_signature(form, dim, degree, Q)
     pmap = form_map(form, sig)
-    node_map, vertex_map, coords, n_nodes, n_verts = unit_mesh(dim, n, degree, brick)
+    if mesh is None:
+        node_map, vertex_map, coords, n_nodes, n_verts = unit_mesh(dim, n, degree, brick)
+    else:
+        node_map, vertex_map, coords = mesh
+        n_nodes, n_verts = (degree * n + 1) ** dim, (n + 1) ** dim
     rng = SynthRng(_seed0(seed))
     tab = _draw_tabulations(sig, rng)
     cells = node_map.shape[0]
@@ -217,8 +223,11 @@ CONFIGS = {
 }
 
 
-def config_problem(name: str, n: int | None = None, seed: int = 7) -> ProblemInstance:
+def config_problem(name: str, n: int | None = None, seed: int = 7, mesh_fn=None) -> ProblemInstance:
+    """Benchmark configuration `name`; mesh_fn(dim, n, degree, brick) -> (node_map, vertex_map,
+    coords) replaces the native mesh generator."""
     c = dict(CONFIGS[name])
     if n is not None:
         c["n"] = n
-    return mesh_problem(c["form"], c["dim"], c["degree"], c["Q"], c["n"], seed=seed)
+    mesh = mesh_fn(c["dim"], c["n"], c["degree"], default_brick(c["dim"])) if mesh_fn else None
+    return mesh_problem(c["form"], c["dim"], c["degree"], c["Q"], c["n"], seed=seed, mesh=mesh)

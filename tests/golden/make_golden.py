@@ -59,6 +59,23 @@ def main():
     inst = os.path.join(os.path.dirname(os.path.abspath(__file__)), "instance_laplace_2d_p2.txt")
     oracle.ref_save_instance(oracle.ref_make_problem("laplace", 2, 2, 6, 16, 7), inst)
     print("wrote", inst)
+    # mesh instances (structured meshes, coefficient / vector-test-space forms) written by the
+    # reference's save_instance_file, with the reference's reference_action output, so the GPU
+    # suite runs reference-written mesh files through the kernels (tests/test_gpu_configs.py)
+    ys = {}
+    for name, args in MESH_FILES.items():
+        import paper_2506_17471_b200 as fg
+        p = fg.mesh_problem(*args)
+        f = os.path.join(os.path.dirname(os.path.abspath(__file__)), name + ".txt")
+        oracle.ref_save_instance(p, f)
+        ys["y:" + name] = oracle.ref_reference_action(oracle.ref_load_instance(f))
+        print("wrote", f)
+    np.savez_compressed(os.path.join(os.path.dirname(os.path.abspath(__file__)), "mesh_instance_outputs.npz"), **ys)
+
+
+# reference-written mesh instance files: (form, dim, degree, Q, n)
+MESH_FILES = {"mesh_helmholtz_coef_2d_p3": ("helmholtz_coef", 2, 3, 12, 3),
+              "mesh_elasticity_3d_p2": ("elasticity", 3, 2, 4, 1)}
 
 
 if __name__ == "__main__":

@@ -50,3 +50,14 @@ def dense_triple_product_problem():
 
 # test_form.cpp:142-193, re-derived with the compiled reference
 DENSE_TRIPLE_PRODUCT_Y = np.array([39.119999999999997, 44.034000000000006, 48.948, 53.862000000000002])
+
+
+def complete_rows(p, m):
+    """Rows of y whose every contribution comes from cells [0, m) (what a reference run over that
+    cell range reproduces exactly)."""
+    tm = p.connectivity.test_map.indices
+    inside = np.zeros(p.output_size, dtype=bool)
+    inside[tm[:m].ravel()] = True
+    if m < tm.shape[0]:
+        inside[tm[m:].ravel()] = False
+    return np.nonzero(inside)[0]

@@ -183,3 +183,12 @@ def test_candidate_files_keep_b200_knobs(tmp_path):
         assert (q.kind, q.scatter, q.group_cells, q.block_cells, q.strict) == (t.kind, t.scatter, t.group_cells,
                                                                                t.block_cells, t.strict)
     assert "b200_mlt" in (tmp_path / "c3.txt").read_text()
+
+
+@pytest.mark.parametrize("name", ["mesh_helmholtz_coef_2d_p3", "mesh_elasticity_3d_p2"])
+def test_reference_written_mesh_instances_load_to_the_golden_y(oracle, name):
+    """Mesh instance files written by the reference (make_golden.py): our reader + the C oracle
+    reproduce the reference's own output bit for bit (no reference needed on this host)."""
+    p = fg.load_instance(os.path.join(GOLDEN, name + ".txt"))
+    gold = np.load(os.path.join(GOLDEN, "mesh_instance_outputs.npz"))["y:" + name]
+    assert np.array_equal(oracle.reference_action(p), gold)
