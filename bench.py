@@ -479,12 +479,28 @@ FORMS_ORDER = ["C1", "C1b", "C2", "C3a", "C3b", "C4", "C5-adv-P1", "C5-adv-P2", 
                "C5-hyp-P1", "C5-hyp-P2", "C5-hyp-P3", "C5-hyp-P4"]
 
 
+def launch_ranks(args):
+    """`--gpus N` without a launcher: start the N ranks (one process per GPU) with
+    torch.distributed.run on 127.0.0.1 and relay rank 0's JSON line."""
+    import socket
+    import subprocess
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, cwd=ROOT)
+
+
 def main():
     args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(launch_ranks(args))
     if args.impl == "reference":
         return run_reference(args)
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1 or args.gpus > 1:
+    if world > 1:
         from paper_2506_17471_b200 import dist
         return dist.bench(args)
     return run_single(args)

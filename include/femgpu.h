@@ -295,6 +295,45 @@ femgpu_status femgpu_action_once(const femgpu_problem* p, double* y_host);
 femgpu_status femgpu_host_alloc(size_t bytes, void** ptr);
 femgpu_status femgpu_host_free(void* ptr);
 
+/* ---- multi-GPU: cell-partitioned action with GPU-to-GPU halo exchange -----
+ * (the reference is single-process.)  One rank per GPU owns a slab of cells
+ * as its own instance (compact local numbering).  Lists are in that local numbering:
+ *   push  (push_peer[i], push_row[i]): rows whose partial sums this rank computes but rank
+ *         push_peer[i] owns; per owner in ascending global-DOF order
+ *   recv  (recv_peer[i], recv_row[i]): owned rows rank recv_peer[i] contributes to, per source in
+ *         the same order as that source's push list to this rank
+ *   pull  (pull_space[i], pull_peer[i], pull_node[i], pull_remote[i]): ghost node pull_node[i] of
+ *         trial space pull_space[i] (scalar spaces first) takes its value from node pull_remote[i]
+ *         of its owner pull_peer[i]
+ * Cells [0, boundary_cells) are the only ones touching shared rows (the local cell order puts
+ * them first); the push of their partial sums overlaps the interior cells.  Owners add what they
+ * receive in ascending rank order (deterministic).  Peer buffers are reached over NVLink (CUDA IPC
+ * across processes, direct pointers within a process); ranks are ordered by device-side flags, so
+ * a step is a fixed launch sequence on one stream with no host synchronisation.  Every rank must
+ * run the same number of actions.  The caller may change owned inputs between actions only once
+ * every rank finished the previous action (e.g. after an all-reduce, as in a Krylov loop). */
+typedef struct femgpu_halo femgpu_halo;
+femgpu_status femgpu_halo_create(femgpu_instance* inst, int32_t rank, int32_t world, int32_t boundary_cells,
+                                 int64_t n_push, const int32_t* push_peer, const int32_t* push_row, int64_t n_recv,
+                                 const int32_t* recv_peer, const int32_t* recv_row, int64_t n_pull,
+                                 const int32_t* pull_space, const int32_t* pull_peer, const int32_t* pull_node,
+                                 const int32_t* pull_remote, femgpu_halo** out);
+femgpu_status femgpu_halo_destroy(femgpu_halo* h);
+/* The bytes this rank publishes (IPC handles and offsets of its flags, receive buffer and input
+ * buffers); *len = the fixed size.  All-gather them over the ranks (any transport). */
+femgpu_status femgpu_halo_export(femgpu_halo* h, void* buf, size_t cap, size_t* len);
+/* The all-gathered exports of ranks 0..world-1, `stride` bytes apart: maps the peers' buffers. */
+femgpu_status femgpu_halo_import(femgpu_halo* h, const void* all, size_t stride);
+/* One distributed action into y_dev (NULL = the instance output): pull ghost inputs, boundary
+ * cells, push (side stream), interior cells, completion of the owned shared rows.  Asynchronous. */
+femgpu_status femgpu_halo_action(femgpu_halo* h, const femgpu_schedule* s, double* y_dev, void* stream);
+/* Exactly `steps` distributed actions on the instance stream, CUDA events, device sync on both
+ * sides: *seconds = this rank's elapsed time (the caller takes the max over ranks). */
+femgpu_status femgpu_halo_time_steps(femgpu_halo* h, const femgpu_schedule* s, int32_t steps, double* seconds);
+/* Synchronizes `stream` (NULL = instance stream) and reports a peer that never reached the
+ * exchange (bounded waits: FEMGPU_HALO_TIMEOUT_MS, default 20000) as FEMGPU_E_CUDA. */
+femgpu_status femgpu_halo_check(femgpu_halo* h, void* stream);
+
 /* ---- instance / candidate files (femsched io.hpp, format_version 1) ------
  * The reference's versioned structured-text format (io.hpp:197-391): doubles with 17
  * significant digits, bit-exact round trip; femgpu_problem_save writes byte-identical text to

@@ -7,13 +7,16 @@
 
 #include "femgpu_internal.hpp"
 
-struct femgpu_instance {
-    std::unique_ptr<femgpu::Instance> impl;
-};
 
 namespace {
 
 thread_local std::string g_last_error;
+
+}  // namespace
+
+void femgpu::set_last_error(const std::string& msg) { g_last_error = msg; }
+
+namespace {
 thread_local int g_device = -1;
 
 template <typename F>

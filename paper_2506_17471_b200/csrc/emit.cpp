@@ -1560,7 +1560,7 @@ EmitResult emit_kernel(const Signature& sig, const KernelPlan& kp) {
     fmas += static_cast<long long>(sig.nW) * sig.Tw;
     // FEMGPU_DEBUG_UNROLL_Q=0/1 overrides the heuristic (I-cache experiments)
     const char* uq = std::getenv("FEMGPU_DEBUG_UNROLL_Q");
-    const bool unroll_q = uq ? std::atoi(uq) != 0 : (!kp.qloop && fmas * sig.Q <= 6000);
+    const bool unroll_q = uq ? std::atoi(uq) != 0 : (!kp.qloop && fmas * sig.Q <= 2000);  // larger bodies: NVRTC time + I-cache
     if (kp.family == Family::Macro) {
         r.kernel = "femgpu_macro";
         r.kernel_checked = "femgpu_macro_checked";
@@ -1592,7 +1592,7 @@ EmitResult emit_kernel(const Signature& sig, const KernelPlan& kp) {
         } else {
             emit_macro_kernel(o, sig, kp, use, unroll_q, r.kernel, 0, ysmem_off);
         }
-        emit_scpt_kernel(o, sig, kp, use, unroll_q, true, r.kernel_checked, 0);
+        emit_scpt_kernel(o, sig, kp, use, false, true, r.kernel_checked, 0);
     } else if (tile) {
         o << kAsync;
         const TilePlan T = plan_tile(sig, kp);
@@ -1600,7 +1600,7 @@ EmitResult emit_kernel(const Signature& sig, const KernelPlan& kp) {
         r.kernel_checked = "femgpu_tile_checked";
         r.smem_bytes = static_cast<size_t>(T.total);
         emit_tile_kernel(o, sig, kp, use, unroll_q, T, r.kernel);
-        emit_scpt_kernel(o, sig, kp, use, unroll_q, true, r.kernel_checked, T.tab_off);
+        emit_scpt_kernel(o, sig, kp, use, false, true, r.kernel_checked, T.tab_off);
     } else {
         r.kernel = "femgpu_scpt";
         r.kernel_checked = "femgpu_scpt_checked";
@@ -1609,7 +1609,7 @@ EmitResult emit_kernel(const Signature& sig, const KernelPlan& kp) {
             emit_scpt_multi_kernel(o, sig, kp, use, unroll_q && kp.G * fmas * sig.Q <= 12000, r.kernel, 0);
         else
             emit_scpt_kernel(o, sig, kp, use, unroll_q, false, r.kernel, 0);
-        emit_scpt_kernel(o, sig, kp, use, unroll_q, true, r.kernel_checked, 0);
+        emit_scpt_kernel(o, sig, kp, use, false, true, r.kernel_checked, 0);
     }
     r.source = o.s.str();
     return r;
@@ -1843,7 +1843,7 @@ EmitResult emit_mlt(const Signature& sig, const KernelPlan& kp) {
     pk.family = Family::Scpt;
     pk.basis = FEMGPU_BASIS_SMEM;
     const bool unroll_q = false;
-    emit_scpt_kernel(o, sig, pk, use, unroll_q, true, r.kernel_checked, 0);
+    emit_scpt_kernel(o, sig, pk, use, false, true, r.kernel_checked, 0);
     r.source = o.s.str();
     r.smem_bytes = std::max<size_t>(r.smem_bytes, static_cast<size_t>(sig.tab_size) * 8);
     return r;
@@ -1875,7 +1875,7 @@ EmitResult emit_dmma(const Signature& sig, const KernelPlan& kp) {
     KernelPlan ck = kp;
     ck.basis = kBasisGlobal;
     ck.min_blocks = 1;
-    emit_scpt_kernel(o, sig, ck, use, fmas * sig.Q <= 6000, true, r.kernel_checked, 0);
+    emit_scpt_kernel(o, sig, ck, use, false, true, r.kernel_checked, 0);  // diagnostic twin: rolled (compile time)
     r.source = o.s.str();
     return r;
 }

@@ -56,7 +56,9 @@ struct Signature {
 };
 
 Signature signature_from(const femgpu_problem* p);
-void dedupe_map(Signature& s);  // commutative value numbering of the map DAG (bit-identical values)
+void dedupe_map(Signature& s);
+std::vector<char> map_live(const Signature& sig);  // emit.cpp: nodes reachable from the outputs
+std::vector<char> map_qdep(const Signature& sig);  // emit.cpp: nodes depending on the quadrature point  // commutative value numbering of the map DAG (bit-identical values)
 
 // Device layout of vector inputs and coordinates: node-major with the components padded to a
 // 16-byte multiple (3D: [node][4]), so a node's components are one aligned 16 B + 8 B pair of
@@ -304,7 +306,28 @@ bool overlapped_zero_action(Instance& inst, const KernelPlan& kp, double* d_y, c
 bool pipelined_host_action(Instance& inst, const KernelPlan& kp, const double* const* scalar_inputs,
                            const double* const* vector_inputs, double* y_host);
 void check_failure(Instance& inst, const KernelPlan& kp, cudaStream_t stream);
+// C-ABI error plumbing shared by the translation units that implement entry points
+void set_last_error(const std::string& msg);
+template <typename F>
+femgpu_status abi_guard(F&& f) {
+    try {
+        f();
+        return FEMGPU_OK;
+    } catch (const Error& e) {
+        set_last_error(e.what());
+        return e.code;
+    } catch (const std::exception& e) {
+        set_last_error(e.what());
+        return FEMGPU_E_INTERNAL;
+    } catch (...) {
+        set_last_error("unknown error");
+        return FEMGPU_E_INTERNAL;
+    }
+}
 }  // namespace femgpu
+struct femgpu_instance {
+    std::unique_ptr<femgpu::Instance> impl;
+};
 const femgpu_problem* femgpu_owned_view(const femgpu_owned_problem* p);
 void femgpu_owned_delete(femgpu_owned_problem* p);
 namespace femgpu {

@@ -48,12 +48,29 @@ femgpu_schedule dmma_variant(int joint, int prefetch, int block, int cells) {
     return s;
 }
 
-// FP64-pipe slots (FMA lanes) per cell of the map DAG evaluated at every quadrature point.
-long long map_ops(const Signature& sig) {
-    long long ops = 0;
-    for (const auto& n : sig.nodes)
-        if (n.op == FEMGPU_OP_ADD || n.op == FEMGPU_OP_MUL) ++ops;
-    return ops;
+// FP64 instructions of the map DAG per cell: (q-dependent, cell-invariant) live ADD/MUL nodes,
+// an ADD fed by a single-use MUL of the same level counted once (contracted to a DFMA).
+std::pair<long long, long long> map_instr(const Signature& sig) {
+    const std::vector<char> live = map_live(sig), qdep = map_qdep(sig);
+    std::vector<int> uses(sig.nodes.size(), 0);
+    for (size_t i = 0; i < sig.nodes.size(); ++i) {
+        const MapNode& n = sig.nodes[i];
+        if (live[i] && (n.op == FEMGPU_OP_ADD || n.op == FEMGPU_OP_MUL)) {
+            ++uses[n.a];
+            ++uses[n.b];
+        }
+    }
+    long long nq = 0, nc = 0;
+    for (size_t i = 0; i < sig.nodes.size(); ++i) {
+        const MapNode& n = sig.nodes[i];
+        if (!live[i] || (n.op != FEMGPU_OP_ADD && n.op != FEMGPU_OP_MUL)) continue;
+        int w = 1;
+        if (n.op == FEMGPU_OP_ADD)
+            for (int c : {n.a, n.b})
+                if (sig.nodes[c].op == FEMGPU_OP_MUL && uses[c] == 1 && qdep[c] == qdep[i]) w = 0;
+        (qdep[i] ? nq : nc) += w;
+    }
+    return {nq, nc};
 }
 
 // Persisted decisions: the timing pass runs once per (form, map, cell count, device) and the winner is
@@ -62,7 +79,7 @@ long long map_ops(const Signature& sig) {
 std::string tune_key(const Instance& I) {
     const Signature& sig = I.sig;
     std::ostringstream k;
-    k << "v5|" << sig.dim << "|" << sig.Q << "|" << sig.nW << "|" << sig.Tw << "|" << I.cells << "|" << I.output_size;
+    k << "v6|" << sig.dim << "|" << sig.Q << "|" << sig.nW << "|" << sig.Tw << "|" << I.cells << "|" << I.output_size;
     for (size_t i = 0; i < sig.sdofs.size(); ++i) k << "|s" << sig.sdofs[i] << ":" << sig.sterms[i];
     for (size_t i = 0; i < sig.vdofs.size(); ++i) {
         k << "|v" << sig.vdofs[i] << ":" << sig.vterms[i];
@@ -159,11 +176,14 @@ femgpu_schedule scpt_variant(int G, int block, int min_blocks, bool qloop) {
     return s;
 }
 
-// Sustained fraction of the FP64 pipe each family reaches when latency is hidden (calibrated
-// on the round-1/2 sweeps: profiles/r02_tuner_calibration.jsonl), and the exposed latency of one
-// work unit's gather chain (index load -> value load, ~2 DRAM round trips) in SM cycles.
-constexpr double kEffMacro = 0.66, kEffScpt = 0.58, kEffDmma = 0.62;
-constexpr double kGatherCycles = 1600.0;
+// Sustained fraction of the FP64 pipe each family reaches, fitted on every candidate of every
+// benchmark configuration timed exhaustively (FEMGPU_TUNE_ALL=1, profiles/r02_tuner_calibration.jsonl):
+// macro 0.64-0.70, SCPT 0.45-0.63 (scalar forms), DMMA 0.56-0.68 of its padded slots; the HBM side
+// reaches ~0.65 of the peak on gather/scatter traffic.  Resident warps hide the gather latency:
+// each warp per SM fewer than the 32 of full occupancy costs ~ kLatency / warps (fitted: 8 warps
+// +15 %, 16 warps +7.5 %); local-memory spills cost ~ spill / kSpillBytes.
+constexpr double kEffMacro = 0.68, kEffScpt = 0.55, kEffDmma = 0.62, kEffHbm = 0.65;
+constexpr double kLatency = 1.2, kSpillBytes = 2048.0;
 
 }  // namespace
 
@@ -197,9 +217,21 @@ void autotune(Instance& I) {
     const double clk = clk_khz * 1e3, lanes = 64.0 * sms;  // FP64 lanes per SM per clock
     // ---- FP64 lane-slots per cell (the paper's "Ops" count on this hardware)
     const double usable_fma = static_cast<double>(sig.usable_flops()) / 2.0;
-    const double map_slots = static_cast<double>(map_ops(sig)) * sig.Q;
+    const std::pair<long long, long long> mi = map_instr(sig);
+    const long long map_q = mi.first, map_c = mi.second;
     const double geo_slots = sig.affine ? 6.0 * sig.dim * sig.dim : 0.0;
-    const double dfma_slots = usable_fma + map_slots + geo_slots;
+    const double dfma_slots = usable_fma + static_cast<double>(map_q) * sig.Q + static_cast<double>(map_c) + geo_slots;
+    // HBM floor: every input, coordinate, output and distinct index array once (SURVEY 8d bytes_alg)
+    double alg_bytes = 8.0 * I.output_size;
+    for (const auto& sp : I.sspaces) alg_bytes += 8.0 * sp.global;
+    for (const auto& sp : I.vspaces) alg_bytes += 8.0 * sp.global * sig.dim;
+    alg_bytes += 8.0 * I.coord_global * sig.dim;
+    for (const auto& m : I.group_maps) alg_bytes += 4.0 * static_cast<double>(m.size());
+    int mem_khz = 0, bus_bits = 0;
+    cudaDeviceGetAttribute(&mem_khz, cudaDevAttrMemoryClockRate, dev);
+    cudaDeviceGetAttribute(&bus_bits, cudaDevAttrGlobalMemoryBusWidth, dev);
+    const double hbm = mem_khz > 0 && bus_bits > 0 ? 2.0 * mem_khz * 1e3 * bus_bits / 8.0 : 8e12;
+    const double t_hbm = alg_bytes / (hbm * kEffHbm);
     // ---- enumerate the schedule space
     std::vector<Cand> C;
     auto add = [&](const femgpu_schedule& sc, int family) {
@@ -217,14 +249,15 @@ void autotune(Instance& I) {
             if (o.label == c.label) return;
         if (family == 2) {
             const DmmaLayout L = dmma_layout(sig, c.kp);
-            const double pad_q = static_cast<double>(4 * L.TQL * L.NCH) / sig.Q;
-            // DMMA slots run at the DMMA rate (measured 37.1 vs 34.2 TF DFMA: x1.085 per slot)
-            c.slots = static_cast<double>(L.nfrag) * 256.0 / 8.0 / 1.085 + map_slots * pad_q + geo_slots;
+            // padded m8n8k4 slots at the DMMA rate (measured 37.1 vs 34.2 TF DFMA: x1.085 per slot);
+            // the map runs per padded quadrature point, the cell-invariant part once per cell
+            c.slots = static_cast<double>(L.nfrag) * 256.0 / 8.0 / 1.085 +
+                      static_cast<double>(map_q) * (4.0 * L.TQL * L.NCH) + static_cast<double>(map_c) + geo_slots;
         } else {
             c.slots = dfma_slots;
         }
         const double eff = family == 0 ? kEffMacro : family == 1 ? kEffScpt : kEffDmma;
-        c.t_pipe = static_cast<double>(I.cells) * c.slots / (lanes * clk) / eff;
+        c.t_pipe = std::max(static_cast<double>(I.cells) * c.slots / (lanes * clk) / eff, t_hbm);
         C.push_back(c);
     };
     add(dfma_default(), 1);  // the paper's SCPT baseline, always timed (b + SCPT)
@@ -301,9 +334,9 @@ void autotune(Instance& I) {
             });
         for (auto& t : pool) t.join();
     }
-    // ---- model with the compiled kernels' attributes: occupancy against the gather latency,
-    // spills rejected
-    const double bytes_floor = 0.0;
+    // ---- model with the compiled kernels' attributes: resident warps against the gather
+    // latency, spills (relative: candidates spilling much more than the least-spilling one are out)
+    long long min_spill = -1;
     for (size_t i : sel) {
         Cand& c = C[i];
         std::shared_ptr<Module> m;
@@ -317,18 +350,14 @@ void autotune(Instance& I) {
         c.regs = m->regs;
         c.spill = m->local_bytes;
         c.warps = m->occupancy * (c.kp.block / 32);
-        const double W = std::max(1.0, c.warps / 4.0);  // warps per SM sub-partition
-        // work unit = one warp's share of one trip through the gather -> compute -> scatter chain
-        double cells_per_warp_unit = 32.0;
-        if (c.family == 0) cells_per_warp_unit = 32.0 * c.kp.G;
-        if (c.family == 1) cells_per_warp_unit = 32.0 * std::max(1, c.kp.G);
-        if (c.family == 2) cells_per_warp_unit = static_cast<double>(c.kp.Nc);
-        const double units = static_cast<double>(I.cells) / cells_per_warp_unit / (4.0 * sms);
-        const double c_unit = 2.0 * cells_per_warp_unit * c.slots / 32.0;  // SMSP cycles at 16 lanes/clk
-        const double lat = (c.family == 2 && c.kp.Tqr > 0) ? kGatherCycles / 4 : kGatherCycles;
-        const double t_lat = units * (c_unit + lat) / W / clk;
-        c.pred = std::max({c.t_pipe, t_lat, bytes_floor});
-        if (c.spill > 0) c.reject = "spills " + std::to_string(c.spill) + " B/thread";
+        if (min_spill < 0 || c.spill < min_spill) min_spill = c.spill;
+    }
+    for (size_t i : sel) {
+        Cand& c = C[i];
+        if (!c.compiled) continue;
+        const double w = std::max(1, c.warps);
+        c.pred = c.t_pipe * (1.0 + kLatency / w) * (1.0 + static_cast<double>(c.spill) / kSpillBytes);
+        if (c.spill > 2 * min_spill + 256) c.reject = "spills " + std::to_string(c.spill) + " B/thread";
         else if (c.warps < 4) c.reject = "occupancy " + std::to_string(c.warps) + " warps/SM";
     }
     std::vector<size_t> ranked;
@@ -382,7 +411,8 @@ void autotune(Instance& I) {
     std::ostringstream log;
     auto us = [](double t) { return static_cast<long long>(t * 1e7) / 10.0; };
     log << "model: " << C.size() << " candidates, " << sel.size() << " compiled, " << first.size()
-        << " timed (FP64 slots/cell: dfma " << static_cast<long long>(dfma_slots) << ")";
+        << " timed (FP64 slots/cell: dfma " << static_cast<long long>(dfma_slots) << "; HBM floor "
+        << us(t_hbm) << " us)";
     for (size_t i : timed)
         if (C[i].timed)
             log << " [" << C[i].label << ": pred " << us(C[i].pred) << " us, meas " << us(C[i].meas) << " us, "

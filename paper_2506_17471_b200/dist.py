@@ -1,46 +1,42 @@
-"""Cell-partitioned multi-GPU action: one process per GPU, torch.distributed
-(NCCL on GPUs, gloo for CPU tests) for the plumbing.
+"""Cell-partitioned multi-GPU action: one process per GPU; torch.distributed (gloo) only
+for the control plane (plan discovery, handle exchange, timing reduction); the data path is
+GPU to GPU inside libfemgpu (csrc/halo.cu: NVLink loads/stores between ranks, device-side flags).
 
 Partition: rank r owns the contiguous cell range [c_r, c_{r+1}) of the brick-major cell order
-(z-slabs of bricks on the structured meshes), aligned to the macro-element group size so every
-rank keeps the compile-time connectivity pattern.  Each rank renumbers the DOFs/vertices its
-cells touch (ascending global index) into a compact local instance.
+(z-slabs of bricks on the structured meshes), aligned to the macro-element group, and builds only
+that slab (femgpu_mesh_build_range; inputs drawn at their global positions of the counter-based
+SynthRng), renumbered compactly (ascending global index) into its own instance.
 
-Ownership: a DOF is owned by the lowest rank touching it.  Per action:
-  1. forward halo: owners send x on shared DOFs to the ranks that also touch them;
-  2. local action on the GPU (femgpu kernels) into the local y;
-  3. reverse halo: non-owners send their partial y on shared DOFs to the owner, which adds
-     them in ascending rank order (deterministic).
-Only interface DOFs move (z-slab interfaces: ~(2N+1)^2 DOFs per neighbour for P2), so the
-exchange is point-to-point send/recv, not an allreduce.
+Discovery (collective, once): every rank publishes the global-index range of each of its maps;
+ranks whose ranges overlap exchange the ids inside the overlap; a DOF/node is owned by the lowest
+rank touching it.  From that each rank derives, in its local numbering:
+  push   rows it computes partial sums for but does not own (per owner, ascending global id)
+  recv   owned rows other ranks contribute to (per source, ascending global id: the same order)
+  pull   ghost trial nodes and their index in the owner's instance (forward halo; every trial
+         space, scalar or vector)
+  serve  owned trial nodes other ranks pull (the owner's side of pull; host emulation only)
+Cells touching a shared row are moved to the front of the local order (whole macro groups), so the
+push overlaps the interior cells on the GPU.  The exchange volume is the slab interfaces only:
+(2N+1)^2 P2 nodes per neighbour for C2 z-slabs.
+
+The same plan drives a host emulation of the exchange (torch.distributed point-to-point, gloo) with
+the local action done by any callable (the CPU oracle in the CPU tests).
 """
 from __future__ import annotations
 
+import ctypes as C
 import json
 import os
 import time
 from dataclasses import dataclass, field
-from typing import Dict, List
+from typing import Dict, List, Optional, Tuple
 
 import numpy as np
 
-from .form import IndexMap, MeshConnectivity, ProblemInstance
+from . import abi
+from .form import IndexMap, MeshConnectivity, ProblemInstance, SynthRng, _draw_tabulations, _seed0
 
-
-@dataclass
-class RankPlan:
-    rank: int
-    cell_range: tuple
-    local: ProblemInstance                      # compact local instance
-    test_global: np.ndarray                     # local test DOF -> global
-    trial_global: List[np.ndarray]              # per trial space (scalar then vector): local node -> global
-    owned_mask: np.ndarray                      # local test DOFs this rank owns
-    # reverse halo (y): to owner q: local indices (sorted by global id); from rank q: local indices
-    y_send: Dict[int, np.ndarray] = field(default_factory=dict)
-    y_recv: Dict[int, np.ndarray] = field(default_factory=dict)
-    # forward halo (x of trial space 0): owner -> ghosts
-    x_send: Dict[int, np.ndarray] = field(default_factory=dict)
-    x_recv: Dict[int, np.ndarray] = field(default_factory=dict)
+# ------------------------------------------------------------------------------- partition
 
 
 def split_cells(cells: int, nranks: int, align: int = 6) -> List[tuple]:
@@ -54,13 +50,84 @@ def split_cells(cells: int, nranks: int, align: int = 6) -> List[tuple]:
     return out
 
 
+def group_align(dim: int) -> int:
+    return 6 if dim == 3 else 4  # one cube (6 Kuhn tets) / two squares: the macro groups
+
+
 def _compact(m: np.ndarray):
     uniq, inv = np.unique(m, return_inverse=True)
     return uniq.astype(np.int64), inv.reshape(m.shape).astype(np.int32)
 
 
+@dataclass
+class Slab:
+    """One rank's compact instance plus the global ids of its local numbering, per map kind."""
+    local: ProblemInstance
+    cell_range: tuple
+    kinds: Dict[str, np.ndarray]          # map kind -> sorted global ids (local index = position)
+    space_kind: List[str]                 # per trial space (scalar then vector): its map kind
+    test_kind: str                        # "node", "vertex" or "node*d" (vector test space)
+    dim: int
+
+
+def slab_instance(form: str, dim: int, degree: int, Q: int, n: int, b: int, e: int, seed: int = 7,
+                  brick: Optional[int] = None, scale_u0: float = 0.05) -> Slab:
+    """Cells [b, e) of mesh_problem(form, dim, degree, Q, n, seed) built without the global mesh:
+    the same maps (rows of femgpu_mesh_build), tabulations and input values (SynthRng draws at the
+    global positions), compactly renumbered.  Equals local_instance(mesh_problem(...), b, e)."""
+    from ._native import check, lib
+    from .mesh import default_brick, form_map, form_signature, mesh_counts
+    brick = default_brick(dim) if brick is None else brick
+    sig = form_signature(form, dim, degree, Q)
+    pmap = form_map(form, sig)
+    _, n_nodes, n_verts, npc = mesh_counts(dim, n, degree)
+    node_map = np.empty((e - b, npc), dtype=np.int32)
+    vertex_map = np.empty((e - b, dim + 1), dtype=np.int32)
+    check(lib().femgpu_mesh_build_range(dim, n, degree, brick, b, e, abi.iptr(node_map), abi.iptr(vertex_map), None))
+    rng = SynthRng(_seed0(seed))
+    tab = _draw_tabulations(sig, rng)
+    nodes_u, nodes_loc = _compact(node_map)
+    verts_u, verts_loc = _compact(vertex_map)
+    kind_of = lambda dofs: "node" if dofs == npc else "vertex"  # noqa: E731  (as mesh_problem)
+    glob = {"node": n_nodes, "vertex": n_verts}
+    ids = {"node": nodes_u, "vertex": verts_u}
+    loc = {"node": nodes_loc, "vertex": verts_loc}
+    conn = MeshConnectivity(cell_count=e - b)
+    sx, vx, space_kind = [], [], []
+    off = 0
+    for s in sig.scalar_spaces:
+        k = kind_of(s.dofs)
+        conn.scalar_maps.append(IndexMap(loc[k], len(ids[k])))
+        sx.append(rng.uniform_at(0.25, 1.0, off + ids[k]))
+        off += glob[k]
+        space_kind.append(k)
+    for i, v in enumerate(sig.vector_spaces):
+        k = kind_of(v.dofs)
+        conn.vector_maps.append(IndexMap(loc[k], len(ids[k])))
+        pos = off + (ids[k][:, None] * dim + np.arange(dim)[None, :]).reshape(-1)
+        x = rng.uniform_at(0.25, 1.0, pos)
+        if form == "hyperelastic" and i == 1:
+            x = x * scale_u0
+        vx.append(x)
+        off += glob[k] * dim
+        space_kind.append(k)
+    if sig.test_dofs == npc:
+        conn.test_map, test_kind = IndexMap(nodes_loc, len(nodes_u)), "node"
+    else:  # vector test space, node-major local order j = a*d + c (as mesh_problem)
+        tm = (nodes_loc[:, :, None].astype(np.int64) * dim + np.arange(dim)[None, None, :]).reshape(e - b, npc * dim)
+        conn.test_map, test_kind = IndexMap(tm.astype(np.int32), len(nodes_u) * dim), "node*d"
+    conn.coord_map = IndexMap(verts_loc, len(verts_u))
+    n1 = n + 1
+    conn.coords = np.stack([((verts_u // n1 ** c) % n1) / n for c in range(dim)], axis=1).astype(np.float64)
+    conn.coord_global_count = len(verts_u)
+    p = ProblemInstance(sig, pmap, tab, conn, sx, vx, conn.test_map.global_count)
+    p.validate()
+    return Slab(p, (b, e), ids, space_kind, test_kind, dim)
+
+
 def local_instance(p: ProblemInstance, b: int, e: int):
-    """Compact sub-instance of cells [b, e) (same restriction as the reference harness)."""
+    """Compact sub-instance of cells [b, e) of a global instance (test reference for slab_instance,
+    and the reference harness's per-thread restriction)."""
     sig, conn = p.signature, p.connectivity
     lc = MeshConnectivity(cell_count=e - b)
     trial_global, sx, vx = [], [], []
@@ -95,194 +162,416 @@ def local_instance(p: ProblemInstance, b: int, e: int):
     return q, ut, trial_global
 
 
-def plan(p: ProblemInstance, nranks: int, align: int = 6) -> List[RankPlan]:
-    ranges = split_cells(p.connectivity.cell_count, nranks, align)
-    plans = []
-    for r, (b, e) in enumerate(ranges):
-        loc, tg, trg = local_instance(p, b, e)
-        plans.append(RankPlan(r, (b, e), loc, tg, trg, np.zeros(len(tg), dtype=bool)))
-    # owner of each global test DOF = lowest rank touching it
-    owner = np.full(p.output_size, nranks, dtype=np.int64)
-    for pl in reversed(plans):
-        owner[pl.test_global] = pl.rank
-    for pl in plans:
-        pl.owned_mask = owner[pl.test_global] == pl.rank
-    for pl in plans:
-        for q in plans:
-            if q.rank == pl.rank:
-                continue
-            common, ia, ib = np.intersect1d(pl.test_global, q.test_global, assume_unique=True, return_indices=True)
-            if common.size == 0:
-                continue
-            # reverse (y): pl -> owner q when q owns; forward (x): owner pl -> q
-            mine_to_q = owner[common] == q.rank
-            if mine_to_q.any():
-                pl.y_send[q.rank] = ia[mine_to_q].astype(np.int64)
-                q.y_recv[pl.rank] = ib[mine_to_q].astype(np.int64)
-            if p.signature.scalar_spaces and np.array_equal(p.connectivity.scalar_maps[0].indices,
-                                                            p.connectivity.test_map.indices):
-                owned_by_pl = owner[common] == pl.rank
-                if owned_by_pl.any():
-                    pl.x_send[q.rank] = ia[owned_by_pl].astype(np.int64)
-                    q.x_recv[pl.rank] = ib[owned_by_pl].astype(np.int64)
-    return plans
+# ------------------------------------------------------------------------------- exchange plan
 
 
-def exchange(plan_: RankPlan, buf, send: Dict[int, np.ndarray], recv: Dict[int, np.ndarray], add: bool, xp):
-    """Point-to-point halo exchange on torch tensors (NCCL or gloo): send buf[send[q]] to q,
-    receive into buf[recv[q]] (added in ascending rank order when add=True)."""
-    import torch.distributed as dist
-    if buf.is_cuda and dist.get_backend() == "gloo":
-        # gloo moves host tensors only: stage through the host (tests run several ranks on one GPU)
-        host = buf.detach().cpu()
-        cpu = lambda d: {q: (v.cpu() if hasattr(v, "cpu") else v) for q, v in d.items()}  # noqa: E731
-        exchange(plan_, host, cpu(send), cpu(recv), add, xp)
-        buf.copy_(host.to(buf.device))
-        return buf
-    ops, recvs = [], []
+@dataclass
+class RankPlan:
+    rank: int
+    world: int
+    cell_range: tuple
+    local: ProblemInstance            # cells ordered boundary-first
+    boundary_cells: int
+    test_global: np.ndarray           # local test row -> global row
+    trial_global: List[np.ndarray]    # per trial space: local node -> global node
+    owned_mask: np.ndarray            # local test rows this rank owns
+    push: Dict[int, np.ndarray] = field(default_factory=dict)   # owner -> local rows (ascending global)
+    recv: Dict[int, np.ndarray] = field(default_factory=dict)   # source -> owned local rows (same order)
+    pull: List[Dict[int, Tuple[np.ndarray, np.ndarray]]] = field(default_factory=list)  # per space: owner -> (local, owner-local)
+    serve: List[Dict[int, np.ndarray]] = field(default_factory=list)  # per space: puller -> owned local nodes
+
+    def halo_rows(self) -> int:
+        return int(sum(len(v) for v in self.push.values()) + sum(len(v) for v in self.recv.values()))
+
+
+def _shared(my_ids: np.ndarray, their_ids: np.ndarray, their_pos: np.ndarray):
+    """(global ids, my local positions, their local positions) of the common ids."""
+    common, ia, ib = np.intersect1d(my_ids, their_ids, assume_unique=True, return_indices=True)
+    return common, ia.astype(np.int64), their_pos[ib].astype(np.int64)
+
+
+def discover(kinds: Dict[str, np.ndarray], rank: int, world: int, gather) -> Dict[str, Dict[int, tuple]]:
+    """Per map kind: {q: (shared global ids, my positions, q's positions)} for every rank q sharing
+    ids with this one.  `gather(obj)` all-gathers a picklable object over the ranks.  Only the ids
+    inside overlapping global ranges travel (the slab interfaces on partitions with locality)."""
+    rng = {k: (int(v[0]), int(v[-1])) if len(v) else (1, 0) for k, v in kinds.items()}
+    ranges = gather(rng)
+    offer = {}
+    for k, ids in kinds.items():
+        offer[k] = {}
+        for q in range(world):
+            if q == rank:
+                continue
+            lo, hi = ranges[q][k]
+            if hi < lo or not len(ids):
+                continue
+            a, z = np.searchsorted(ids, lo), np.searchsorted(ids, hi, side="right")
+            if z > a:
+                offer[k][q] = (ids[a:z], np.arange(a, z, dtype=np.int64))
+    offers = gather(offer)
+    out = {}
+    for k, ids in kinds.items():
+        out[k] = {}
+        for q in range(world):
+            if q == rank or rank not in offers[q][k]:
+                continue
+            their_ids, their_pos = offers[q][k][rank]
+            common, mine, theirs = _shared(ids, their_ids, their_pos)
+            if common.size:
+                out[k][q] = (common, mine, theirs)
+    return out
+
+
+def _owner_of(n_local: int, shared: Dict[int, tuple], rank: int) -> np.ndarray:
+    owner = np.full(n_local, rank, dtype=np.int64)
+    for q, (_, mine, _) in shared.items():
+        owner[mine] = np.minimum(owner[mine], q)
+    return owner
+
+
+def _expand_rows(shared_nodes: Dict[int, tuple], dim: int) -> Dict[int, tuple]:
+    """Node sharing -> row sharing of an interleaved vector test space (row = node*dim + c)."""
+    out = {}
+    for q, (g, mine, theirs) in shared_nodes.items():
+        c = np.arange(dim)[None, :]
+        out[q] = ((g[:, None] * dim + c).reshape(-1), (mine[:, None] * dim + c).reshape(-1),
+                  (theirs[:, None] * dim + c).reshape(-1))
+    return out
+
+
+def build_plan(slab: Slab, rank: int, world: int, gather) -> RankPlan:
+    """Collective: the exchange plan of this rank's slab (see the module docstring)."""
+    p = slab.local
+    shared = discover(slab.kinds, rank, world, gather)
+    test_shared = shared["node"] if slab.test_kind == "node" else (
+        shared["vertex"] if slab.test_kind == "vertex" else _expand_rows(shared["node"], slab.dim))
+    if slab.test_kind == "node*d":
+        test_global = (slab.kinds["node"][:, None] * slab.dim + np.arange(slab.dim)[None, :]).reshape(-1)
+    else:
+        test_global = slab.kinds[slab.test_kind]
+    n_rows = p.output_size
+    owner = _owner_of(n_rows, test_shared, rank)
+    push, recv = {}, {}
+    shared_row = np.zeros(n_rows, dtype=bool)
+    for q, (g, mine, _) in sorted(test_shared.items()):
+        shared_row[mine] = True
+        order = np.argsort(g, kind="stable")
+        mine = mine[order]
+        to_q = owner[mine] == q
+        if to_q.any():
+            push[q] = mine[to_q]
+        mine_owned = owner[mine] == rank
+        if mine_owned.any():
+            recv[q] = mine[mine_owned]
+    # boundary-first cell order (whole macro groups: the compile-time group pattern survives)
+    G = group_align(slab.dim)
+    tm = p.connectivity.test_map.indices
+    cells = tm.shape[0]
+    touch = shared_row[tm].any(axis=1)
+    if cells % G == 0:
+        grp = touch.reshape(-1, G).any(axis=1)
+        perm = np.concatenate([np.nonzero(grp)[0], np.nonzero(~grp)[0]])
+        perm = (perm[:, None] * G + np.arange(G)[None, :]).reshape(-1)
+        nb = int(grp.sum()) * G
+    else:
+        perm = np.arange(cells)
+        nb = cells
+    local = _permute_cells(p, perm)
+    pull, serve, trial_global = [], [], []
+    for s, k in enumerate(slab.space_kind):
+        ids = slab.kinds[k]
+        trial_global.append(ids)
+        own = _owner_of(len(ids), shared[k], rank)
+        ps, sv = {}, {}
+        for q, (g, mine, theirs) in sorted(shared[k].items()):
+            order = np.argsort(g, kind="stable")
+            mine, theirs = mine[order], theirs[order]
+            from_q = own[mine] == q
+            if from_q.any():
+                ps[q] = (mine[from_q], theirs[from_q])
+            # q pulls from me the shared nodes I own (q > me: the owner is the lowest rank)
+            q_ghost = own[mine] == rank
+            if q_ghost.any() and q > rank:
+                sv[q] = mine[q_ghost]
+        pull.append(ps)
+        serve.append(sv)
+    return RankPlan(rank, world, slab.cell_range, local, nb, test_global, trial_global, owner == rank,
+                    push, recv, pull, serve)
+
+
+def _permute_cells(p: ProblemInstance, perm: np.ndarray) -> ProblemInstance:
+    if np.array_equal(perm, np.arange(len(perm))):
+        return p
+    conn = p.connectivity
+    c = MeshConnectivity(cell_count=conn.cell_count)
+    c.scalar_maps = [IndexMap(np.ascontiguousarray(m.indices[perm]), m.global_count) for m in conn.scalar_maps]
+    c.vector_maps = [IndexMap(np.ascontiguousarray(m.indices[perm]), m.global_count) for m in conn.vector_maps]
+    c.test_map = IndexMap(np.ascontiguousarray(conn.test_map.indices[perm]), conn.test_map.global_count)
+    if p.signature.affine_geometry:
+        c.coord_map = IndexMap(np.ascontiguousarray(conn.coord_map.indices[perm]), conn.coord_map.global_count)
+        c.coords = conn.coords
+        c.coord_global_count = conn.coord_global_count
+    q = ProblemInstance(p.signature, p.map, p.tabulations, c, p.scalar_inputs, p.vector_inputs, p.output_size)
+    q.validate()
+    return q
+
+
+def config_slab(name: str, rank: int, world: int, n: Optional[int] = None, seed: int = 7) -> Slab:
+    from .mesh import CONFIGS, mesh_counts
+    c = dict(CONFIGS[name])
+    if n is not None:
+        c["n"] = n
+    cells = mesh_counts(c["dim"], c["n"], c["degree"])[0]
+    b, e = split_cells(cells, world, group_align(c["dim"]))[rank]
+    return slab_instance(c["form"], c["dim"], c["degree"], c["Q"], c["n"], b, e, seed=seed)
+
+
+def torch_gather():
+    import torch.distributed as tdist
+
+    def gather(obj):
+        out = [None] * tdist.get_world_size()
+        tdist.all_gather_object(out, obj)
+        return out
+    return gather
+
+
+# ------------------------------------------------------------------------------- device path
+
+
+class DistInstance:
+    """One rank's GPU instance + its halo (femgpu_halo_*): distributed actions with the exchange
+    GPU to GPU (csrc/halo.cu).  Collective construction (handle exchange over `gather`)."""
+
+    def __init__(self, plan: RankPlan, gather):
+        from . import action as fa
+        from ._native import lib
+        self.plan = plan
+        self.inst = fa.GpuInstance(plan.local)
+        L = lib()
+
+        def cat(parts):
+            return np.concatenate(parts) if parts else np.zeros(0)
+
+        push_peer = cat([np.full(len(v), q) for q, v in sorted(plan.push.items())])
+        push_row = cat([v for _, v in sorted(plan.push.items())])
+        recv_peer = cat([np.full(len(v), q) for q, v in sorted(plan.recv.items())])
+        recv_row = cat([v for _, v in sorted(plan.recv.items())])
+        ps, pp, pn, pr = [], [], [], []
+        for s, d in enumerate(plan.pull):
+            for q, (mine, theirs) in sorted(d.items()):
+                ps.append(np.full(len(mine), s))
+                pp.append(np.full(len(mine), q))
+                pn.append(mine)
+                pr.append(theirs)
+        self._keep = [np.ascontiguousarray(np.asarray(x, dtype=np.int32))
+                      for x in (push_peer, push_row, recv_peer, recv_row, cat(ps), cat(pp), cat(pn), cat(pr))]
+        ptr = [a.ctypes.data_as(C.POINTER(C.c_int32)) for a in self._keep]
+        h = C.c_void_p()
+        fa._call(L.femgpu_halo_create(self.inst.handle, plan.rank, plan.world, plan.boundary_cells,
+                                      len(self._keep[0]), ptr[0], ptr[1], len(self._keep[2]), ptr[2], ptr[3],
+                                      len(self._keep[4]), ptr[4], ptr[5], ptr[6], ptr[7], C.byref(h)))
+        self.halo = h
+        n = C.c_size_t()
+        fa._call(L.femgpu_halo_export(h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        fa._call(L.femgpu_halo_export(h, buf, n.value, C.byref(n)))
+        blob = b"".join(gather(bytes(buf.raw)))
+        fa._call(L.femgpu_halo_import(h, blob, n.value))
+
+    def action(self, params=None, y_dev: int = 0, stream: int = 0):
+        from . import action as fa
+        from ._native import lib
+        sp = fa._sched(params)
+        fa._call(lib().femgpu_halo_action(self.halo, sp[0] if sp else None, C.c_void_p(y_dev), C.c_void_p(stream)))
+
+    def time_steps(self, steps: int, params=None) -> float:
+        from . import action as fa
+        from ._native import lib
+        s = C.c_double()
+        sp = fa._sched(params)
+        fa._call(lib().femgpu_halo_time_steps(self.halo, sp[0] if sp else None, steps, C.byref(s)))
+        return s.value
+
+    def check(self, stream: int = 0):
+        from . import action as fa
+        from ._native import lib
+        fa._call(lib().femgpu_halo_check(self.halo, C.c_void_p(stream)))
+
+    def owned_output(self) -> Tuple[np.ndarray, np.ndarray]:
+        """(global rows, values) of the rows this rank owns (complete after an action)."""
+        y = self.inst.read_output()
+        m = self.plan.owned_mask
+        return self.plan.test_global[m], y[m]
+
+    def close(self):
+        from ._native import lib
+        if self.halo:
+            lib().femgpu_halo_destroy(self.halo)
+            self.halo = None
+        self.inst.close()
+
+
+# ------------------------------------------------------------------------------- host emulation
+
+
+def host_exchange(buf, send: Dict[int, np.ndarray], recv: Dict[int, np.ndarray], add: bool):
+    """Point-to-point exchange of torch CPU tensors over torch.distributed (gloo): send buf[send[q]]
+    to q, receive into buf[recv[q]], adding in ascending rank order when add=True."""
+    import torch
+    import torch.distributed as tdist
+    ops, got = [], []
     for q in sorted(set(send) | set(recv)):
         if q in send:
-            ops.append(dist.P2POp(dist.isend, buf[send[q]].contiguous(), q))
+            ops.append(tdist.P2POp(tdist.isend, buf[torch.as_tensor(send[q])].contiguous(), q))
         if q in recv:
-            t = xp.empty(len(recv[q]), dtype=buf.dtype, device=buf.device)
-            recvs.append((q, t))
-            ops.append(dist.P2POp(dist.irecv, t, q))
+            t = torch.empty(len(recv[q]), dtype=buf.dtype)
+            got.append((q, t))
+            ops.append(tdist.P2POp(tdist.irecv, t, q))
     if ops:
-        for w in dist.batch_isend_irecv(ops):
+        for w in tdist.batch_isend_irecv(ops):
             w.wait()
-    for q, t in sorted(recvs, key=lambda x: x[0]):
+    for q, t in sorted(got, key=lambda x: x[0]):
+        idx = torch.as_tensor(recv[q])
         if add:
-            buf.index_add_(0, recv[q], t)
+            buf.index_add_(0, idx, t)
         else:
-            buf[recv[q]] = t
+            buf[idx] = t
     return buf
 
 
-def _index_tensors(pl: RankPlan, device):
+def host_halo_action(plan: RankPlan, local_apply, xs: Optional[List[np.ndarray]] = None) -> np.ndarray:
+    """The distributed action with the plan's exchanges on the host (gloo) and the local compute
+    by local_apply(problem) -> y: pull of ghost trial nodes from their owners (every space, vector
+    spaces node-wise), local action, push of partial rows to the owners, owners add in ascending
+    rank order.  xs: this rank's local trial inputs (owned values current; ghosts refreshed here)."""
     import torch
-    conv = lambda d: {q: torch.as_tensor(v, device=device) for q, v in d.items()}  # noqa: E731
-    return conv(pl.y_send), conv(pl.y_recv), conv(pl.x_send), conv(pl.x_recv)
+    p = plan.local
+    xs = [np.array(x, dtype=np.float64) for x in (xs if xs is not None else list(p.scalar_inputs) + list(p.vector_inputs))]
+    d = p.signature.dim
+    ns = len(p.scalar_inputs)
+    for s, x in enumerate(xs):
+        comps = 1 if s < ns else d
+        t = torch.as_tensor(x.reshape(-1, comps).copy())
+        recv = {q: mine for q, (mine, _) in plan.pull[s].items()}
+        for c in range(comps):
+            col = t[:, c].contiguous()
+            host_exchange(col, plan.serve[s], recv, False)
+            t[:, c] = col
+        xs[s] = t.numpy().reshape(-1).copy()
+    q = ProblemInstance(p.signature, p.map, p.tabulations, p.connectivity, xs[:ns], xs[ns:], p.output_size)
+    y = torch.as_tensor(np.asarray(local_apply(q), dtype=np.float64).copy())
+    host_exchange(y, plan.push, plan.recv, True)
+    return y.numpy()
 
 
-class _CudaArray:
-    """Zero-copy torch view of a libfemgpu device buffer (__cuda_array_interface__)."""
+def rank_slab(name_or_args, rank: int, world: int, n: Optional[int] = None) -> Slab:
+    if isinstance(name_or_args, str):
+        return config_slab(name_or_args, rank, world, n=n)
+    form, dim, degree, Q, nn = name_or_args
+    from .mesh import mesh_counts
+    cells = mesh_counts(dim, nn, degree)[0]
+    b, e = split_cells(cells, world, group_align(dim))[rank]
+    return slab_instance(form, dim, degree, Q, nn, b, e)
 
-    def __init__(self, ptr, n):
-        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False), "version": 3}
+
+def cpu_action_with_halo(name_or_args, rank: int, world: int, action, n: Optional[int] = None):
+    """CPU leg for the gloo tests: this rank's slab, the collective plan and the host exchange with
+    `action` (the oracle) as local compute; returns (owned global rows, owned y)."""
+    plan = build_plan(rank_slab(name_or_args, rank, world, n), rank, world, torch_gather())
+    y = host_halo_action(plan, action)
+    m = plan.owned_mask
+    return plan.test_global[m], y[m]
+
+
+# ------------------------------------------------------------------------------- bench leg
 
 
 def bench(args):
-    """Multi-GPU bench leg (torchrun): strong scaling of the C2 action on the fixed mesh."""
+    """Multi-GPU bench leg (one process per GPU): strong scaling of the action on the fixed mesh,
+    each rank building only its slab, halos GPU to GPU; max over ranks of the CUDA-event step time;
+    rank 0 checks the gathered owned rows against the reference CPU action."""
     import torch
-    import torch.distributed as dist
+    import torch.distributed as tdist
 
-    import paper_2506_17471_b200 as fg
-    from paper_2506_17471_b200._native import lib
+    from . import action as fa
+    from ._native import lib
+    from .mesh import CONFIGS, mesh_counts
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    device = local_rank % max(1, torch.cuda.device_count())
-    torch.cuda.set_device(device)
-    backend = os.environ.get("FEMGPU_DIST_BACKEND", "nccl")  # gloo: functional tests with ranks sharing a GPU
-    if backend == "nccl":
-        dist.init_process_group("nccl", device_id=torch.device("cuda", device))
-    else:
-        dist.init_process_group(backend)
+    ndev = max(1, fa.device_count())
+    device = local_rank % ndev
+    tdist.init_process_group("gloo")  # control plane only; the data path is csrc/halo.cu
+    gather = torch_gather()
     lib().femgpu_set_device(device)
-    p = fg.config_problem(args.config, n=args.n)
-    plans = plan(p, world)
-    pl = plans[rank]
-    g = fg.GpuInstance(pl.local)
-    dev = torch.device("cuda", device)
-    ysend, yrecv, xsend, xrecv = _index_tensors(pl, dev)
-    y = torch.zeros(pl.local.output_size, dtype=torch.float64, device=dev)
-    import ctypes as C
-    x = None
-    if pl.x_send or pl.x_recv:
-        # forward halo of trial space 0 (scalar, same numbering as the test space)
-        xp = C.c_void_p()
-        lib().femgpu_device_input(g.handle, 0, C.byref(xp))
-        x = torch.as_tensor(_CudaArray(xp.value, pl.local.scalar_inputs[0].size), device=dev)
-    stream = torch.cuda.current_stream(dev)
-
-    def step():
-        if x is not None:
-            exchange(pl, x, xsend, xrecv, False, torch)
-        g.action_device(y_dev=y.data_ptr(), stream=stream.cuda_stream or 1)
-        exchange(pl, y, ysend, yrecv, True, torch)
-
+    torch.cuda.set_device(device)
+    t0 = time.perf_counter()
+    slab = config_slab(args.config, rank, world, n=args.n)
+    plan = build_plan(slab, rank, world, gather)
+    t_plan = time.perf_counter() - t0
+    di = DistInstance(plan, gather)
+    di.inst.action()  # JIT + automatic schedule of the local instance (outside the timed region)
+    tdist.barrier()
     for _ in range(max(args.warmup, 3)):
-        step()
-    dist.barrier()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        step()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    dist.barrier()
-    t = torch.tensor([e0.elapsed_time(e1) * 1e-3 / args.steps], dtype=torch.float64,
-                     device=dev if backend == "nccl" else "cpu")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        di.action()
+    di.check()
+    tdist.barrier()
+    t_rank = di.time_steps(args.steps) / args.steps
+    di.check()
+    t = torch.tensor([t_rank], dtype=torch.float64)
+    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
     t_step = float(t.item())
-    # parity: gather owned y to rank 0 and compare with the single-instance GPU result
-    gdev = dev if backend == "nccl" else torch.device("cpu")  # gloo collectives on host tensors
-    owned = y[torch.as_tensor(np.nonzero(pl.owned_mask)[0], device=dev)].to(gdev)
-    gids = torch.as_tensor(pl.test_global[pl.owned_mask], device=gdev)
-    sizes = [None] * world
-    dist.all_gather_object(sizes, int(owned.numel()))
-    mx = max(sizes)
-    pad = lambda t: torch.cat([t, t.new_zeros(mx - t.numel())])  # noqa: E731  (all_gather needs equal sizes)
-    outs = [torch.empty(mx, dtype=torch.float64, device=gdev) for _ in sizes]
-    ids = [torch.empty(mx, dtype=torch.int64, device=gdev) for _ in sizes]
-    dist.all_gather(outs, pad(owned))
-    dist.all_gather(ids, pad(gids))
-    outs = [o[:s] for o, s in zip(outs, sizes)]
-    ids = [i[:s] for i, s in zip(ids, sizes)]
+    gids, ys = di.owned_output()
+    parts = gather((gids, ys))
+    stats = gather({"rank": rank, "device": device, "cells": int(plan.local.connectivity.cell_count),
+                    "boundary_cells": plan.boundary_cells, "halo_rows": plan.halo_rows(),
+                    "pull_nodes": int(sum(len(m) for d in plan.pull for m, _ in d.values())),
+                    "step_us": t_rank * 1e6, "plan_s": round(t_plan, 2),
+                    "schedule": di.inst.describe().split(" | auto: ")[0]})
     if rank == 0:
-        yfull = np.zeros(p.output_size)
-        for o, i in zip(outs, ids):
-            yfull[i.cpu().numpy()] = o.cpu().numpy()
-        halo = sum(len(v) for v in pl.y_send.values()) + sum(len(v) for v in pl.y_recv.values())
+        c = dict(CONFIGS[args.config])
+        if args.n is not None:
+            c["n"] = args.n
+        cells = mesh_counts(c["dim"], c["n"], c["degree"])[0]
+        dofs = sum(len(g) for g, _ in parts)
         out = {
-            "metric": "FP64 operator-action GDOF/s", "value": p.output_size / t_step / 1e9, "unit": "GDOF/s",
+            "metric": "FP64 operator-action GDOF/s", "value": dofs / t_step / 1e9, "unit": "GDOF/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "%s cell-partitioned over %d GPUs (contiguous brick-major ranges), %s"
-                                   "action + reverse y halo over %s per step"
-                                   % (args.config, world, "forward x halo + " if x is not None else
-                                      "(x static: no forward halo planned for this trial space) + ", backend.upper()),
-                       "cells": int(p.connectivity.cell_count), "dofs": int(p.output_size),
-                       "rank0_halo_dofs": int(halo), "parallelism": "cells%d" % world},
-            "gpu_launches": args.steps,
+            "config": {"workload": "%s cell-partitioned over %d ranks (contiguous brick-major slabs, each rank builds "
+                                   "only its own); per step: ghost inputs pulled from their owners, boundary cells, "
+                                   "partial rows pushed to their owners over NVLink (CUDA IPC / peer pointers, "
+                                   "device-side flags) overlapping the interior cells, owned rows completed in "
+                                   "ascending rank order" % (args.config, world),
+                       "cells": int(cells), "dofs": int(dofs), "parallelism": "cells%d" % world,
+                       "devices_visible": ndev, "control_plane": "torch.distributed gloo (plan + handle exchange)"},
+            "gpu_launches": args.steps * max(1, di.inst.stats()["launches_last_action"]),
+            "ranks": stats,
         }
-        with fg.GpuInstance(p) as gi:
-            ref = gi.action()
-        out["parity_vs_1gpu_rel_l2"] = float(np.linalg.norm(yfull - ref) / np.linalg.norm(ref))
-        out["backend"] = backend
-        print(json.dumps(out))
-    dist.destroy_process_group()
-    g.close()
-
-
-def cpu_action_with_halo(p: ProblemInstance, rank: int, world: int, action):
-    """CPU leg for the gloo tests: the same plan and exchange, local compute by `action`
-    (the oracle), returning (owned global ids, owned y)."""
-    import torch
-    plans = plan(p, world)
-    pl = plans[rank]
-    ys, yr, xs, xr = (
-        {q: torch.as_tensor(v) for q, v in d.items()} for d in (pl.y_send, pl.y_recv, pl.x_send, pl.x_recv))
-    x = torch.as_tensor(pl.local.scalar_inputs[0].copy()) if pl.local.scalar_inputs else None
-    if x is not None:
-        # ghosts start stale (zero) and must be filled by the forward halo from the owners
-        ghost = np.concatenate([v for v in pl.x_recv.values()]) if pl.x_recv else np.zeros(0, dtype=np.int64)
-        x[torch.as_tensor(ghost)] = 0.0
-        exchange(pl, x, xs, xr, False, torch)
-        pl.local.scalar_inputs[0] = x.numpy().copy()
-    y = torch.as_tensor(action(pl.local))
-    exchange(pl, y, ys, yr, True, torch)
-    m = pl.owned_mask
-    return pl.test_global[m], y.numpy()[m]
+        y = np.full(dofs, np.nan)
+        for g, v in parts:
+            y[g] = v
+        out["parity_complete"] = bool(not np.isnan(y).any())
+        if not args.no_cpu_baseline:
+            from . import mesh as fm
+            p = fm.config_problem(args.config, n=args.n)
+            try:
+                from oracle import oracle  # the checker (reference build) on rank 0
+                if oracle.ref_available():
+                    _, ref = oracle.ref_time_threads(p, max(1, min(os.cpu_count() or 1, 64)), reps=1)
+                    kind = "oracle/_ref reference_action, full workload"
+                else:
+                    ref = oracle.reference_action(p)
+                    kind = "C restatement (oracle/femoracle.c), full workload"
+                rel = float(np.linalg.norm(y - ref) / np.linalg.norm(ref))
+                mx = float(np.max(np.abs(y - ref) / np.maximum(np.abs(ref), 1e-30)))
+                out["parity_vs_reference"] = {"rel_l2": rel, "max_rel": mx, "reference": kind,
+                                              "pass": bool(rel <= 1e-12 and mx <= 1e-10)}
+            except Exception as e:  # noqa: BLE001
+                out["parity_vs_reference"] = {"error": str(e)[:200]}
+        print(json.dumps(out), flush=True)
+    tdist.barrier()
+    di.close()
+    tdist.destroy_process_group()

@@ -105,32 +105,51 @@ def cg(apply: Callable, b, x0=None, rtol: float = 1e-10, maxiter: int = 1000,
     return x, maxiter, hist
 
 
-def dist_cg(plan_, local_apply: Callable, b_local, rtol: float = 1e-10, maxiter: int = 1000, check_every: int = 1):
-    """Distributed CG over the cell partition of dist.plan (one rank per GPU, persistent halos).
+def dist_cg(plan_, dist_apply: Callable, b_local, rtol: float = 1e-10, maxiter: int = 1000, check_every: int = 1):
+    """Distributed CG over the cell partition of dist.build_plan (one rank per GPU).
 
-    Vectors live in the rank's local test numbering (owned DOFs + ghosts).  Per iteration: forward halo
-    of the search direction (owners -> ghosts, dist.exchange), the local action `local_apply(v, out)`,
-    reverse halo of the partial products (ghost contributions -> owners, summed in ascending rank
-    order), and all-reduced dot products over owned DOFs.  Requires a scalar trial space numbered like
-    the test space (plan_.x_send / x_recv); the halo index tensors are built once (persistent)."""
+    Vectors live in the rank's local test numbering (owned rows + ghosts; the trial space is numbered
+    like the test space).  `dist_apply(v, out)` is the complete distributed action -- ghost inputs
+    pulled from their owners, local action, partial rows pushed to their owners -- either on the
+    device (DistOperator: csrc/halo.cu, GPU to GPU) or emulated on the host (dist.host_halo_action);
+    afterwards only owned rows are meaningful and ghost rows are zeroed.  Dots run over owned rows and
+    are all-reduced; each all-reduce also orders the ranks' input updates after every rank's pulls."""
     import torch
     import torch.distributed as dist
-
-    from .dist import exchange
-    dev = b_local.device
-    conv = lambda d: {q: torch.as_tensor(v, device=dev) for q, v in d.items()}  # noqa: E731
-    xs, xr, ys, yr = conv(plan_.x_send), conv(plan_.x_recv), conv(plan_.y_send), conv(plan_.y_recv)
-    owned = torch.as_tensor(plan_.owned_mask, device=dev)
+    owned = torch.as_tensor(plan_.owned_mask, device=b_local.device)
 
     def dot(a, c):
-        t = torch.sum(a[owned] * c[owned]).reshape(1)
+        t = torch.sum(a[owned] * c[owned]).reshape(1).cpu()
         dist.all_reduce(t)
-        return t[0]
+        return t[0].to(a.device)
 
     def apply(v, out):
-        exchange(plan_, v, xs, xr, False, torch)   # ghosts of v <- owners
-        local_apply(v, out)
-        exchange(plan_, out, ys, yr, True, torch)  # owners += ghost partial products
+        dist_apply(v, out)
         out[~owned] = 0.0
 
     return cg(apply, b_local, rtol=rtol, maxiter=maxiter, check_every=check_every, dot=dot)
+
+
+class DistOperator:
+    """Distributed y = A x on the devices: a dist.DistInstance (scalar trial space 0 numbered like the
+    test space); apply(v, out) writes v into the instance input, runs the halo action into out."""
+
+    def __init__(self, di):
+        import torch
+        self.di = di
+        p = di.plan.local
+        if p.signature.vector_spaces or len(p.signature.scalar_spaces) != 1:
+            raise ValueError("DistOperator: one scalar trial space required")
+        n = int(p.output_size)
+        xp = C.c_void_p()
+        _call(lib().femgpu_device_input(di.inst.handle, 0, C.byref(xp)))
+        self.dev = torch.device("cuda", torch.cuda.current_device())
+        self.x = torch.as_tensor(_CudaArray(xp.value, n), device=self.dev)
+        self.launches = 0
+
+    def apply(self, v, out) -> None:
+        import torch
+        self.x.copy_(v)
+        stream = torch.cuda.current_stream(self.dev).cuda_stream or 1
+        self.di.action(y_dev=out.data_ptr(), stream=stream)
+        self.launches += 1

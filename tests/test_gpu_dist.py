@@ -1,81 +1,180 @@
-"""End-to-end multi-process run of the multi-GPU bench path (bench.py under torch.distributed.run,
-paper_2506_17471_b200/dist.py) on the one GPU this environment provides: two ranks share cuda:0 and
-exchange halos over gloo (FEMGPU_DIST_BACKEND=gloo; NCCL refuses two ranks on one device).  Checks the
-partitioned action (local GPU kernels + reverse y halo, forward x halo where planned) against the
-single-instance GPU result: rel L2 <= 1e-12.  The NCCL transport itself needs >= 2 GPUs."""
+"""GPU tests of the cell-partitioned action with the GPU-to-GPU exchange (csrc/halo.cu).
+
+The box has one GPU, so ranks share cuda:0:
+* in one process, one thread per rank (peer pointers used directly, kernels of the ranks run
+  concurrently): world 2 and 3, scalar / vector / coefficient forms, inputs changing between
+  actions (ghost inputs poisoned with NaN on the device: the pull must refill them), and a
+  distributed CG through DistOperator;
+* two processes launched by bench.py --gpus 2 itself (CUDA IPC path, the multi-GPU bench leg):
+  parity of the gathered owned rows against the reference CPU action."""
+import ctypes as C
 import json
 import os
-import socket
 import subprocess
 import sys
+import threading
 
+import numpy as np
 import pytest
+
+import paper_2506_17471_b200 as fg
+from paper_2506_17471_b200 import dist as fdist
+from tests.helpers import max_rel, rel_l2
+from tests.test_dist import ThreadGather
 
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _port():
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    p = s.getsockname()[1]
-    s.close()
-    return p
+@pytest.fixture(scope="module", autouse=True)
+def need_gpu():
+    if fg.device_count() < 1:
+        pytest.fail("no CUDA device visible: the gpu-marked tests require a B200")
 
 
-@pytest.mark.parametrize("config,n", [("C2", 10), ("C4", 8), ("C3a", 40)])
-def test_two_ranks_on_one_gpu_match_single_instance(config, n):
-    env = dict(os.environ, FEMGPU_DIST_BACKEND="gloo", FEMGPU_AUTOTUNE="0")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "2",
-           "--config", config, "--mesh-n", str(n), "--steps", "3", "--warmup", "3"]
-    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
-    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[:6000]
-    line = [l for l in r.stdout.splitlines() if l.startswith("{")][-1]
-    out = json.loads(line)
-    assert out["n_gpus"] == 2 and out["backend"] == "gloo"
-    assert out["parity_vs_1gpu_rel_l2"] <= 1e-12, out
+def run_ranks(world, fn):
+    """fn(rank, gather) in `world` threads; re-raises the first failure."""
+    tg = ThreadGather(world)
+    res, err = [None] * world, []
+
+    def body(r):
+        try:
+            from paper_2506_17471_b200._native import lib
+            lib().femgpu_set_device(0)
+            res[r] = fn(r, tg.for_rank(r))
+        except BaseException as e:  # noqa: BLE001
+            err.append(e)
+            tg.bar.abort()
+    th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if err:
+        raise err[0]
+    return res
 
 
-def _cg_worker(rank, world, port, out_dir):
-    import numpy as np
+def device_view(inst, space, n, comps, stride):
     import torch
-    import torch.distributed as dist
-
-    import paper_2506_17471_b200 as fg
-    from paper_2506_17471_b200 import dist as fdist
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    torch.cuda.set_device(0)
-    p = fg.symmetric_problem("helmholtz", 3, 2, 14, 4)
-    b = np.random.default_rng(3).uniform(0.5, 1.5, p.output_size)
-    pl = fdist.plan(p, world)[rank]
-    dev = torch.device("cuda", 0)
-    with fg.GpuInstance(pl.local) as g:
-        op = fg.DeviceOperator(g)
-        b_loc = torch.from_numpy(b[pl.test_global] * pl.owned_mask).to(dev)
-        x, it, hist = fg.krylov.dist_cg(pl, op.apply, b_loc, rtol=1e-10, maxiter=2000, check_every=5)
-        np.savez(os.path.join(out_dir, "r%d.npz" % rank), gids=pl.test_global[pl.owned_mask],
-                 xs=x.cpu().numpy()[pl.owned_mask], it=it, launches=op.launches)
-    dist.barrier()
-    dist.destroy_process_group()
+    from paper_2506_17471_b200.krylov import _CudaArray
+    from paper_2506_17471_b200._native import lib
+    p = C.c_void_p()
+    lib().femgpu_device_input(inst.handle, space, C.byref(p))
+    t = torch.as_tensor(_CudaArray(p.value, n * stride), device="cuda")
+    return t.view(n, stride)[:, :comps]
 
 
-def test_distributed_device_cg_two_ranks_one_gpu(tmp_path, oracle):
-    """dist_cg with the local action on the GPU (DeviceOperator) and halos over gloo, two ranks on
-    cuda:0: the assembled solution satisfies the oracle's A x = b."""
-    import numpy as np
-    import torch.multiprocessing as mp
+FORMS = [("laplace", 3, 2, 4, 6), ("elasticity", 3, 2, 4, 4), ("helmholtz_coef", 2, 3, 12, 12),
+         ("hyperelastic", 3, 2, 14, 2)]
 
-    import paper_2506_17471_b200 as fg
-    mp.spawn(_cg_worker, args=(2, _port(), str(tmp_path)), nprocs=2, join=True)
-    p = fg.symmetric_problem("helmholtz", 3, 2, 14, 4)
-    b = np.random.default_rng(3).uniform(0.5, 1.5, p.output_size)
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("args", FORMS, ids=lambda a: "-".join(map(str, a)))
+def test_halo_action_matches_oracle_with_changing_inputs(oracle, args, world):
+    import torch
+    p = fg.mesh_problem(*args)
+    d = p.signature.dim
+    ns = len(p.scalar_inputs)
+
+    def new_x(gl, comps, step):
+        return (0.5 + 0.25 * step + 1e-3 * ((gl[:, None] * comps + np.arange(comps)) % 97))
+
+    def rank(r, gather):
+        plan = fdist.build_plan(fdist.rank_slab(args, r, world), r, world, gather)
+        di = fdist.DistInstance(plan, gather)
+        out = []
+        try:
+            for step in range(3):
+                if step:  # new owned inputs written on the device, ghosts poisoned
+                    for s, gl in enumerate(plan.trial_global):
+                        comps = 1 if s < ns else d
+                        stride = 1 if s < ns else (4 if d == 3 else d)
+                        v = new_x(gl, comps, step)
+                        for q, (mine, _) in plan.pull[s].items():
+                            v[mine] = np.nan
+                        device_view(di.inst, s, len(gl), comps, stride).copy_(torch.from_numpy(v))
+                    torch.cuda.synchronize()
+                di.action()
+                di.check()
+                out.append(di.owned_output())
+        finally:
+            di.close()
+        return out
+
+    res = run_ranks(world, rank)
+    for step in range(3):
+        if step:
+            for i in range(ns):
+                g = np.arange(len(p.scalar_inputs[i]))
+                p.scalar_inputs[i] = new_x(g, 1, step).reshape(-1)
+            for i in range(len(p.vector_inputs)):
+                g = np.arange(len(p.vector_inputs[i]) // d)
+                p.vector_inputs[i] = new_x(g, d, step).reshape(-1)
+        ref = oracle.reference_action(p)
+        y = np.full(p.output_size, np.nan)
+        for r in range(world):
+            g, v = res[r][step]
+            assert np.all(np.isnan(y[g]))
+            y[g] = v
+        assert not np.isnan(y).any(), step
+        assert rel_l2(y, ref) <= 1e-12 and max_rel(y, ref) <= 1e-10, (step, rel_l2(y, ref))
+
+
+def test_distributed_device_cg(oracle):
+    """dist_cg with the distributed action on the device (DistOperator): the assembled solution
+    satisfies the global A x = b of the oracle."""
+    import torch
+    args = ("helmholtz", 3, 2, 14, 4)
+    world = 2
+
+    def rank(r, gather):
+        slab = fdist.rank_slab(args, r, world)
+        tab = slab.local.tabulations
+        tab.psi = np.ascontiguousarray(np.transpose(tab.scalar_phi[0], (0, 2, 1)))
+        plan = fdist.build_plan(slab, r, world, gather)
+        di = fdist.DistInstance(plan, gather)
+        try:
+            op = fg.krylov.DistOperator(di)
+            b = 0.5 + 1e-3 * (plan.test_global % 89)
+            b_loc = torch.from_numpy(b * plan.owned_mask).cuda()
+            import torch.distributed  # noqa: F401  (dist_cg all-reduces: emulate with the thread gather)
+
+            def dot(a, c):
+                owned = torch.as_tensor(plan.owned_mask, device=a.device)
+                part = float(torch.sum(a[owned] * c[owned]))
+                return torch.tensor(sum(gather(part)), dtype=torch.float64, device=a.device)
+
+            def apply(v, out):
+                op.apply(v, out)
+                out[~torch.as_tensor(plan.owned_mask, device=out.device)] = 0.0
+            x, it, _ = fg.krylov.cg(apply, b_loc, rtol=1e-10, maxiter=800, check_every=5, dot=dot)
+            return plan.test_global[plan.owned_mask], x.cpu().numpy()[plan.owned_mask], it
+        finally:
+            di.close()
+
+    res = run_ranks(world, rank)
+    p = fg.symmetric_problem(*args)
     x = np.full(p.output_size, np.nan)
-    for r in range(2):
-        d = np.load(os.path.join(tmp_path, "r%d.npz" % r))
-        x[d["gids"]] = d["xs"]
-    assert not np.any(np.isnan(x))
+    for g, v, _ in res:
+        x[g] = v
+    assert not np.isnan(x).any()
+    b = 0.5 + 1e-3 * (np.arange(p.output_size) % 89)
     p.scalar_inputs[0] = x
     assert np.linalg.norm(oracle.reference_action(p) - b) <= 1e-8 * np.linalg.norm(b)
+
+
+@pytest.mark.parametrize("config,n", [("C2", 12), ("C4", 8)])
+def test_bench_launches_its_own_ranks_ipc_path(config, n):
+    """bench.py --gpus 2 without torchrun launches its two ranks itself; they share cuda:0 through
+    CUDA IPC (the cross-process path of csrc/halo.cu) and rank 0 checks the gathered owned rows
+    against the reference CPU action."""
+    env = dict(os.environ, FEMGPU_AUTOTUNE="0")
+    env.pop("WORLD_SIZE", None)
+    cmd = [sys.executable, "bench.py", "--gpus", "2", "--config", config, "--mesh-n", str(n), "--steps", "5",
+           "--warmup", "3"]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-6000:]
+    out = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert out["n_gpus"] == 2 and out["parity_complete"]
+    assert out["parity_vs_reference"]["pass"], out["parity_vs_reference"]

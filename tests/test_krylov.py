@@ -64,17 +64,17 @@ def _dist_worker(rank, world, port, out_dir):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from oracle import oracle
     from paper_2506_17471_b200 import dist as fdist
-    p = fg.symmetric_problem("helmholtz", 2, 2, 6, 6)
-    b = np.random.default_rng(3).uniform(0.5, 1.5, p.output_size)
-    pl = fdist.plan(p, world, align=2)[rank]
-    loc = pl.local
+    slab = fdist.rank_slab(("helmholtz", 2, 2, 6, 6), rank, world)
+    tab = slab.local.tabulations
+    tab.psi = np.ascontiguousarray(np.transpose(tab.scalar_phi[0], (0, 2, 1)))  # as symmetric_problem
+    pl = fdist.build_plan(slab, rank, world, fdist.torch_gather())
+    b = np.random.default_rng(3).uniform(0.5, 1.5, (2 * 6 + 1) ** 2)
 
-    def local_apply(v, out):
-        loc.scalar_inputs[0] = v.numpy().copy()
-        out.copy_(torch.from_numpy(oracle.reference_action(loc)))
+    def dist_apply(v, out):  # pull ghosts, local oracle action, push partial rows (host emulation)
+        out.copy_(torch.from_numpy(fdist.host_halo_action(pl, oracle.reference_action, [v.numpy().copy()])))
 
     b_loc = torch.from_numpy(b[pl.test_global] * pl.owned_mask)
-    x, it, hist = fg.krylov.dist_cg(pl, local_apply, b_loc, rtol=1e-10, maxiter=500)
+    x, it, hist = fg.krylov.dist_cg(pl, dist_apply, b_loc, rtol=1e-10, maxiter=500)
     np.savez(os.path.join(out_dir, "r%d.npz" % rank), gids=pl.test_global[pl.owned_mask],
              xs=x.numpy()[pl.owned_mask], it=it)
     dist.barrier()
