@@ -17,7 +17,7 @@
 // Flags of rank r (int64, in r's memory; peers write the `pushed` slots):
 //   [0] xready   the step whose owned inputs r has published (written by r)
 //   [1] consumed the step whose received contributions r has added (written by r)
-//   [2] error    bit 0: a wait timed out
+//   [2..5] error: which wait timed out (1 pull, 2 push, 4 receive), the peer, value seen, wanted
 //   [8 + q]      pushed: the step whose contributions rank q has stored into r's receive buffer
 // Receive buffers are double-buffered by step parity; a push of step k waits until the owner
 // consumed step k - 2, so a fast rank cannot overwrite contributions still being added.
@@ -49,15 +49,21 @@ __device__ __forceinline__ void st_release(long long* p, long long v) {
     asm volatile("st.release.sys.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// Spins (one thread) until *p >= want or the timeout; on timeout sets the local error flag.
-__device__ void wait_geq(const long long* p, long long want, long long* err, unsigned long long timeout_ns) {
+// Spins (one thread) until *p >= want or the timeout; on timeout records in the local error
+// words which wait (bit `what`: 1 pull, 2 push, 4 receive), on which peer, and the value seen.
+__device__ void wait_geq(const long long* p, long long want, long long* err, unsigned long long timeout_ns, int what,
+                         int peer) {
     unsigned long long t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    while (ld_acquire(p) < want) {
+    long long v;
+    while ((v = ld_acquire(p)) < want) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         if (t - t0 > timeout_ns) {
-            atomicOr(reinterpret_cast<unsigned long long*>(err), 1ULL);
+            atomicOr(reinterpret_cast<unsigned long long*>(err), static_cast<unsigned long long>(what));
+            err[1] = peer;
+            err[2] = v;
+            err[3] = want;
             return;
         }
         __nanosleep(200);
@@ -90,7 +96,7 @@ __global__ void pull_kernel(PullArgs a) {
             st_release(a.my_flags + 0, a.step);
         }
         for (int i = 0; i < a.n_pull_peers; ++i)
-            wait_geq(a.peer_flags[a.pull_peers[i]] + 0, a.step, a.my_flags + 2, a.timeout_ns);
+            wait_geq(a.peer_flags[a.pull_peers[i]] + 0, a.step, a.my_flags + 2, a.timeout_ns, 1, a.pull_peers[i]);
     }
     __syncthreads();
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < a.n;
@@ -123,7 +129,7 @@ struct PushArgs {
 __global__ void push_kernel(PushArgs a) {
     if (threadIdx.x == 0)  // slot reuse: the owner must have consumed step - 2
         for (int i = 0; i < a.n_targets; ++i)
-            wait_geq(a.peer_flags[a.targets[i]] + 1, a.step - 2, a.my_flags + 2, a.timeout_ns);
+            wait_geq(a.peer_flags[a.targets[i]] + 1, a.step - 2, a.my_flags + 2, a.timeout_ns, 2, a.targets[i]);
     __syncthreads();
     const long long par = a.step & 1;
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < a.n;
@@ -162,7 +168,7 @@ struct RecvArgs {
 __global__ void recv_kernel(RecvArgs a) {
     if (threadIdx.x == 0)
         for (int i = 0; i < a.n_sources; ++i)
-            wait_geq(a.my_flags + kFlagPushed + a.sources[i], a.step, a.my_flags + 2, a.timeout_ns);
+            wait_geq(a.my_flags + kFlagPushed + a.sources[i], a.step, a.my_flags + 2, a.timeout_ns, 4, a.sources[i]);
     __syncthreads();
     const double* r = a.recv + (a.step & 1) * a.slot;
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < a.n_rows;
@@ -453,6 +459,13 @@ femgpu_status femgpu_halo_create(femgpu_instance* inst, int32_t rank, int32_t wo
         H->d_stride = dev_copy(stride, H->keep);
         H->d_comps = dev_copy(comps, H->keep);
         H->d_my_x = dev_copy(my_x, H->keep);
+        // load the exchange kernels now (lazy module loading would otherwise load them at the first
+        // launch, which may wait for the device while a peer spins on this rank)
+        for (const void* k : {reinterpret_cast<const void*>(pull_kernel), reinterpret_cast<const void*>(push_kernel),
+                              reinterpret_cast<const void*>(recv_kernel)}) {
+            cudaFuncAttributes fa{};
+            FG_CUDA(cudaFuncGetAttributes(&fa, k));
+        }
         FG_CUDA(cudaStreamCreateWithFlags(&H->side, cudaStreamNonBlocking));
         FG_CUDA(cudaEventCreateWithFlags(&H->ev_boundary, cudaEventDisableTiming));
         FG_CUDA(cudaEventCreateWithFlags(&H->ev_pushed, cudaEventDisableTiming));
@@ -590,11 +603,17 @@ femgpu_status femgpu_halo_check(femgpu_halo* h, void* stream) {
         if (!h) femgpu::invalid("halo: null handle");
         FG_CUDA(cudaSetDevice(h->device));
         cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : h->inst->stream;
-        long long err = 0;
-        FG_CUDA(cudaMemcpyAsync(&err, h->flags + 2, sizeof err, cudaMemcpyDeviceToHost, s));
+        long long err[4] = {0, 0, 0, 0};
+        FG_CUDA(cudaStreamSynchronize(h->side));
+        FG_CUDA(cudaMemcpyAsync(err, h->flags + 2, sizeof err, cudaMemcpyDeviceToHost, s));
         FG_CUDA(cudaStreamSynchronize(s));
-        if (err) femgpu::fail(FEMGPU_E_CUDA, "halo: a peer did not reach the exchange in time (rank " +
-                                                 std::to_string(h->rank) + ", step " + std::to_string(h->step) + ")");
+        if (err[0]) {
+            const char* what = (err[0] & 1) ? "pull" : (err[0] & 2) ? "push" : "receive";
+            femgpu::fail(FEMGPU_E_CUDA, std::string("halo: a peer did not reach the exchange in time (rank ") +
+                                            std::to_string(h->rank) + ", step " + std::to_string(h->step) + ": " + what +
+                                            " wait on rank " + std::to_string(err[1]) + " saw " + std::to_string(err[2]) +
+                                            ", wanted " + std::to_string(err[3]) + ")");
+        }
     });
 }
 

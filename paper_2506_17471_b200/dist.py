@@ -348,6 +348,9 @@ class DistInstance:
         from ._native import lib
         self.plan = plan
         self.inst = fa.GpuInstance(plan.local)
+        # JIT, automatic schedule and every allocation before the first exchange: a module load or
+        # cudaMalloc may wait for the device, which must never happen while a peer spins on this rank
+        self.inst.action()
         L = lib()
 
         def cat(parts):
@@ -378,6 +381,7 @@ class DistInstance:
         fa._call(L.femgpu_halo_export(h, buf, n.value, C.byref(n)))
         blob = b"".join(gather(bytes(buf.raw)))
         fa._call(L.femgpu_halo_import(h, blob, n.value))
+        gather(None)  # every rank has mapped its peers before anyone starts exchanging
 
     def action(self, params=None, y_dev: int = 0, stream: int = 0):
         from . import action as fa

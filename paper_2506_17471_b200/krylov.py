@@ -148,6 +148,8 @@ class DistOperator:
         self.launches = 0
 
     def apply(self, v, out) -> None:
+        """Ordered on torch's current stream.  Ranks sharing a device in one process must each run on
+        their own stream (torch.cuda.ExternalStream(inst.stream())), never the legacy default stream."""
         import torch
         self.x.copy_(v)
         stream = torch.cuda.current_stream(self.dev).cuda_stream or 1

@@ -86,15 +86,17 @@ def test_halo_action_matches_oracle_with_changing_inputs(oracle, args, world):
         out = []
         try:
             for step in range(3):
-                if step:  # new owned inputs written on the device, ghosts poisoned
+                if step:  # new owned inputs uploaded on the instance stream, ghosts poisoned (NaN)
+                    xs = []
                     for s, gl in enumerate(plan.trial_global):
                         comps = 1 if s < ns else d
-                        stride = 1 if s < ns else (4 if d == 3 else d)
                         v = new_x(gl, comps, step)
                         for q, (mine, _) in plan.pull[s].items():
                             v[mine] = np.nan
-                        device_view(di.inst, s, len(gl), comps, stride).copy_(torch.from_numpy(v))
-                    torch.cuda.synchronize()
+                        xs.append(np.ascontiguousarray(v.reshape(-1)))
+                    # (femgpu_set_inputs: stream-ordered copies only -- a device-wide synchronising
+                    # call would wait for the other ranks' exchange kernels, which wait for this rank)
+                    di.inst.set_inputs(xs[:ns], xs[ns:])
                 di.action()
                 di.check()
                 out.append(di.owned_output())
@@ -134,24 +136,28 @@ def test_distributed_device_cg(oracle):
         tab.psi = np.ascontiguousarray(np.transpose(tab.scalar_phi[0], (0, 2, 1)))
         plan = fdist.build_plan(slab, r, world, gather)
         di = fdist.DistInstance(plan, gather)
-        try:
-            op = fg.krylov.DistOperator(di)
-            b = 0.5 + 1e-3 * (plan.test_global % 89)
-            b_loc = torch.from_numpy(b * plan.owned_mask).cuda()
-            import torch.distributed  # noqa: F401  (dist_cg all-reduces: emulate with the thread gather)
+        # each rank on its own (instance) stream: ranks sharing a device in one process must not
+        # meet on the legacy default stream, where one rank's waiting exchange kernel would block
+        # the other rank's work queued behind it
+        with torch.cuda.stream(torch.cuda.ExternalStream(di.inst.stream())):
+            try:
+                op = fg.krylov.DistOperator(di)
+                b = 0.5 + 1e-3 * (plan.test_global % 89)
+                b_loc = torch.from_numpy(b * plan.owned_mask).cuda()
+                owned = torch.from_numpy(plan.owned_mask.astype(np.float64)).cuda()
 
-            def dot(a, c):
-                owned = torch.as_tensor(plan.owned_mask, device=a.device)
-                part = float(torch.sum(a[owned] * c[owned]))
-                return torch.tensor(sum(gather(part)), dtype=torch.float64, device=a.device)
+                def dot(a, c):  # dist_cg's all-reduce, emulated with the thread gather
+                    part = float(torch.dot(a * owned, c))
+                    return torch.tensor(sum(gather(part)), dtype=torch.float64, device=a.device)
 
-            def apply(v, out):
-                op.apply(v, out)
-                out[~torch.as_tensor(plan.owned_mask, device=out.device)] = 0.0
-            x, it, _ = fg.krylov.cg(apply, b_loc, rtol=1e-10, maxiter=800, check_every=5, dot=dot)
-            return plan.test_global[plan.owned_mask], x.cpu().numpy()[plan.owned_mask], it
-        finally:
-            di.close()
+                def apply(v, out):
+                    op.apply(v, out)
+                    out.mul_(owned)  # ghost rows hold partial sums: only owned rows are the product
+                x, it, _ = fg.krylov.cg(apply, b_loc, rtol=1e-10, maxiter=800, check_every=5, dot=dot)
+                di.check()
+                return plan.test_global[plan.owned_mask], x.cpu().numpy()[plan.owned_mask], it
+            finally:
+                di.close()
 
     res = run_ranks(world, rank)
     p = fg.symmetric_problem(*args)
