@@ -99,7 +99,7 @@ class TilingParams:
                          | (self.zero_slabs & 0xff) << 8)
         s.reserved[1] = self.reg_target
         s.reserved[2] = self.min_blocks
-        s.reserved[3] = (self.stage_smem & 0xff) | (self.split & 0xff) << 8 | (self.qmopt & 0xff) << 16
+        s.reserved[3] = (self.stage_smem & 0xff) | (self.split & 0xff) << 8 | (self.qmopt & 0xffff) << 16
         return s
 
     @staticmethod
@@ -112,7 +112,7 @@ class TilingParams:
                             scatter=s.scatter, block_cells=s.block_cells, group_cells=s.group_cells,
                             strict=bool(s.reserved[0] & abi.FLAG_STRICT), reg_target=s.reserved[1],
                             min_blocks=s.reserved[2], stage_smem=s.reserved[3] & 0xff, split=(s.reserved[3] >> 8) & 0xff,
-                            qmopt=(s.reserved[3] >> 16) & 0xff,
+                            qmopt=(s.reserved[3] >> 16) & 0xffff,
                             fused_zero=bool(s.reserved[0] & abi.FLAG_FUSED_ZERO),
                             zero_slabs=(s.reserved[0] >> 8) & 0xff)
 

@@ -502,7 +502,7 @@ std::string KernelPlan::key() const {
     std::ostringstream s;
     s << int(family) << "/" << basis << "/" << block << "/" << tile_cells << "/" << Nc << "x" << Nwi << "/" << TQ << "/"
       << Ter << "/" << Tqr << "/" << Tqc << "/" << strict << "/" << min_blocks << "/G" << G << "/ms" << mstage << "/ys" << ysmem
-      << "/qm" << qmajor << "x" << msplit << "o" << qmopt << "/ql" << qloop << "/col" << colour << "/zf" << zfused;
+      << "/qm" << qmajor << "x" << msplit << "o" << qmopt << "m" << merge.size() << "/ql" << qloop << "/col" << colour << "/zf" << zfused;
     for (int t : Tcs) s << "s" << t;
     for (int t : Tcv) s << "v" << t;
     for (size_t g = 0; g < group_cap.size(); ++g) s << "g" << group_entries[g] << ":" << group_cap[g];
@@ -512,6 +512,8 @@ std::string KernelPlan::key() const {
     uint64_t h = 0xcbf29ce484222325ULL;
     for (const auto& p : mpat)
         for (int v : p) h = (h ^ static_cast<uint64_t>(v + 1)) * 0x100000001b3ULL;
+    for (const auto& m : merge)
+        for (int v : m) h = (h ^ static_cast<uint64_t>(v + 7)) * 0x100000001b3ULL;
     s << "P" << h;
     return s.str();
 }
@@ -1496,6 +1498,26 @@ void emit_macro_qmajor_kernel(Out& o, const Signature& sig, const KernelPlan& kp
                 if (used(gt, u)) chk += " | NF(ya" + S(u) + ")";
             o.line("if (nf" + chk + ") atomicMin(P.bad, (unsigned long long)grp * " + S(G) + ");");
         }
+        const bool merging = !kp.merge.empty() && SPL == 1 && gathered.count(gt) && !(kp.qmopt & 2) && !staged;
+        if (merging) {
+            // warp merge: lane l's contribution to node u moves to lane l+s when that lane's group has
+            // the same global node (as u'): one red.add per node of the warp's block of groups instead
+            // of one per (group, node); the owner of a moved contribution then skips it (zeroed).
+            // The pairing is a hint from the layout; equality of the global indices decides at run time.
+            o.line("if (__activemask() == 0xffffffffu) {");
+            o.ind++;
+            o.line("const int lane = threadIdx.x & 31;");
+            for (const auto& m : kp.merge) {
+                const int sft = m[0], u = m[1], u2 = m[2];
+                const std::string a = "ya" + S(u), b = "ya" + S(u2), ia = "ig" + S(gt) + "_" + S(u), ib = "ig" + S(gt) + "_" + S(u2);
+                o.line("{ const double v = __shfl_up_sync(0xffffffffu, " + a + ", " + S(sft) + "); const int i = __shfl_up_sync(0xffffffffu, " +
+                       ia + ", " + S(sft) + "); const int j = __shfl_down_sync(0xffffffffu, " + ib + ", " + S(sft) + ");");
+                o.line("  if (lane >= " + S(sft) + " && i == " + ib + ") " + b + " += v;");
+                o.line("  if (lane + " + S(sft) + " < 32 && j == " + ia + ") " + a + " = 0.0; }");
+            }
+            o.ind--;
+            o.line("}");
+        }
         for (int u = 0; u < kp.group_cap[gt]; ++u) {
             if (!used(gt, u)) continue;
             // qmopt bit 1: reload the scatter indices (an opaque load the compiler cannot merge with
@@ -1507,6 +1529,8 @@ void emit_macro_qmajor_kernel(Out& o, const Signature& sig, const KernelPlan& kp
                 o.line("P.y[" + idx + "] = ya" + S(u) + ";");
             else if (kp.qmopt & 8)  // timing experiment only (wrong results): no scatter traffic
                 o.line("if (ya" + S(u) + " == 1234.5678) P.y[" + idx + "] = 0.0;");
+            else if (merging)  // a merged-away contribution is exactly 0.0: nothing to add
+                o.line("if (ya" + S(u) + " != 0.0) atomicAdd(&P.y[" + idx + "], ya" + S(u) + ");");
             else
                 o.line("atomicAdd(&P.y[" + idx + "], ya" + S(u) + ");");
         }
@@ -1842,7 +1866,6 @@ EmitResult emit_mlt(const Signature& sig, const KernelPlan& kp) {
     KernelPlan pk = kp;
     pk.family = Family::Scpt;
     pk.basis = FEMGPU_BASIS_SMEM;
-    const bool unroll_q = false;
     emit_scpt_kernel(o, sig, pk, use, false, true, r.kernel_checked, 0);
     r.source = o.s.str();
     r.smem_bytes = std::max<size_t>(r.smem_bytes, static_cast<size_t>(sig.tab_size) * 8);

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <algorithm>
+#include <array>
 #include <cstdint>
 #include <iosfwd>
 #include <map>
@@ -102,7 +103,9 @@ struct KernelPlan {
     bool qmajor = false;                  // macro: quadrature-point-major, statements interleaved over the G cells
     int msplit = 1;                       // macro q-major: cells of a group split over this many warps
     int qmopt = 0;                        // macro q-major: bit 0 hoisted column read from smem, bit 1 reload scatter
-                                          // indices, bit 4 rolled quadrature loop, bit 5 persistent cp.async staging
+                                          // indices, bit 4 rolled quadrature loop, bit 5 persistent cp.async staging,
+                                          // bit 8 warp merge of shared-node contributions before the scatter
+    std::vector<std::array<int, 3>> merge;  // macro: warp-merge pairs (MacroLayout::merge of the test group)
     long long stage_off = 0;              // macro q-major staging: byte offset of the staging area (emitter-internal)
     bool qloop = false;                   // scpt: keep the quadrature loop rolled (I-cache / registers)
     bool colour = false;                  // scpt: one launch per cell colour, plain y updates (deterministic)
@@ -185,6 +188,9 @@ struct MacroLayout {
     std::vector<int> unique;                 // per map group: unique entries per cell group
     std::vector<std::vector<int>> pattern;   // per map group: G*entries local indices
     std::vector<int32_t*> d_gidx;            // per map group: [unique][n_groups] global indices
+    // warp merge of the test map (q-major kernels, qmopt bit 8): (lane shift s, unique u, unique u')
+    // such that group g's node u is group g+s's node u' for at least half of the group pairs of a warp
+    std::vector<std::array<int, 3>> merge;
 };
 
 // Greedy colouring of the test map (femgpu_color_cells) with the cells sorted by colour.

@@ -602,6 +602,29 @@ const MacroLayout& Instance::macro_layout(int G) {
             }
             M->unique.push_back(U);
             M->pattern.push_back(pat);
+            if (static_cast<int>(g) == test_group) {
+                // warp merge candidates: lanes l and l+s of a warp hold groups g and g+s; count how
+                // often g's unique node u is g+s's node u' (a sample of warps is enough)
+                const long long warps = ng / 32;
+                const long long step = std::max(1LL, warps / 4096);
+                for (int sft : {1, 2, 4, 8, 16}) {
+                    std::vector<long long> hits(static_cast<size_t>(U) * U, 0);
+                    long long pairs = 0;
+                    for (long long w = 0; w < warps; w += step)
+                        for (int l = 0; l + sft < 32; ++l) {
+                            const long long g0 = w * 32 + l, g1 = g0 + sft;
+                            ++pairs;
+                            for (int u = 0; u < U; ++u) {
+                                const int32_t v = gidx[static_cast<size_t>(u) * ng + g0];
+                                for (int u2 = 0; u2 < U; ++u2)
+                                    if (gidx[static_cast<size_t>(u2) * ng + g1] == v) ++hits[static_cast<size_t>(u) * U + u2];
+                            }
+                        }
+                    for (int u = 0; u < U && pairs; ++u)
+                        for (int u2 = 0; u2 < U; ++u2)
+                            if (hits[static_cast<size_t>(u) * U + u2] * 2 >= pairs) M->merge.push_back({sft, u, u2});
+                }
+            }
             int32_t* d = alloc<int32_t>(gidx.size());
             FG_CUDA(cudaMemcpy(d, gidx.data(), gidx.size() * 4, cudaMemcpyHostToDevice));
             M->d_gidx.push_back(d);
@@ -655,7 +678,7 @@ void host_macro_plan(const femgpu_problem* p, const Signature& sig, KernelPlan& 
     kp.ysmem = (s->reserved[3] & 0xff) == 2;
     kp.qmajor = (s->reserved[3] & 0xff) == 3;
     kp.msplit = kp.qmajor ? std::max(1, (s->reserved[3] >> 8) & 0xff) : 1;
-    kp.qmopt = kp.qmajor ? (s->reserved[3] >> 16) & 0xff : 0;
+    kp.qmopt = kp.qmajor ? (s->reserved[3] >> 16) & 0xffff : 0;
     kp.block = s->block_cells > 0 ? s->block_cells : 64;
     check_macro_split(kp);
     const int reg_target = s->reserved[1] > 0 ? s->reserved[1] : 168;
@@ -799,7 +822,8 @@ KernelPlan resolve_schedule_impl(Instance& I, const femgpu_schedule* s) {
             kp.ysmem = (s->reserved[3] & 0xff) == 2;
             kp.qmajor = (s->reserved[3] & 0xff) == 3;
             kp.msplit = kp.qmajor ? std::max(1, (s->reserved[3] >> 8) & 0xff) : 1;
-    kp.qmopt = kp.qmajor ? (s->reserved[3] >> 16) & 0xff : 0;
+            kp.qmopt = kp.qmajor ? (s->reserved[3] >> 16) & 0xffff : 0;
+            if ((kp.qmopt & 256) && kp.msplit == 1) kp.merge = M.merge;
             kp.block = s->block_cells > 0 ? s->block_cells : 64;
             check_macro_split(kp);
             const int reg_target = s->reserved[1] > 0 ? s->reserved[1] : 168;

@@ -79,7 +79,7 @@ std::pair<long long, long long> map_instr(const Signature& sig) {
 std::string tune_key(const Instance& I) {
     const Signature& sig = I.sig;
     std::ostringstream k;
-    k << "v6|" << sig.dim << "|" << sig.Q << "|" << sig.nW << "|" << sig.Tw << "|" << I.cells << "|" << I.output_size;
+    k << "v7|" << sig.dim << "|" << sig.Q << "|" << sig.nW << "|" << sig.Tw << "|" << I.cells << "|" << I.output_size;
     for (size_t i = 0; i < sig.sdofs.size(); ++i) k << "|s" << sig.sdofs[i] << ":" << sig.sterms[i];
     for (size_t i = 0; i < sig.vdofs.size(); ++i) {
         k << "|v" << sig.vdofs[i] << ":" << sig.vterms[i];
@@ -119,7 +119,10 @@ std::string describe_plan(const KernelPlan& kp) {
     std::ostringstream s;
     switch (kp.family) {
         case Family::Macro:
-            s << "femgpu_macro G=" << kp.G << " block=" << kp.block << (kp.qmajor ? " q-major" : "") << (kp.msplit > 1 ? " split=" + std::to_string(kp.msplit) : std::string()) << (kp.ysmem ? " y-smem" : "");
+            s << "femgpu_macro G=" << kp.G << " block=" << kp.block << (kp.qmajor ? " q-major" : "")
+              << (kp.qmajor && !(kp.qmopt & 16) ? " unrolled" : "")
+              << (kp.msplit > 1 ? " split=" + std::to_string(kp.msplit) : std::string())
+              << (!kp.merge.empty() ? " warp-merge=" + std::to_string(kp.merge.size()) : std::string()) << (kp.ysmem ? " y-smem" : "");
             break;
         case Family::Scpt:
             s << "femgpu_scpt cells/thread=" << std::max(1, kp.G) << " block=" << kp.block << " minCTAs=" << kp.min_blocks
@@ -265,6 +268,7 @@ void autotune(Instance& I) {
         if (!I.macro_layout(G).ok) continue;
         const size_t before = C.size();
         add(macro_variant(G, 32, 3 | (16 << 16), 232, 0), 0);  // q-major, rolled quadrature loop
+        add(macro_variant(G, 32, 3 | (272 << 16), 232, 0), 0); // + warp merge of shared-node contributions
         add(macro_variant(G, 64, 3 | (16 << 16), 232, 0), 0);
         add(macro_variant(G, 32, 3, 232, 0), 0);                // q-major, unrolled
         add(macro_variant(G, 32, 0, 0, 8), 0);                  // cell-major, uncapped
