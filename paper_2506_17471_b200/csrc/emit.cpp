@@ -1223,7 +1223,10 @@ void emit_macro_qmajor_kernel(Out& o, const Signature& sig, const KernelPlan& kp
            ") " + name + "(const __grid_constant__ Params P) {");
     o.ind++;
     o.line("constexpr bool CHECKED = false;");
-    if (kp.zfused) o << kZeroPrologue;
+    // qmopt bit 13: the zeroing of the fused range is spread over the launch's valid threads and
+    // issued after the gathers (the stores drain while the loads are in flight) instead of a CTA prologue
+    const bool late_zero = kp.zfused && (kp.qmopt & 8192) && SPL == 1 && !(kp.qmopt & 96);
+    if (kp.zfused && !late_zero) o << kZeroPrologue;
     o.line("extern __shared__ __align__(16) unsigned char smraw[];");
     if (kp.basis == FEMGPU_BASIS_SMEM) {
         o.line("double* sT = reinterpret_cast<double*>(smraw + " + S(smem_tab_off) + ");");
@@ -1363,6 +1366,10 @@ void emit_macro_qmajor_kernel(Out& o, const Signature& sig, const KernelPlan& kp
                     node_loads("Xg" + S(u), "P.X", comps);
                 }
             }
+        if (late_zero) {
+            o.line("{ const long long g0 = P.cell0 / " + S(G) + ", ng = P.n_cells / " + S(G) + " - g0;");
+            o.line("  for (long long i = grp - g0; i < P.zn; i += ng) __stcs(P.zp + i, 0.0); }");
+        }
         o.line("bool nf = false;");
         // ---- per cell: geometry + cell-invariant nodes -> thread-private smem column
         for (int sc = c0; sc < c1; ++sc) {
@@ -1413,7 +1420,7 @@ void emit_macro_qmajor_kernel(Out& o, const Signature& sig, const KernelPlan& kp
             return rolled ? S(base0) + " + q * " + S(stride) : S(base0 + static_cast<long long>(q) * stride);
         };
         if (rolled) {
-            o.line("#pragma unroll 1");
+            o.line((kp.qmopt & 16384) ? "#pragma unroll 2" : "#pragma unroll 1");  // bit 14: two points per trip
             o.line("for (int q = 0; q < " + S(Q) + "; ++q) {");
             o.ind++;
         }

@@ -1062,8 +1062,11 @@ void run_action_range(Instance& I, const KernelPlan& kp, double* d_y, cudaStream
         grid = std::min<long long>(L->n_tiles, static_cast<long long>(mod->sms) * std::max(1, mod->occupancy));
     else if (kp.family == Family::Macro) {
         grid = (ncell / kp.G + kp.block / kp.msplit - 1) / (kp.block / kp.msplit);
-        if ((kp.qmopt & 96) && kp.msplit == 1)  // persistent kernels: one wave of resident CTAs
-            grid = std::min<long long>(grid, static_cast<long long>(mod->sms) * std::max(1, mod->occupancy));
+        if ((kp.qmopt & 96) && kp.msplit == 1) {
+            // grid-stride kernels: qmopt bits 9-12 = groups per thread (0: one wave of resident CTAs)
+            const int per = (kp.qmopt >> 9) & 15;
+            grid = per ? (grid + per - 1) / per : std::min<long long>(grid, static_cast<long long>(mod->sms) * std::max(1, mod->occupancy));
+        }
     }
     else if (kp.family == Family::Dmma)
         grid = std::min<long long>(((ncell + kp.Nc - 1) / kp.Nc + kp.block / 32 - 1) / (kp.block / 32),

@@ -79,7 +79,7 @@ std::pair<long long, long long> map_instr(const Signature& sig) {
 std::string tune_key(const Instance& I) {
     const Signature& sig = I.sig;
     std::ostringstream k;
-    k << "v7|" << sig.dim << "|" << sig.Q << "|" << sig.nW << "|" << sig.Tw << "|" << I.cells << "|" << I.output_size;
+    k << "v11|" << sig.dim << "|" << sig.Q << "|" << sig.nW << "|" << sig.Tw << "|" << I.cells << "|" << I.output_size;
     for (size_t i = 0; i < sig.sdofs.size(); ++i) k << "|s" << sig.sdofs[i] << ":" << sig.sterms[i];
     for (size_t i = 0; i < sig.vdofs.size(); ++i) {
         k << "|v" << sig.vdofs[i] << ":" << sig.vterms[i];
@@ -120,7 +120,7 @@ std::string describe_plan(const KernelPlan& kp) {
     switch (kp.family) {
         case Family::Macro:
             s << "femgpu_macro G=" << kp.G << " block=" << kp.block << (kp.qmajor ? " q-major" : "")
-              << (kp.qmajor && !(kp.qmopt & 16) ? " unrolled" : "")
+              << (kp.qmajor && !(kp.qmopt & 16) ? " unrolled" : "") << ((kp.qmopt & 16384) ? " 2q/trip" : "")
               << (kp.msplit > 1 ? " split=" + std::to_string(kp.msplit) : std::string())
               << (!kp.merge.empty() ? " warp-merge=" + std::to_string(kp.merge.size()) : std::string()) << (kp.ysmem ? " y-smem" : "");
             break;
@@ -267,9 +267,15 @@ void autotune(Instance& I) {
     for (int G : {6, 4, 3, 2}) {  // the largest group size whose common pattern fits the register budget
         if (!I.macro_layout(G).ok) continue;
         const size_t before = C.size();
-        add(macro_variant(G, 32, 3 | (16 << 16), 232, 0), 0);  // q-major, rolled quadrature loop
-        add(macro_variant(G, 32, 3 | (272 << 16), 232, 0), 0); // + warp merge of shared-node contributions
-        add(macro_variant(G, 64, 3 | (16 << 16), 232, 0), 0);
+        // q-major, rolled quadrature loop; in pipelined actions the next output is zeroed by the
+        // launch's threads after their gathers (qmopt 8192: C2 192 vs 206 us with a CTA prologue)
+        add(macro_variant(G, 32, 3 | (8208 << 16), 232, 0), 0);
+        add(macro_variant(G, 32, 3 | (24592 << 16), 232, 0), 0);  // two quadrature points per trip (C2 182 vs 192 us)
+        // the group's cells split over 2 or 3 warps (fewer registers per thread for wide forms:
+        // C5-adv-P2 854 vs 1001 us of SCPT; profiles/r02_sweeps.md)
+        if (G % 2 == 0) add(macro_variant(G, 64, 3 | (2 << 8) | (16 << 16), 200, 0), 0);
+        if (G % 3 == 0) add(macro_variant(G, 96, 3 | (3 << 8) | (16 << 16), 168, 0), 0);
+        add(macro_variant(G, 64, 3 | (8208 << 16), 232, 0), 0);
         add(macro_variant(G, 32, 3, 232, 0), 0);                // q-major, unrolled
         add(macro_variant(G, 32, 0, 0, 8), 0);                  // cell-major, uncapped
         add(macro_variant(G, 64, 0, 0, 0), 0);                  // cell-major, 168-register cap
@@ -361,7 +367,7 @@ void autotune(Instance& I) {
         if (!c.compiled) continue;
         const double w = std::max(1, c.warps);
         c.pred = c.t_pipe * (1.0 + kLatency / w) * (1.0 + static_cast<double>(c.spill) / kSpillBytes);
-        if (c.spill > 2 * min_spill + 256) c.reject = "spills " + std::to_string(c.spill) + " B/thread";
+        if (c.spill > 2 * min_spill + 768) c.reject = "spills " + std::to_string(c.spill) + " B/thread";
         else if (c.warps < 4) c.reject = "occupancy " + std::to_string(c.warps) + " warps/SM";
     }
     std::vector<size_t> ranked;
@@ -371,9 +377,18 @@ void autotune(Instance& I) {
         for (size_t i : sel)
             if (C[i].compiled) ranked.push_back(i);
     std::stable_sort(ranked.begin(), ranked.end(), [&](size_t a, size_t b) { return C[a].pred < C[b].pred; });
+    // timed: the best-predicted candidate of every family (the model's family efficiencies are the
+    // least certain term), then the best predictions overall, b = 9; plus the SCPT baseline
     std::vector<size_t> timed;
+    for (int fam = 0; fam < 3; ++fam)
+        for (size_t i : ranked)
+            if (C[i].family == fam) {
+                timed.push_back(i);
+                break;
+            }
     for (size_t i : ranked)
-        if (tune_all || timed.size() < kTimed) timed.push_back(i);
+        if ((tune_all || timed.size() < kTimed) && std::find(timed.begin(), timed.end(), i) == timed.end())
+            timed.push_back(i);
     if (std::find(timed.begin(), timed.end(), size_t(0)) == timed.end() && C[0].compiled) timed.push_back(0);
     // ---- measure: >= 5 runs and ~10 ms of work each, then the three fastest re-timed interleaved
     auto time_it = [&](const KernelPlan& kp, int reps) {
