@@ -275,6 +275,15 @@ femgpu_status femgpu_describe_schedule(femgpu_instance* inst, const femgpu_sched
 /* Introspection: kernel launches issued by the last action, device bytes held. */
 femgpu_status femgpu_stats(const femgpu_instance* inst, int64_t* launches_last_action,
                            int64_t* device_bytes, int64_t* tiles, int64_t* max_tile_dofs);
+/* The execution census of schedule s on this instance, in the field order of femsched::TraceCounters
+ * (simulate.hpp:91-104) followed by the workgroup count (ExecutionOutcome::workgroups, search.hpp:263):
+ * [0] barriers per workgroup, [1] flops_matvec, [2] flops_masked_padding (DMMA m8n8k4 padding),
+ * [3] gather_words (trial words read: each unique node of a macro group once), [4] scatter_words
+ * (red.add issued), [5] reference_words (tabulation words staged per CTA), [6] reference_cached_words
+ * (constant-bank reads), [7] coord_words, [8..10] local eval/quad words (0: registers), [11] shared-memory
+ * words per CTA, [12] CTAs launched.  n >= FEMGPU_TRACE_COUNTERS. */
+#define FEMGPU_TRACE_COUNTERS 13
+femgpu_status femgpu_trace_counters(femgpu_instance* inst, const femgpu_schedule* s, int64_t* out, int32_t n);
 /* Copies the instance's output buffer (the y of the last action, or of the last step of
  * femgpu_time_steps / femgpu_time_steps_ex) into y_host (output_size doubles); synchronous. */
 femgpu_status femgpu_read_output(femgpu_instance* inst, double* y_host);

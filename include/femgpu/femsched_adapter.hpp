@@ -265,7 +265,22 @@ inline femsched::Executor executor() {
             const femgpu_schedule s = schedule_from(t);
             out.output = d->action(&s);
             out.measured_seconds = d->measure(&s);
-            out.workgroups = femsched::ceil_div(inst.connectivity.cell_count, t.group_size() / std::max(1, t.kind == femsched::ScheduleKind::SingleCellPerWorkItem ? 1 : t.lanes_per_cell));
+            // the execution census of the kernel that ran (femgpu_trace_counters)
+            int64_t c[FEMGPU_TRACE_COUNTERS] = {};
+            check(femgpu_trace_counters(d->handle(), &s, c, FEMGPU_TRACE_COUNTERS));
+            out.counters.barriers_per_workgroup = c[0];
+            out.counters.flops_matvec = c[1];
+            out.counters.flops_masked_padding = c[2];
+            out.counters.gather_words = c[3];
+            out.counters.scatter_words = c[4];
+            out.counters.reference_words = c[5];
+            out.counters.reference_cached_words = c[6];
+            out.counters.coord_words = c[7];
+            out.counters.local_eval_read_words = c[8];
+            out.counters.local_eval_write_words = c[9];
+            out.counters.local_quad_read_words = c[10];
+            out.counters.local_words_highwater = c[11];
+            out.workgroups = c[12];
             out.ok = true;
         } catch (const std::exception& e) {
             out.error = e.what();  // search.hpp:278-280

@@ -28,7 +28,7 @@ EXPORTS = (
     "femgpu_schedule_save", "femgpu_schedule_load", "femgpu_action_device_pipelined", "femgpu_check_finite",
     "femgpu_time_steps_ex", "femgpu_reference_counters", "femgpu_read_output", "femgpu_mesh_build_range",
     "femgpu_halo_create", "femgpu_halo_destroy", "femgpu_halo_export", "femgpu_halo_import", "femgpu_halo_action",
-    "femgpu_halo_time_steps", "femgpu_halo_check",
+    "femgpu_halo_time_steps", "femgpu_halo_check", "femgpu_trace_counters",
 )
 
 
@@ -107,6 +107,7 @@ def lib():
                                                    C.c_int),
                 "femgpu_check_finite": ([C.c_void_p, _P(abi.Schedule), C.c_void_p], C.c_int),
                 "femgpu_read_output": ([C.c_void_p, _P(C.c_double)], C.c_int),
+                "femgpu_trace_counters": ([C.c_void_p, _P(abi.Schedule), _P(C.c_int64), C.c_int32], C.c_int),
                 "femgpu_halo_create": ([C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int64, _P(C.c_int32),
                                         _P(C.c_int32), C.c_int64, _P(C.c_int32), _P(C.c_int32), C.c_int64,
                                         _P(C.c_int32), _P(C.c_int32), _P(C.c_int32), _P(C.c_int32), _pp], C.c_int),

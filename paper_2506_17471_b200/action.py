@@ -271,6 +271,18 @@ class GpuInstance:
         _call(lib().femgpu_stream(self._h, C.byref(p)))
         return p.value or 0
 
+    TRACE_FIELDS = ("barriers_per_workgroup", "flops_matvec", "flops_masked_padding", "gather_words", "scatter_words",
+                    "reference_words", "reference_cached_words", "coord_words", "local_eval_read_words",
+                    "local_eval_write_words", "local_quad_read_words", "local_words_highwater", "workgroups")
+
+    def trace_counters(self, params: Optional[TilingParams] = None) -> dict:
+        """Execution census of the kernel schedule `params` runs (femsched::TraceCounters field names,
+        simulate.hpp:91-104, plus ExecutionOutcome::workgroups)."""
+        out = (C.c_int64 * len(self.TRACE_FIELDS))()
+        sp = _sched(params)
+        _call(lib().femgpu_trace_counters(self._h, sp[0] if sp else None, out, len(self.TRACE_FIELDS)))
+        return dict(zip(self.TRACE_FIELDS, [int(v) for v in out]))
+
     def read_output(self) -> np.ndarray:
         """Host copy of the instance's output buffer (the last action's / timed step's y)."""
         y = np.empty(self.problem.output_size, dtype=np.float64)
@@ -308,6 +320,7 @@ class ExecutionOutcome:
     error: str = ""
     output: Optional[np.ndarray] = None
     measured_seconds: Optional[float] = None
+    counters: dict = field(default_factory=dict)  # femsched::TraceCounters fields (femgpu_trace_counters)
     workgroups: int = 0
 
 
@@ -327,9 +340,9 @@ def gpu_executor(measure: bool = True, cache: bool = True):
             out.output = g.action(params)
             if measure:
                 out.measured_seconds = g.time(params)
+            out.counters = g.trace_counters(params)
+            out.workgroups = out.counters.pop("workgroups")
             out.ok = True
-            n = inst.connectivity.cell_count
-            out.workgroups = -(-n // (params.cells_per_group if params.kind == abi.MLT else 32))
         except Exception as e:  # search.hpp:278-280: failures become ok=false + message
             out.error = str(e)
         return out

@@ -437,6 +437,51 @@ femgpu_status femgpu_stats(const femgpu_instance* h, int64_t* launches, int64_t*
     });
 }
 
+femgpu_status femgpu_trace_counters(femgpu_instance* h, const femgpu_schedule* s, int64_t* out, int32_t n) {
+    return guard([&] {
+        auto& I = get(h);
+        if (!out || n < FEMGPU_TRACE_COUNTERS) femgpu::invalid("trace_counters: need FEMGPU_TRACE_COUNTERS outputs");
+        std::lock_guard<std::mutex> lk(I.mu);
+        FG_CUDA(cudaSetDevice(I.device));
+        const femgpu::KernelPlan kp = femgpu::plan_for(I, s);
+        auto mod = I.module_for(kp);
+        const femgpu::Signature& sig = I.sig;
+        const long long C = I.cells, d = sig.dim;
+        int64_t c[FEMGPU_TRACE_COUNTERS] = {};
+        const bool staged = kp.basis == FEMGPU_BASIS_SMEM || kp.family == femgpu::Family::Dmma ||
+                            kp.family == femgpu::Family::Mlt;
+        c[0] = staged ? 1 : 0;                                              // barriers per workgroup
+        c[1] = sig.usable_flops() * C;                                      // flops_matvec
+        if (kp.family == femgpu::Family::Dmma) {                            // flops_masked_padding
+            const femgpu::DmmaLayout L = femgpu::dmma_layout(sig, kp);
+            c[2] = std::max<long long>(0, L.nfrag * 64 - sig.usable_flops()) * C;
+        }
+        long long gather = 0, coord = 0, scatter = 0;
+        if (kp.family == femgpu::Family::Macro) {  // unique nodes of each group, once
+            const femgpu::MacroLayout& M = I.macro_layout(kp.G);
+            const long long ng = C / kp.G;
+            for (size_t i = 0; i < I.sspaces.size(); ++i) gather += M.unique[I.sspaces[i].group] * ng;
+            for (size_t i = 0; i < I.vspaces.size(); ++i) gather += d * M.unique[I.vspaces[i].group] * ng;
+            if (sig.affine) coord = d * M.unique[I.coord_group] * ng;
+            scatter = static_cast<long long>(M.unique[I.test_group]) * ng;
+        } else {
+            for (int i = 0; i < sig.ns(); ++i) gather += static_cast<long long>(sig.sdofs[i]) * C;
+            for (int i = 0; i < sig.nv(); ++i) gather += d * sig.vdofs[i] * C;
+            if (sig.affine) coord = static_cast<long long>(sig.coord_dofs) * d * C;
+            scatter = static_cast<long long>(sig.nW) * C;
+        }
+        const long long grid = femgpu::launch_grid(I, kp, *mod, C);
+        c[3] = gather;                                                      // gather_words
+        c[4] = scatter;                                                     // scatter_words (red.add)
+        c[5] = kp.basis == FEMGPU_BASIS_CONST ? 0 : sig.tab_size * grid;    // reference_words (staged per CTA)
+        c[6] = kp.basis == FEMGPU_BASIS_CONST ? sig.tab_size * C : 0;       // reference_cached_words (constant bank)
+        c[7] = coord;                                                       // coord_words
+        c[11] = static_cast<long long>(mod->emitted.smem_bytes / 8);        // local_words_highwater
+        c[12] = grid;                                                       // workgroups (CTAs)
+        std::copy(c, c + FEMGPU_TRACE_COUNTERS, out);
+    });
+}
+
 femgpu_status femgpu_read_output(femgpu_instance* h, double* y_host) {
     return guard([&] {
         auto& I = get(h);

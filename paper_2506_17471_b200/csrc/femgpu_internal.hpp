@@ -299,6 +299,7 @@ void run_action(Instance& inst, const KernelPlan& kp, double* d_y, cudaStream_t 
 void run_action_range(Instance& inst, const KernelPlan& kp, double* d_y, cudaStream_t stream, int c_begin, int c_end,
                       bool zero_y, cudaEvent_t after_zero = nullptr, double* zero_ptr = nullptr,
                       long long zero_n = 0);
+long long launch_grid(Instance& inst, const KernelPlan& kp, const Module& mod, long long ncell);  // CTAs of one launch
 extern const char* kZeroPrologue;  // emit.cpp
 // Output-pipelined action: d_y is all zeros on entry; the action kernel also zeroes d_next (the next
 // step's output) in its prologue, so back-to-back steps need no separate memset (femgpu_action_device_pipelined).

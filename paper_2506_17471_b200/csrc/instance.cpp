@@ -1055,6 +1055,16 @@ void run_action_range(Instance& I, const KernelPlan& kp, double* d_y, cudaStream
     if (after_zero) FG_CUDA(cudaEventRecord(after_zero, stream));
     const long long ncell = static_cast<long long>(c_end) - c_begin;
     if (ncell <= 0) return;
+    const long long grid = launch_grid(I, kp, *mod, ncell);
+    if (grid > INT_MAX) fail(FEMGPU_E_INFEASIBLE, "launch: grid too large");
+    FG_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(mod->fast), dim3(static_cast<unsigned>(grid)),
+                             dim3(kp.block), args, mod->emitted.smem_bytes, stream));
+    I.last_launches = 1;
+}
+
+long long launch_grid(Instance& I, const KernelPlan& kp, const Module& m, long long ncell) {
+    const Module* mod = &m;
+    const TileLayout* L = kp.family == Family::Tile ? &I.tile_layout(kp.tile_cells) : nullptr;
     long long grid = 0;
     if (kp.family == Family::Mlt)
         grid = (static_cast<long long>(I.cells) + kp.Nc - 1) / kp.Nc;
@@ -1074,10 +1084,7 @@ void run_action_range(Instance& I, const KernelPlan& kp, double* d_y, cudaStream
     else
         grid = (ncell + static_cast<long long>(kp.block) * std::max(1, kp.G) - 1) /
                (static_cast<long long>(kp.block) * std::max(1, kp.G));
-    if (grid > INT_MAX) fail(FEMGPU_E_INFEASIBLE, "launch: grid too large");
-    FG_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(mod->fast), dim3(static_cast<unsigned>(grid)),
-                             dim3(kp.block), args, mod->emitted.smem_bytes, stream));
-    I.last_launches = 1;
+    return grid;
 }
 
 void check_failure(Instance& I, const KernelPlan& kp, cudaStream_t stream) {

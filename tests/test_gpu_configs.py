@@ -123,3 +123,21 @@ def test_host_pipeline_with_a_gap_of_untouched_rows(oracle):
             yh = np.full(p.output_size, np.nan)
             g.action_host(list(p.scalar_inputs), list(p.vector_inputs), yh)
             assert rel_l2(yh, ref) <= 1e-12 and max_rel(yh, ref) <= 1e-10
+
+
+def test_executor_fills_trace_counters():
+    """ExecutionOutcome::counters (search.hpp:257-264) from femgpu_trace_counters: the usable matvec
+    flops are exact; the macro layout reads each unique node of a group once, so it gathers and
+    scatters fewer words than one-thread-per-cell SCPT; DMMA reports its m8n8k4 padding."""
+    p = fg.config_problem("C2", n=10)
+    run = fg.gpu_executor(measure=False)
+    cells, usable = p.connectivity.cell_count, fg.usable_flops(p.signature)
+    scpt = run(fg.TilingParams.scpt(scatter=abi.SCATTER_ATOMIC), p)
+    macro = run(fg.TilingParams.scpt(scatter=abi.SCATTER_MACRO, group_cells=6, block_cells=32), p)
+    dmma = run(fg.TilingParams.dmma(), p)
+    for o in (scpt, macro, dmma):
+        assert o.ok and o.counters["flops_matvec"] == usable * cells and o.workgroups > 0
+    assert scpt.counters["gather_words"] == 10 * cells and scpt.counters["scatter_words"] == 10 * cells
+    assert macro.counters["gather_words"] == 27 * cells // 6 and macro.counters["scatter_words"] == 27 * cells // 6
+    assert macro.counters["coord_words"] == 3 * 8 * cells // 6 and scpt.counters["coord_words"] == 3 * 4 * cells
+    assert dmma.counters["flops_masked_padding"] > 0 and scpt.counters["flops_masked_padding"] == 0
