@@ -18,6 +18,8 @@
 //   [0] xready   the step whose owned inputs r has published (written by r)
 //   [1] consumed the step whose received contributions r has added (written by r)
 //   [2..5] error: which wait timed out (1 pull, 2 push, 4 receive), the peer, value seen, wanted
+//   [6] step     this rank's step counter, advanced on the device by the first kernel of a step (so a
+//                captured CUDA graph of one step replays correctly)
 //   [8 + q]      pushed: the step whose contributions rank q has stored into r's receive buffer
 // Receive buffers are double-buffered by step parity; a push of step k waits until the owner
 // consumed step k - 2, so a fast rank cannot overwrite contributions still being added.
@@ -36,6 +38,7 @@ namespace {
 
 constexpr int kMaxWorld = 64;
 constexpr int kFlagPushed = 8;
+constexpr int kFlagStep = 6;
 constexpr int kFlagWords = kFlagPushed + kMaxWorld;
 constexpr int kMaxSpaces = 2 * FEMGPU_MAX_SPACES;
 
@@ -89,7 +92,14 @@ struct PullArgs {
     const int* comps;                    // [kMaxSpaces] components per node
 };
 
+__device__ __forceinline__ long long cur_step(const long long* flags) {
+    return *reinterpret_cast<const volatile long long*>(flags + kFlagStep);
+}
+
+__global__ void bump_step_kernel(long long* flags) { flags[kFlagStep] += 1; }
+
 __global__ void pull_kernel(PullArgs a) {
+    a.step = cur_step(a.my_flags);
     if (threadIdx.x == 0) {
         if (blockIdx.x == 0) {
             __threadfence_system();  // the caller's updates of the owned inputs precede the flag
@@ -127,6 +137,7 @@ struct PushArgs {
 };
 
 __global__ void push_kernel(PushArgs a) {
+    a.step = cur_step(a.my_flags);
     if (threadIdx.x == 0)  // slot reuse: the owner must have consumed step - 2
         for (int i = 0; i < a.n_targets; ++i)
             wait_geq(a.peer_flags[a.targets[i]] + 1, a.step - 2, a.my_flags + 2, a.timeout_ns, 2, a.targets[i]);
@@ -166,6 +177,7 @@ struct RecvArgs {
 };
 
 __global__ void recv_kernel(RecvArgs a) {
+    a.step = cur_step(a.my_flags);
     if (threadIdx.x == 0)
         for (int i = 0; i < a.n_sources; ++i)
             wait_geq(a.my_flags + kFlagPushed + a.sources[i], a.step, a.my_flags + 2, a.timeout_ns, 4, a.sources[i]);
@@ -259,7 +271,9 @@ namespace {
 
 void halo_step(femgpu_halo& H, const femgpu::KernelPlan& kp, double* y, cudaStream_t s) {
     femgpu::Instance& I = *H.inst;
-    const long long k = ++H.step;
+    ++H.step;  // host mirror (messages); the kernels read the device counter
+    bump_step_kernel<<<1, 1, 0, s>>>(H.flags);
+    FG_CUDA(cudaGetLastError());
     FG_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * static_cast<size_t>(I.output_size), s));
     {  // publish my inputs, pull the ghosts (always launched: peers wait for my xready)
         PullArgs a{};
@@ -267,7 +281,6 @@ void halo_step(femgpu_halo& H, const femgpu::KernelPlan& kp, double* y, cudaStre
         a.peer_flags = const_cast<const long long* const*>(H.d_peer_flags);
         a.pull_peers = H.d_pull_peers;
         a.n_pull_peers = static_cast<int>(H.pull_peers.size());
-        a.step = k;
         a.timeout_ns = H.timeout_ns;
         a.n = static_cast<long long>(H.pull_node.size());
         a.space = H.d_pull_space;
@@ -295,7 +308,6 @@ void halo_step(femgpu_halo& H, const femgpu::KernelPlan& kp, double* y, cudaStre
         a.targets = H.d_targets;
         a.n_targets = static_cast<int>(H.push_targets.size());
         a.rank = H.rank;
-        a.step = k;
         a.timeout_ns = H.timeout_ns;
         a.n = static_cast<long long>(H.push_row.size());
         a.row = H.d_push_row;
@@ -316,7 +328,6 @@ void halo_step(femgpu_halo& H, const femgpu::KernelPlan& kp, double* y, cudaStre
         a.my_flags = H.flags;
         a.sources = H.d_sources;
         a.n_sources = static_cast<int>(H.recv_sources.size());
-        a.step = k;
         a.timeout_ns = H.timeout_ns;
         a.n_rows = static_cast<long long>(H.recv_row_u.size());
         a.row = H.d_recv_row;
@@ -462,7 +473,7 @@ femgpu_status femgpu_halo_create(femgpu_instance* inst, int32_t rank, int32_t wo
         // load the exchange kernels now (lazy module loading would otherwise load them at the first
         // launch, which may wait for the device while a peer spins on this rank)
         for (const void* k : {reinterpret_cast<const void*>(pull_kernel), reinterpret_cast<const void*>(push_kernel),
-                              reinterpret_cast<const void*>(recv_kernel)}) {
+                              reinterpret_cast<const void*>(recv_kernel), reinterpret_cast<const void*>(bump_step_kernel)}) {
             cudaFuncAttributes fa{};
             FG_CUDA(cudaFuncGetAttributes(&fa, k));
         }
@@ -588,12 +599,34 @@ femgpu_status femgpu_halo_time_steps(femgpu_halo* h, const femgpu_schedule* s, i
         // wait on each other's spinning exchange kernels from the host
         FG_CUDA(cudaStreamSynchronize(I.stream));
         FG_CUDA(cudaStreamSynchronize(h->side));
+        // one step captured as a CUDA graph (its step numbers live on the device), replayed per step:
+        // one graph launch per action instead of six launches (FEMGPU_HALO_GRAPH=0: direct launches)
+        const char* ge = std::getenv("FEMGPU_HALO_GRAPH");
+        const bool use_graph = !(ge && std::strcmp(ge, "0") == 0);
+        cudaGraphExec_t exec = nullptr;
+        if (use_graph) {
+            cudaGraph_t graph = nullptr;
+            FG_CUDA(cudaStreamBeginCapture(I.stream, cudaStreamCaptureModeThreadLocal));
+            halo_step(*h, kp, I.d_y, I.stream);
+            FG_CUDA(cudaStreamEndCapture(I.stream, &graph));
+            FG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+            cudaGraphDestroy(graph);
+            --h->step;  // capture did not run a step
+        }
         FG_CUDA(cudaEventRecord(I.ev0, I.stream));
-        for (int i = 0; i < steps; ++i) halo_step(*h, kp, I.d_y, I.stream);
+        for (int i = 0; i < steps; ++i) {
+            if (exec) {
+                FG_CUDA(cudaGraphLaunch(exec, I.stream));
+                ++h->step;
+            } else {
+                halo_step(*h, kp, I.d_y, I.stream);
+            }
+        }
         FG_CUDA(cudaEventRecord(I.ev1, I.stream));
         FG_CUDA(cudaEventSynchronize(I.ev1));
         float ms = 0.f;
         FG_CUDA(cudaEventElapsedTime(&ms, I.ev0, I.ev1));
+        if (exec) cudaGraphExecDestroy(exec);
         *seconds = ms * 1e-3;
     });
 }

@@ -348,9 +348,13 @@ class DistInstance:
         from ._native import lib
         self.plan = plan
         self.inst = fa.GpuInstance(plan.local)
-        # JIT, automatic schedule and every allocation before the first exchange: a module load or
-        # cudaMalloc may wait for the device, which must never happen while a peer spins on this rank
-        self.inst.action()
+        # one schedule for every rank: rank 0 runs the automatic schedule on its slab (alone on the
+        # device), the others take its decision, so all slabs run the same kernel
+        sched = self.inst.default_schedule() if plan.rank == 0 else None
+        self.params = gather(sched)[0]
+        # JIT and every allocation before the first exchange: a module load or cudaMalloc may wait
+        # for the device, which must never happen while a peer spins on this rank
+        self.inst.action(self.params)
         L = lib()
 
         def cat(parts):
@@ -386,14 +390,14 @@ class DistInstance:
     def action(self, params=None, y_dev: int = 0, stream: int = 0):
         from . import action as fa
         from ._native import lib
-        sp = fa._sched(params)
+        sp = fa._sched(params if params is not None else self.params)
         fa._call(lib().femgpu_halo_action(self.halo, sp[0] if sp else None, C.c_void_p(y_dev), C.c_void_p(stream)))
 
     def time_steps(self, steps: int, params=None) -> float:
         from . import action as fa
         from ._native import lib
         s = C.c_double()
-        sp = fa._sched(params)
+        sp = fa._sched(params if params is not None else self.params)
         fa._call(lib().femgpu_halo_time_steps(self.halo, sp[0] if sp else None, steps, C.byref(s)))
         return s.value
 
@@ -516,7 +520,6 @@ def bench(args):
     plan = build_plan(slab, rank, world, gather)
     t_plan = time.perf_counter() - t0
     di = DistInstance(plan, gather)
-    di.inst.action()  # JIT + automatic schedule of the local instance (outside the timed region)
     tdist.barrier()
     for _ in range(max(args.warmup, 3)):
         di.action()
@@ -533,7 +536,7 @@ def bench(args):
                     "boundary_cells": plan.boundary_cells, "halo_rows": plan.halo_rows(),
                     "pull_nodes": int(sum(len(m) for d in plan.pull for m, _ in d.values())),
                     "step_us": t_rank * 1e6, "plan_s": round(t_plan, 2),
-                    "schedule": di.inst.describe().split(" | auto: ")[0]})
+                    "schedule": di.inst.describe(di.params).split(" | auto: ")[0]})
     if rank == 0:
         c = dict(CONFIGS[args.config])
         if args.n is not None:
