@@ -342,7 +342,8 @@ void halo_step(femgpu_halo& H, const femgpu::KernelPlan& kp, double* y, cudaStre
         FG_CUDA(cudaGetLastError());
     }
     if (!H.push_targets.empty()) FG_CUDA(cudaStreamWaitEvent(s, H.ev_pushed, 0));
-    I.last_launches = split ? 4 + (H.push_targets.empty() ? 0 : 1) : 3;
+    // bump + pull + action launch(es) + push + completion (the memset is the driver's)
+    I.last_launches = 3 + (split ? 2 : 1) + (H.push_targets.empty() ? 0 : 1);
 }
 
 }  // namespace

@@ -524,13 +524,39 @@ def bench(args):
     for _ in range(max(args.warmup, 3)):
         di.action()
     di.check()
+    # ---- timed region: exactly K distributed actions per rank (one CUDA graph launch each), CUDA
+    # events on the rank's stream, barrier + device synchronize on both sides, max over ranks
+    torch.cuda.synchronize()
     tdist.barrier()
     t_rank = di.time_steps(args.steps) / args.steps
+    torch.cuda.synchronize()
+    tdist.barrier()
     di.check()
     t = torch.tensor([t_rank], dtype=torch.float64)
     tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
     t_step = float(t.item())
+    launches = di.inst.stats()["launches_last_action"]
     gids, ys = di.owned_output()
+    # ---- e2e through the public API with host buffers: each rank uploads its slab's inputs
+    # (femgpu_set_inputs), runs the distributed action, downloads its output (femgpu_read_output)
+    p = plan.local
+    xs_h = [np.ascontiguousarray(x) for x in p.scalar_inputs]
+    vs_h = [np.ascontiguousarray(x) for x in p.vector_inputs]
+    h2d = sum(x.nbytes for x in xs_h + vs_h)
+    d2h = 8 * p.output_size
+    e2e_steps = max(2, min(args.e2e_steps, 20))
+    tdist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        di.inst.set_inputs(xs_h, vs_h)
+        di.action()
+        di.inst.read_output()
+    tdist.barrier()
+    te = torch.tensor([(time.perf_counter() - t0) / e2e_steps], dtype=torch.float64)
+    tdist.all_reduce(te, op=tdist.ReduceOp.MAX)
+    io = torch.tensor([float(h2d), float(d2h)], dtype=torch.float64)
+    tdist.all_reduce(io)
+    di.check()
     parts = gather((gids, ys))
     stats = gather({"rank": rank, "device": device, "cells": int(plan.local.connectivity.cell_count),
                     "boundary_cells": plan.boundary_cells, "halo_rows": plan.halo_rows(),
@@ -554,7 +580,11 @@ def bench(args):
                                    "ascending rank order" % (args.config, world),
                        "cells": int(cells), "dofs": int(dofs), "parallelism": "cells%d" % world,
                        "devices_visible": ndev, "control_plane": "torch.distributed gloo (plan + handle exchange)"},
-            "gpu_launches": args.steps * max(1, di.inst.stats()["launches_last_action"]),
+            "gpu_launches": args.steps * max(1, launches) * world,
+            "e2e": {"value": dofs / float(te.item()) / 1e9, "unit": "GDOF/s", "h2d_bytes_per_step": int(io[0].item()),
+                    "d2h_bytes_per_step": int(io[1].item()), "ms_per_step": float(te.item()) * 1e3,
+                    "api": "per rank femgpu_set_inputs + femgpu_halo_action + femgpu_read_output (host buffers), "
+                           "wall clock, max over ranks"},
             "ranks": stats,
         }
         y = np.full(dofs, np.nan)
