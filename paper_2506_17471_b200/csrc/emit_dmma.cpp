@@ -404,7 +404,8 @@ void emit_dmma_kernel(std::ostringstream& o, const Signature& sig, const KernelP
         for (int nb = 0; nb < L.NBQ; ++nb)
             o << "      double y" << nb << J << j << "_0 = 0.0, y" << nb << J << j << "_1 = 0.0;\n";
     }
-    o << "      #pragma unroll 1\n";
+    // quadrature chunks: rolled, or two per trip (qmopt bit 14: more independent DMMA chains)
+    o << ((kp.qmopt & 16384) ? "      #pragma unroll 2\n" : "      #pragma unroll 1\n");
     o << "      for (int ch = 0; ch < " << L.NCH << "; ++ch) {\n";
     o << "        const double* const Fc = FR + (size_t)ch * " << L.FPC * 32 << "; (void)Fc;\n";
     // ---- evaluation GEMMs (one B fragment load feeds MBJ DMMAs)

@@ -523,6 +523,7 @@ void resolve_dmma(const Signature& sig, KernelPlan& kp, const femgpu_schedule* s
         fail(FEMGPU_E_INFEASIBLE, "dmma: joint m-blocks (eval_row_tile) must divide the m-blocks of a warp task");
     kp.Tqr = s->quad_row_tile > 0 ? 1 : 0;
     kp.breg = (s->reserved[3] & 0xff) == 1;  // B fragments in registers (honoured for a single quadrature chunk)
+    kp.qmopt = (s->reserved[3] >> 16) & 0x4000;  // two quadrature chunks per trip
     const int q4 = (sig.Q + 3) / 4 * 4;
     if (s->quad_tile > 0) {
         kp.TQ = std::min(q4, (s->quad_tile + 3) / 4 * 4);

@@ -79,7 +79,7 @@ std::pair<long long, long long> map_instr(const Signature& sig) {
 std::string tune_key(const Instance& I) {
     const Signature& sig = I.sig;
     std::ostringstream k;
-    k << "v11|" << sig.dim << "|" << sig.Q << "|" << sig.nW << "|" << sig.Tw << "|" << I.cells << "|" << I.output_size;
+    k << "v12|" << sig.dim << "|" << sig.Q << "|" << sig.nW << "|" << sig.Tw << "|" << I.cells << "|" << I.output_size;
     for (size_t i = 0; i < sig.sdofs.size(); ++i) k << "|s" << sig.sdofs[i] << ":" << sig.sterms[i];
     for (size_t i = 0; i < sig.vdofs.size(); ++i) {
         k << "|v" << sig.vdofs[i] << ":" << sig.vterms[i];
@@ -131,7 +131,8 @@ std::string describe_plan(const KernelPlan& kp) {
         case Family::Tile: s << "femgpu_tile cells=" << kp.tile_cells; break;
         case Family::Mlt: s << "femgpu_mlt Nc=" << kp.Nc << " Nwi=" << kp.Nwi << " TQ=" << kp.TQ; break;
         case Family::Dmma:
-            s << "femgpu_dmma cells/task=" << kp.Nc << " TQ=" << kp.TQ << " joint=" << kp.Ter << " prefetch=" << kp.Tqr
+            s << "femgpu_dmma cells/task=" << kp.Nc << " TQ=" << kp.TQ << ((kp.qmopt & 16384) ? " 2ch/trip" : "")
+              << " joint=" << kp.Ter << " prefetch=" << kp.Tqr
               << " block=" << kp.block << " basis=" << (kp.basis == FEMGPU_BASIS_SMEM ? "smem" : "l1");
             break;
     }
@@ -309,6 +310,18 @@ void autotune(Instance& I) {
                         femgpu_schedule s = dmma_variant(joint, pf, block, 32);
                         s.quad_tile = tq;
                         add(s, 2);
+                        if (joint == 1 && block == 128) {
+                            KernelPlan kt;
+                            try {
+                                resolve_dmma(sig, kt, &s);
+                            } catch (const Error&) {
+                                continue;
+                            }
+                            if (dmma_layout(sig, kt).NCH > 1) {
+                                s.reserved[3] = 0x4000 << 16;  // two quadrature chunks per trip (hyp-P4 2815 vs 2895 us)
+                                add(s, 2);
+                            }
+                        }
                     }
     }
     // ---- static pruning: the best kCompile by FP64-pipe time (each family keeps its best two)

@@ -66,6 +66,8 @@ def sched(name):
                 d["min_blocks"] = int(p[1:])
             elif p == "breg":
                 d["stage_smem"] = 1
+            elif p == "u2":
+                d["qmopt"] = 16384
             elif p.startswith("b"):
                 d["block_cells"] = int(p[1:])
             elif p == "smem":
