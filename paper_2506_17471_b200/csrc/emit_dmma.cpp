@@ -207,6 +207,8 @@ void emit_dmma_kernel(std::ostringstream& o, const Signature& sig, const KernelP
     const bool smemA = kp.basis == FEMGPU_BASIS_SMEM;
     // timing experiments only (wrong results): plain stores instead of red.add in the scatter
     const bool scatter_store = std::getenv("FEMGPU_DEBUG_SCATTER_STORE") != nullptr;
+    // timing experiments only (wrong results): value gathers from 64 nodes (L1-resident, few wavefronts)
+    const std::string gx = std::getenv("FEMGPU_DEBUG_GATHER_LOCAL") != nullptr ? " & 63)" : ")";
     bool uses_inv = false;
     for (size_t id = 0; id < sig.nodes.size(); ++id)
         if (live[id] && sig.nodes[id].op == FEMGPU_OP_INV_JACOBIAN) uses_inv = true;
@@ -319,7 +321,7 @@ void emit_dmma_kernel(std::ostringstream& o, const Signature& sig, const KernelP
                     const std::string pv = "pv" + S(sp.i) + "_" + S(ks) + J + S(j) + "_" + upre;
                     if (pair)
                         o << ind << "const double2 " << pv << " = " << ix << " >= 0 ? __ldg(reinterpret_cast<const double2*>(P.v"
-                          << sp.i << " + (size_t)" << ix << " * " << vec_stride(sig.dim) << ")) : make_double2(0.0, 0.0);\n";
+                          << sp.i << " + (size_t)(" << ix << gx << " * " << vec_stride(sig.dim) << ")) : make_double2(0.0, 0.0);\n";
                     for (int gid : sp.gids) {
                         o << ind << (decl ? "const double " : "") << uname(upre, gid, ks, j) << " = ";
                         if (pair && gid == g0c)
@@ -327,10 +329,10 @@ void emit_dmma_kernel(std::ostringstream& o, const Signature& sig, const KernelP
                         else if (pair && gid == g1c)
                             o << pv << ".y;\n";
                         else if (sp.vec)
-                            o << ix << " >= 0 ? __ldg(&P.v" << sp.i << "[(size_t)" << ix << " * " << vec_stride(sig.dim) << " + "
+                            o << ix << " >= 0 ? __ldg(&P.v" << sp.i << "[(size_t)(" << ix << gx << " * " << vec_stride(sig.dim) << " + "
                               << L.groups[gid].comp << "]) : 0.0;\n";
                         else
-                            o << ix << " >= 0 ? __ldg(&P.x" << sp.i << "[" << ix << "]) : 0.0;\n";
+                            o << ix << " >= 0 ? __ldg(&P.x" << sp.i << "[(" << ix << gx << "]) : 0.0;\n";
                     }
                 }
             }

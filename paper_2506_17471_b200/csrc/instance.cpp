@@ -606,8 +606,10 @@ const MacroLayout& Instance::macro_layout(int G) {
             if (static_cast<int>(g) == test_group) {
                 // warp merge candidates: lanes l and l+s of a warp hold groups g and g+s; count how
                 // often g's unique node u is g+s's node u' (a sample of warps is enough)
+                // (256 sampled warps; g+s's nodes sorted once per pair: O(U log U), not O(U^2))
                 const long long warps = ng / 32;
-                const long long step = std::max(1LL, warps / 4096);
+                const long long step = std::max(1LL, warps / 256);
+                std::vector<std::pair<int32_t, int>> nodes1(static_cast<size_t>(U));
                 for (int sft : {1, 2, 4, 8, 16}) {
                     std::vector<long long> hits(static_cast<size_t>(U) * U, 0);
                     long long pairs = 0;
@@ -615,10 +617,12 @@ const MacroLayout& Instance::macro_layout(int G) {
                         for (int l = 0; l + sft < 32; ++l) {
                             const long long g0 = w * 32 + l, g1 = g0 + sft;
                             ++pairs;
+                            for (int u2 = 0; u2 < U; ++u2) nodes1[u2] = {gidx[static_cast<size_t>(u2) * ng + g1], u2};
+                            std::sort(nodes1.begin(), nodes1.end());
                             for (int u = 0; u < U; ++u) {
                                 const int32_t v = gidx[static_cast<size_t>(u) * ng + g0];
-                                for (int u2 = 0; u2 < U; ++u2)
-                                    if (gidx[static_cast<size_t>(u2) * ng + g1] == v) ++hits[static_cast<size_t>(u) * U + u2];
+                                auto it = std::lower_bound(nodes1.begin(), nodes1.end(), std::make_pair(v, -1));
+                                for (; it != nodes1.end() && it->first == v; ++it) ++hits[static_cast<size_t>(u) * U + it->second];
                             }
                         }
                     for (int u = 0; u < U && pairs; ++u)

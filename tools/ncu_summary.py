@@ -28,6 +28,10 @@ def main():
         if k in h:
             i = h.index(k)
             print("%-72s %s %s" % (k, v[i], units[i]))
+    # L1 data-pipe wavefronts by kind (shared / global / reductions ...)
+    for i, k in enumerate(h):
+        if k.startswith("l1tex__data_pipe_lsu_wavefronts") and k.endswith(".sum") and k not in KEYS:
+            print("%-72s %s %s" % (k, v[i], units[i]))
     stalls = []
     for i, k in enumerate(h):
         if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued"):

@@ -7,6 +7,7 @@ usage: python tools/tune_report.py C2,C4 out.jsonl [all]
 import json
 import os
 import sys
+import tempfile
 import time
 
 sys.path.insert(0, ".")
@@ -22,6 +23,7 @@ for cfg in cfgs or list(fg.CONFIGS):
     if os.path.exists(out + ".tmp"):
         os.remove(out + ".tmp")
     p = fg.config_problem(cfg)
+    os.environ["FEMGPU_CACHE"] = tempfile.mkdtemp(prefix="femgpu_tune_")  # cold JIT cache: honest tune wall
     t0 = time.perf_counter()
     with fg.GpuInstance(p) as g:
         sched = g.default_schedule()
@@ -33,7 +35,8 @@ for cfg in cfgs or list(fg.CONFIGS):
         f.write(json.dumps(rec) + "\n")
     timed = [c for c in rec.get("candidates", []) if c["meas_us"] > 0]
     best = min(timed, key=lambda c: c["meas_us"]) if timed else None
-    print(cfg, "tune %.1f s" % t_tune, "timed", len(timed), "winner", rec.get("winner"),
+    print(cfg, "tune %.1f s (model %.1f, jit %.1f, timing %.1f)" % (t_tune, rec.get("model_s", 0), rec.get("jit_s", 0),
+                                                              rec.get("timing_s", 0)), "timed", len(timed), "winner", rec.get("winner"),
           "best %.1f us" % best["meas_us"] if best else "", "spearman %.2f" % rec.get("spearman", 0), flush=True)
 if os.path.exists(out + ".tmp"):
     os.remove(out + ".tmp")
