@@ -80,7 +80,7 @@ std::pair<long long, long long> map_instr(const Signature& sig) {
 std::string tune_key(const Instance& I) {
     const Signature& sig = I.sig;
     std::ostringstream k;
-    k << "v13|" << sig.dim << "|" << sig.Q << "|" << sig.nW << "|" << sig.Tw << "|" << I.cells << "|" << I.output_size;
+    k << "v17|" << sig.dim << "|" << sig.Q << "|" << sig.nW << "|" << sig.Tw << "|" << I.cells << "|" << I.output_size;
     for (size_t i = 0; i < sig.sdofs.size(); ++i) k << "|s" << sig.sdofs[i] << ":" << sig.sterms[i];
     for (size_t i = 0; i < sig.vdofs.size(); ++i) {
         k << "|v" << sig.vdofs[i] << ":" << sig.vterms[i];
@@ -186,9 +186,11 @@ femgpu_schedule scpt_variant(int G, int block, int min_blocks, bool qloop) {
 // macro 0.64-0.70, SCPT 0.45-0.63 (scalar forms), DMMA 0.56-0.68 of its padded slots; the HBM side
 // reaches ~0.65 of the peak on gather/scatter traffic.  Resident warps hide the gather latency:
 // each warp per SM fewer than the 32 of full occupancy costs ~ kLatency / warps (fitted: 8 warps
-// +15 %, 16 warps +7.5 %); local-memory spills cost ~ spill / kSpillBytes.
+// +15 %, 16 warps +7.5 %); local-memory spills cost ~ (spill / kSpillBytes)^2: up to ~800 B/thread they
+// stay in L1 and cost 0-10 % (C5-hyp-P1 q-major macro: 544 B, 11 % faster than the best non-spilling
+// kernel), 1.4-2.8 KB cost 10-40 %, 8.5 KB 10x (profiles/r02_tuner_calibration.jsonl)
 constexpr double kEffMacro = 0.68, kEffScpt = 0.55, kEffDmma = 0.62, kEffHbm = 0.65;
-constexpr double kLatency = 1.2, kSpillBytes = 2048.0;
+constexpr double kLatency = 1.2, kSpillBytes = 4096.0;
 // DMMA B-fragment share of the L1 data pipe at one m-block per fragment load (C4: joint 1/2 at
 // 2034/1919 us without prefetch, joint 2/4 at 1869/1831 us with it; C5-adv-P1 joint 1/2 at 5010/4642 us)
 constexpr double kBfrag = 0.15;
@@ -386,8 +388,12 @@ void autotune(Instance& I) {
     for (size_t i : sel) {
         Cand& c = C[i];
         if (!c.compiled) continue;
-        const double w = std::max(1, c.warps);
-        c.pred = c.t_pipe * (1.0 + kLatency / w) * (1.0 + static_cast<double>(c.spill) / kSpillBytes);
+        // DMMA gather prefetch (values one m-group ahead) hides latency like ~1.5x the resident warps
+        // (C3b 234.7 vs 242.0 us, C5-adv-P3 826.8 vs 845.4, C5-hyp-P1 2874 vs 2959 at 2/3 the warps)
+        const double w = std::max(1, c.warps) * (c.family == 2 && c.kp.Tqr ? 1.5 : 1.0);
+        // (SCPT spills sit inside the unrolled point loop: 240-650 B/thread cost it 2-5x)
+        const double sp = static_cast<double>(c.spill) / (c.family == 1 ? kSpillBytes / 8.0 : kSpillBytes);
+        c.pred = c.t_pipe * (1.0 + kLatency / w) * (1.0 + sp * sp);
         // DMMA: every B-fragment load (shared memory, one per DMMA) feeds `joint` m-blocks; the loads
         // compete with the gathers and the scatter for the L1 data pipe (kEffDmma is fitted at joint 2)
         if (c.family == 2) c.pred *= (1.0 + kBfrag / std::max(1, c.kp.Ter)) / (1.0 + kBfrag / 2.0);
@@ -401,19 +407,6 @@ void autotune(Instance& I) {
         for (size_t i : sel)
             if (C[i].compiled) ranked.push_back(i);
     std::stable_sort(ranked.begin(), ranked.end(), [&](size_t a, size_t b) { return C[a].pred < C[b].pred; });
-    // timed: the best-predicted candidate of every family (the model's family efficiencies are the
-    // least certain term), then the best predictions overall, b = 9; plus the SCPT baseline
-    std::vector<size_t> timed;
-    for (int fam = 0; fam < 3; ++fam)
-        for (size_t i : ranked)
-            if (C[i].family == fam) {
-                timed.push_back(i);
-                break;
-            }
-    for (size_t i : ranked)
-        if ((tune_all || timed.size() < kTimed) && std::find(timed.begin(), timed.end(), i) == timed.end())
-            timed.push_back(i);
-    if (std::find(timed.begin(), timed.end(), size_t(0)) == timed.end() && C[0].compiled) timed.push_back(0);
     // ---- measure: >= 5 runs and ~10 ms of work each, then the three fastest re-timed interleaved
     t_jit1 = Clock::now();
     auto time_it = [&](const KernelPlan& kp, int reps) {
@@ -427,21 +420,10 @@ void autotune(Instance& I) {
     };
     std::vector<int> reps_of(C.size(), 5);
     std::vector<std::pair<double, size_t>> first;
-    // clocks up before the first timed candidate (~40 ms of the first candidate's work): a GPU coming
-    // out of idle timed C5-adv-P4's first candidate 19 % slow
-    for (size_t i : timed) {
-        try {
-            run_action(I, C[i].kp, I.d_y, I.stream);
-            const double t1 = time_it(C[i].kp, 1);
-            time_it(C[i].kp, std::max(1, std::min(400, static_cast<int>(0.04 / std::max(t1, 1e-6)))));
-        } catch (const Error& e) {
-            if (e.code != FEMGPU_E_INFEASIBLE && e.code != FEMGPU_E_JIT) throw;
-            continue;
-        }
-        break;
-    }
-    for (size_t i : timed) {
+    std::vector<size_t> timed;
+    auto measure = [&](size_t i) {
         Cand& c = C[i];
+        timed.push_back(i);
         try {
             for (int k = 0; k < 2; ++k) run_action(I, c.kp, I.d_y, I.stream);
             const double t1 = time_it(c.kp, 1);
@@ -453,7 +435,65 @@ void autotune(Instance& I) {
             if (e.code != FEMGPU_E_INFEASIBLE && e.code != FEMGPU_E_JIT) throw;
             c.reject = std::string("launch: ") + e.what();
         }
+    };
+    // clocks up before the first timed candidate (~40 ms of the best prediction's work): a GPU coming
+    // out of idle timed C5-adv-P4's first candidate 19 % slow
+    for (size_t i : ranked) {
+        try {
+            run_action(I, C[i].kp, I.d_y, I.stream);
+            const double t1 = time_it(C[i].kp, 1);
+            time_it(C[i].kp, std::max(1, std::min(400, static_cast<int>(0.04 / std::max(t1, 1e-6)))));
+        } catch (const Error& e) {
+            if (e.code != FEMGPU_E_INFEASIBLE && e.code != FEMGPU_E_JIT) throw;
+            continue;
+        }
+        break;
     }
+    // stage 1: the best prediction of every kernel class (the model's cross-class efficiencies are
+    // its least certain term; within a class its ranking holds better).  Classes: macro q-major
+    // (one warp per group), macro split/cell-major, SCPT, DMMA -- the split and cell-major macro
+    // kernels measured 1.2-1.9x their prediction on the heavy forms, q-major 0.6-0.95x
+    auto cls = [&](size_t i) {
+        const Cand& c = C[i];
+        return c.family == 0 && !(c.kp.qmajor && c.kp.msplit == 1) ? 3 : c.family;
+    };
+    for (int k = 0; k < 4; ++k)
+        for (size_t i : ranked)
+            if (cls(i) == k) {
+                measure(i);
+                break;
+            }
+    // stage 2: the remaining slots (b = 9) in prediction order within the classes as measured in
+    // stage 1: two thirds to the fastest class, the rest to a runner-up within 25 % (C3b: macro candidates
+    // predicted ahead of the DMMA ones measured 1.3-1.9x slower and took the slots of the winner)
+    {
+        std::vector<std::pair<double, int>> fam_t;
+        for (auto& f : first) fam_t.push_back({f.first, cls(f.second)});
+        std::sort(fam_t.begin(), fam_t.end());
+        const size_t left = kTimed > timed.size() ? kTimed - timed.size() : 0;
+        std::vector<size_t> quota(4, 0);
+        // (a runner-up measured more than 25 % behind gets nothing: the slots go to the fastest class)
+        const bool close = fam_t.size() > 1 && fam_t[1].first <= 1.25 * fam_t[0].first;
+        if (!fam_t.empty()) quota[fam_t[0].second] = close ? (2 * left + 2) / 3 : left;
+        if (close) quota[fam_t[1].second] = left - quota[fam_t[0].second];
+        std::vector<size_t> extra;
+        for (size_t k = 0; k < fam_t.size() && k < 2; ++k)
+            for (size_t i : ranked) {
+                if (quota[fam_t[k].second] == 0) break;
+                if (cls(i) == fam_t[k].second && std::find(timed.begin(), timed.end(), i) == timed.end() &&
+                    std::find(extra.begin(), extra.end(), i) == extra.end()) {
+                    extra.push_back(i);
+                    --quota[fam_t[k].second];
+                }
+            }
+        // unused quota (a family ran out of candidates): the best remaining predictions overall
+        for (size_t i : ranked)
+            if ((tune_all || timed.size() + extra.size() < kTimed) && std::find(timed.begin(), timed.end(), i) == timed.end() &&
+                std::find(extra.begin(), extra.end(), i) == extra.end())
+                extra.push_back(i);
+        for (size_t i : extra) measure(i);
+    }
+    if (std::find(timed.begin(), timed.end(), size_t(0)) == timed.end() && C[0].compiled) measure(0);  // + SCPT
     std::sort(first.begin(), first.end());
     const size_t top = std::min<size_t>(3, first.size());
     std::vector<double> retime(top, 1e300);
