@@ -26,10 +26,13 @@ constexpr long long kPipeMinCells = 1000000;
 constexpr long long kZeroOverlapMinRows = 1 << 21;  // 16 MB of y: ~3 us of memset
 constexpr long long kZeroOverlapMinCells = 1 << 16;
 
-int slab_count() {
+// Slabs of the overlapped host-buffer action: FEMGPU_PIPE_SLABS, else ~1 per 0.9 M cells in [4, 16].
+// Each slab costs ~11 us (a sub-wave kernel tail plus its copies and events): C2 (7.35 M cells)
+// e2e 2.265 / 2.227 / 2.302 / 2.601 / 2.828 ms at 4 / 8 / 16 / 32 / 64 slabs (tools/e2e_slabs.py).
+int slab_count(long long cells) {
     const char* e = std::getenv("FEMGPU_PIPE_SLABS");
-    const int k = e ? std::atoi(e) : 16;
-    return std::max(2, std::min(128, k));
+    const long long k = e ? std::atoi(e) : std::max(4LL, std::min(16LL, (cells + 450000) / 900000));
+    return static_cast<int>(std::max(2LL, std::min(128LL, k)));
 }
 
 // slabs for fused zeroing: FEMGPU_ZERO_SLABS, else the schedule's count (reserved[0] >> 8), else 8
@@ -42,7 +45,7 @@ int zero_slab_count(int sched_slabs) {
 }  // namespace
 
 const PipePlan& Instance::pipe_plan(int align) {
-    const int K = slab_count();
+    const int K = slab_count(cells);
     if (pipe && pipe->align == align && static_cast<int>(pipe->cb.size()) == K + 1) return *pipe;
     pipe = slab_plan(K, align);
     return *pipe;
