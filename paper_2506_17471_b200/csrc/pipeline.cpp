@@ -13,6 +13,7 @@
 // without locality the plan degenerates to the sequential order (and is then not used).
 #include <algorithm>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <limits>
 
@@ -205,13 +206,29 @@ bool pipelined_host_action(Instance& I, const KernelPlan& kp, const double* cons
     FG_CUDA(cudaStreamWaitEvent(I.s_h2d, I.ev_pipe[2 * K], 0));
     std::vector<long long> done(P.up.size(), 0);
     long long zeroed = 0, sent = 0;
+    // FEMGPU_PIPE_TRACE=1: timing events after every H2D chunk, slab kernel and D2H chunk, printed to
+    // stderr as a timeline (us from the start of the action) -- a measurement aid, off by default
+    const bool trace = std::getenv("FEMGPU_PIPE_TRACE") != nullptr;
+    // (trace experiments: FEMGPU_PIPE_TRACE_SKIP=copies|kernels drops one side -- wrong results)
+    const char* skip = std::getenv("FEMGPU_PIPE_TRACE_SKIP");
+    const bool no_copy = trace && skip && std::strcmp(skip, "copies") == 0;
+    const bool no_kernel = trace && skip && std::strcmp(skip, "kernels") == 0;
+    std::vector<cudaEvent_t> tev;
+    auto mark = [&](cudaStream_t st) {
+        if (!trace) return;
+        cudaEvent_t e;
+        FG_CUDA(cudaEventCreate(&e));
+        FG_CUDA(cudaEventRecord(e, st));
+        tev.push_back(e);
+    };
+    mark(I.s_h2d);
     for (int k = 0; k < K; ++k) {
         // H2D: every trial space up to what slab k reads
         for (size_t i = 0; i < I.sspaces.size(); ++i) {
             const long long a = done[i], b = P.up[i][k];
             if (b > a) {
                 if (!scalar_inputs || !scalar_inputs[i]) invalid("instance: scalar input length mismatch");
-                FG_CUDA(cudaMemcpyAsync(I.sspaces[i].d_x + a, scalar_inputs[i] + a, sizeof(double) * (b - a),
+                if (!no_copy) FG_CUDA(cudaMemcpyAsync(I.sspaces[i].d_x + a, scalar_inputs[i] + a, sizeof(double) * (b - a),
                                         cudaMemcpyHostToDevice, I.s_h2d));
                 done[i] = b;
             }
@@ -227,6 +244,7 @@ bool pipelined_host_action(Instance& I, const KernelPlan& kp, const double* cons
                 done[j] = b;
             }
         }
+        mark(I.s_h2d);
         FG_CUDA(cudaEventRecord(I.ev_pipe[k], I.s_h2d));
         // compute: zero the y rows slab k can newly reach, then the slab
         FG_CUDA(cudaStreamWaitEvent(I.stream, I.ev_pipe[k], 0));
@@ -234,18 +252,30 @@ bool pipelined_host_action(Instance& I, const KernelPlan& kp, const double* cons
             FG_CUDA(cudaMemsetAsync(I.d_y + zeroed, 0, sizeof(double) * (P.zero_hi[k] - zeroed), I.stream));
             zeroed = P.zero_hi[k];
         }
-        run_action_range(I, kp, I.d_y, I.stream, P.cb[k], P.cb[k + 1], false);
+        if (!no_kernel) run_action_range(I, kp, I.d_y, I.stream, P.cb[k], P.cb[k + 1], false);
+        mark(I.stream);
         FG_CUDA(cudaEventRecord(I.ev_pipe[K + k], I.stream));
         // D2H: the rows no later slab touches
         FG_CUDA(cudaStreamWaitEvent(I.s_d2h, I.ev_pipe[K + k], 0));
         if (P.fin[k] > sent) {
-            FG_CUDA(cudaMemcpyAsync(y_host + sent, I.d_y + sent, sizeof(double) * (P.fin[k] - sent),
+            if (!no_copy) FG_CUDA(cudaMemcpyAsync(y_host + sent, I.d_y + sent, sizeof(double) * (P.fin[k] - sent),
                                     cudaMemcpyDeviceToHost, I.s_d2h));
             sent = P.fin[k];
         }
+        mark(I.s_d2h);
     }
     FG_CUDA(cudaEventRecord(I.ev_pipe[2 * K], I.s_d2h));
     FG_CUDA(cudaStreamWaitEvent(I.stream, I.ev_pipe[2 * K], 0));
+    if (trace) {
+        FG_CUDA(cudaStreamSynchronize(I.stream));
+        std::fprintf(stderr, "pipe trace K=%d (us: h2d done, kernel done, d2h done per slab)\n", K);
+        for (int k = 0; k < K; ++k) {
+            float t[3];
+            for (int j = 0; j < 3; ++j) FG_CUDA(cudaEventElapsedTime(&t[j], tev[0], tev[1 + 3 * k + j]));
+            std::fprintf(stderr, "  slab %2d: %8.1f %8.1f %8.1f\n", k, t[0] * 1e3, t[1] * 1e3, t[2] * 1e3);
+        }
+        for (cudaEvent_t e : tev) cudaEventDestroy(e);
+    }
     I.last_launches = K;
     return true;
 }
