@@ -19,6 +19,8 @@ memset where that measures faster -- the automatic schedule decides per instance
           output is the parity check of the timed output (parity_vs_reference).
   forms   every benchmark configuration of SURVEY §8d (C1..C5) with the automatic schedule:
           step time, roofline fraction, parity against the reference CPU path.
+  fused   operator pairs sharing their trial function (fuse.py): the fused action's step against
+          the two separate actions' steps, parity of both parts against the reference.
 
 --impl reference: the reference's CPU implementation of the path (oracle/_ref) on all host
 threads, same config/metric, each step a bounded cell sample of the same mesh (built by
@@ -62,6 +64,8 @@ def parse():
     ap.add_argument("--forms-budget", type=float, default=900.0, help="seconds for the forms table")
     ap.add_argument("--ref-budget", type=float, default=20.0,
                     help="seconds of reference CPU work per forms row (full action if it fits, else complete rows)")
+    ap.add_argument("--no-fused", dest="fused", action="store_false",
+                    help="skip the fused multi-operator rows (fuse.py, PAPER.md:2477-2482)")
     return ap.parse_args()
 
 
@@ -471,8 +475,47 @@ def run_single(args):
                         "parity_pass": sum(1 for r in ok if (r.get("parity_vs_reference") or {}).get("pass")),
                         "definition": "frac_step = t_roof / pipelined step time (SURVEY 8d); automatic schedule; "
                                       "parity of the last timed step's y against the reference's reference_action"}
+    if args.fused and args.n is None:
+        out["fused"] = []
+        for name in FUSED_ORDER:
+            try:
+                out["fused"].append(fused_row(name, args.ref_budget))
+            except Exception as e:  # noqa: BLE001
+                out["fused"].append({"pair": name, "error": str(e)[:300]})
     out["wall_s"] = round(time.perf_counter() - wall0, 1)
     print(json.dumps(out))
+
+
+FUSED_ORDER = ["laplace+mass-P2", "stokes-P2"]
+
+
+def fused_row(name, ref_budget):
+    """One fused pair: pipelined steps of A, of B and of the fused action (automatic schedules),
+    parity of both parts of the fused output against the reference's reference_action."""
+    import paper_2506_17471_b200 as fg
+    t0 = time.perf_counter()
+    a, b = fg.fused_pair(name)
+    f, offs = fg.fuse_problems([a, b])
+
+    def step(p):
+        with fg.GpuInstance(p) as g:
+            g.action()
+            g.time_steps(3, pipelined=True)
+            k = int(max(10, min(300, 0.2 / max(g.time_steps(1, pipelined=True), 1e-6))))
+            t = g.time_steps(k, pipelined=True) / k
+            return t, g.read_output(), g.describe().split(" | auto: ")[0]
+    ta, _, pa = step(a)
+    tb, _, pb = step(b)
+    tf, yf, pf = step(f)
+    parts = fg.split_output(yf, offs)
+    checks = []
+    for y, p in zip(parts, (a, b)):
+        par, sec, kind = reference_check(p, y, budget_s=ref_budget)
+        checks.append(dict(par, reference=kind))
+    return {"pair": name, "cells": int(a.connectivity.cell_count), "rows": offs,
+            "separate_step_us": [ta * 1e6, tb * 1e6], "fused_step_us": tf * 1e6, "speedup": (ta + tb) / tf,
+            "plans": {"A": pa, "B": pb, "fused": pf}, "parity_vs_reference": checks,
+            "pass": all(c["pass"] for c in checks), "wall_s": round(time.perf_counter() - t0, 1)}
 
 
 FORMS_ORDER = ["C1", "C1b", "C2", "C3a", "C3b", "C4", "C5-adv-P1", "C5-adv-P2", "C5-adv-P3", "C5-adv-P4",

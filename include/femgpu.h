@@ -356,6 +356,18 @@ femgpu_status femgpu_problem_save(const femgpu_problem* p, const char* path);
 femgpu_status femgpu_schedule_save(const femgpu_schedule* s, int32_t n_scalar, int32_t n_vector, const char* path);
 femgpu_status femgpu_schedule_load(const char* path, femgpu_schedule* s);
 
+/* ---- fused multi-operator actions (csrc/fuse.cpp) ----
+ * n problems on the same cells, geometry (coordinate map + coordinates) and quadrature weights
+ * become one problem whose output is [y_0; y_1; ...; y_{n-1}] (offsets[p] .. offsets[p+1], n+1
+ * entries, may be NULL).  Trial spaces with the same map, global count and input are merged (their
+ * derivative terms united, identical terms shared): shared trial values are gathered and evaluated
+ * once per cell.  The test space is the disjoint union with a block-diagonal Psi; kernels skip the
+ * Psi entries that are zero at every quadrature point.  Create an instance on *view like any
+ * problem; free with femgpu_problem_free.  Differing meshes, weights or dimensions are
+ * FEMGPU_E_INVALID. */
+femgpu_status femgpu_problem_fuse(const femgpu_problem* const* problems, int32_t n, femgpu_owned_problem** out,
+                                  const femgpu_problem** view, int64_t* offsets);
+
 /* ---- structured meshes (synthetic unit square / unit cube) -------------
  * Unit square: n x n squares, 2 triangles each; unit cube: n^3 cubes, 6 Kuhn
  * tetrahedra each.  P_degree nodes live on the degree-refined lattice and the

@@ -28,7 +28,7 @@ EXPORTS = (
     "femgpu_schedule_save", "femgpu_schedule_load", "femgpu_action_device_pipelined", "femgpu_check_finite",
     "femgpu_time_steps_ex", "femgpu_reference_counters", "femgpu_read_output", "femgpu_mesh_build_range",
     "femgpu_halo_create", "femgpu_halo_destroy", "femgpu_halo_export", "femgpu_halo_import", "femgpu_halo_action",
-    "femgpu_halo_time_steps", "femgpu_halo_check", "femgpu_trace_counters",
+    "femgpu_halo_time_steps", "femgpu_halo_check", "femgpu_trace_counters", "femgpu_problem_fuse",
 )
 
 
@@ -98,6 +98,8 @@ def lib():
                 "femgpu_fp64_dmma_peak": ([_P(C.c_double)], C.c_int),
                 "femgpu_problem_load": ([C.c_char_p, _P(C.c_void_p), _P(_P(abi.Problem))], C.c_int),
                 "femgpu_problem_free": ([C.c_void_p], C.c_int),
+                "femgpu_problem_fuse": ([_P(_P(abi.Problem)), C.c_int32, _P(C.c_void_p), _P(_P(abi.Problem)),
+                                         _P(C.c_int64)], C.c_int),
                 "femgpu_problem_save": ([_P(abi.Problem), C.c_char_p], C.c_int),
                 "femgpu_schedule_save": ([_P(abi.Schedule), C.c_int32, C.c_int32, C.c_char_p], C.c_int),
                 "femgpu_schedule_load": ([C.c_char_p, _P(abi.Schedule)], C.c_int),

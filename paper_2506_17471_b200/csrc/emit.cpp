@@ -363,8 +363,13 @@ void emit_cell_body(Out& o, const Signature& sig, const KernelPlan& kp, const Ma
             o.line("if (CHECKED && (false" + chk + ")) { stage = 2; goto report; }");
         }
         // quadrature (form.hpp:575-585): acc = cell_out[jw]; acc += psi_k(jw,q) * e_k, k inner
+        // (Psi entries zero at every point are skipped: acc + 0 * e_k == acc for finite e_k, and an
+        // output no entry reads is checked on its own)
+        for (int k = 0; k < sig.Tw; ++k)
+            if (sig.output_dead(k)) o.line("nf = nf | NF(e" + std::to_string(k) + ");");
         for (int jw = 0; jw < sig.nW; ++jw)
             for (int k = 0; k < sig.Tw; ++k) {
+                if (!sig.pnz(k, jw)) continue;
                 const long long idx = sig.psi_off + (static_cast<long long>(k) * sig.nW + jw) * Q;
                 o.line("o" + std::to_string(jw) + " = FMA(" + TAB(std::to_string(idx) + "+(" + qs + ")") + ", e" +
                        std::to_string(k) + ", o" + std::to_string(jw) + ");");
@@ -713,8 +718,13 @@ void emit_scpt_multi_kernel(Out& o, const Signature& sig, const KernelPlan& kp, 
             o.line("}");
         }
         // quadrature: one Psi load per (jw, term) for all G cells, k inner as in the reference
+        // (all-zero Psi entries skipped, see emit_cell_body)
+        for (int kt = 0; kt < sig.Tw; ++kt)
+            if (sig.output_dead(kt))
+                for (int k = 0; k < G; ++k) o.line("nf_c" + S(k) + " = nf_c" + S(k) + " | NF(" + K("e" + S(kt), k) + ");");
         for (int jw = 0; jw < sig.nW; ++jw)
             for (int kt = 0; kt < sig.Tw; ++kt) {
+                if (!sig.pnz(kt, jw)) continue;
                 const long long idx = sig.psi_off + (static_cast<long long>(kt) * sig.nW + jw) * Q;
                 std::string l = "{ const double tb = " + TAB(S(idx) + "+(" + qs + ")") + ";";
                 for (int k = 0; k < G; ++k)
@@ -1481,8 +1491,13 @@ void emit_macro_qmajor_kernel(Out& o, const Signature& sig, const KernelPlan& kp
                 o.line("}");
             }
             // quadrature straight into the group's y accumulators, one Psi load for the subset's cells
+            // (all-zero Psi entries skipped, see emit_cell_body)
+            for (int k = 0; k < sig.Tw; ++k)
+                if (sig.output_dead(k))
+                    for (int sc = c0; sc < c1; ++sc) o.line("nf = nf | NF(e" + S(k) + "_c" + S(sc) + ");");
             for (int jw = 0; jw < sig.nW; ++jw)
                 for (int k = 0; k < sig.Tw; ++k) {
+                    if (!sig.pnz(k, jw)) continue;
                     const long long idx = sig.psi_off + (static_cast<long long>(k) * sig.nW + jw) * Q;
                     std::string l = "{ const double tb = " + TAB(QI(idx, 1, q)) + ";";
                     for (int sc = c0; sc < c1; ++sc) {

@@ -474,6 +474,11 @@ void emit_dmma_kernel(std::ostringstream& o, const Signature& sig, const KernelP
         for (int k = 0; k < sig.Tw; ++k) {
             const int kq = k * TQL + s;
             for (int nb = 0; nb < L.NBQ; ++nb) {
+                // a fragment whose test DOFs all have Psi(k, jw, .) == 0 adds nothing (fused problems'
+                // off-diagonal blocks): no DMMA
+                bool zero = true;
+                for (int jw = nb * 8; jw < std::min(sig.nW, nb * 8 + 8) && zero; ++jw) zero = !sig.pnz(k, jw);
+                if (zero) continue;
                 const long long f = L.foff_q + static_cast<long long>(nb) * L.KQ + kq;
                 o << "        { const double b = " << (breg ? "Bf" + S(f) : "Fc[" + S(f * 32) + "]") << ";";
                 for (int j = 0; j < MBJ; ++j)

@@ -50,10 +50,21 @@ struct Signature {
     int ns() const { return static_cast<int>(sdofs.size()); }
     int nv() const { return static_cast<int>(vdofs.size()); }
     long long usable_flops() const;
+    long long useful_flops() const;  // minus the skipped all-zero Psi entries (= usable_flops for dense Psi)
     // Offsets into the packed tabulation array (phi scalar, phi vector, psi, weights).
     std::vector<long long> phi_off_s, phi_off_v;
     long long psi_off = 0, w_off = 0, tab_size = 0;
     void layout();
+    // Psi(k, jw, .) != 0 at some quadrature point ([k * nW + jw]; empty = all nonzero).  The emitters
+    // skip the quadrature FMAs of all-zero entries (fused problems: the off-diagonal Psi blocks,
+    // fuse.cpp); an output with no nonzero entry is checked for finiteness on its own.
+    std::vector<char> psi_nz;
+    bool pnz(int k, int jw) const { return psi_nz.empty() || psi_nz[static_cast<size_t>(k) * nW + jw]; }
+    bool output_dead(int k) const {
+        for (int jw = 0; jw < nW; ++jw)
+            if (pnz(k, jw)) return false;
+        return true;
+    }
 };
 
 Signature signature_from(const femgpu_problem* p);
@@ -332,6 +343,16 @@ femgpu_status abi_guard(F&& f) {
     }
 }
 }  // namespace femgpu
+// An owned problem (io.cpp load_problem, fuse.cpp fuse_problems): the flat descriptor plus its storage.
+struct femgpu_owned_problem {
+    femgpu_problem desc{};
+    std::vector<femgpu_space> sspaces, vspaces;
+    std::vector<std::vector<int32_t>> smaps, vmaps, comps;
+    std::vector<std::vector<double>> sphi, vphi, sin, vin;
+    std::vector<double> psi, weights, coords;
+    std::vector<int32_t> test_map, coord_map, outputs;
+    std::vector<femgpu_map_node> nodes;
+};
 struct femgpu_instance {
     std::unique_ptr<femgpu::Instance> impl;
 };

@@ -36,6 +36,14 @@ long long Signature::usable_flops() const {  // form.hpp:164-173
     return ops;
 }
 
+long long Signature::useful_flops() const {  // usable_flops without the all-zero Psi entries the kernels skip
+    long long ops = usable_flops() - 2LL * Tw * Q * nW;
+    for (int k = 0; k < Tw; ++k)
+        for (int jw = 0; jw < nW; ++jw)
+            if (pnz(k, jw)) ops += 2LL * Q;
+    return ops;
+}
+
 void Signature::layout() {
     long long off = 0;
     phi_off_s.clear();
@@ -81,6 +89,15 @@ Signature signature_from(const femgpu_problem* p) {
     s.outputs.assign(p->map_outputs, p->map_outputs + p->n_map_outputs);
     s.layout();
     dedupe_map(s);
+    if (p->psi) {
+        std::vector<char> nz(static_cast<size_t>(s.Tw) * s.nW, 0);
+        bool any_zero = false;
+        for (size_t e = 0; e < nz.size(); ++e) {
+            for (int q = 0; q < s.Q && !nz[e]; ++q) nz[e] = p->psi[e * s.Q + q] != 0.0;
+            any_zero = any_zero || !nz[e];
+        }
+        if (any_zero) s.psi_nz = std::move(nz);  // dense Psi (every benchmark form): no mask, same kernels
+    }
     return s;
 }
 

@@ -20,15 +20,6 @@
 
 #include "femgpu_internal.hpp"
 
-struct femgpu_owned_problem {
-    femgpu_problem desc{};
-    std::vector<femgpu_space> sspaces, vspaces;
-    std::vector<std::vector<int32_t>> smaps, vmaps, comps;
-    std::vector<std::vector<double>> sphi, vphi, sin, vin;
-    std::vector<double> psi, weights, coords;
-    std::vector<int32_t> test_map, coord_map, outputs;
-    std::vector<femgpu_map_node> nodes;
-};
 
 const femgpu_problem* femgpu_owned_view(const femgpu_owned_problem* p) { return &p->desc; }
 void femgpu_owned_delete(femgpu_owned_problem* p) { delete p; }

@@ -229,7 +229,7 @@ void autotune(Instance& I) {
     cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, dev);
     const double clk = clk_khz * 1e3, lanes = 64.0 * sms;  // FP64 lanes per SM per clock
     // ---- FP64 lane-slots per cell (the paper's "Ops" count on this hardware)
-    const double usable_fma = static_cast<double>(sig.usable_flops()) / 2.0;
+    const double usable_fma = static_cast<double>(sig.useful_flops()) / 2.0;
     const std::pair<long long, long long> mi = map_instr(sig);
     const long long map_q = mi.first, map_c = mi.second;
     const double geo_slots = sig.affine ? 6.0 * sig.dim * sig.dim : 0.0;

@@ -24,7 +24,7 @@ import numpy as np
 from . import abi
 from ._native import check, lib
 from .form import (FormSignature, IndexMap, MeshConnectivity, PointwiseMap, ProblemInstance, ScalarSpace,
-                   SynthRng, VectorSpace, _draw_tabulations, _metric_entry, _seed0, preset_map,
+                   SynthRng, Tabulations, VectorSpace, _draw_tabulations, _metric_entry, _seed0, preset_map,
                    preset_signature, simplex_space_dim)
 
 FORMS = ("mass", "laplace", "helmholtz", "elasticity", "hyperelasticity", "helmholtz_coef", "advection",
@@ -231,3 +231,50 @@ def config_problem(name: str, n: int | None = None, seed: int = 7, mesh_fn=None)
         c["n"] = n
     mesh = mesh_fn(c["dim"], c["n"], c["degree"], default_brick(c["dim"])) if mesh_fn else None
     return mesh_problem(c["form"], c["dim"], c["degree"], c["Q"], c["n"], seed=seed, mesh=mesh)
+
+
+# Fused-action pairs (fuse.py): operators that share their trial function on one mesh.
+FUSED_PAIRS = {
+    # velocity block and divergence constraint of a Stokes-type system on P2 velocities (C4's mesh):
+    # both read the P2 vector field u; the divergence terms are 3 of the velocity block's 9 gradients
+    "stokes-P2": dict(dim=3, degree=2, Q=4, n=128),
+    # stiffness and mass on the same P2 scalar field (C2's mesh; the operators of M + dt K)
+    "laplace+mass-P2": dict(dim=3, degree=2, Q=4, n=107),
+}
+
+
+def fused_pair(name: str, n: int | None = None, seed: int = 7):
+    """(A, B): two problems on one mesh, quadrature and trial vector (the operands of fuse_problems)."""
+    c = dict(FUSED_PAIRS[name])
+    if n is not None:
+        c["n"] = n
+    d, deg, Q, nn = c["dim"], c["degree"], c["Q"], c["n"]
+    if name.startswith("laplace+mass"):
+        a = mesh_problem("laplace", d, deg, Q, nn, seed=seed)
+        b = mesh_problem("mass", d, deg, Q, nn, seed=seed + 1)
+        b.tabulations.weights = a.tabulations.weights.copy()
+        b.scalar_inputs = [x.copy() for x in a.scalar_inputs]
+        return a, b
+    a = mesh_problem("elasticity", d, deg, Q, nn, seed=seed)
+    # divergence: trial = a's vector space restricted to the terms d_a u_a (a's term a*d + a, component
+    # a, same tabulation rows), test = P1 scalar on the vertices, w det (sum_a d_a u_a)
+    sig = FormSignature(dim=d, quad_points=Q, coord_dofs=d + 1, affine_geometry=True, word_bytes=8)
+    npc = a.signature.vector_spaces[0].dofs
+    sig.vector_spaces = [VectorSpace(npc, d, list(range(d)))]
+    sig.test_dofs, sig.test_deriv_terms = d + 1, 1
+    sig.validate()
+    m = PointwiseMap()
+    wd = m.mul(m.weight(), m.determinant())
+    m.add_output(m.mul(wd, m.sum([m.vector_deriv(0, k) for k in range(d)])))
+    m.validate(sig)
+    rng = SynthRng(_seed0(seed + 1))
+    tab = Tabulations()
+    tab.vector_phi = [np.ascontiguousarray(a.tabulations.vector_phi[0][[k * d + k for k in range(d)]])]
+    tab.psi = np.asarray(rng.uniform(0.1, 1.1, (d + 1) * Q)).reshape(1, d + 1, Q)
+    tab.weights = a.tabulations.weights.copy()
+    ca = a.connectivity
+    conn = MeshConnectivity(cell_count=ca.cell_count, vector_maps=[ca.vector_maps[0]], test_map=ca.coord_map,
+                            coord_map=ca.coord_map, coords=ca.coords, coord_global_count=ca.coord_global_count)
+    b = ProblemInstance(sig, m, tab, conn, [], [a.vector_inputs[0].copy()], ca.coord_map.global_count)
+    b.validate()
+    return a, b
