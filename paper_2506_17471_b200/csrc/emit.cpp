@@ -519,6 +519,8 @@ std::string KernelPlan::key() const {
         for (int v : p) h = (h ^ static_cast<uint64_t>(v + 1)) * 0x100000001b3ULL;
     for (const auto& m : merge)
         for (int v : m) h = (h ^ static_cast<uint64_t>(v + 7)) * 0x100000001b3ULL;
+    for (const auto& t : talias)
+        for (long long v : t) h = (h ^ static_cast<uint64_t>(v + 11)) * 0x100000001b3ULL;
     s << "P" << h;
     return s.str();
 }
@@ -1064,8 +1066,12 @@ void emit_macro_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const
     auto emit_reds = [&](int s_now) {
         for (int u = 0; u < kp.group_cap[gt]; ++u) {
             if (stream && last_use(gt, u) != s_now) continue;
-            const std::string idx =
+            std::string idx =
                 gathered.count(gt) ? "ig" + S(gt) + "_" + S(u) : "__ldg(&P.gidx" + S(gt) + "[" + S(u) + " * NG + grp])";
+            if (!kp.talias.empty() && kp.talias[u][0] >= 0 && !kp.mstage) {  // row = scale * gathered node + add
+                const auto& al = kp.talias[u];
+                idx = "(ig" + S(al[0]) + "_" + S(al[1]) + (al[2] != 1 ? " * " + S(al[2]) : "") + (al[3] ? " + " + S(al[3]) : "") + ")";
+            }
             o.line("atomicAdd(&P.y[" + idx + "], " + (kp.ysmem ? "SY(" + S(u) + ")" : "ya" + S(u)) + ");");
         }
     };
@@ -1544,9 +1550,17 @@ void emit_macro_qmajor_kernel(Out& o, const Signature& sig, const KernelPlan& kp
             if (!used(gt, u)) continue;
             // qmopt bit 1: reload the scatter indices (an opaque load the compiler cannot merge with
             // the gather's) instead of keeping them live in registers across the quadrature loop
-            const std::string idx = ((kp.qmopt & 2) || staged) ? "ldidx(&P.gidx" + S(gt) + "[" + S(u) + " * NG + grp])"
-                                    : gathered.count(gt) ? "ig" + S(gt) + "_" + S(u)
-                                                         : "__ldg(&P.gidx" + S(gt) + "[" + S(u) + " * NG + grp])";
+            std::string idx = ((kp.qmopt & 2) || staged) ? "ldidx(&P.gidx" + S(gt) + "[" + S(u) + " * NG + grp])"
+                              : gathered.count(gt) ? "ig" + S(gt) + "_" + S(u)
+                                                   : "__ldg(&P.gidx" + S(gt) + "[" + S(u) + " * NG + grp])";
+            if (!kp.talias.empty() && kp.talias[u][0] >= 0) {
+                // the row is an image of a gathered node: scale * node + add (no test-map load)
+                const auto& al = kp.talias[u];
+                const std::string src = ((kp.qmopt & 2) || staged)
+                                            ? "ldidx(&P.gidx" + S(al[0]) + "[" + S(al[1]) + " * NG + grp])"
+                                            : "ig" + S(al[0]) + "_" + S(al[1]);
+                idx = "(" + src + (al[2] != 1 ? " * " + S(al[2]) : "") + (al[3] ? " + " + S(al[3]) : "") + ")";
+            }
             if (kp.qmopt & 4)  // timing experiment only (wrong results): plain store instead of red.add
                 o.line("P.y[" + idx + "] = ya" + S(u) + ";");
             else if (kp.qmopt & 8)  // timing experiment only (wrong results): no scatter traffic

@@ -117,6 +117,7 @@ struct KernelPlan {
                                           // indices, bit 4 rolled quadrature loop, bit 5 persistent cp.async staging,
                                           // bit 8 warp merge of shared-node contributions before the scatter
     std::vector<std::array<int, 3>> merge;  // macro: warp-merge pairs (MacroLayout::merge of the test group)
+    std::vector<std::array<long long, 4>> talias;  // macro: scatter rows derived from gathered indices (MacroLayout::talias)
     long long stage_off = 0;              // macro q-major staging: byte offset of the staging area (emitter-internal)
     bool qloop = false;                   // scpt: keep the quadrature loop rolled (I-cache / registers)
     bool colour = false;                  // scpt: one launch per cell colour, plain y updates (deterministic)
@@ -202,6 +203,9 @@ struct MacroLayout {
     // warp merge of the test map (q-major kernels, qmopt bit 8): (lane shift s, unique u, unique u')
     // such that group g's node u is group g+s's node u' for at least half of the group pairs of a warp
     std::vector<std::array<int, 3>> merge;
+    // per unique node of the test group: (group, unique, scale, add) with row = scale * node + add of
+    // another group's unique node (Instance::test_alias), group -1 = loaded from the test group's gidx
+    std::vector<std::array<long long, 4>> talias;
 };
 
 // Greedy colouring of the test map (femgpu_color_cells) with the cells sorted by colour.
@@ -245,6 +249,15 @@ struct Instance {
     // test space, form.hpp:664-665 convention), or -1: the scatter can then reuse the gathered node
     // indices instead of reading the (dim x larger) test map
     int test_vspace = -1;
+    // per test column j: test_map[c][j] == scale * map_g[c][col] + add for every cell c (another
+    // map group g), or group -1.  Fused problems (fuse.cpp): problem p's test rows are its trial (or
+    // vertex) rows shifted by its output offset; vector test spaces: node * dim + comp.  The macro
+    // kernels then scatter through indices they already gathered instead of loading the test map.
+    struct TestAlias {
+        int group = -1, col = 0, scale = 1;
+        long long add = 0;
+    };
+    std::vector<TestAlias> test_alias;
     std::vector<std::vector<int32_t>> group_maps;  // host copies of distinct maps ([cell][entry])
     std::vector<int> group_global;
     double* d_y = nullptr;

@@ -394,6 +394,39 @@ std::unique_ptr<Instance> create_instance(const femgpu_problem* p) {
         I.group_maps.emplace_back(g.m, g.m + static_cast<size_t>(I.cells) * g.entries);
         I.group_global.push_back(g.global);
     }
+    // test columns that are an affine image of another map's column (candidates from the first
+    // cells, then verified on every cell)
+    I.test_alias.assign(static_cast<size_t>(p->test_dofs), Instance::TestAlias{});
+    for (int j = 0; j < p->test_dofs; ++j) {
+        if (I.cells == 0) break;
+        const int32_t* tm = p->test_map;
+        const long long nt = p->test_dofs;
+        bool found = false;
+        for (size_t g = 0; g < groups.size() && !found; ++g) {
+            if (static_cast<int>(g) == I.test_group) continue;
+            const int E = groups[g].entries;
+            const int32_t* m = groups[g].m;
+            for (int col = 0; col < E && !found; ++col)
+                for (int scale : {1, s.dim}) {
+                    const long long add = static_cast<long long>(tm[j]) - static_cast<long long>(scale) * m[col];
+                    auto holds = [&](long long c) {
+                        return static_cast<long long>(tm[c * nt + j]) == static_cast<long long>(scale) * m[c * E + col] + add;
+                    };
+                    bool ok = true;
+                    for (long long c = 0; c < std::min<long long>(I.cells, 64) && ok; ++c) ok = holds(c);
+                    if (!ok) continue;
+                    std::atomic<bool> all{true};
+                    parallel_for(I.cells, [&](long long b0, long long e0) {
+                        for (long long c = b0; c < e0 && all.load(std::memory_order_relaxed); ++c)
+                            if (!holds(c)) all.store(false, std::memory_order_relaxed);
+                    });
+                    if (!all) continue;
+                    I.test_alias[j] = {static_cast<int>(g), col, scale, add};
+                    found = true;
+                    break;
+                }
+        }
+    }
     I.d_y = I.alloc<double>(static_cast<size_t>(I.output_size));
     I.d_bad = reinterpret_cast<int32_t*>(I.alloc<unsigned long long>(2));
     FG_CUDA(cudaMemset(I.d_bad, 0xff, 2 * sizeof(unsigned long long)));
@@ -621,6 +654,32 @@ const MacroLayout& Instance::macro_layout(int G) {
             M->unique.push_back(U);
             M->pattern.push_back(pat);
             if (static_cast<int>(g) == test_group) {
+                // scatter rows as images of other groups' unique nodes (Instance::test_alias)
+                M->talias.assign(static_cast<size_t>(U), {-1, 0, 1, 0});
+                std::vector<char> seen(static_cast<size_t>(U), 0);
+                bool ok = true;
+                for (int k = 0; k < G * E && ok; ++k) {
+                    const int sl = k / E, j = k % E, u = pat[k];
+                    const TestAlias& t = test_alias[j];
+                    if (t.group < 0) {
+                        ok = false;
+                        break;
+                    }
+                    // the source group's pattern is that of group 0 too (built before or after this one)
+                    const std::vector<int32_t>& ms = group_maps[t.group];
+                    const int Es = static_cast<int>(ms.size() / cells);
+                    std::vector<int32_t> us(ms.begin(), ms.begin() + static_cast<long long>(G) * Es);
+                    std::sort(us.begin(), us.end());
+                    us.erase(std::unique(us.begin(), us.end()), us.end());
+                    const int up = static_cast<int>(std::lower_bound(us.begin(), us.end(), ms[sl * Es + t.col]) - us.begin());
+                    const std::array<long long, 4> al{t.group, up, t.scale, t.add};
+                    if (seen[u] && M->talias[u] != al) ok = false;
+                    M->talias[u] = al;
+                    seen[u] = 1;
+                }
+                if (!ok) M->talias.clear();
+            }
+            if (static_cast<int>(g) == test_group) {
                 // warp merge candidates: lanes l and l+s of a warp hold groups g and g+s; count how
                 // often g's unique node u is g+s's node u' (a sample of warps is enough)
                 // (256 sampled warps; g+s's nodes sorted once per pair: O(U log U), not O(U^2))
@@ -846,6 +905,20 @@ KernelPlan resolve_schedule_impl(Instance& I, const femgpu_schedule* s) {
             kp.msplit = kp.qmajor ? std::max(1, (s->reserved[3] >> 8) & 0xff) : 1;
             kp.qmopt = kp.qmajor ? (s->reserved[3] >> 16) & 0xffff : 0;
             if ((kp.qmopt & 256) && kp.msplit == 1) kp.merge = M.merge;
+            {
+                // test rows not gathered themselves (fused problems, vector test spaces): derive them
+                // from gathered indices when every row has an alias into a gathered group
+                auto gathered = [&](long long g) {
+                    for (const auto& sp : I.sspaces)
+                        if (sp.group == g) return true;
+                    for (const auto& sp : I.vspaces)
+                        if (sp.group == g) return true;
+                    return sig.affine && I.coord_group == g;
+                };
+                bool use = !M.talias.empty() && !gathered(I.test_group);
+                for (const auto& al : M.talias) use = use && gathered(al[0]);
+                if (use) kp.talias = M.talias;
+            }
             kp.block = s->block_cells > 0 ? s->block_cells : 64;
             check_macro_split(kp);
             const int reg_target = s->reserved[1] > 0 ? s->reserved[1] : 168;
