@@ -521,6 +521,8 @@ std::string KernelPlan::key() const {
         for (int v : m) h = (h ^ static_cast<uint64_t>(v + 7)) * 0x100000001b3ULL;
     for (const auto& t : talias)
         for (long long v : t) h = (h ^ static_cast<uint64_t>(v + 11)) * 0x100000001b3ULL;
+    for (const auto& t : dalias)
+        for (long long v : t) h = (h ^ static_cast<uint64_t>(v + 13)) * 0x100000001b3ULL;
     s << "P" << h;
     return s.str();
 }

@@ -342,6 +342,14 @@ void emit_dmma_kernel(std::ostringstream& o, const Signature& sig, const KernelP
     const Sp* tsp = nullptr;
     for (const Sp& sp : sps)
         if (tv && sp.vec && sp.i == kp.tvec) tsp = &sp;
+    // spaces whose current-m-group indices the scatter reads (tvec, or the per-column aliases)
+    auto kept = [&](const Sp& sp) {
+        if (&sp == tsp) return true;
+        if (tsp || kp.dalias.empty()) return false;
+        for (const auto& a : kp.dalias)
+            if (a[0] >= 0 && (a[0] == 1) == sp.vec && a[1] == sp.i) return true;
+        return false;
+    };
     if (PF) {
         // loop-carried prefetch registers: ixN = indices of m-group grp+1, uN = values of grp,
         // ixK = indices of grp (only the test-space indices are kept)
@@ -350,16 +358,18 @@ void emit_dmma_kernel(std::ostringstream& o, const Signature& sig, const KernelP
                 const DmmaGroup& g0 = L.groups[sp.gids[0]];
                 for (int ks = 0; ks < g0.KS; ++ks) {
                     o << "    int " << ixname("ixN", sp, ks, j) << " = -1;\n";
-                    if (&sp == tsp) o << "    int " << ixname("ixK", sp, ks, j) << " = -1;\n";
+                    if (kept(sp)) o << "    int " << ixname("ixK", sp, ks, j) << " = -1;\n";
                     for (int gid : sp.gids) o << "    double " << uname("uN", gid, ks, j) << " = 0.0;\n";
                 }
             }
     }
     auto copy_tidx = [&](const std::string& ind, const std::string& dst, const std::string& src) {
-        if (!tsp) return;
-        for (int j = 0; j < MBJ; ++j)
-            for (int ks = 0; ks < L.groups[tsp->gids[0]].KS; ++ks)
-                o << ind << ixname(dst, *tsp, ks, j) << " = " << ixname(src, *tsp, ks, j) << ";\n";
+        for (const Sp& sp : sps) {
+            if (!kept(sp)) continue;
+            for (int j = 0; j < MBJ; ++j)
+                for (int ks = 0; ks < L.groups[sp.gids[0]].KS; ++ks)
+                    o << ind << ixname(dst, sp, ks, j) << " = " << ixname(src, sp, ks, j) << ";\n";
+        }
     };
     if (PF) {
         // stage chain: m-group 0 loads its own indices+values (before the geometry), later m-groups
@@ -378,7 +388,7 @@ void emit_dmma_kernel(std::ostringstream& o, const Signature& sig, const KernelP
                 for (int ks = 0; ks < L.groups[sp.gids[0]].KS; ++ks) {
                     for (int gid : sp.gids)
                         o << "      const double " << uname("uA", gid, ks, j) << " = " << uname("uN", gid, ks, j) << ";\n";
-                    if (&sp == tsp)
+                    if (kept(sp))
                         o << "      const int " << ixname("ixC", sp, ks, j) << " = " << ixname("ixK", sp, ks, j) << ";\n";
                 }
         if (NG > 1) {
@@ -511,6 +521,44 @@ void emit_dmma_kernel(std::ostringstream& o, const Signature& sig, const KernelP
                     o << "        ty" << nb << "_" << i << J << j << " = " << sel << " * " << d << " + jw % " << d << ";\n      }\n";
                 }
         }
+        // per-column aliases (no tvec): rows = scale * gathered node + add, shuffled from the lane that
+        // gathered the node; columns without an alias load the test map
+        const bool dal = !tsp && !kp.dalias.empty();
+        if (dal) {
+            for (int nb = 0; nb < L.NBQ; ++nb)
+                for (int i = 0; i < 2; ++i) {
+                    if (nb * 8 + i >= sig.nW) continue;
+                    std::string srcl = "0", scale = "1", add = "0LL", al = "false";
+                    std::vector<std::pair<int, int>> srcs;  // distinct (space slot in sps, k-step)
+                    std::string pick = "0";
+                    for (int gg = 3; gg >= 0; --gg) {
+                        const int jw = nb * 8 + i + 2 * gg;
+                        if (jw >= sig.nW || kp.dalias[jw][0] < 0) continue;
+                        const auto& a = kp.dalias[jw];
+                        int spi = -1;
+                        for (size_t q = 0; q < sps.size(); ++q)
+                            if (sps[q].vec == (a[0] == 1) && sps[q].i == a[1]) spi = static_cast<int>(q);
+                        if (spi < 0) continue;
+                        const int ks = static_cast<int>(a[2] >> 2);
+                        if (std::find(srcs.begin(), srcs.end(), std::make_pair(spi, ks)) == srcs.end()) srcs.push_back({spi, ks});
+                        const std::string gq = "g == " + S(gg);
+                        srcl = "(" + gq + " ? " + S(a[2] & 3) + " : " + srcl + ")";
+                        scale = "(" + gq + " ? " + S(a[3]) + " : " + scale + ")";
+                        add = "(" + gq + " ? " + S(a[4]) + "LL : " + add + ")";
+                        al = "(" + gq + " || " + al + ")";
+                        pick = "(" + gq + " ? t" + S(spi) + "_" + S(ks) + " : " + pick + ")";
+                    }
+                    o << "      int ta" << nb << "_" << i << J << j << " = 0;\n";
+                    o << "      const bool al" << nb << "_" << i << J << j << " = " << al << ";\n";
+                    if (srcs.empty()) continue;
+                    o << "      {\n        const int src = (r << 2) | " << srcl << ";\n";
+                    for (const auto& sk : srcs)
+                        o << "        const int t" << sk.first << "_" << sk.second << " = __shfl_sync(0xffffffffu, "
+                          << ixname(PF ? "ixC" : "ix", sps[sk.first], sk.second, j) << ", src);\n";
+                    o << "        ta" << nb << "_" << i << J << j << " = (int)((long long)" << pick << " * " << scale << " + " << add
+                      << ");\n      }\n";
+                }
+        }
         o << "      if (cok" << j << ") {\n";
         for (int nb = 0; nb < L.NBQ; ++nb)
             for (int i = 0; i < 2; ++i) {
@@ -519,8 +567,10 @@ void emit_dmma_kernel(std::ostringstream& o, const Signature& sig, const KernelP
                 const bool partial = nb * 8 + 8 > sig.nW;
                 o << "        " << (partial ? "if (" + S(nb * 8 + i) + " + 2 * g < " + S(sig.nW) + ") " : "") << "{\n";
                 o << "          if (NF(" << v << ")) badc = min(badc, (unsigned long long)cell" << j << ");\n";
+                const std::string load = "__ldg(&P.tm[(" + S(nb * 8 + i) + " + 2 * g) * STR + cell" + S(j) + "])";
                 const std::string yi = tsp ? "ty" + S(nb) + "_" + S(i) + J + S(j)
-                                           : "__ldg(&P.tm[(" + S(nb * 8 + i) + " + 2 * g) * STR + cell" + S(j) + "])";
+                                       : dal ? "(al" + S(nb) + "_" + S(i) + J + S(j) + " ? ta" + S(nb) + "_" + S(i) + J + S(j) + " : " + load + ")"
+                                             : load;
                 o << "          " << (scatter_store ? "P.y[" : "atomicAdd(&P.y[") << yi << "]" << (scatter_store ? " = " : ", ") << v
                   << (scatter_store ? ";\n" : ");\n");
                 o << "        }\n";

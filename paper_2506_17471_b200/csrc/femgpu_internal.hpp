@@ -118,6 +118,9 @@ struct KernelPlan {
                                           // bit 8 warp merge of shared-node contributions before the scatter
     std::vector<std::array<int, 3>> merge;  // macro: warp-merge pairs (MacroLayout::merge of the test group)
     std::vector<std::array<long long, 4>> talias;  // macro: scatter rows derived from gathered indices (MacroLayout::talias)
+    // DMMA without tvec: per test column (trial kind 0 scalar / 1 vector / -1 none, space, column,
+    // scale, add): the row is scale * (that space's gathered node index) + add (Instance::test_alias)
+    std::vector<std::array<long long, 5>> dalias;
     long long stage_off = 0;              // macro q-major staging: byte offset of the staging area (emitter-internal)
     bool qloop = false;                   // scpt: keep the quadrature loop rolled (I-cache / registers)
     bool colour = false;                  // scpt: one launch per cell colour, plain y updates (deterministic)

@@ -868,6 +868,22 @@ KernelPlan resolve_schedule_impl(Instance& I, const femgpu_schedule* s) {
     if (s->kind == FEMGPU_DMMA) {
         resolve_dmma(sig, kp, s);
         kp.tvec = I.test_vspace;
+        if (kp.tvec < 0) {
+            // test columns that are images of a gathered trial space's node column: the scatter then
+            // shuffles the gathered index instead of loading the test map (fused problems)
+            bool any = false;
+            for (int j = 0; j < sig.nW; ++j) {
+                std::array<long long, 5> al{-1, 0, 0, 1, 0};
+                const Instance::TestAlias& t = I.test_alias[static_cast<size_t>(j)];
+                for (size_t v = 0; v < I.vspaces.size() && al[0] < 0 && t.group >= 0; ++v)
+                    if (I.vspaces[v].group == t.group) al = {1, static_cast<long long>(v), t.col, t.scale, t.add};
+                for (size_t v = 0; v < I.sspaces.size() && al[0] < 0 && t.group >= 0; ++v)
+                    if (I.sspaces[v].group == t.group) al = {0, static_cast<long long>(v), t.col, t.scale, t.add};
+                any = any || al[0] >= 0;
+                kp.dalias.push_back(al);
+            }
+            if (!any) kp.dalias.clear();
+        }
         return kp;
     }
     // SCPT: one thread per cell.
