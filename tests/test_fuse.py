@@ -71,3 +71,18 @@ def test_incompatible_problems_are_rejected():
         fg.fuse_problems([a, c])
     with pytest.raises(ValueError):
         fg.fuse_problems([])
+
+
+def test_non_affine_problems_fuse_through_their_coordinate_space(oracle):
+    """Coordinates as a vector trial space (test_io.cpp:10-42): the fused problem keeps one coordinate
+    space (merged), re-pointed by coordinate_space, and reproduces both actions."""
+    from tests.test_io import non_affine_problem
+    a = non_affine_problem()
+    b = non_affine_problem()
+    m = b.map  # a second operator: the same DAG with every output doubled
+    m.outputs = [m.mul(m.constant(2.0), o) for o in m.outputs]
+    f, offs = fg.fuse_problems([a, b])
+    assert not f.signature.affine_geometry and len(f.signature.vector_spaces) == 1
+    assert f.signature.coordinate_space == 0
+    fa, fb = fg.split_output(oracle.reference_action(f), offs)
+    assert np.array_equal(fa, oracle.reference_action(a)) and np.array_equal(fb, oracle.reference_action(b))

@@ -76,3 +76,15 @@ def test_non_finite_in_either_operator_is_reported(which):
     assert len(f.signature.scalar_spaces) == 2
     with pytest.raises(RuntimeError, match="non-finite value at cell"):
         fg.gpu_action(f)
+
+
+@pytest.mark.parametrize("sched", ["auto", "scpt", "dmma"])
+def test_fused_non_affine_problems(oracle, sched):
+    from tests.test_io import non_affine_problem
+    a, b = non_affine_problem(), non_affine_problem()
+    b.map.outputs = [b.map.mul(b.map.constant(2.0), o) for o in b.map.outputs]
+    f, offs = fg.fuse_problems([a, b])
+    y = fg.gpu_action(f, SCHEDULES[sched])
+    for yk, p in zip(fg.split_output(y, offs), (a, b)):
+        ref = oracle.reference_action(p)
+        assert rel_l2(yk, ref) <= 1e-12 and max_rel(yk, ref) <= 1e-10
