@@ -264,7 +264,15 @@ void autotune(Instance& I) {
             const DmmaLayout L = dmma_layout(sig, c.kp);
             // padded m8n8k4 slots at the DMMA rate (measured 37.1 vs 34.2 TF DFMA: x1.085 per slot);
             // the map runs per padded quadrature point, the cell-invariant part once per cell
-            c.slots = static_cast<double>(L.nfrag) * 256.0 / 8.0 / 1.085 +
+            // (quad fragments whose Psi block is all zero are skipped by the kernel: fused problems)
+            long long zero_frags = 0;
+            for (int k = 0; k < sig.Tw; ++k)
+                for (int nb = 0; nb < L.NBQ; ++nb) {
+                    bool zero = true;
+                    for (int jw = nb * 8; jw < std::min(sig.nW, nb * 8 + 8) && zero; ++jw) zero = !sig.pnz(k, jw);
+                    zero_frags += zero ? static_cast<long long>(L.TQL) * L.NCH : 0;
+                }
+            c.slots = static_cast<double>(L.nfrag - zero_frags) * 256.0 / 8.0 / 1.085 +
                       static_cast<double>(map_q) * (4.0 * L.TQL * L.NCH) + static_cast<double>(map_c) + geo_slots;
         } else {
             c.slots = dfma_slots;
