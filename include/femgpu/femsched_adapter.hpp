@@ -171,6 +171,31 @@ inline std::vector<double> action(const femsched::ProblemInstance& p, femsched::
     return y;
 }
 
+// Fused multi-operator action (femgpu_problem_fuse): instances on the same cells,
+// geometry and quadrature run as one kernel; returns each instance's reference_action-shaped output.
+inline std::vector<std::vector<double>> fused_action(const std::vector<const femsched::ProblemInstance*>& ps) {
+    std::vector<std::unique_ptr<ProblemView>> views;
+    std::vector<const femgpu_problem*> flat;
+    for (const auto* p : ps) {
+        p->validate();
+        views.push_back(std::make_unique<ProblemView>(*p));
+        flat.push_back(views.back()->get());
+    }
+    femgpu_owned_problem* own = nullptr;
+    const femgpu_problem* fused = nullptr;
+    std::vector<int64_t> off(ps.size() + 1);
+    check(femgpu_problem_fuse(flat.data(), static_cast<int32_t>(flat.size()), &own, &fused, off.data()));
+    std::unique_ptr<femgpu_owned_problem, femgpu_status (*)(femgpu_owned_problem*)> guard(own, femgpu_problem_free);
+    femgpu_instance* h = nullptr;
+    check(femgpu_create(fused, &h));
+    std::unique_ptr<femgpu_instance, femgpu_status (*)(femgpu_instance*)> hg(h, femgpu_destroy);
+    std::vector<double> y(static_cast<std::size_t>(off.back()));
+    check(femgpu_action(h, nullptr, y.data()));
+    std::vector<std::vector<double>> out;
+    for (std::size_t i = 0; i < ps.size(); ++i) out.emplace_back(y.begin() + off[i], y.begin() + off[i + 1]);
+    return out;
+}
+
 // Content fingerprint of an instance (sizes, maps, inputs, tabulations, map DAG): the executor's
 // device-instance cache is keyed on it, not on the address, so an instance rebuilt at the same
 // address or modified in place is re-uploaded.

@@ -45,6 +45,24 @@ int main() {
                     c.cells, err, cnt_ok ? "equal" : "DIFFER");
         if (!(err <= 1e-12) || got.size() != ref.size() || !cnt_ok) ++fails;
     }
+    // fused multi-operator action: stiffness and mass on one mesh, quadrature and trial vector
+    {
+        const auto sa = preset_signature(Operator::laplace, 3, 2, 8);
+        const auto sb = preset_signature(Operator::mass, 3, 2, 8);
+        const auto a = make_problem(sa, preset_map(Operator::laplace, sa), 40, 9);
+        auto b = make_problem(sb, preset_map(Operator::mass, sb), 40, 9);
+        b.tabulations.weights = a.tabulations.weights;
+        b.connectivity.coords = a.connectivity.coords;
+        b.connectivity.coord_map = a.connectivity.coord_map;
+        b.connectivity.scalar_maps = a.connectivity.scalar_maps;
+        b.connectivity.test_map = a.connectivity.test_map;
+        b.scalar_inputs = a.scalar_inputs;
+        b.output_size = a.output_size;
+        const auto ys = femgpu::fused_action({&a, &b});
+        const double ea = rel_l2(ys.at(0), reference_action(a)), eb = rel_l2(ys.at(1), reference_action(b));
+        std::printf("fused laplace+mass: rel_l2 %.3e %.3e\n", ea, eb);
+        if (!(ea <= 1e-12) || !(eb <= 1e-12)) ++fails;
+    }
     // error mapping: invalid instance -> std::invalid_argument, NaN -> runtime_error naming the cell
     {
         const auto sig = preset_signature(Operator::mass, 2, 1, 2);
