@@ -6,7 +6,7 @@ PKG := paper_2506_17471_b200
 SRC := $(PKG)/csrc
 OBJDIR := build/obj
 LIB := $(PKG)/_lib/libfemgpu.so
-CXXSRC := $(SRC)/api.cpp $(SRC)/instance.cpp $(SRC)/emit.cpp $(SRC)/emit_dmma.cpp $(SRC)/jit.cpp $(SRC)/mesh.cpp $(SRC)/tune.cpp $(SRC)/io.cpp $(SRC)/pipeline.cpp $(SRC)/fuse.cpp
+CXXSRC := $(SRC)/api.cpp $(SRC)/instance.cpp $(SRC)/emit.cpp $(SRC)/emit_dmma.cpp $(SRC)/jit.cpp $(SRC)/mesh.cpp $(SRC)/tune.cpp $(SRC)/io.cpp $(SRC)/pipeline.cpp $(SRC)/fuse.cpp $(SRC)/reorder.cpp
 CUSRC := $(wildcard $(SRC)/*.cu)
 HDRS := include/femgpu.h $(SRC)/femgpu_internal.hpp
 NVFLAGS := -gencode arch=compute_100a,code=sm_100a -lineinfo -O3 -std=c++17 -Xcompiler -fPIC,-O2 --expt-relaxed-constexpr

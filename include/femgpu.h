@@ -368,6 +368,18 @@ femgpu_status femgpu_schedule_load(const char* path, femgpu_schedule* s);
 femgpu_status femgpu_problem_fuse(const femgpu_problem* const* problems, int32_t n, femgpu_owned_problem** out,
                                   const femgpu_problem** view, int64_t* offsets);
 
+/* ---- locality-restoring renumbering of a general mesh (csrc/reorder.cpp) -------------------
+ * Cells sorted by the Morton code of their centroid; every global index space renumbered in
+ * first-touch order (spaces with equal global counts share a numbering; a node*dim+comp vector test
+ * space follows its trial space).  *view is the same problem in the new numbering (inputs and
+ * coordinates permuted).  Optional outputs, new -> old: cell_perm[cell_count],
+ * output_perm[output_size] (y_new[r] = y_old[output_perm[r]]), scalar_input_perms[i][global_count]
+ * and vector_input_perms[i][global_count] (node level) for later inputs.  Free with
+ * femgpu_problem_free. */
+femgpu_status femgpu_problem_reorder(const femgpu_problem* p, femgpu_owned_problem** out, const femgpu_problem** view,
+                                     int32_t* cell_perm, int32_t* output_perm, int32_t* const* scalar_input_perms,
+                                     int32_t* const* vector_input_perms);
+
 /* ---- structured meshes (synthetic unit square / unit cube) -------------
  * Unit square: n x n squares, 2 triangles each; unit cube: n^3 cubes, 6 Kuhn
  * tetrahedra each.  P_degree nodes live on the degree-refined lattice and the

@@ -29,6 +29,7 @@ EXPORTS = (
     "femgpu_time_steps_ex", "femgpu_reference_counters", "femgpu_read_output", "femgpu_mesh_build_range",
     "femgpu_halo_create", "femgpu_halo_destroy", "femgpu_halo_export", "femgpu_halo_import", "femgpu_halo_action",
     "femgpu_halo_time_steps", "femgpu_halo_check", "femgpu_trace_counters", "femgpu_problem_fuse",
+    "femgpu_problem_reorder",
 )
 
 
@@ -100,6 +101,8 @@ def lib():
                 "femgpu_problem_free": ([C.c_void_p], C.c_int),
                 "femgpu_problem_fuse": ([_P(_P(abi.Problem)), C.c_int32, _P(C.c_void_p), _P(_P(abi.Problem)),
                                          _P(C.c_int64)], C.c_int),
+                "femgpu_problem_reorder": ([_P(abi.Problem), _P(C.c_void_p), _P(_P(abi.Problem)), _P(C.c_int32),
+                                            _P(C.c_int32), _P(_P(C.c_int32)), _P(_P(C.c_int32))], C.c_int),
                 "femgpu_problem_save": ([_P(abi.Problem), C.c_char_p], C.c_int),
                 "femgpu_schedule_save": ([_P(abi.Schedule), C.c_int32, C.c_int32, C.c_char_p], C.c_int),
                 "femgpu_schedule_load": ([C.c_char_p, _P(abi.Schedule)], C.c_int),

@@ -10,6 +10,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -340,6 +341,20 @@ bool overlapped_zero_action(Instance& inst, const KernelPlan& kp, double* d_y, c
 bool pipelined_host_action(Instance& inst, const KernelPlan& kp, const double* const* scalar_inputs,
                            const double* const* vector_inputs, double* y_host);
 void check_failure(Instance& inst, const KernelPlan& kp, cudaStream_t stream);
+// Host-side data-parallel loop over [0, n) in up to 32 contiguous chunks (re-blocking, layouts, reorder).
+template <typename F>
+void parallel_for(long long n, F&& f) {
+    const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    const long long chunks = std::min<long long>(hw, std::max<long long>(1, n / 4096));
+    if (chunks <= 1) {
+        f(0LL, n);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (long long c = 0; c < chunks; ++c)
+        th.emplace_back([&, c] { f(n * c / chunks, n * (c + 1) / chunks); });
+    for (auto& t : th) t.join();
+}
 // C-ABI error plumbing shared by the translation units that implement entry points
 void set_last_error(const std::string& msg);
 template <typename F>

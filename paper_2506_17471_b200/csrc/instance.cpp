@@ -268,20 +268,6 @@ Instance::~Instance() {
 
 namespace {
 
-template <typename F>
-void parallel_for(long long n, F&& f) {
-    const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
-    const long long chunks = std::min<long long>(hw, std::max<long long>(1, n / 4096));
-    if (chunks <= 1) {
-        f(0LL, n);
-        return;
-    }
-    std::vector<std::thread> th;
-    for (long long c = 0; c < chunks; ++c)
-        th.emplace_back([&, c] { f(n * c / chunks, n * (c + 1) / chunks); });
-    for (auto& t : th) t.join();
-}
-
 // Upload a [cell][entry] map as [entry][cell].
 int32_t* upload_transposed(Instance& inst, const int32_t* m, int cells, int entries) {
     std::vector<int32_t> t(static_cast<size_t>(cells) * entries);

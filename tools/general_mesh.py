@@ -3,7 +3,9 @@
 repeats (the macro families do not apply) while spatial locality is kept (or not).  Times the
 automatic schedule and named schedules (tools/sweep.py names).
 
-usage: python tools/general_mesh.py C2 local|global sched,sched,... [reps]
+usage: python tools/general_mesh.py C2 local|global|global+reorder sched,sched,... [reps]
+  global+reorder: the globally shuffled mesh renumbered by femgpu_problem_reorder (Morton cells,
+  first-touch nodes)
 """
 import json
 import sys
@@ -45,6 +47,8 @@ def main():
     else:
         perm = rng.permutation(C)
     p = permuted(p, perm)
+    if mode.endswith("+reorder"):
+        p, _ = fg.reorder_problem(p)
     ref = None
     with fg.GpuInstance(p) as g:
         for nm in names:
