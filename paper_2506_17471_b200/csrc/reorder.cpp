@@ -82,7 +82,7 @@ femgpu_owned_problem* reorder_problem(const femgpu_problem* p, int32_t* cell_per
                                 : d == 2 ? spread2(q[0]) | spread2(q[1]) << 1 : q[0];
             }
         });
-    } else {
+    } else if (p->n_scalar + p->n_vector > 0) {
         const femgpu_space& s = p->n_scalar ? p->scalar_spaces[0] : p->vector_spaces[0];
         for (long long c = 0; c < C; ++c) {
             int32_t m = INT32_MAX;

@@ -57,3 +57,11 @@ def test_vector_test_space_follows_its_trial_nodes(oracle):
     assert np.array_equal(perms["output"], expect)
     _, vs = fg.inputs_to_new([], [p.vector_inputs[0]], perms, d)
     assert np.array_equal(vs[0], q.vector_inputs[0])
+
+
+def test_non_affine_problem_reorders_by_node_index(oracle):
+    from tests.test_io import non_affine_problem
+    p = non_affine_problem()
+    q, perms = fg.reorder_problem(p)
+    y = fg.output_to_original(oracle.reference_action(q), perms)
+    assert rel_l2(y, oracle.reference_action(p)) <= 1e-14
