@@ -326,6 +326,44 @@ def config_slab(name: str, rank: int, world: int, n: Optional[int] = None, seed:
     return slab_instance(c["form"], c["dim"], c["degree"], c["Q"], c["n"], b, e, seed=seed)
 
 
+def problem_slab(p: ProblemInstance, rank: int, world: int) -> Slab:
+    """This rank's contiguous cell range of a general (already built) problem, e.g. a mesh renumbered
+    by reorder.reorder_problem: Morton-ordered cells make contiguous ranges spatially compact, the
+    partition SURVEY 8e names for general meshes.  Trial spaces must live on the test space's nodes
+    ("node") or on the coordinate map's vertices ("vertex"), as the benchmark forms do."""
+    C, d = p.connectivity.cell_count, p.signature.dim
+    b, e = split_cells(C, world, 1)[rank]
+    local, ut, trial_global = local_instance(p, b, e)
+    conn = p.connectivity
+    tm = conn.test_map.indices
+    vec_test = p.signature.test_dofs != tm.shape[1] or any(
+        m.indices.shape[1] * d == tm.shape[1] and np.array_equal(tm[:1], (m.indices[:1, :, None] * d + np.arange(d)).reshape(1, -1))
+        for m in conn.vector_maps)
+    node_map = None
+    if vec_test:
+        for m in conn.vector_maps:
+            if m.indices.shape[1] * d == tm.shape[1] and np.array_equal(tm, (m.indices[:, :, None].astype(np.int64) * d
+                                                                              + np.arange(d)).reshape(C, -1)):
+                node_map = m.indices
+        if node_map is None:
+            raise ValueError("problem_slab: vector test space is not node*dim+comp of a vector trial space")
+    else:
+        node_map = tm
+    nodes_u = np.unique(node_map[b:e]).astype(np.int64)
+    kinds = {"node": nodes_u}
+    if conn.coord_map is not None:
+        kinds["vertex"] = np.unique(conn.coord_map.indices[b:e]).astype(np.int64)
+    space_kind = []
+    for im in conn.scalar_maps + conn.vector_maps:
+        if np.array_equal(im.indices, node_map):
+            space_kind.append("node")
+        elif conn.coord_map is not None and np.array_equal(im.indices, conn.coord_map.indices):
+            space_kind.append("vertex")
+        else:
+            raise ValueError("problem_slab: a trial space is neither on the test nodes nor on the vertices")
+    return Slab(local, (b, e), kinds, space_kind, "node*d" if vec_test else "node", d)
+
+
 def torch_gather():
     import torch.distributed as tdist
 

@@ -142,6 +142,33 @@ def _worker(rank, world, port, args, out_dir, mode):
     dist.destroy_process_group()
 
 
+def _general_worker(rank, world, port, name, n, out_dir):
+    """A general mesh (cells shuffled, then femgpu_problem_reorder): contiguous Morton ranges per rank
+    (dist.problem_slab), the collective plan and the host exchange with the oracle as local compute."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import oracle
+    from tests.test_reorder import shuffled
+    q, _ = fg.reorder_problem(shuffled(name, n))
+    plan = fdist.build_plan(fdist.problem_slab(q, rank, world), rank, world, fdist.torch_gather())
+    y = fdist.host_halo_action(plan, oracle.reference_action)
+    m = plan.owned_mask
+    np.savez(os.path.join(out_dir, "r%d.npz" % rank), gids=plan.test_global[m], ys=y[m])
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,n", [("C2", 4), ("C4", 3)])
+def test_general_mesh_partition_after_reorder(tmp_path, name, n):
+    from oracle import oracle
+    from tests.test_reorder import shuffled
+    world = 3
+    mp.spawn(_general_worker, args=(world, _free_port(), name, n, str(tmp_path)), nprocs=world, join=True)
+    q, _ = fg.reorder_problem(shuffled(name, n))
+    assert rel_l2(_assemble(str(tmp_path), world, q.output_size), oracle.reference_action(q)) <= 1e-12
+
+
 def _assemble(out_dir, world, n, suffix=""):
     y = np.full(n, np.nan)
     for r in range(world):

@@ -184,3 +184,30 @@ def test_bench_launches_its_own_ranks_ipc_path(config, n):
     out = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
     assert out["n_gpus"] == 2 and out["parity_complete"]
     assert out["parity_vs_reference"]["pass"], out["parity_vs_reference"]
+
+
+@pytest.mark.parametrize("name,n", [("C2", 5), ("C4", 4)])
+def test_halo_action_on_a_reordered_general_mesh(oracle, name, n):
+    """A general mesh (cells shuffled, then femgpu_problem_reorder) split into contiguous Morton
+    ranges (dist.problem_slab): the GPU-to-GPU exchange reproduces the reference action."""
+    from tests.test_reorder import shuffled
+    world = 2
+    q, _ = fg.reorder_problem(shuffled(name, n))
+
+    def rank(r, gather):
+        plan = fdist.build_plan(fdist.problem_slab(q, r, world), r, world, gather)
+        di = fdist.DistInstance(plan, gather)
+        try:
+            di.action()
+            di.check()
+            return di.owned_output()
+        finally:
+            di.close()
+
+    res = run_ranks(world, rank)
+    y = np.full(q.output_size, np.nan)
+    for g, v in res:
+        y[g] = v
+    ref = oracle.reference_action(q)
+    assert not np.isnan(y).any()
+    assert rel_l2(y, ref) <= 1e-12 and max_rel(y, ref) <= 1e-10
