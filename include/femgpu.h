@@ -217,6 +217,16 @@ femgpu_status femgpu_action(femgpu_instance* inst, const femgpu_schedule* s, dou
 femgpu_status femgpu_action_host(femgpu_instance* inst, const femgpu_schedule* s,
                                  const double* const* scalar_inputs,
                                  const double* const* vector_inputs, double* y_host);
+/* Streaming end-to-end actions: like femgpu_action_host, but returns once the step is enqueued.
+ * Two sets of device inputs/outputs alternate, so step i+1's H2D overlaps step i's D2H (PCIe is
+ * full duplex).  Every step still copies its inputs in and its y out.  Host buffers must stay valid
+ * (inputs) and unread (y) until femgpu_action_host_wait, which completes all steps, leaves the
+ * instance holding the last step's inputs and output, and reports a non-finite value in any step.
+ * Every other call on the instance completes pending steps first.  Instances without a slab plan
+ * run each step synchronously. */
+femgpu_status femgpu_action_host_async(femgpu_instance* inst, const femgpu_schedule* s, const double* const* scalar_inputs,
+                                       const double* const* vector_inputs, double* y_host);
+femgpu_status femgpu_action_host_wait(femgpu_instance* inst);
 /* Device-resident: y_dev is a device pointer of output_size doubles; stream is a
  * cudaStream_t (NULL = the instance stream, a non-blocking stream; pass cudaStreamLegacy to order
  * after work on the legacy default stream, e.g. torch's default stream whose handle is 0).

@@ -29,7 +29,7 @@ EXPORTS = (
     "femgpu_time_steps_ex", "femgpu_reference_counters", "femgpu_read_output", "femgpu_mesh_build_range",
     "femgpu_halo_create", "femgpu_halo_destroy", "femgpu_halo_export", "femgpu_halo_import", "femgpu_halo_action",
     "femgpu_halo_time_steps", "femgpu_halo_check", "femgpu_trace_counters", "femgpu_problem_fuse",
-    "femgpu_problem_reorder",
+    "femgpu_problem_reorder", "femgpu_action_host_async", "femgpu_action_host_wait",
 )
 
 
@@ -74,6 +74,8 @@ def lib():
                 "femgpu_set_inputs": ([C.c_void_p, _dpp, _dpp], C.c_int),
                 "femgpu_action": ([C.c_void_p, _P(abi.Schedule), _P(C.c_double)], C.c_int),
                 "femgpu_action_host": ([C.c_void_p, _P(abi.Schedule), _dpp, _dpp, _P(C.c_double)], C.c_int),
+                "femgpu_action_host_async": ([C.c_void_p, _P(abi.Schedule), _dpp, _dpp, _P(C.c_double)], C.c_int),
+                "femgpu_action_host_wait": ([C.c_void_p], C.c_int),
                 "femgpu_action_device": ([C.c_void_p, _P(abi.Schedule), C.c_void_p, C.c_void_p], C.c_int),
                 "femgpu_time_action": ([C.c_void_p, _P(abi.Schedule), C.c_int32, C.c_int32, C.c_double,
                                         _P(C.c_double)], C.c_int),

@@ -205,6 +205,17 @@ class GpuInstance:
                                        self._ptr_array(vector_inputs), out.ctypes.data_as(C.POINTER(C.c_double))))
         return out
 
+    def action_host_async(self, scalar_inputs, vector_inputs, out: np.ndarray, params: Optional[TilingParams] = None):
+        """Streaming end-to-end step (femgpu_action_host_async): enqueued, completed by
+        action_host_wait; the arrays must stay alive and unread until then."""
+        sp = _sched(params)
+        _call(lib().femgpu_action_host_async(self._h, sp[0] if sp else None, self._ptr_array(scalar_inputs),
+                                             self._ptr_array(vector_inputs), out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
+    def action_host_wait(self):
+        _call(lib().femgpu_action_host_wait(self._h))
+
     def action_device(self, params: Optional[TilingParams] = None, y_dev: int = 0, stream: int = 0):
         sp = _sched(params)
         _call(lib().femgpu_action_device(self._h, sp[0] if sp else None, C.c_void_p(y_dev), C.c_void_p(stream)))

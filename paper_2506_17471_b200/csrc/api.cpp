@@ -79,6 +79,49 @@ int32_t femgpu_device_count(void) {
     return n;
 }
 
+namespace {
+
+// Buffer set b's device inputs swapped into the instance's spaces for the duration of a call
+// (kernel parameters capture the pointers at launch).
+void swap_inputs(femgpu::Instance& I, int b) {
+    if (b != 1) return;
+    const size_t n = I.sspaces.size() + I.vspaces.size();
+    if (I.x_alt.empty()) {
+        const int vs = femgpu::vec_stride(I.sig.dim);
+        for (const auto& sp : I.sspaces) I.x_alt.push_back(I.alloc<double>(static_cast<size_t>(sp.global)));
+        for (const auto& sp : I.vspaces) I.x_alt.push_back(I.alloc<double>(static_cast<size_t>(sp.global) * vs));
+    }
+    for (size_t i = 0; i < n; ++i) {
+        auto& ds = i < I.sspaces.size() ? I.sspaces[i] : I.vspaces[i - I.sspaces.size()];
+        std::swap(ds.d_x, I.x_alt[i]);
+    }
+}
+
+// Completes the streaming steps: both sets' downloads and computes; the instance then holds the last
+// step's inputs and output (set 1 copied into set 0), and a non-finite value in any step is reported
+// (diagnosed on the last step's inputs).
+void async_drain(femgpu::Instance& I) {
+    if (I.async_pending == 0) return;
+    FG_CUDA(cudaStreamSynchronize(I.s_d2h));
+    FG_CUDA(cudaStreamSynchronize(I.stream));
+    if (I.async_last == 1) {
+        const int vs = femgpu::vec_stride(I.sig.dim);
+        size_t i = 0;
+        for (auto& sp : I.sspaces)
+            FG_CUDA(cudaMemcpyAsync(sp.d_x, I.x_alt[i++], sizeof(double) * sp.global, cudaMemcpyDeviceToDevice, I.stream));
+        for (auto& sp : I.vspaces)
+            FG_CUDA(cudaMemcpyAsync(sp.d_x, I.x_alt[i++], sizeof(double) * sp.global * vs, cudaMemcpyDeviceToDevice, I.stream));
+        FG_CUDA(cudaMemcpyAsync(I.d_y, I.second_output(), sizeof(double) * static_cast<size_t>(I.output_size),
+                                cudaMemcpyDeviceToDevice, I.stream));
+    }
+    I.async_pending = 0;
+    I.async_used[0] = I.async_used[1] = false;
+    I.async_next = 0;
+    femgpu::check_failure(I, I.async_kp, I.stream);
+}
+
+}  // namespace
+
 femgpu_status femgpu_set_device(int32_t device) {
     return guard([&] {
         FG_CUDA(cudaSetDevice(device));
@@ -208,6 +251,7 @@ femgpu_status femgpu_set_inputs(femgpu_instance* h, const double* const* scalar_
     return guard([&] {
         auto& I = get(h);
         std::lock_guard<std::mutex> lk(I.mu);
+        async_drain(I);  // streaming steps complete first
         FG_CUDA(cudaSetDevice(I.device));
         copy_inputs(I, scalar_inputs, vector_inputs, I.stream);
         FG_CUDA(cudaStreamSynchronize(I.stream));
@@ -219,6 +263,7 @@ femgpu_status femgpu_action(femgpu_instance* h, const femgpu_schedule* s, double
         auto& I = get(h);
         if (!y_host) femgpu::invalid("null output buffer");
         std::lock_guard<std::mutex> lk(I.mu);
+        async_drain(I);  // streaming steps complete first
         FG_CUDA(cudaSetDevice(I.device));
         const femgpu::KernelPlan kp = femgpu::plan_for(I, s);
         femgpu::run_action(I, kp, I.d_y, I.stream);
@@ -234,6 +279,7 @@ femgpu_status femgpu_action_host(femgpu_instance* h, const femgpu_schedule* s, c
         auto& I = get(h);
         if (!y_host) femgpu::invalid("null output buffer");
         std::lock_guard<std::mutex> lk(I.mu);
+        async_drain(I);  // streaming steps complete first
         FG_CUDA(cudaSetDevice(I.device));
         const femgpu::KernelPlan kp = femgpu::plan_for(I, s);
         // overlapped H2D / slabs / D2H when the instance has locality (pipeline.cpp), else sequential
@@ -247,10 +293,56 @@ femgpu_status femgpu_action_host(femgpu_instance* h, const femgpu_schedule* s, c
     });
 }
 
+femgpu_status femgpu_action_host_async(femgpu_instance* h, const femgpu_schedule* s, const double* const* scalar_inputs,
+                                       const double* const* vector_inputs, double* y_host) {
+    return guard([&] {
+        auto& I = get(h);
+        if (!y_host) femgpu::invalid("null output buffer");
+        std::lock_guard<std::mutex> lk(I.mu);
+        FG_CUDA(cudaSetDevice(I.device));
+        const femgpu::KernelPlan kp = femgpu::plan_for(I, s);
+        if (I.async_pending && kp.key() != I.async_kp.key()) async_drain(I);  // one schedule per stream of steps
+        const int b = I.async_next;
+        swap_inputs(I, b);
+        bool ok = false;
+        try {
+            ok = femgpu::pipelined_host_action(I, kp, scalar_inputs, vector_inputs, y_host, b,
+                                               b ? I.second_output() : I.d_y);
+        } catch (...) {
+            swap_inputs(I, b);
+            throw;
+        }
+        swap_inputs(I, b);
+        if (!ok) {  // no slab plan for this instance: a synchronous step
+            async_drain(I);
+            copy_inputs(I, scalar_inputs, vector_inputs, I.stream);
+            femgpu::run_action(I, kp, I.d_y, I.stream);
+            FG_CUDA(cudaMemcpyAsync(y_host, I.d_y, sizeof(double) * static_cast<size_t>(I.output_size),
+                                    cudaMemcpyDeviceToHost, I.stream));
+            femgpu::check_failure(I, kp, I.stream);
+            return;
+        }
+        I.async_kp = kp;
+        I.async_last = b;
+        I.async_next = b ^ 1;
+        ++I.async_pending;
+    });
+}
+
+femgpu_status femgpu_action_host_wait(femgpu_instance* h) {
+    return guard([&] {
+        auto& I = get(h);
+        std::lock_guard<std::mutex> lk(I.mu);
+        FG_CUDA(cudaSetDevice(I.device));
+        async_drain(I);
+    });
+}
+
 femgpu_status femgpu_action_device(femgpu_instance* h, const femgpu_schedule* s, double* y_dev, void* stream) {
     return guard([&] {
         auto& I = get(h);
         std::lock_guard<std::mutex> lk(I.mu);
+        async_drain(I);  // streaming steps complete first
         FG_CUDA(cudaSetDevice(I.device));
         const femgpu::KernelPlan kp = femgpu::plan_for(I, s);
         femgpu::run_action(I, kp, y_dev ? y_dev : I.d_y, stream ? static_cast<cudaStream_t>(stream) : I.stream);
@@ -264,6 +356,7 @@ femgpu_status femgpu_action_device_pipelined(femgpu_instance* h, const femgpu_sc
         if (!y_dev) femgpu::invalid("action_device_pipelined: null output buffer");
         if (y_next_dev == y_dev) femgpu::invalid("action_device_pipelined: y_next must not alias y");
         std::lock_guard<std::mutex> lk(I.mu);
+        async_drain(I);  // streaming steps complete first
         FG_CUDA(cudaSetDevice(I.device));
         const femgpu::KernelPlan kp = femgpu::plan_for(I, s);
         femgpu::run_action_pipelined(I, kp, y_dev, y_next_dev, stream ? static_cast<cudaStream_t>(stream) : I.stream);
@@ -274,6 +367,7 @@ femgpu_status femgpu_check_finite(femgpu_instance* h, const femgpu_schedule* s, 
     return guard([&] {
         auto& I = get(h);
         std::lock_guard<std::mutex> lk(I.mu);
+        async_drain(I);  // streaming steps complete first
         FG_CUDA(cudaSetDevice(I.device));
         const femgpu::KernelPlan kp = femgpu::plan_for(I, s);
         femgpu::check_failure(I, kp, stream ? static_cast<cudaStream_t>(stream) : I.stream);
@@ -286,6 +380,7 @@ femgpu_status femgpu_time_action(femgpu_instance* h, const femgpu_schedule* s, i
         auto& I = get(h);
         if (!seconds) femgpu::invalid("null output");
         std::lock_guard<std::mutex> lk(I.mu);
+        async_drain(I);  // streaming steps complete first
         FG_CUDA(cudaSetDevice(I.device));
         const femgpu::KernelPlan kp = femgpu::plan_for(I, s);
         for (int i = 0; i < warmup; ++i) femgpu::run_action(I, kp, I.d_y, I.stream);
@@ -319,6 +414,7 @@ femgpu_status femgpu_time_steps_ex(femgpu_instance* h, const femgpu_schedule* s,
         auto& I = get(h);
         if (steps < 1 || !seconds) femgpu::invalid("time_steps: steps >= 1 and an output are required");
         std::lock_guard<std::mutex> lk(I.mu);
+        async_drain(I);  // streaming steps complete first
         FG_CUDA(cudaSetDevice(I.device));
         const femgpu::KernelPlan kp = femgpu::plan_for(I, s);
         const bool piped = (flags & FEMGPU_STEPS_PIPELINED) != 0;
@@ -355,6 +451,7 @@ femgpu_status femgpu_profile_action(femgpu_instance* h, const femgpu_schedule* s
         auto& I = get(h);
         if (reps < 1) femgpu::invalid("profile: reps must be >= 1");
         std::lock_guard<std::mutex> lk(I.mu);
+        async_drain(I);  // streaming steps complete first
         FG_CUDA(cudaSetDevice(I.device));
         const femgpu::KernelPlan kp = femgpu::plan_for(I, s);
         for (int i = 0; i < warmup; ++i) femgpu::run_action(I, kp, I.d_y, I.stream);
@@ -442,6 +539,7 @@ femgpu_status femgpu_trace_counters(femgpu_instance* h, const femgpu_schedule* s
         auto& I = get(h);
         if (!out || n < FEMGPU_TRACE_COUNTERS) femgpu::invalid("trace_counters: need FEMGPU_TRACE_COUNTERS outputs");
         std::lock_guard<std::mutex> lk(I.mu);
+        async_drain(I);  // streaming steps complete first
         FG_CUDA(cudaSetDevice(I.device));
         const femgpu::KernelPlan kp = femgpu::plan_for(I, s);
         auto mod = I.module_for(kp);
@@ -487,6 +585,7 @@ femgpu_status femgpu_read_output(femgpu_instance* h, double* y_host) {
         auto& I = get(h);
         if (!y_host) femgpu::invalid("null output buffer");
         std::lock_guard<std::mutex> lk(I.mu);
+        async_drain(I);  // streaming steps complete first
         FG_CUDA(cudaSetDevice(I.device));
         FG_CUDA(cudaMemcpyAsync(y_host, I.d_y, sizeof(double) * static_cast<size_t>(I.output_size),
                                 cudaMemcpyDeviceToHost, I.stream));

@@ -289,7 +289,16 @@ struct Instance {
     const Colouring& colour_plan();
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
     std::vector<cudaEvent_t> ev_pipe;
+    // streaming host actions (femgpu_action_host_async): two sets of device inputs/outputs, so step
+    // i+1's uploads run while step i's results download.  Set 0 is the instance's own d_x / d_y.
+    std::vector<double*> x_alt;                 // per trial space (scalar then vector): set-1 inputs
+    cudaEvent_t ev_async_comp[2] = {nullptr, nullptr}, ev_async_d2h[2] = {nullptr, nullptr};
+    bool async_used[2] = {false, false};
+    int async_next = 0, async_pending = 0, async_last = -1;
+    KernelPlan async_kp;
     const PipePlan& pipe_plan(int align);
+    std::unique_ptr<PipePlan> pipe_stream;         // streaming steps: few large slabs (stream_slab_count)
+    const PipePlan& stream_plan(int align);
     // fused zeroing of y (pipeline.cpp): slab plan, worker stream, per-slab events
     std::map<std::pair<int, int>, std::unique_ptr<PipePlan>> zplans;  // by (align, slabs): host scan of the maps
     const PipePlan& zero_plan(int align, int slabs, int max_slabs);
@@ -338,8 +347,10 @@ int range_align(const KernelPlan& kp);
 bool overlapped_zero_action(Instance& inst, const KernelPlan& kp, double* d_y, cudaStream_t stream,
                             cudaEvent_t after_zero);
 // pipeline.cpp: femgpu_action_host overlapped over H2D / compute / D2H streams; false = not applicable
+// buf = -1: one synchronous action into inst.d_y; buf = 0/1: a streaming step on buffer set `buf`
+// (inputs already swapped in by the caller) writing y_dev, ordered against the previous use of the set
 bool pipelined_host_action(Instance& inst, const KernelPlan& kp, const double* const* scalar_inputs,
-                           const double* const* vector_inputs, double* y_host);
+                           const double* const* vector_inputs, double* y_host, int buf = -1, double* y_dev = nullptr);
 void check_failure(Instance& inst, const KernelPlan& kp, cudaStream_t stream);
 // Host-side data-parallel loop over [0, n) in up to 32 contiguous chunks (re-blocking, layouts, reorder).
 template <typename F>

@@ -255,6 +255,10 @@ Instance::~Instance() {
     }
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
+    for (int b = 0; b < 2; ++b) {
+        if (ev_async_comp[b]) cudaEventDestroy(ev_async_comp[b]);
+        if (ev_async_d2h[b]) cudaEventDestroy(ev_async_d2h[b]);
+    }
     for (cudaStream_t s : {s_h2d, s_d2h, s_work})
         if (s) {
             cudaStreamSynchronize(s);

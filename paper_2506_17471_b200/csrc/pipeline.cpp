@@ -52,6 +52,17 @@ const PipePlan& Instance::pipe_plan(int align) {
     return *pipe;
 }
 
+// Streaming steps (femgpu_action_host_async) overlap one step's download with the next step's upload,
+// so fill and drain are hidden and per-slab costs dominate: 2 slabs by default
+// (C2: 1.775 / 1.884 / 2.016 ms per step at 2 / 4 / 8 slabs; FEMGPU_STREAM_SLABS overrides).
+const PipePlan& Instance::stream_plan(int align) {
+    const char* e = std::getenv("FEMGPU_STREAM_SLABS");
+    const int K = std::max(2, std::min(128, e ? std::atoi(e) : 2));
+    if (pipe_stream && pipe_stream->align == align && static_cast<int>(pipe_stream->cb.size()) == K + 1) return *pipe_stream;
+    pipe_stream = slab_plan(K, align);
+    return *pipe_stream;
+}
+
 const PipePlan& Instance::zero_plan(int align, int slabs, int max_slabs) {
     const int K = std::min(zero_slab_count(slabs), std::max(2, max_slabs));
     auto& z = zplans[{align, K}];
@@ -185,10 +196,11 @@ bool overlapped_zero_action(Instance& I, const KernelPlan& plan, double* d_y, cu
 }
 
 bool pipelined_host_action(Instance& I, const KernelPlan& kp, const double* const* scalar_inputs,
-                           const double* const* vector_inputs, double* y_host) {
+                           const double* const* vector_inputs, double* y_host, int buf, double* y_dev) {
+    double* const Y = y_dev ? y_dev : I.d_y;
     const char* env = std::getenv("FEMGPU_PIPELINE");
     if ((env && std::strcmp(env, "0") == 0) || I.cells < kPipeMinCells || !supports_cell_range(kp)) return false;
-    const PipePlan& P = I.pipe_plan(range_align(kp));
+    const PipePlan& P = buf < 0 ? I.pipe_plan(range_align(kp)) : I.stream_plan(range_align(kp));
     if (!P.useful) return false;
     const int K = static_cast<int>(P.cb.size()) - 1;
     if (!I.s_h2d) {
@@ -201,9 +213,23 @@ bool pipelined_host_action(Instance& I, const KernelPlan& kp, const double* cons
         I.ev_pipe.push_back(e);
     }
     const int d = I.sig.dim;
-    // previous work on the instance stream (an earlier action) must finish before inputs change
-    FG_CUDA(cudaEventRecord(I.ev_pipe[2 * K], I.stream));
-    FG_CUDA(cudaStreamWaitEvent(I.s_h2d, I.ev_pipe[2 * K], 0));
+    if (buf < 0) {
+        // previous work on the instance stream (an earlier action) must finish before inputs change
+        FG_CUDA(cudaEventRecord(I.ev_pipe[2 * K], I.stream));
+        FG_CUDA(cudaStreamWaitEvent(I.s_h2d, I.ev_pipe[2 * K], 0));
+    } else {
+        // streaming step: this buffer set's inputs were last read by the compute two steps ago and
+        // its output last read by that step's download; the other set's step may still be running
+        for (int b = 0; b < 2; ++b)
+            if (!I.ev_async_comp[b]) {
+                FG_CUDA(cudaEventCreateWithFlags(&I.ev_async_comp[b], cudaEventDisableTiming));
+                FG_CUDA(cudaEventCreateWithFlags(&I.ev_async_d2h[b], cudaEventDisableTiming));
+            }
+        if (I.async_used[buf]) {
+            FG_CUDA(cudaStreamWaitEvent(I.s_h2d, I.ev_async_comp[buf], 0));
+            FG_CUDA(cudaStreamWaitEvent(I.stream, I.ev_async_d2h[buf], 0));
+        }
+    }
     std::vector<long long> done(P.up.size(), 0);
     long long zeroed = 0, sent = 0;
     // FEMGPU_PIPE_TRACE=1: timing events after every H2D chunk, slab kernel and D2H chunk, printed to
@@ -249,23 +275,29 @@ bool pipelined_host_action(Instance& I, const KernelPlan& kp, const double* cons
         // compute: zero the y rows slab k can newly reach, then the slab
         FG_CUDA(cudaStreamWaitEvent(I.stream, I.ev_pipe[k], 0));
         if (P.zero_hi[k] > zeroed) {
-            FG_CUDA(cudaMemsetAsync(I.d_y + zeroed, 0, sizeof(double) * (P.zero_hi[k] - zeroed), I.stream));
+            FG_CUDA(cudaMemsetAsync(Y + zeroed, 0, sizeof(double) * (P.zero_hi[k] - zeroed), I.stream));
             zeroed = P.zero_hi[k];
         }
-        if (!no_kernel) run_action_range(I, kp, I.d_y, I.stream, P.cb[k], P.cb[k + 1], false);
+        if (!no_kernel) run_action_range(I, kp, Y, I.stream, P.cb[k], P.cb[k + 1], false);
         mark(I.stream);
         FG_CUDA(cudaEventRecord(I.ev_pipe[K + k], I.stream));
         // D2H: the rows no later slab touches
         FG_CUDA(cudaStreamWaitEvent(I.s_d2h, I.ev_pipe[K + k], 0));
         if (P.fin[k] > sent) {
-            if (!no_copy) FG_CUDA(cudaMemcpyAsync(y_host + sent, I.d_y + sent, sizeof(double) * (P.fin[k] - sent),
+            if (!no_copy) FG_CUDA(cudaMemcpyAsync(y_host + sent, Y + sent, sizeof(double) * (P.fin[k] - sent),
                                     cudaMemcpyDeviceToHost, I.s_d2h));
             sent = P.fin[k];
         }
         mark(I.s_d2h);
     }
-    FG_CUDA(cudaEventRecord(I.ev_pipe[2 * K], I.s_d2h));
-    FG_CUDA(cudaStreamWaitEvent(I.stream, I.ev_pipe[2 * K], 0));
+    if (buf >= 0) {
+        FG_CUDA(cudaEventRecord(I.ev_async_comp[buf], I.stream));
+        FG_CUDA(cudaEventRecord(I.ev_async_d2h[buf], I.s_d2h));
+        I.async_used[buf] = true;
+    } else {
+        FG_CUDA(cudaEventRecord(I.ev_pipe[2 * K], I.s_d2h));
+        FG_CUDA(cudaStreamWaitEvent(I.stream, I.ev_pipe[2 * K], 0));
+    }
     if (trace) {
         FG_CUDA(cudaStreamSynchronize(I.stream));
         std::fprintf(stderr, "pipe trace K=%d (us: h2d done, kernel done, d2h done per slab)\n", K);
