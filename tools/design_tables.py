@@ -31,12 +31,14 @@ b = ("**{} of 14** benchmark configurations reach ≥ 50 % of the roofline (roun
      "own `reference_action` (oracle/_ref, 16 host threads) at rel L2 ≤ {:.1e} and elementwise ≤ {:.1e} — the full "
      "action, or ({}, whose CPU reference exceeds the per-row budget) the complete rows of a contiguous cell sample. "
      "Bench line (`profiles/r02_bench_final.json`): C2 {:.2f} GDOF/s, {:.1f} µs/step, roofline frac {:.3f} (kernel = "
-     "step: one launch per pipelined step), clocks {} MHz, e2e through `femgpu_action_host` {:.2f} GDOF/s (PCIe-bound: "
-     "80 MB in + 80 MB out per step; the duplex copy alone takes 1.63 ms, the e2e step {:.2f} ms), reference CPU path "
+     "step: one launch per pipelined step), clocks {} MHz, e2e from pinned host buffers {:.2f} GDOF/s ({:.2f} ms per "
+     "streaming step, `femgpu_action_host_async`; PCIe-bound: 80 MB in + 80 MB out per step, 1.63 ms at full duplex; "
+     "one `femgpu_action_host` at a time {:.2f} GDOF/s), reference CPU path "
      "{:.4f} GDOF/s on {} host threads ({}).").format(
     d["forms"]["at_least_half_roofline"], max(r["parity_vs_reference"]["rel_l2"] for r in fr),
     max(r["parity_vs_reference"]["max_rel"] for r in fr), ", ".join(part), d["value"], d["ms_per_step"] * 1e3,
-    d["roofline"]["frac"], d["clocks"]["sm_mhz"], d["e2e"]["value"], d["e2e"]["ms_per_step"], d["cpu_baseline"]["value"],
+    d["roofline"]["frac"], d["clocks"]["sm_mhz"], d["e2e"]["value"], d["e2e"]["ms_per_step"],
+    d["e2e"].get("sync", d["e2e"])["value"], d["cpu_baseline"]["value"],
     d["cpu_baseline"]["cores"], d["cpu_baseline"]["cpu_model"])
 s = s.replace(a, b)
 open("DESIGN.md", "w").write(s)
