@@ -300,6 +300,7 @@ femgpu_status femgpu_action_host_async(femgpu_instance* h, const femgpu_schedule
         if (!y_host) femgpu::invalid("null output buffer");
         std::lock_guard<std::mutex> lk(I.mu);
         FG_CUDA(cudaSetDevice(I.device));
+        if (!s && !I.auto_ready) async_drain(I);  // the automatic schedule's timing pass uses the instance buffers
         const femgpu::KernelPlan kp = femgpu::plan_for(I, s);
         if (I.async_pending && kp.key() != I.async_kp.key()) async_drain(I);  // one schedule per stream of steps
         const int b = I.async_next;
