@@ -496,7 +496,10 @@ femgpu_status femgpu_default_schedule(const femgpu_instance* h, femgpu_schedule*
         auto& I = *h->impl;  // the automatic schedule is a lazily computed cache of the instance
         std::lock_guard<std::mutex> lk(I.mu);
         FG_CUDA(cudaSetDevice(I.device));
-        if (!I.auto_ready) femgpu::autotune(I);
+        if (!I.auto_ready) {
+            async_drain(I);  // the timing pass uses the instance buffers
+            femgpu::autotune(I);
+        }
         *s = I.auto_sched;
     });
 }
@@ -507,6 +510,7 @@ femgpu_status femgpu_describe_schedule(femgpu_instance* h, const femgpu_schedule
         auto& I = get(h);
         std::lock_guard<std::mutex> lk(I.mu);
         FG_CUDA(cudaSetDevice(I.device));
+        if (!s && !I.auto_ready) async_drain(I);
         std::string d = femgpu::describe_plan(femgpu::plan_for(I, s));
         if (!s) d += " | auto: " + I.auto_log;
         if (len) *len = d.size();
