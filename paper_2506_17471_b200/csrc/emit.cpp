@@ -199,7 +199,10 @@ void emit_cell_body(Out& o, const Signature& sig, const KernelPlan& kp, const Ma
             else if (tile && kp.sgroup[i] >= 0)
                 o.line("const double " + nm("u", i, j) + " = xs" + std::to_string(i) + "[sl" +
                        std::to_string(kp.sgroup[i]) + "[" + std::to_string(j * kp.tile_cells) + " + threadIdx.x]];");
-            else
+            else if (!kp.salias.empty()) {  // node index named: the scatter reuses it (salias)
+                o.line("const int " + nm("sn", i, j) + " = __ldg(&P.m" + std::to_string(i) + "[" + idx + "]);");
+                o.line("const double " + nm("u", i, j) + " = __ldg(&P.x" + std::to_string(i) + "[" + nm("sn", i, j) + "]);");
+            } else
                 o.line("const double " + nm("u", i, j) + " = __ldg(&P.x" + std::to_string(i) + "[__ldg(&P.m" +
                        std::to_string(i) + "[" + idx + "])]);");
         }
@@ -406,6 +409,13 @@ void emit_cell_body(Out& o, const Signature& sig, const KernelPlan& kp, const Ma
     o.ind++;
     for (int jw = 0; jw < sig.nW; ++jw) {
         std::string idx = std::to_string(jw) + "*(size_t)" + C + "+cell";
+        std::string row = "__ldg(&P.tm[" + idx + "])";
+        if (!mc && !tile && !kp.salias.empty() && kp.salias[jw][0] >= 0) {
+            // row = scale * (gathered node index) + add (Instance::test_alias): no test-map load
+            const auto& a = kp.salias[jw];
+            row = "(" + nm(a[0] == 1 ? "vn" : "sn", static_cast<int>(a[1]), static_cast<int>(a[2])) +
+                  (a[3] != 1 ? " * " + std::to_string(a[3]) : "") + (a[4] ? " + " + std::to_string(a[4]) : "") + ")";
+        }
         if (mc && kp.ysmem)
             o.line("SY(" + std::to_string(pat(kp.tgroup, jw)) + ") += o" + std::to_string(jw) + ";");
         else if (mc)
@@ -413,9 +423,9 @@ void emit_cell_body(Out& o, const Signature& sig, const KernelPlan& kp, const Ma
         else if (tile)
             o.line("st[" + std::to_string(jw * kp.tile_cells) + " + threadIdx.x] = o" + std::to_string(jw) + ";");
         else if (kp.colour)  // no other cell of this launch (colour) touches the DOF
-            o.line("P.y[__ldg(&P.tm[" + idx + "])] += o" + std::to_string(jw) + ";");
+            o.line("P.y[" + row + "] += o" + std::to_string(jw) + ";");
         else
-            o.line("atomicAdd(&P.y[__ldg(&P.tm[" + idx + "])], o" + std::to_string(jw) + ");");
+            o.line("atomicAdd(&P.y[" + row + "], o" + std::to_string(jw) + ");");
     }
     o.ind--;
     o.line("}");
@@ -523,6 +533,8 @@ std::string KernelPlan::key() const {
         for (long long v : t) h = (h ^ static_cast<uint64_t>(v + 11)) * 0x100000001b3ULL;
     for (const auto& t : dalias)
         for (long long v : t) h = (h ^ static_cast<uint64_t>(v + 13)) * 0x100000001b3ULL;
+    for (const auto& t : salias)
+        for (long long v : t) h = (h ^ static_cast<uint64_t>(v + 17)) * 0x100000001b3ULL;
     s << "P" << h;
     return s.str();
 }

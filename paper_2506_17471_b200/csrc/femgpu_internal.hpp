@@ -122,6 +122,8 @@ struct KernelPlan {
     // DMMA without tvec: per test column (trial kind 0 scalar / 1 vector / -1 none, space, column,
     // scale, add): the row is scale * (that space's gathered node index) + add (Instance::test_alias)
     std::vector<std::array<long long, 5>> dalias;
+    // SCPT (one cell per thread): the same per-column aliases, rows from the gathered node indices
+    std::vector<std::array<long long, 5>> salias;
     long long stage_off = 0;              // macro q-major staging: byte offset of the staging area (emitter-internal)
     bool qloop = false;                   // scpt: keep the quadrature loop rolled (I-cache / registers)
     bool colour = false;                  // scpt: one launch per cell colour, plain y updates (deterministic)

@@ -812,6 +812,26 @@ namespace {
 KernelPlan resolve_schedule_impl(Instance& I, const femgpu_schedule* s);
 }
 
+
+// Per test column: (trial kind 0 scalar / 1 vector, space, column, scale, add) when the column is an
+// affine image of a trial space's map column (Instance::test_alias), else kind -1; empty if none.
+std::vector<std::array<long long, 5>> column_aliases(const Instance& I, const Signature& sig) {
+    std::vector<std::array<long long, 5>> out;
+    bool any = false;
+    for (int j = 0; j < sig.nW; ++j) {
+        std::array<long long, 5> al{-1, 0, 0, 1, 0};
+        const Instance::TestAlias& t = I.test_alias[static_cast<size_t>(j)];
+        for (size_t v = 0; v < I.vspaces.size() && al[0] < 0 && t.group >= 0; ++v)
+            if (I.vspaces[v].group == t.group) al = {1, static_cast<long long>(v), t.col, t.scale, t.add};
+        for (size_t v = 0; v < I.sspaces.size() && al[0] < 0 && t.group >= 0; ++v)
+            if (I.sspaces[v].group == t.group) al = {0, static_cast<long long>(v), t.col, t.scale, t.add};
+        any = any || al[0] >= 0;
+        out.push_back(al);
+    }
+    if (!any) out.clear();
+    return out;
+}
+
 KernelPlan resolve_schedule(Instance& I, const femgpu_schedule* s) {
     KernelPlan kp = resolve_schedule_impl(I, s);
     kp.zfused = s && (s->reserved[0] & FEMGPU_FLAG_FUSED_ZERO) && supports_cell_range(kp);
@@ -858,22 +878,7 @@ KernelPlan resolve_schedule_impl(Instance& I, const femgpu_schedule* s) {
     if (s->kind == FEMGPU_DMMA) {
         resolve_dmma(sig, kp, s);
         kp.tvec = I.test_vspace;
-        if (kp.tvec < 0) {
-            // test columns that are images of a gathered trial space's node column: the scatter then
-            // shuffles the gathered index instead of loading the test map (fused problems)
-            bool any = false;
-            for (int j = 0; j < sig.nW; ++j) {
-                std::array<long long, 5> al{-1, 0, 0, 1, 0};
-                const Instance::TestAlias& t = I.test_alias[static_cast<size_t>(j)];
-                for (size_t v = 0; v < I.vspaces.size() && al[0] < 0 && t.group >= 0; ++v)
-                    if (I.vspaces[v].group == t.group) al = {1, static_cast<long long>(v), t.col, t.scale, t.add};
-                for (size_t v = 0; v < I.sspaces.size() && al[0] < 0 && t.group >= 0; ++v)
-                    if (I.sspaces[v].group == t.group) al = {0, static_cast<long long>(v), t.col, t.scale, t.add};
-                any = any || al[0] >= 0;
-                kp.dalias.push_back(al);
-            }
-            if (!any) kp.dalias.clear();
-        }
+        if (kp.tvec < 0) kp.dalias = column_aliases(I, sig);
         return kp;
     }
     // SCPT: one thread per cell.
@@ -1004,6 +1009,10 @@ KernelPlan resolve_schedule_impl(Instance& I, const femgpu_schedule* s) {
     kp.G = scatter == FEMGPU_SCATTER_ATOMIC && s->group_cells > 1 ? s->group_cells : 1;
     kp.qloop = (s->reserved[3] & 0xff) == 4;
     if (kp.G > 8) fail(FEMGPU_E_INFEASIBLE, "schedule: at most 8 cells per thread in the SCPT family");
+    {
+        const char* e = std::getenv("FEMGPU_SCPT_ALIAS");
+        if (kp.G == 1 && !(e && std::strcmp(e, "0") == 0)) kp.salias = column_aliases(I, sig);
+    }
     if (s->reserved[2] > 0) kp.min_blocks = s->reserved[2];
     (void)int_dim;
     return kp;
