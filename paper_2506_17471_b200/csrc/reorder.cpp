@@ -2,8 +2,8 @@
 //
 // The action's gathers and red.add scatter are fast when consecutive cells touch nearby index
 // ranges: then a warp's loads share L1/L2 lines and the resident working set stays small.  A
-// mesh numbered without locality (tools/general_mesh.py "global": C2 with shuffled cells, 1596 us
-// per step instead of 373) is made local again here, once, on the host:
+// mesh numbered without locality (tools/general_mesh.py "global": C2 with shuffled cells, 1657 us
+// per step instead of 370) is made local again here, once, on the host:
 //   * cells are sorted by the Morton code of their centroid (affine geometry; otherwise by their
 //     smallest node index), ties by the old cell index;
 //   * every global index space is renumbered in first-touch order over the sorted cells (nodes no
