@@ -424,6 +424,8 @@ void emit_cell_body(Out& o, const Signature& sig, const KernelPlan& kp, const Ma
             o.line("st[" + std::to_string(jw * kp.tile_cells) + " + threadIdx.x] = o" + std::to_string(jw) + ";");
         else if (kp.colour)  // no other cell of this launch (colour) touches the DOF
             o.line("P.y[" + row + "] += o" + std::to_string(jw) + ";");
+        else if (std::getenv("FEMGPU_DEBUG_SCATTER_STORE") && !mc && !tile)  // timing experiment only (wrong results)
+            o.line("P.y[" + row + "] = o" + std::to_string(jw) + ";");
         else
             o.line("atomicAdd(&P.y[" + row + "], o" + std::to_string(jw) + ");");
     }
