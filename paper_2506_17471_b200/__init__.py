@@ -6,5 +6,5 @@ from . import abi  # noqa: F401
 from .mesh import CONFIGS, FUSED_PAIRS, color_cells, config_problem, fused_pair, mesh_problem, unit_mesh  # noqa: F401
 from .io import load_instance, load_schedule, save_instance, save_schedule  # noqa: F401,E402
 from .krylov import DeviceOperator, cg, symmetric_problem  # noqa: F401,E402
-from .fuse import fuse_problems, split_output  # noqa: F401,E402
+from .fuse import FusedOperator, fuse_problems, split_output  # noqa: F401,E402
 from .reorder import inputs_to_new, output_to_original, reorder_problem  # noqa: F401,E402

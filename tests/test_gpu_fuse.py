@@ -88,3 +88,18 @@ def test_fused_non_affine_problems(oracle, sched):
     for yk, p in zip(fg.split_output(y, offs), (a, b)):
         ref = oracle.reference_action(p)
         assert rel_l2(yk, ref) <= 1e-12 and max_rel(yk, ref) <= 1e-10
+
+
+@pytest.mark.parametrize("name", sorted(fg.FUSED_PAIRS))
+def test_fused_operator_picks_the_faster_mode_and_matches_the_reference(oracle, name):
+    a, b = fg.fused_pair(name, n=40 if name.startswith("laplace") else 36)
+    with fg.FusedOperator([a, b]) as op:
+        assert op.mode in ("fused", "separate")
+        assert op.times[op.mode] == min(op.times.values())
+        ys = op.action()
+    for y, p in zip(ys, (a, b)):
+        m = min(p.connectivity.cell_count, 60000)
+        from tests.helpers import complete_rows
+        rows = complete_rows(p, m)
+        ref = oracle.reference_action(p, cell_range=(0, m))
+        assert rel_l2(y[rows], ref[rows]) <= 1e-12
