@@ -86,3 +86,22 @@ def test_non_affine_problems_fuse_through_their_coordinate_space(oracle):
     assert f.signature.coordinate_space == 0
     fa, fb = fg.split_output(oracle.reference_action(f), offs)
     assert np.array_equal(fa, oracle.reference_action(a)) and np.array_equal(fb, oracle.reference_action(b))
+
+
+def test_fusing_a_single_problem_is_the_problem(oracle):
+    a, _ = fg.fused_pair("stokes-P2", n=2)
+    f, offs = fg.fuse_problems([a])
+    assert offs == [0, a.output_size]
+    assert np.array_equal(oracle.reference_action(f), oracle.reference_action(a))
+
+
+def test_fused_then_reordered(oracle):
+    """Fusion and renumbering compose: the fused problem of a pair, renumbered, maps back to the two
+    separate reference actions."""
+    a, b = fg.fused_pair("laplace+mass-P2", n=3)
+    f, offs = fg.fuse_problems([a, b])
+    q, perms = fg.reorder_problem(f)
+    y = fg.output_to_original(oracle.reference_action(q), perms)
+    ya, yb = fg.split_output(y, offs)
+    from tests.helpers import rel_l2
+    assert rel_l2(ya, oracle.reference_action(a)) <= 1e-14 and rel_l2(yb, oracle.reference_action(b)) <= 1e-14
