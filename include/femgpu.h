@@ -227,6 +227,14 @@ femgpu_status femgpu_action_host(femgpu_instance* inst, const femgpu_schedule* s
 femgpu_status femgpu_action_host_async(femgpu_instance* inst, const femgpu_schedule* s, const double* const* scalar_inputs,
                                        const double* const* vector_inputs, double* y_host);
 femgpu_status femgpu_action_host_wait(femgpu_instance* inst);
+/* The action's caller: conjugate gradients for A x = b with A the instance's operator
+ * (one scalar trial space numbered like the test space; symmetric positive definite), entirely on the
+ * instance stream: one output-pipelined action + fused update kernels per iteration, scalars in device
+ * memory, fixed-order reductions (no float atomics outside the action); the host reads the residual every check_every
+ * iterations.  b_dev, x_dev: device vectors of output_size doubles; x_dev = initial guess in, solution
+ * out.  Stops at ||r|| <= rtol ||b|| or maxiter; *iterations, *rel_residual = ||r|| / ||b||. */
+femgpu_status femgpu_cg(femgpu_instance* inst, const femgpu_schedule* s, const double* b_dev, double* x_dev, double rtol,
+                        int32_t maxiter, int32_t check_every, int32_t* iterations, double* rel_residual);
 /* Device-resident: y_dev is a device pointer of output_size doubles; stream is a
  * cudaStream_t (NULL = the instance stream, a non-blocking stream; pass cudaStreamLegacy to order
  * after work on the legacy default stream, e.g. torch's default stream whose handle is 0).

@@ -30,6 +30,7 @@ EXPORTS = (
     "femgpu_halo_create", "femgpu_halo_destroy", "femgpu_halo_export", "femgpu_halo_import", "femgpu_halo_action",
     "femgpu_halo_time_steps", "femgpu_halo_check", "femgpu_trace_counters", "femgpu_problem_fuse",
     "femgpu_problem_reorder", "femgpu_action_host_async", "femgpu_action_host_wait",
+    "femgpu_cg",
 )
 
 
@@ -76,6 +77,8 @@ def lib():
                 "femgpu_action_host": ([C.c_void_p, _P(abi.Schedule), _dpp, _dpp, _P(C.c_double)], C.c_int),
                 "femgpu_action_host_async": ([C.c_void_p, _P(abi.Schedule), _dpp, _dpp, _P(C.c_double)], C.c_int),
                 "femgpu_action_host_wait": ([C.c_void_p], C.c_int),
+                "femgpu_cg": ([C.c_void_p, _P(abi.Schedule), C.c_void_p, C.c_void_p, C.c_double, C.c_int32, C.c_int32,
+                               _P(C.c_int32), _P(C.c_double)], C.c_int),
                 "femgpu_action_device": ([C.c_void_p, _P(abi.Schedule), C.c_void_p, C.c_void_p], C.c_int),
                 "femgpu_time_action": ([C.c_void_p, _P(abi.Schedule), C.c_int32, C.c_int32, C.c_double,
                                         _P(C.c_double)], C.c_int),

@@ -339,6 +339,21 @@ femgpu_status femgpu_action_host_wait(femgpu_instance* h) {
     });
 }
 
+femgpu_status femgpu_cg(femgpu_instance* h, const femgpu_schedule* s, const double* b_dev, double* x_dev, double rtol,
+                        int32_t maxiter, int32_t check_every, int32_t* iterations, double* rel_residual) {
+    return guard([&] {
+        auto& I = get(h);
+        if (!b_dev || !x_dev) femgpu::invalid("cg: null vector");
+        std::lock_guard<std::mutex> lk(I.mu);
+        async_drain(I);  // streaming steps complete first
+        FG_CUDA(cudaSetDevice(I.device));
+        const femgpu::KernelPlan kp = femgpu::plan_for(I, s);
+        int it = 0;
+        femgpu::device_cg(I, kp, b_dev, x_dev, rtol, maxiter, check_every, &it, rel_residual);
+        if (iterations) *iterations = it;
+    });
+}
+
 femgpu_status femgpu_action_device(femgpu_instance* h, const femgpu_schedule* s, double* y_dev, void* stream) {
     return guard([&] {
         auto& I = get(h);

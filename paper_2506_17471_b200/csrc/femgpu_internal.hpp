@@ -294,6 +294,7 @@ struct Instance {
     // streaming host actions (femgpu_action_host_async): two sets of device inputs/outputs, so step
     // i+1's uploads run while step i's results download.  Set 0 is the instance's own d_x / d_y.
     std::vector<double*> x_alt;                 // per trial space (scalar then vector): set-1 inputs
+    std::vector<double*> cg_work;               // device CG (cg.cu): r, p, two A p buffers, partials + scalars
     cudaEvent_t ev_async_comp[2] = {nullptr, nullptr}, ev_async_d2h[2] = {nullptr, nullptr};
     bool async_used[2] = {false, false};
     int async_next = 0, async_pending = 0, async_last = -1;
@@ -354,6 +355,9 @@ bool overlapped_zero_action(Instance& inst, const KernelPlan& kp, double* d_y, c
 bool pipelined_host_action(Instance& inst, const KernelPlan& kp, const double* const* scalar_inputs,
                            const double* const* vector_inputs, double* y_host, int buf = -1, double* y_dev = nullptr);
 void check_failure(Instance& inst, const KernelPlan& kp, cudaStream_t stream);
+// cg.cu: conjugate gradients on the instance stream for a square scalar SPD operator
+void device_cg(Instance& I, const KernelPlan& kp, const double* b, double* x, double rtol, int maxiter, int check_every,
+               int* iterations, double* rel_residual);
 // Host-side data-parallel loop over [0, n) in up to 32 contiguous chunks (re-blocking, layouts, reorder).
 template <typename F>
 void parallel_for(long long n, F&& f) {

@@ -105,6 +105,23 @@ def cg(apply: Callable, b, x0=None, rtol: float = 1e-10, maxiter: int = 1000,
     return x, maxiter, hist
 
 
+def native_cg(inst: GpuInstance, b, x0=None, rtol: float = 1e-10, maxiter: int = 1000, check_every: int = 10,
+              params: Optional[TilingParams] = None):
+    """CG inside libfemgpu (femgpu_cg, csrc/cg.cu): the whole loop on the instance stream, fused update
+    kernels, deterministic reductions.  b, x0: float64 CUDA tensors.  Returns (x, iterations, relative
+    residual)."""
+    import torch
+    from .action import _sched
+    x = torch.zeros_like(b) if x0 is None else x0.clone()
+    torch.cuda.synchronize()  # b and x are ready before the instance stream reads them
+    it = C.c_int32()
+    rel = C.c_double()
+    sp = _sched(params)
+    _call(lib().femgpu_cg(inst.handle, sp[0] if sp else None, C.c_void_p(b.data_ptr()), C.c_void_p(x.data_ptr()),
+                          rtol, maxiter, check_every, C.byref(it), C.byref(rel)))
+    return x, it.value, rel.value
+
+
 def dist_cg(plan_, dist_apply: Callable, b_local, rtol: float = 1e-10, maxiter: int = 1000, check_every: int = 1):
     """Distributed CG over the cell partition of dist.build_plan (one rank per GPU).
 

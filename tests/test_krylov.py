@@ -56,6 +56,30 @@ def test_device_cg_converges(oracle, form, dim, deg, Q, n):
     assert np.linalg.norm(r) <= 1e-8 * np.linalg.norm(b.cpu().numpy())
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("form,dim,deg,Q,n", [("helmholtz", 3, 2, 14, 4), ("laplace", 3, 2, 4, 5), ("mass", 2, 3, 12, 8)])
+def test_native_cg_converges_and_is_reproducible(oracle, form, dim, deg, Q, n):
+    """femgpu_cg (csrc/cg.cu): the loop inside libfemgpu converges to the oracle's solution and needs
+    about the iterations of the torch loop; a second solve agrees to rounding (the reductions are
+    fixed-order, the action's red.add scatter is not)."""
+    p = fg.symmetric_problem(form, dim, deg, Q, n)
+    if form == "laplace":  # Laplace is only semi-definite: shift by the mass-like Helmholtz term instead
+        p = fg.symmetric_problem("helmholtz", dim, deg, Q, n)
+    dev = torch.device("cuda", 0)
+    b = torch.from_numpy(np.random.default_rng(5).uniform(0.5, 1.5, p.output_size)).to(dev)
+    with fg.GpuInstance(p) as g:
+        x, it, rel = fg.krylov.native_cg(g, b, rtol=1e-10, maxiter=3000, check_every=1)
+        x2, it2, rel2 = fg.krylov.native_cg(g, b, rtol=1e-10, maxiter=3000, check_every=1)
+        op = fg.DeviceOperator(g)
+        _, it_t, _ = fg.cg(op.apply, b, rtol=1e-10, maxiter=3000, check_every=1)
+    assert rel <= 1e-10 and it < 3000
+    assert abs(it - it2) <= 2 and float(torch.linalg.norm(x - x2) / torch.linalg.norm(x)) <= 1e-9
+    assert abs(it - it_t) <= max(2, it_t // 20)
+    p.scalar_inputs[0] = x.cpu().numpy().copy()
+    r = oracle.reference_action(p) - b.cpu().numpy()
+    assert np.linalg.norm(r) <= 1e-8 * np.linalg.norm(b.cpu().numpy())
+
+
 def _dist_worker(rank, world, port, out_dir):
     import os
     import torch.distributed as dist
