@@ -5,7 +5,7 @@
 // the same launch), one fused update kernel (x += alpha p, r -= alpha A p, block partials of r.r),
 // one fused direction kernel (p = r + beta p), and fixed-order reductions.  The scalars alpha, beta,
 // r.r and p.Ap stay in device memory: no host round trip except the residual check every
-// `check_every` iterations.  Reductions use a fixed grid and fixed in-block order (no floating-point
+// `check_every` iterations (between checks, pairs of iterations replay as a CUDA graph).  Reductions use a fixed grid and fixed in-block order (no floating-point
 // atomics); the action's red.add scatter is the only order-dependent step (colour scatter, SCATTER_COLOR,
 // makes it bitwise reproducible too).
 #include <cmath>
@@ -122,7 +122,7 @@ void device_cg(Instance& I, const KernelPlan& kp, const double* b, double* x, do
     const double bnorm = std::sqrt(host[3]);
     double res = std::sqrt(host[0]);
     int it = 0, cur = 0, a = 1;  // r.r in sc[cur]; ap[a] is zero on entry (zeroed by the first action)
-    while (res > rtol * bnorm && it < maxiter) {
+    auto iteration = [&]() {
         apply_into(I, kp, p, ap[a], ap[a ^ 1], s);  // ap[a] = A p, ap[a ^ 1] zeroed for the next iteration
         dot_partial<<<g, t, 0, s>>>(p, ap[a], n, part);
         dot_final<<<1, t, 0, s>>>(part, sc + 2);
@@ -132,14 +132,41 @@ void device_cg(Instance& I, const KernelPlan& kp, const double* b, double* x, do
         FG_CUDA(cudaGetLastError());
         cur ^= 1;
         a ^= 1;
-        ++it;
-        if (it % check_every == 0 || it == maxiter) {
+    };
+    // Between residual checks the iterations replay as a CUDA graph of two iterations (the buffer
+    // roles alternate with period 2): one launch instead of ~14 (small meshes are launch-bound).
+    cudaGraphExec_t pair = nullptr;
+    if (check_every % 2 == 0 && maxiter >= 2 && res > rtol * bnorm) {
+        cudaGraph_t gr = nullptr;
+        FG_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        try {
+            iteration();
+            iteration();
+        } catch (...) {
+            cudaStreamEndCapture(s, &gr);
+            if (gr) cudaGraphDestroy(gr);
+            throw;
+        }
+        FG_CUDA(cudaStreamEndCapture(s, &gr));
+        FG_CUDA(cudaGraphInstantiate(&pair, gr, 0));
+        FG_CUDA(cudaGraphDestroy(gr));
+    }
+    while (res > rtol * bnorm && it < maxiter) {
+        if (pair && it % 2 == 0 && maxiter - it >= 2) {
+            FG_CUDA(cudaGraphLaunch(pair, s));  // two iterations; cur and a come back to their values
+            it += 2;
+        } else {
+            iteration();
+            ++it;
+        }
+        if (it % check_every == 0 || it >= maxiter) {
             FG_CUDA(cudaMemcpyAsync(host, sc + cur, sizeof(double), cudaMemcpyDeviceToHost, s));
             FG_CUDA(cudaStreamSynchronize(s));
             res = std::sqrt(host[0]);
             if (!std::isfinite(res)) break;
         }
     }
+    if (pair) cudaGraphExecDestroy(pair);
     check_failure(I, kp, s);
     if (iterations) *iterations = it;
     if (rel_residual) *rel_residual = bnorm > 0 ? res / bnorm : res;

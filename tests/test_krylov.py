@@ -70,10 +70,13 @@ def test_native_cg_converges_and_is_reproducible(oracle, form, dim, deg, Q, n):
     with fg.GpuInstance(p) as g:
         x, it, rel = fg.krylov.native_cg(g, b, rtol=1e-10, maxiter=3000, check_every=1)
         x2, it2, rel2 = fg.krylov.native_cg(g, b, rtol=1e-10, maxiter=3000, check_every=1)
+        # residual checks every 10 iterations: the iterations between checks replay as a CUDA graph
+        x3, it3, rel3 = fg.krylov.native_cg(g, b, rtol=1e-10, maxiter=3000, check_every=10)
         op = fg.DeviceOperator(g)
         _, it_t, _ = fg.cg(op.apply, b, rtol=1e-10, maxiter=3000, check_every=1)
     assert rel <= 1e-10 and it < 3000
     assert abs(it - it2) <= 2 and float(torch.linalg.norm(x - x2) / torch.linalg.norm(x)) <= 1e-9
+    assert rel3 <= 1e-10 and it - 2 <= it3 <= it + 12 and float(torch.linalg.norm(x - x3) / torch.linalg.norm(x)) <= 1e-8
     assert abs(it - it_t) <= max(2, it_t // 20)
     p.scalar_inputs[0] = x.cpu().numpy().copy()
     r = oracle.reference_action(p) - b.cpu().numpy()
