@@ -105,3 +105,20 @@ def test_fused_then_reordered(oracle):
     ya, yb = fg.split_output(y, offs)
     from tests.helpers import rel_l2
     assert rel_l2(ya, oracle.reference_action(a)) <= 1e-14 and rel_l2(yb, oracle.reference_action(b)) <= 1e-14
+
+
+def test_fuse_merges_one_of_two_scalar_spaces(oracle):
+    """Helmholtz with a P1 coefficient (two scalar spaces) fused with Laplace on the same P3 field:
+    the P3 spaces merge (terms united, the gradients' rows shared when identical), the coefficient
+    space stays its own, and both actions are reproduced."""
+    a = fg.mesh_problem("helmholtz_coef", 2, 3, 12, 4)
+    b = fg.mesh_problem("laplace", 2, 3, 12, 4, seed=11)
+    b.tabulations.weights = a.tabulations.weights.copy()
+    b.scalar_inputs = [a.scalar_inputs[0].copy()]
+    # Laplace's gradient rows equal to Helmholtz's: shared terms
+    b.tabulations.scalar_phi = [np.ascontiguousarray(a.tabulations.scalar_phi[0][:2])]
+    f, offs = fg.fuse_problems([a, b])
+    assert len(f.signature.scalar_spaces) == 2
+    assert f.signature.scalar_spaces[0].deriv_terms == a.signature.scalar_spaces[0].deriv_terms
+    fa, fb = fg.split_output(oracle.reference_action(f), offs)
+    assert np.array_equal(fa, oracle.reference_action(a)) and np.array_equal(fb, oracle.reference_action(b))
