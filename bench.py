@@ -361,9 +361,10 @@ def run_single(args):
     g = fg.GpuInstance(p)
     cfg = workload_desc(args.config, p, args.n)
     cfg["l2"] = "no flush: per-step footprint (maps + x + coords + y ~ 0.5 GB) exceeds the 126 MB L2"
-    cfg["step"] = ("one full zeroing of an output vector + one full action; femgpu_action_device_pipelined "
-                   "into two alternating outputs (next output zeroed inside the action kernel or by a memset, "
-                   "as the automatic schedule measured faster)")
+    # (what a step is lives outside `config`, which both arms share verbatim)
+    step_definition = ("one full zeroing of an output vector + one full action; femgpu_action_device_pipelined "
+                       "into two alternating outputs (next output zeroed inside the action kernel or by a memset, "
+                       "as the automatic schedule measured faster)")
     flops_cell = cfg["usable_flops_per_cell"]
     cells = p.connectivity.cell_count
     # warm-up (JIT compile + automatic schedule on the first action, outside any timed region)
@@ -453,7 +454,8 @@ def run_single(args):
         "metric": "FP64 operator-action GDOF/s", "value": value, "unit": "GDOF/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": cfg, "roofline": roof, "e2e": e2e, "gpu_launches": args.steps * launches_per_step,
+        "config": cfg, "step_definition": step_definition, "roofline": roof, "e2e": e2e,
+        "gpu_launches": args.steps * launches_per_step,
         "clocks": clk.summary(),
         "step_split_us": {"pipelined_step": t_step * 1e6, "memset_step": step_s * 1e6, "kernel_only": kern_s * 1e6,
                           "memset": zero_s * 1e6},
