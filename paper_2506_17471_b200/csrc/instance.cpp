@@ -10,6 +10,7 @@
 //     global indices of every tile of consecutive cells (shared-with-another-tile
 //     flag in bit 31) and a uint16 tile-local [entry][cell] map.
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <climits>
 #include <cstring>
