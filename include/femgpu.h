@@ -360,6 +360,14 @@ femgpu_status femgpu_halo_time_steps(femgpu_halo* h, const femgpu_schedule* s, i
 /* Synchronizes `stream` (NULL = instance stream) and reports a peer that never reached the
  * exchange (bounded waits: FEMGPU_HALO_TIMEOUT_MS, default 20000) as FEMGPU_E_CUDA. */
 femgpu_status femgpu_halo_check(femgpu_halo* h, void* stream);
+/* Distributed CG on the devices over the exchange (call on every rank, same arguments): vectors in the
+ * rank's local test numbering (owned rows + ghosts; trial space 0 numbered like it), dots over owned
+ * rows all-reduced GPU to GPU through the peers' flag words (values summed in rank order), no host
+ * round trip except the residual check every check_every iterations.  b_dev: the right-hand side on
+ * owned rows; x_dev: initial guess in, solution out (owned rows meaningful).  Call femgpu_halo_check
+ * afterwards: a rank that never arrives is reported, not waited for. */
+femgpu_status femgpu_halo_cg(femgpu_halo* h, const femgpu_schedule* s, const double* b_dev, double* x_dev, double rtol,
+                             int32_t maxiter, int32_t check_every, int32_t* iterations, double* rel_residual);
 
 /* ---- instance / candidate files (femsched io.hpp, format_version 1) ------
  * The reference's versioned structured-text format (io.hpp:197-391): doubles with 17

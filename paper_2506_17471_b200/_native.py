@@ -30,7 +30,7 @@ EXPORTS = (
     "femgpu_halo_create", "femgpu_halo_destroy", "femgpu_halo_export", "femgpu_halo_import", "femgpu_halo_action",
     "femgpu_halo_time_steps", "femgpu_halo_check", "femgpu_trace_counters", "femgpu_problem_fuse",
     "femgpu_problem_reorder", "femgpu_action_host_async", "femgpu_action_host_wait",
-    "femgpu_cg",
+    "femgpu_cg", "femgpu_halo_cg",
 )
 
 
@@ -127,6 +127,8 @@ def lib():
                 "femgpu_halo_action": ([C.c_void_p, _P(abi.Schedule), C.c_void_p, C.c_void_p], C.c_int),
                 "femgpu_halo_time_steps": ([C.c_void_p, _P(abi.Schedule), C.c_int32, _P(C.c_double)], C.c_int),
                 "femgpu_halo_check": ([C.c_void_p, C.c_void_p], C.c_int),
+                "femgpu_halo_cg": ([C.c_void_p, _P(abi.Schedule), C.c_void_p, C.c_void_p, C.c_double, C.c_int32,
+                                    C.c_int32, _P(C.c_int32), _P(C.c_double)], C.c_int),
                 "femgpu_mesh_build_range": ([C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_int64,
                                              _P(C.c_int32), _P(C.c_int32), _P(C.c_double)], C.c_int),
                 "femgpu_reference_counters": ([_P(abi.Problem), _P(C.c_int64), _P(C.c_int64), _P(C.c_int64)], C.c_int),

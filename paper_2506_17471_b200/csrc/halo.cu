@@ -27,6 +27,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cmath>
 #include <cstring>
 #include <numeric>
 #include <vector>
@@ -39,7 +40,8 @@ namespace {
 constexpr int kMaxWorld = 64;
 constexpr int kFlagPushed = 8;
 constexpr int kFlagStep = 6;
-constexpr int kFlagWords = kFlagPushed + kMaxWorld;
+constexpr int kRed = kFlagPushed + kMaxWorld;     // all-reduce slots: [parity][source rank][value bits, epoch]
+constexpr int kFlagWords = kRed + 4 * kMaxWorld;
 constexpr int kMaxSpaces = 2 * FEMGPU_MAX_SPACES;
 
 __device__ __forceinline__ long long ld_acquire(const long long* p) {
@@ -201,6 +203,82 @@ __global__ void recv_kernel(RecvArgs a) {
     }
 }
 
+// ---- device-side all-reduce (sum of one double over the ranks) through the peers' flag words: rank r
+// stores its value into slot r of every rank's flags (double-buffered by the epoch's parity), then a
+// release of the epoch; each rank acquires every slot's epoch and sums the values in rank order
+// (deterministic).  One thread; bounded waits like the exchange (error bit 8).
+__global__ void allreduce_kernel(long long* const* peer_flags, long long* my_flags, int rank, int world,
+                                 const double* in, double* out, long long epoch, unsigned long long timeout_ns) {
+    const int par = static_cast<int>(epoch & 1);
+    const long long bits = __double_as_longlong(*in);
+    for (int q = 0; q < world; ++q) {
+        long long* slot = peer_flags[q] + kRed + par * 2 * kMaxWorld + 2 * rank;
+        slot[0] = bits;
+        st_release(slot + 1, epoch);
+    }
+    double sum = 0.0;
+    for (int q = 0; q < world; ++q) {
+        const long long* slot = my_flags + kRed + par * 2 * kMaxWorld + 2 * q;
+        wait_geq(slot + 1, epoch, my_flags + 2, timeout_ns, 8, q);
+        sum += __longlong_as_double(*(volatile const long long*)slot);
+    }
+    *out = sum;
+}
+
+constexpr int kCgBlocks = 1184, kCgThreads = 256;
+
+__device__ __forceinline__ void cg_block_sum(double v, double* out) {
+    __shared__ double red[kCgThreads];
+    red[threadIdx.x] = v;
+    __syncthreads();
+    for (int s = kCgThreads / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = red[0];
+}
+
+#define CG_LOOP(i, n) for (long long i = blockIdx.x * (long long)kCgThreads + threadIdx.x; i < (n); i += (long long)kCgBlocks * kCgThreads)
+
+__global__ void cg_mask_dot(const double* a, const double* b, const unsigned char* owned, long long n, double* part) {
+    double s = 0.0;
+    CG_LOOP(i, n) if (owned[i]) s += a[i] * b[i];
+    cg_block_sum(s, part + blockIdx.x);
+}
+__global__ void cg_final(const double* part, double* out) {
+    double s = 0.0;
+    for (int i = threadIdx.x; i < kCgBlocks; i += kCgThreads) s += part[i];
+    cg_block_sum(s, out);
+}
+// r = owned ? b - ax : 0; p = r
+__global__ void cg_init(double* r, double* p, const double* b, const double* ax, const unsigned char* owned, long long n) {
+    CG_LOOP(i, n) {
+        const double ri = owned[i] ? b[i] - ax[i] : 0.0;
+        r[i] = ri;
+        p[i] = ri;
+    }
+}
+// ghost rows of A p hold partial sums: zero them (only owned rows are the product)
+__global__ void cg_mask(double* v, const unsigned char* owned, long long n) {
+    CG_LOOP(i, n) if (!owned[i]) v[i] = 0.0;
+}
+__global__ void cg_update_xr(double* x, double* r, const double* p, const double* ap, const unsigned char* owned, long long n,
+                             const double* rr, const double* pap, double* part) {
+    const double alpha = *rr / *pap;
+    double s = 0.0;
+    CG_LOOP(i, n) {
+        x[i] += alpha * p[i];
+        const double ri = r[i] - alpha * ap[i];
+        r[i] = ri;
+        if (owned[i]) s += ri * ri;
+    }
+    cg_block_sum(s, part + blockIdx.x);
+}
+__global__ void cg_update_p(double* p, const double* r, long long n, const double* rr_new, const double* rr_old) {
+    const double beta = *rr_new / *rr_old;
+    CG_LOOP(i, n) p[i] = r[i] + beta * p[i];
+}
+
 // What one rank publishes: IPC handles of its flags, receive buffer and input buffers, plus raw
 // pointers for peers in the same process.
 struct Export {
@@ -254,6 +332,9 @@ struct femgpu_halo {
     const double** d_peer_x = nullptr;
     std::vector<void*> opened;  // IPC-opened peer allocations
     bool imported = false;
+    long long red_epoch = 0;    // device all-reduces issued (identical sequence on every rank)
+    unsigned char* d_owned = nullptr;  // rows this rank owns (not pushed elsewhere)
+    std::vector<double*> cg_work;      // r, p, ap, partials + scalars
 
     ~femgpu_halo() {
         cudaSetDevice(device);
@@ -474,7 +555,11 @@ femgpu_status femgpu_halo_create(femgpu_instance* inst, int32_t rank, int32_t wo
         // load the exchange kernels now (lazy module loading would otherwise load them at the first
         // launch, which may wait for the device while a peer spins on this rank)
         for (const void* k : {reinterpret_cast<const void*>(pull_kernel), reinterpret_cast<const void*>(push_kernel),
-                              reinterpret_cast<const void*>(recv_kernel), reinterpret_cast<const void*>(bump_step_kernel)}) {
+                              reinterpret_cast<const void*>(recv_kernel), reinterpret_cast<const void*>(bump_step_kernel),
+                              reinterpret_cast<const void*>(allreduce_kernel), reinterpret_cast<const void*>(cg_mask_dot),
+                              reinterpret_cast<const void*>(cg_final), reinterpret_cast<const void*>(cg_init),
+                              reinterpret_cast<const void*>(cg_mask), reinterpret_cast<const void*>(cg_update_xr),
+                              reinterpret_cast<const void*>(cg_update_p)}) {
             cudaFuncAttributes fa{};
             FG_CUDA(cudaFuncGetAttributes(&fa, k));
         }
@@ -569,6 +654,17 @@ femgpu_status femgpu_halo_import(femgpu_halo* h, const void* all, size_t stride)
             for (size_t i = 0; i < h->push_row.size(); ++i)
                 if (h->push_peer[i] == q) push_off[i] = e.recv_off[me] + h->push_local_idx[i];
         }
+        // device CG buffers (femgpu_halo_cg) allocated here, while every rank is in this collective:
+        // a cudaMalloc later could wait on the device behind a peer's spinning exchange kernel
+        {
+            femgpu::Instance& I = *h->inst;
+            const long long n = I.output_size;
+            std::vector<unsigned char> owned(static_cast<size_t>(n), 1);
+            for (int r : h->push_row) owned[static_cast<size_t>(r)] = 0;
+            h->d_owned = dev_copy(owned, h->keep);
+            for (int k = 0; k < 3; ++k) h->cg_work.push_back(I.alloc<double>(static_cast<size_t>(n)));
+            h->cg_work.push_back(I.alloc<double>(kCgBlocks + 8));
+        }
         h->d_peer_flags = dev_copy(pflags, h->keep);
         h->d_peer_recv = dev_copy(precv, h->keep);
         h->d_peer_x = dev_copy(px, h->keep);
@@ -632,6 +728,74 @@ femgpu_status femgpu_halo_time_steps(femgpu_halo* h, const femgpu_schedule* s, i
     });
 }
 
+femgpu_status femgpu_halo_cg(femgpu_halo* h, const femgpu_schedule* s, const double* b_dev, double* x_dev, double rtol,
+                             int32_t maxiter, int32_t check_every, int32_t* iterations, double* rel_residual) {
+    return femgpu::abi_guard([&] {
+        if (!h || !h->imported) femgpu::invalid("halo: not imported");
+        if (!b_dev || !x_dev) femgpu::invalid("halo_cg: null vector");
+        femgpu::Instance& I = *h->inst;
+        std::lock_guard<std::mutex> lk(I.mu);
+        FG_CUDA(cudaSetDevice(I.device));
+        if (I.sspaces.size() != 1 || !I.vspaces.empty() || I.sspaces[0].global != I.output_size)
+            femgpu::invalid("halo_cg: one scalar trial space numbered like the test space required");
+        const femgpu::KernelPlan kp = femgpu::plan_for(I, s);
+        const long long n = I.output_size;
+        cudaStream_t st = I.stream;
+        if (check_every < 1) check_every = 1;
+        double *r = h->cg_work[0], *p = h->cg_work[1], *ap = h->cg_work[2], *part = h->cg_work[3];
+        double* sc = part + kCgBlocks;  // [0] local, [1] b.b, [2] p.Ap, [3]/[4] r.r alternating
+        double* xin = I.sspaces[0].d_x;  // the instance input the exchange pulls from and into
+        const dim3 g(kCgBlocks), t(kCgThreads);
+        auto allreduce = [&](const double* in, double* out) {
+            allreduce_kernel<<<1, 1, 0, st>>>(h->d_peer_flags, h->flags, h->rank, h->world, in, out, ++h->red_epoch,
+                                              h->timeout_ns);
+            FG_CUDA(cudaGetLastError());
+        };
+        auto apply = [&](const double* v, double* out) {  // out = A v (owned rows), ghost rows zero
+            FG_CUDA(cudaMemcpyAsync(xin, v, sizeof(double) * static_cast<size_t>(n), cudaMemcpyDeviceToDevice, st));
+            halo_step(*h, kp, out, st);
+            cg_mask<<<g, t, 0, st>>>(out, h->d_owned, n);
+        };
+        apply(x_dev, ap);
+        cg_init<<<g, t, 0, st>>>(r, p, b_dev, ap, h->d_owned, n);
+        cg_mask_dot<<<g, t, 0, st>>>(b_dev, b_dev, h->d_owned, n, part);
+        cg_final<<<1, t, 0, st>>>(part, sc);
+        allreduce(sc, sc + 1);
+        cg_mask_dot<<<g, t, 0, st>>>(r, r, h->d_owned, n, part);
+        cg_final<<<1, t, 0, st>>>(part, sc);
+        allreduce(sc, sc + 3);
+        double host[5];
+        FG_CUDA(cudaMemcpyAsync(host, sc, sizeof host, cudaMemcpyDeviceToHost, st));
+        FG_CUDA(cudaStreamSynchronize(st));  // this rank's stream only: peers' kernels may still spin
+        const double bnorm = std::sqrt(host[1]);
+        double res = std::sqrt(host[3]);
+        int it = 0, cur = 3;
+        while (res > rtol * bnorm && it < maxiter) {
+            apply(p, ap);
+            cg_mask_dot<<<g, t, 0, st>>>(p, ap, h->d_owned, n, part);
+            cg_final<<<1, t, 0, st>>>(part, sc);
+            allreduce(sc, sc + 2);
+            cg_update_xr<<<g, t, 0, st>>>(x_dev, r, p, ap, h->d_owned, n, sc + cur, sc + 2, part);
+            cg_final<<<1, t, 0, st>>>(part, sc);
+            allreduce(sc, sc + (7 - cur));
+            cg_update_p<<<g, t, 0, st>>>(p, r, n, sc + (7 - cur), sc + cur);
+            FG_CUDA(cudaGetLastError());
+            cur = 7 - cur;
+            ++it;
+            if (it % check_every == 0 || it == maxiter) {
+                long long err = 0;
+                FG_CUDA(cudaMemcpyAsync(host, sc + cur, sizeof(double), cudaMemcpyDeviceToHost, st));
+                FG_CUDA(cudaMemcpyAsync(&err, h->flags + 2, sizeof err, cudaMemcpyDeviceToHost, st));
+                FG_CUDA(cudaStreamSynchronize(st));
+                res = std::sqrt(host[0]);
+                if (err || !std::isfinite(res)) break;  // a timed-out exchange: femgpu_halo_check reports it
+            }
+        }
+        if (iterations) *iterations = it;
+        if (rel_residual) *rel_residual = bnorm > 0 ? res / bnorm : res;
+    });
+}
+
 femgpu_status femgpu_halo_check(femgpu_halo* h, void* stream) {
     return femgpu::abi_guard([&] {
         if (!h) femgpu::invalid("halo: null handle");
@@ -642,7 +806,7 @@ femgpu_status femgpu_halo_check(femgpu_halo* h, void* stream) {
         FG_CUDA(cudaMemcpyAsync(err, h->flags + 2, sizeof err, cudaMemcpyDeviceToHost, s));
         FG_CUDA(cudaStreamSynchronize(s));
         if (err[0]) {
-            const char* what = (err[0] & 1) ? "pull" : (err[0] & 2) ? "push" : "receive";
+            const char* what = (err[0] & 1) ? "pull" : (err[0] & 2) ? "push" : (err[0] & 4) ? "receive" : "all-reduce";
             femgpu::fail(FEMGPU_E_CUDA, std::string("halo: a peer did not reach the exchange in time (rank ") +
                                             std::to_string(h->rank) + ", step " + std::to_string(h->step) + ": " + what +
                                             " wait on rank " + std::to_string(err[1]) + " saw " + std::to_string(err[2]) +

@@ -444,6 +444,23 @@ class DistInstance:
         from ._native import lib
         fa._call(lib().femgpu_halo_check(self.halo, C.c_void_p(stream)))
 
+    def cg(self, b, x0=None, rtol: float = 1e-10, maxiter: int = 1000, check_every: int = 10, params=None):
+        """Distributed CG on the devices (femgpu_halo_cg): dots over owned rows all-reduced GPU to GPU.
+        b, x0: float64 CUDA tensors in the local test numbering.  Returns (x, iterations, rel residual)."""
+        import torch
+
+        from . import action as fa
+        from ._native import lib
+        x = torch.zeros_like(b) if x0 is None else x0.clone()
+        torch.cuda.current_stream().synchronize()  # b and x are written before the instance stream reads them
+        it, rel = C.c_int32(), C.c_double()
+        # the ranks' common schedule: an automatic-schedule pass here would load modules (which may
+        # wait for the device) while a peer already spins on this rank
+        sp = fa._sched(params if params is not None else self.params)
+        fa._call(lib().femgpu_halo_cg(self.halo, sp[0] if sp else None, C.c_void_p(b.data_ptr()),
+                                      C.c_void_p(x.data_ptr()), rtol, maxiter, check_every, C.byref(it), C.byref(rel)))
+        return x, it.value, rel.value
+
     def owned_output(self) -> Tuple[np.ndarray, np.ndarray]:
         """(global rows, values) of the rows this rank owns (complete after an action)."""
         y = self.inst.read_output()

@@ -170,6 +170,40 @@ def test_distributed_device_cg(oracle):
     assert np.linalg.norm(oracle.reference_action(p) - b) <= 1e-8 * np.linalg.norm(b)
 
 
+@pytest.mark.parametrize("world", [2, 3])
+def test_native_distributed_cg_with_device_allreduce(oracle, world):
+    """femgpu_halo_cg: the whole distributed CG on the devices, dots all-reduced GPU to GPU through the
+    peers' flag words; the assembled solution satisfies the global A x = b."""
+    import torch
+    args = ("helmholtz", 3, 2, 14, 4)
+
+    def rank(r, gather):
+        slab = fdist.rank_slab(args, r, world)
+        tab = slab.local.tabulations
+        tab.psi = np.ascontiguousarray(np.transpose(tab.scalar_phi[0], (0, 2, 1)))
+        plan = fdist.build_plan(slab, r, world, gather)
+        di = fdist.DistInstance(plan, gather)
+        try:
+            b = 0.5 + 1e-3 * (plan.test_global % 89)
+            b_loc = torch.from_numpy(b * plan.owned_mask).cuda()
+            x, it, rel = di.cg(b_loc, rtol=1e-10, maxiter=800, check_every=5)
+            di.check()
+            return plan.test_global[plan.owned_mask], x.cpu().numpy()[plan.owned_mask], it, rel
+        finally:
+            di.close()
+
+    res = run_ranks(world, rank)
+    assert len({r[2] for r in res}) == 1  # every rank ran the same iterations (same all-reduced scalars)
+    p = fg.symmetric_problem(*args)
+    x = np.full(p.output_size, np.nan)
+    for g, v, _, _ in res:
+        x[g] = v
+    assert not np.isnan(x).any()
+    b = 0.5 + 1e-3 * (np.arange(p.output_size) % 89)
+    p.scalar_inputs[0] = x
+    assert np.linalg.norm(oracle.reference_action(p) - b) <= 1e-8 * np.linalg.norm(b)
+
+
 @pytest.mark.parametrize("config,n", [("C2", 12), ("C4", 8)])
 def test_bench_launches_its_own_ranks_ipc_path(config, n):
     """bench.py --gpus 2 without torchrun launches its two ranks itself; they share cuda:0 through
