@@ -23,6 +23,8 @@ memset where that measures faster -- the automatic schedule decides per instance
           step time, roofline fraction, parity against the reference CPU path.
   fused   operator pairs sharing their trial function (fuse.py): the fused action's step against
           the two separate actions' steps, parity of both parts against the reference.
+  caller  femgpu_cg on C2's mesh (symmetric Helmholtz): time per CG iteration against the action's
+          step, iterations to a 1e-10 relative residual.
 
 --impl reference: the reference's CPU implementation of the path (oracle/_ref) on all host
 threads, same config/metric, each step a bounded cell sample of the same mesh (built by
@@ -68,6 +70,8 @@ def parse():
                     help="seconds of reference CPU work per forms row (full action if it fits, else complete rows)")
     ap.add_argument("--no-fused", dest="fused", action="store_false",
                     help="skip the fused multi-operator rows (fuse.py, PAPER.md:2477-2482)")
+    ap.add_argument("--no-caller", dest="caller", action="store_false",
+                    help="skip the caller row (femgpu_cg per iteration on C2's mesh)")
     return ap.parse_args()
 
 
@@ -503,8 +507,37 @@ def run_single(args):
                 out["fused"].append(fused_row(name, args.ref_budget))
             except Exception as e:  # noqa: BLE001
                 out["fused"].append({"pair": name, "error": str(e)[:300]})
+    if args.caller and args.n is None:
+        try:
+            out["caller"] = caller_row()
+        except Exception as e:  # noqa: BLE001
+            out["caller"] = {"error": str(e)[:300]}
     out["wall_s"] = round(time.perf_counter() - wall0, 1)
     print(json.dumps(out))
+
+
+def caller_row(iters=100):
+    """The action's caller: femgpu_cg on C2's mesh with a symmetric Helmholtz operator,
+    time per CG iteration against the action's own pipelined step, and the relative residual reached."""
+    import torch
+
+    import paper_2506_17471_b200 as fg
+    from paper_2506_17471_b200.mesh import CONFIGS
+    c = CONFIGS["C2"]
+    p = fg.symmetric_problem("helmholtz", c["dim"], c["degree"], c["Q"], c["n"])
+    b = torch.from_numpy(np.random.default_rng(5).uniform(0.5, 1.5, p.output_size)).cuda()
+    with fg.GpuInstance(p) as g:
+        g.action()
+        step = g.time_steps(20, pipelined=True) / 20
+        fg.krylov.native_cg(g, b, rtol=0.0, maxiter=4, check_every=4)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _, it, _ = fg.krylov.native_cg(g, b, rtol=0.0, maxiter=iters, check_every=iters)
+        t_it = (time.perf_counter() - t0) / it
+        _, it_conv, rel = fg.krylov.native_cg(g, b, rtol=1e-10, maxiter=2000, check_every=10)
+    return {"api": "femgpu_cg (csrc/cg.cu)", "problem": "C2 mesh, P2 Helmholtz with Psi = Phi^T (symmetric)",
+            "dofs": int(p.output_size), "us_per_iteration": t_it * 1e6, "action_step_us": step * 1e6,
+            "iterations_to_1e-10": it_conv, "rel_residual": rel}
 
 
 FUSED_ORDER = ["laplace+mass-P2", "stokes-P2"]
