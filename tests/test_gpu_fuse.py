@@ -103,3 +103,28 @@ def test_fused_operator_picks_the_faster_mode_and_matches_the_reference(oracle, 
         rows = complete_rows(p, m)
         ref = oracle.reference_action(p, cell_range=(0, m))
         assert rel_l2(y[rows], ref[rows]) <= 1e-12
+
+
+def test_fused_three_operators_with_a_repeated_one(oracle):
+    a, b = fg.fused_pair("laplace+mass-P2", n=5)
+    f, offs = fg.fuse_problems([a, b, a])
+    ys = fg.split_output(fg.gpu_action(f), offs)
+    for y, p in zip(ys, (a, b, a)):
+        ref = oracle.reference_action(p)
+        assert rel_l2(y, ref) <= 1e-12 and max_rel(y, ref) <= 1e-10
+
+
+@pytest.mark.parametrize("sched", ["auto", "dmma", "scpt"])
+def test_fused_advection_and_mass_share_the_scalar_field(oracle, sched):
+    """Advection (a P1 velocity coefficient + the P2 scalar) fused with the mass operator of the same
+    P2 field: the scalar space merges (value + gradient terms), the velocity space stays its own."""
+    a = fg.mesh_problem("advection", 3, 2, 14, 3)
+    b = fg.mesh_problem("mass", 3, 2, 14, 3, seed=13)
+    b.tabulations.weights = a.tabulations.weights.copy()
+    b.scalar_inputs = [a.scalar_inputs[0].copy()]
+    f, offs = fg.fuse_problems([a, b])
+    assert len(f.signature.scalar_spaces) == 1 and len(f.signature.vector_spaces) == 1
+    ys = fg.split_output(fg.gpu_action(f, SCHEDULES[sched]), offs)
+    for y, p in zip(ys, (a, b)):
+        ref = oracle.reference_action(p)
+        assert rel_l2(y, ref) <= 1e-12 and max_rel(y, ref) <= 1e-10
