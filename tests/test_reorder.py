@@ -65,3 +65,18 @@ def test_non_affine_problem_reorders_by_node_index(oracle):
     q, perms = fg.reorder_problem(p)
     y = fg.output_to_original(oracle.reference_action(q), perms)
     assert rel_l2(y, oracle.reference_action(p)) <= 1e-14
+
+
+def test_c_abi_accepts_null_permutation_outputs():
+    """femgpu_problem_reorder's permutation outputs are optional (C callers that only want the
+    renumbered problem)."""
+    import ctypes as C
+    from paper_2506_17471_b200 import abi
+    from paper_2506_17471_b200._native import lib
+    p = shuffled("C2", 3)
+    cp = p.to_c()
+    h = C.c_void_p()
+    view = C.POINTER(abi.Problem)()
+    assert lib().femgpu_problem_reorder(C.byref(cp.desc), C.byref(h), C.byref(view), None, None, None, None) == 0
+    assert view.contents.cell_count == p.connectivity.cell_count
+    lib().femgpu_problem_free(h)
