@@ -122,3 +122,17 @@ def test_fuse_merges_one_of_two_scalar_spaces(oracle):
     assert f.signature.scalar_spaces[0].deriv_terms == a.signature.scalar_spaces[0].deriv_terms
     fa, fb = fg.split_output(oracle.reference_action(f), offs)
     assert np.array_equal(fa, oracle.reference_action(a)) and np.array_equal(fb, oracle.reference_action(b))
+
+
+def test_c_abi_accepts_null_offsets():
+    import ctypes as C
+    from paper_2506_17471_b200 import abi
+    from paper_2506_17471_b200._native import lib
+    a, b = fg.fused_pair("laplace+mass-P2", n=2)
+    cps = [a.to_c(), b.to_c()]
+    arr = (C.POINTER(abi.Problem) * 2)(*[C.pointer(cp.desc) for cp in cps])
+    h = C.c_void_p()
+    view = C.POINTER(abi.Problem)()
+    assert lib().femgpu_problem_fuse(arr, 2, C.byref(h), C.byref(view), None) == 0
+    assert view.contents.output_size == a.output_size + b.output_size
+    lib().femgpu_problem_free(h)

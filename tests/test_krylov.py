@@ -128,3 +128,12 @@ def test_distributed_cg_matches_single_process(tmp_path, oracle, world):
     p.scalar_inputs[0] = x
     res = oracle.reference_action(p) - b
     assert np.linalg.norm(res) <= 1e-9 * np.linalg.norm(b)
+
+
+@pytest.mark.gpu
+def test_native_cg_rejects_non_square_operators():
+    p = fg.mesh_problem("helmholtz_coef", 2, 3, 12, 4)  # two scalar spaces: not a square scalar operator
+    b = torch.ones(p.output_size, dtype=torch.float64, device="cuda")
+    with fg.GpuInstance(p) as g:
+        with pytest.raises(ValueError, match="cg:"):
+            fg.krylov.native_cg(g, b)
