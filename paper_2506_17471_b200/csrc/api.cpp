@@ -251,8 +251,8 @@ femgpu_status femgpu_set_inputs(femgpu_instance* h, const double* const* scalar_
     return guard([&] {
         auto& I = get(h);
         std::lock_guard<std::mutex> lk(I.mu);
-        async_drain(I);  // streaming steps complete first
         FG_CUDA(cudaSetDevice(I.device));
+        async_drain(I);  // streaming steps complete first
         copy_inputs(I, scalar_inputs, vector_inputs, I.stream);
         FG_CUDA(cudaStreamSynchronize(I.stream));
     });
@@ -263,8 +263,8 @@ femgpu_status femgpu_action(femgpu_instance* h, const femgpu_schedule* s, double
         auto& I = get(h);
         if (!y_host) femgpu::invalid("null output buffer");
         std::lock_guard<std::mutex> lk(I.mu);
-        async_drain(I);  // streaming steps complete first
         FG_CUDA(cudaSetDevice(I.device));
+        async_drain(I);  // streaming steps complete first
         const femgpu::KernelPlan kp = femgpu::plan_for(I, s);
         femgpu::run_action(I, kp, I.d_y, I.stream);
         FG_CUDA(cudaMemcpyAsync(y_host, I.d_y, sizeof(double) * static_cast<size_t>(I.output_size),
@@ -279,8 +279,8 @@ femgpu_status femgpu_action_host(femgpu_instance* h, const femgpu_schedule* s, c
         auto& I = get(h);
         if (!y_host) femgpu::invalid("null output buffer");
         std::lock_guard<std::mutex> lk(I.mu);
-        async_drain(I);  // streaming steps complete first
         FG_CUDA(cudaSetDevice(I.device));
+        async_drain(I);  // streaming steps complete first
         const femgpu::KernelPlan kp = femgpu::plan_for(I, s);
         // overlapped H2D / slabs / D2H when the instance has locality (pipeline.cpp), else sequential
         if (!femgpu::pipelined_host_action(I, kp, scalar_inputs, vector_inputs, y_host)) {
@@ -345,8 +345,8 @@ femgpu_status femgpu_cg(femgpu_instance* h, const femgpu_schedule* s, const doub
         auto& I = get(h);
         if (!b_dev || !x_dev) femgpu::invalid("cg: null vector");
         std::lock_guard<std::mutex> lk(I.mu);
-        async_drain(I);  // streaming steps complete first
         FG_CUDA(cudaSetDevice(I.device));
+        async_drain(I);  // streaming steps complete first
         const femgpu::KernelPlan kp = femgpu::plan_for(I, s);
         int it = 0;
         femgpu::device_cg(I, kp, b_dev, x_dev, rtol, maxiter, check_every, &it, rel_residual);
@@ -358,8 +358,8 @@ femgpu_status femgpu_action_device(femgpu_instance* h, const femgpu_schedule* s,
     return guard([&] {
         auto& I = get(h);
         std::lock_guard<std::mutex> lk(I.mu);
-        async_drain(I);  // streaming steps complete first
         FG_CUDA(cudaSetDevice(I.device));
+        async_drain(I);  // streaming steps complete first
         const femgpu::KernelPlan kp = femgpu::plan_for(I, s);
         femgpu::run_action(I, kp, y_dev ? y_dev : I.d_y, stream ? static_cast<cudaStream_t>(stream) : I.stream);
     });
@@ -372,8 +372,8 @@ femgpu_status femgpu_action_device_pipelined(femgpu_instance* h, const femgpu_sc
         if (!y_dev) femgpu::invalid("action_device_pipelined: null output buffer");
         if (y_next_dev == y_dev) femgpu::invalid("action_device_pipelined: y_next must not alias y");
         std::lock_guard<std::mutex> lk(I.mu);
-        async_drain(I);  // streaming steps complete first
         FG_CUDA(cudaSetDevice(I.device));
+        async_drain(I);  // streaming steps complete first
         const femgpu::KernelPlan kp = femgpu::plan_for(I, s);
         femgpu::run_action_pipelined(I, kp, y_dev, y_next_dev, stream ? static_cast<cudaStream_t>(stream) : I.stream);
     });
@@ -383,8 +383,8 @@ femgpu_status femgpu_check_finite(femgpu_instance* h, const femgpu_schedule* s, 
     return guard([&] {
         auto& I = get(h);
         std::lock_guard<std::mutex> lk(I.mu);
-        async_drain(I);  // streaming steps complete first
         FG_CUDA(cudaSetDevice(I.device));
+        async_drain(I);  // streaming steps complete first
         const femgpu::KernelPlan kp = femgpu::plan_for(I, s);
         femgpu::check_failure(I, kp, stream ? static_cast<cudaStream_t>(stream) : I.stream);
     });
@@ -396,8 +396,8 @@ femgpu_status femgpu_time_action(femgpu_instance* h, const femgpu_schedule* s, i
         auto& I = get(h);
         if (!seconds) femgpu::invalid("null output");
         std::lock_guard<std::mutex> lk(I.mu);
-        async_drain(I);  // streaming steps complete first
         FG_CUDA(cudaSetDevice(I.device));
+        async_drain(I);  // streaming steps complete first
         const femgpu::KernelPlan kp = femgpu::plan_for(I, s);
         for (int i = 0; i < warmup; ++i) femgpu::run_action(I, kp, I.d_y, I.stream);
         femgpu::check_failure(I, kp, I.stream);
@@ -430,8 +430,8 @@ femgpu_status femgpu_time_steps_ex(femgpu_instance* h, const femgpu_schedule* s,
         auto& I = get(h);
         if (steps < 1 || !seconds) femgpu::invalid("time_steps: steps >= 1 and an output are required");
         std::lock_guard<std::mutex> lk(I.mu);
-        async_drain(I);  // streaming steps complete first
         FG_CUDA(cudaSetDevice(I.device));
+        async_drain(I);  // streaming steps complete first
         const femgpu::KernelPlan kp = femgpu::plan_for(I, s);
         const bool piped = (flags & FEMGPU_STEPS_PIPELINED) != 0;
         double* ybuf[2] = {I.d_y, piped ? I.second_output() : I.d_y};
@@ -467,8 +467,8 @@ femgpu_status femgpu_profile_action(femgpu_instance* h, const femgpu_schedule* s
         auto& I = get(h);
         if (reps < 1) femgpu::invalid("profile: reps must be >= 1");
         std::lock_guard<std::mutex> lk(I.mu);
-        async_drain(I);  // streaming steps complete first
         FG_CUDA(cudaSetDevice(I.device));
+        async_drain(I);  // streaming steps complete first
         const femgpu::KernelPlan kp = femgpu::plan_for(I, s);
         for (int i = 0; i < warmup; ++i) femgpu::run_action(I, kp, I.d_y, I.stream);
         femgpu::check_failure(I, kp, I.stream);
@@ -559,8 +559,8 @@ femgpu_status femgpu_trace_counters(femgpu_instance* h, const femgpu_schedule* s
         auto& I = get(h);
         if (!out || n < FEMGPU_TRACE_COUNTERS) femgpu::invalid("trace_counters: need FEMGPU_TRACE_COUNTERS outputs");
         std::lock_guard<std::mutex> lk(I.mu);
-        async_drain(I);  // streaming steps complete first
         FG_CUDA(cudaSetDevice(I.device));
+        async_drain(I);  // streaming steps complete first
         const femgpu::KernelPlan kp = femgpu::plan_for(I, s);
         auto mod = I.module_for(kp);
         const femgpu::Signature& sig = I.sig;
@@ -605,8 +605,8 @@ femgpu_status femgpu_read_output(femgpu_instance* h, double* y_host) {
         auto& I = get(h);
         if (!y_host) femgpu::invalid("null output buffer");
         std::lock_guard<std::mutex> lk(I.mu);
-        async_drain(I);  // streaming steps complete first
         FG_CUDA(cudaSetDevice(I.device));
+        async_drain(I);  // streaming steps complete first
         FG_CUDA(cudaMemcpyAsync(y_host, I.d_y, sizeof(double) * static_cast<size_t>(I.output_size),
                                 cudaMemcpyDeviceToHost, I.stream));
         FG_CUDA(cudaStreamSynchronize(I.stream));
@@ -614,7 +614,14 @@ femgpu_status femgpu_read_output(femgpu_instance* h, double* y_host) {
 }
 
 femgpu_status femgpu_device_output(femgpu_instance* h, double** y_dev) {
-    return guard([&] { *y_dev = get(h).d_y; });
+    return guard([&] {
+        auto& I = get(h);
+        if (!y_dev) femgpu::invalid("device_output: null output pointer");
+        std::lock_guard<std::mutex> lk(I.mu);
+        FG_CUDA(cudaSetDevice(I.device));
+        async_drain(I);  // streaming steps complete first: d_y then holds the last step's output
+        *y_dev = I.d_y;
+    });
 }
 
 femgpu_status femgpu_device_input(femgpu_instance* h, int32_t space, double** x_dev) {
@@ -622,6 +629,9 @@ femgpu_status femgpu_device_input(femgpu_instance* h, int32_t space, double** x_
         auto& I = get(h);
         const int ns = static_cast<int>(I.sspaces.size()), nv = static_cast<int>(I.vspaces.size());
         if (!x_dev || space < 0 || space >= ns + nv) femgpu::invalid("device_input: space out of range");
+        std::lock_guard<std::mutex> lk(I.mu);
+        FG_CUDA(cudaSetDevice(I.device));
+        async_drain(I);  // streaming steps complete first: the caller may write the buffer next
         *x_dev = space < ns ? I.sspaces[space].d_x : I.vspaces[space - ns].d_x;
     });
 }

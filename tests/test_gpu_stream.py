@@ -85,3 +85,35 @@ def test_streaming_non_finite_is_reported_by_the_wait():
             assert np.all(np.isfinite(g.action()))
     finally:
         pin.free()
+
+
+def test_other_calls_complete_pending_steps_first():
+    """A synchronous action, a schedule change and set_inputs each drain the pending steps; after an
+    even number of steps (the last one in buffer set 1) the instance holds that step's inputs."""
+    p = fg.config_problem("C2", n=60)
+    pin = Pinned()
+    try:
+        xs = [[pin.like(x * (1.0 + 0.25 * k)) for x in p.scalar_inputs] for k in range(4)]
+        ys = [pin.like(np.zeros(p.output_size)) for _ in range(4)]
+        with fg.GpuInstance(p) as g:
+            want = []
+            for k in range(4):
+                g.set_inputs([np.array(x) for x in xs[k]], [])
+                want.append(g.action())
+            g.action_host_async(xs[0], [], ys[0])
+            g.action_host_async(xs[1], [], ys[1])
+            y_sync = g.action()  # drains: the instance now holds step 1's inputs (set 1 copied back)
+            assert rel_l2(y_sync, want[1]) <= 1e-12
+            g.action_host_async(xs[2], [], ys[2])
+            g.action_host_async(xs[3], [], ys[3], params=fg.TilingParams.scpt())  # another schedule: drains first
+            g.action_host_wait()
+            for k in range(4):
+                y = np.array(ys[k])
+                assert rel_l2(y, want[k]) <= 1e-12 and max_rel(y, want[k]) <= 1e-10, k
+            assert rel_l2(g.read_output(), want[3]) <= 1e-12
+            g.action_host_async(xs[0], [], ys[0])
+            g.set_inputs([np.array(x) for x in xs[2]], [])  # drains, then replaces the inputs
+            assert rel_l2(np.array(ys[0]), want[0]) <= 1e-12
+            assert rel_l2(g.action(), want[2]) <= 1e-12
+    finally:
+        pin.free()
