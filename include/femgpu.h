@@ -173,6 +173,9 @@ typedef struct femgpu_schedule {
 #define FEMGPU_FLAG_PIPE_MEMSET 4 /* femgpu_action_device_pipelined zeroes the next output with a separate
                                      memset instead of inside the action kernel (the automatic schedule
                                      sets it where the in-kernel zeroing measures slower) */
+#define FEMGPU_FLAG_INDEX_LOADS 8 /* macro kernels load every unique index of a cell group even when the
+                                     mesh numbering makes them one base plus fixed offsets (the
+                                     automatic schedule sets it where the offset form measures slower) */
 
 typedef struct femgpu_instance femgpu_instance;
 

@@ -20,7 +20,7 @@ OP_CONSTANT, OP_SCALAR_DERIV, OP_VECTOR_DERIV, OP_JACOBIAN, OP_DETERMINANT, OP_W
 SCPT, MLT, DMMA = 0, 1, 2
 BASIS_AUTO, BASIS_CONST, BASIS_SMEM = 0, 1, 2
 SCATTER_AUTO, SCATTER_ATOMIC, SCATTER_TILE, SCATTER_MACRO, SCATTER_COLOR = 0, 1, 2, 3, 4
-FLAG_STRICT, FLAG_FUSED_ZERO = 1, 2  # femgpu_schedule.reserved[0] flags (femgpu.h)
+FLAG_STRICT, FLAG_FUSED_ZERO, FLAG_PIPE_MEMSET, FLAG_INDEX_LOADS = 1, 2, 4, 8  # femgpu_schedule.reserved[0] flags (femgpu.h)
 MAX_SPACES = 8
 
 _dp = C.POINTER(C.c_double)

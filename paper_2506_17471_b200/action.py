@@ -51,6 +51,8 @@ class TilingParams:
     qmopt: int = 0  # macro q-major: bit 0 hoisted map nodes read back from smem, bit 1 scatter indices reloaded
     fused_zero: bool = False  # y zeroing fused into slab launches (FEMGPU_FLAG_FUSED_ZERO)
     zero_slabs: int = 0  # slabs for fused zeroing (0 = default 8)
+    pipe_memset: bool = False  # pipelined actions zero the next output by a memset (FEMGPU_FLAG_PIPE_MEMSET)
+    index_loads: bool = False  # macro: load every unique index, no affine offsets (FEMGPU_FLAG_INDEX_LOADS)
 
     @staticmethod
     def scpt(**knobs) -> "TilingParams":
@@ -96,7 +98,8 @@ class TilingParams:
         s.basis, s.scatter, s.block_cells = self.basis, self.scatter, self.block_cells
         s.group_cells = self.group_cells
         s.reserved[0] = ((abi.FLAG_STRICT if self.strict else 0) | (abi.FLAG_FUSED_ZERO if self.fused_zero else 0)
-                         | (self.zero_slabs & 0xff) << 8)
+                         | (abi.FLAG_PIPE_MEMSET if self.pipe_memset else 0)
+                         | (abi.FLAG_INDEX_LOADS if self.index_loads else 0) | (self.zero_slabs & 0xff) << 8)
         s.reserved[1] = self.reg_target
         s.reserved[2] = self.min_blocks
         s.reserved[3] = (self.stage_smem & 0xff) | (self.split & 0xff) << 8 | (self.qmopt & 0xffff) << 16
@@ -114,7 +117,9 @@ class TilingParams:
                             min_blocks=s.reserved[2], stage_smem=s.reserved[3] & 0xff, split=(s.reserved[3] >> 8) & 0xff,
                             qmopt=(s.reserved[3] >> 16) & 0xffff,
                             fused_zero=bool(s.reserved[0] & abi.FLAG_FUSED_ZERO),
-                            zero_slabs=(s.reserved[0] >> 8) & 0xff)
+                            zero_slabs=(s.reserved[0] >> 8) & 0xff,
+                            pipe_memset=bool(s.reserved[0] & abi.FLAG_PIPE_MEMSET),
+                            index_loads=bool(s.reserved[0] & abi.FLAG_INDEX_LOADS))
 
     def describe(self) -> str:  # search.hpp:301-310
         if self.kind == abi.SCPT:

@@ -537,6 +537,10 @@ std::string KernelPlan::key() const {
         for (long long v : t) h = (h ^ static_cast<uint64_t>(v + 13)) * 0x100000001b3ULL;
     for (const auto& t : salias)
         for (long long v : t) h = (h ^ static_cast<uint64_t>(v + 17)) * 0x100000001b3ULL;
+    for (const auto& a : maff) {
+        h = (h ^ 0x5bd1e995ULL) * 0x100000001b3ULL;
+        for (int v : a) h = (h ^ static_cast<uint64_t>(v + 19)) * 0x100000001b3ULL;
+    }
     s << "P" << h;
     return s.str();
 }
@@ -994,6 +998,25 @@ void emit_tile_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const 
 // Gathers each unique node of the group once, computes the G cells in order with the
 // per-cell operation order of the reference, accumulates y per unique node in registers
 // (cells ascending), and issues one red.global.add.f64 per unique test DOF.
+// Affine index pattern of a map group (MacroLayout::aoff): one index load per cell group, the
+// unique nodes at compile-time offsets from it (address arithmetic folds into the loads' immediates).
+bool macro_affine(const KernelPlan& kp, int g) {
+    return g >= 0 && static_cast<size_t>(g) < kp.maff.size() && !kp.maff[g].empty();
+}
+
+void emit_macro_bases(Out& o, const KernelPlan& kp, const std::set<int>& gathered) {
+    std::set<int> gs = gathered;
+    gs.insert(kp.tgroup);
+    for (int g : gs)
+        if (macro_affine(kp, g)) o.line("const int igb" + S(g) + " = __ldg(&P.gidx" + S(g) + "[grp]);");
+}
+
+std::string macro_index(const KernelPlan& kp, int g, int u) {
+    if (!macro_affine(kp, g)) return "__ldg(&P.gidx" + S(g) + "[" + S(u) + " * NG + grp])";
+    const int off = kp.maff[g][u];
+    return off ? "(igb" + S(g) + " + " + S(off) + ")" : "igb" + S(g);
+}
+
 void emit_macro_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const MapUse& use, bool unroll_q,
                        const std::string& name, long long smem_tab_off, long long ysmem_off = 0) {
     const int D = sig.dim;
@@ -1027,6 +1050,7 @@ void emit_macro_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const
     for (int i = 0; i < sig.ns(); ++i) gathered.insert(kp.sgroup[i]);
     for (int i = 0; i < sig.nv(); ++i) gathered.insert(kp.vgroup[i]);
     if (sig.affine) gathered.insert(kp.cgroup);
+    emit_macro_bases(o, kp, gathered);
     // streaming order (mstage == 0): a unique node is loaded just before the first cell of the
     // group that reads it, and its y contribution is issued right after the last cell that
     // writes it, so register live ranges follow the cells instead of spanning the group.
@@ -1049,7 +1073,7 @@ void emit_macro_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const
         for (int g : gathered)
             for (int u = 0; u < kp.group_cap[g]; ++u) {
                 if (stream && first_use(g, u) != s_now) continue;
-                o.line("const int ig" + S(g) + "_" + S(u) + " = __ldg(&P.gidx" + S(g) + "[" + S(u) + " * NG + grp]);");
+                o.line("const int ig" + S(g) + "_" + S(u) + " = " + macro_index(kp, g, u) + ";");
                 if (kp.mstage) continue;
                 for (int i = 0; i < sig.ns(); ++i)
                     if (kp.sgroup[i] == g)
@@ -1082,8 +1106,7 @@ void emit_macro_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const
     auto emit_reds = [&](int s_now) {
         for (int u = 0; u < kp.group_cap[gt]; ++u) {
             if (stream && last_use(gt, u) != s_now) continue;
-            std::string idx =
-                gathered.count(gt) ? "ig" + S(gt) + "_" + S(u) : "__ldg(&P.gidx" + S(gt) + "[" + S(u) + " * NG + grp])";
+            std::string idx = gathered.count(gt) ? "ig" + S(gt) + "_" + S(u) : macro_index(kp, gt, u);
             if (!kp.talias.empty() && kp.talias[u][0] >= 0 && !kp.mstage) {  // row = scale * gathered node + add
                 const auto& al = kp.talias[u];
                 idx = "(ig" + S(al[0]) + "_" + S(al[1]) + (al[2] != 1 ? " * " + S(al[2]) : "") + (al[3] ? " + " + S(al[3]) : "") + ")";
@@ -1340,7 +1363,9 @@ void emit_macro_qmajor_kernel(Out& o, const Signature& sig, const KernelPlan& kp
     } else {
         o.line("if (grp >= P.n_cells / " + S(G) + ") return;");
         o.line("const size_t NG = (size_t)P.n_groups;");
+        emit_macro_bases(o, kp, gathered);
     }
+    const bool affine_ok = !staged && !persistent;  // base indices declared (one-shot groups)
     for (int part = 0; part < SPL; ++part) {
         const int c0 = part * G / SPL, c1 = (part + 1) * G / SPL;
         if (SPL > 1) {
@@ -1376,7 +1401,8 @@ void emit_macro_qmajor_kernel(Out& o, const Signature& sig, const KernelPlan& kp
         for (int g : gathered)
             for (int u = 0; u < kp.group_cap[g]; ++u) {
                 if (!used(g, u) || staged) continue;
-                o.line("const int ig" + S(g) + "_" + S(u) + " = __ldg(&P.gidx" + S(g) + "[" + S(u) + " * NG + grp]);");
+                o.line("const int ig" + S(g) + "_" + S(u) + " = " +
+                       (affine_ok ? macro_index(kp, g, u) : "__ldg(&P.gidx" + S(g) + "[" + S(u) + " * NG + grp])") + ";");
                 for (int i = 0; i < sig.ns(); ++i)
                     if (kp.sgroup[i] == g)
                         o.line("const double xg" + S(i) + "_" + S(u) + " = __ldg(&P.x" + S(i) + "[ig" + S(g) + "_" + S(u) + "]);");
@@ -1568,6 +1594,7 @@ void emit_macro_qmajor_kernel(Out& o, const Signature& sig, const KernelPlan& kp
             // the gather's) instead of keeping them live in registers across the quadrature loop
             std::string idx = ((kp.qmopt & 2) || staged) ? "ldidx(&P.gidx" + S(gt) + "[" + S(u) + " * NG + grp])"
                               : gathered.count(gt) ? "ig" + S(gt) + "_" + S(u)
+                              : affine_ok          ? macro_index(kp, gt, u)
                                                    : "__ldg(&P.gidx" + S(gt) + "[" + S(u) + " * NG + grp])";
             if (!kp.talias.empty() && kp.talias[u][0] >= 0) {
                 // the row is an image of a gathered node: scale * node + add (no test-map load)

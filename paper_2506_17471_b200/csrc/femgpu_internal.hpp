@@ -128,6 +128,7 @@ struct KernelPlan {
     bool qloop = false;                   // scpt: keep the quadrature loop rolled (I-cache / registers)
     bool colour = false;                  // scpt: one launch per cell colour, plain y updates (deterministic)
     std::vector<std::vector<int>> mpat;   // per map group: G*entries local indices
+    std::vector<std::vector<int>> maff;   // per map group: MacroLayout::aoff (empty: indices loaded)
     std::string key() const;
 };
 
@@ -212,6 +213,10 @@ struct MacroLayout {
     // per unique node of the test group: (group, unique, scale, add) with row = scale * node + add of
     // another group's unique node (Instance::test_alias), group -1 = loaded from the test group's gidx
     std::vector<std::array<long long, 4>> talias;
+    // per map group: gidx[u][grp] = gidx[0][grp] + aoff[u] for every cell group (a lattice-numbered
+    // structured mesh), so one index load per group and compile-time offsets replace the U loads;
+    // empty = not affine
+    std::vector<std::vector<int>> aoff;
 };
 
 // Greedy colouring of the test map (femgpu_color_cells) with the cells sorted by colour.

@@ -697,6 +697,22 @@ const MacroLayout& Instance::macro_layout(int G) {
                             if (hits[static_cast<size_t>(u) * U + u2] * 2 >= pairs) M->merge.push_back({sft, u, u2});
                 }
             }
+            {  // affine index pattern: every group's unique nodes are group 0's shifted by one base
+                std::vector<int> off(static_cast<size_t>(U));
+                for (int u = 0; u < U; ++u) off[u] = gidx[static_cast<size_t>(u) * ng] - gidx[0];
+                std::atomic<bool> aff{true};
+                parallel_for(ng, [&](long long b, long long e) {
+                    for (long long grp = b; grp < e && aff.load(std::memory_order_relaxed); ++grp) {
+                        const int32_t b0 = gidx[grp];
+                        for (int u = 1; u < U; ++u)
+                            if (gidx[static_cast<size_t>(u) * ng + grp] - b0 != off[u]) {
+                                aff.store(false, std::memory_order_relaxed);
+                                break;
+                            }
+                    }
+                });
+                M->aoff.push_back(aff.load() ? off : std::vector<int>{});
+            }
             int32_t* d = alloc<int32_t>(gidx.size());
             FG_CUDA(cudaMemcpy(d, gidx.data(), gidx.size() * 4, cudaMemcpyHostToDevice));
             M->d_gidx.push_back(d);
@@ -712,6 +728,12 @@ void check_macro_split(KernelPlan& kp) {
     if (kp.msplit < 1 || kp.msplit > kp.G) fail(FEMGPU_E_INFEASIBLE, "macro: split must be in [1, cells per group]");
     if (kp.msplit > 1 && kp.block % (32 * kp.msplit))
         fail(FEMGPU_E_INFEASIBLE, "macro: threads per CTA must be a multiple of 32 x split");
+}
+
+// FEMGPU_MACRO_AFFINE=0: macro kernels load every unique index even when the pattern is affine (A/B)
+bool macro_affine_enabled() {
+    const char* e = std::getenv("FEMGPU_MACRO_AFFINE");
+    return !(e && std::strcmp(e, "0") == 0);
 }
 
 void host_macro_plan(const femgpu_problem* p, const Signature& sig, KernelPlan& kp, const femgpu_schedule* s) {
@@ -743,6 +765,19 @@ void host_macro_plan(const femgpu_problem* p, const Signature& sig, KernelPlan& 
         kp.group_entries.push_back(E);
         kp.group_cap.push_back(static_cast<int>(u0.size()));
         kp.mpat.push_back(pat);
+        // affine index pattern over every cell group (as MacroLayout::aoff)
+        std::vector<int> off(u0.size());
+        for (size_t u = 0; u < u0.size(); ++u) off[u] = u0[u] - u0[0];
+        bool aff = macro_affine_enabled() && !(s->reserved[0] & FEMGPU_FLAG_INDEX_LOADS);
+        std::vector<int32_t> buf;
+        for (long long grp = 1; grp < C / G && aff; ++grp) {
+            buf.assign(maps[g] + grp * G * E, maps[g] + (grp + 1) * G * E);
+            std::sort(buf.begin(), buf.end());
+            buf.erase(std::unique(buf.begin(), buf.end()), buf.end());
+            aff = buf.size() == u0.size();
+            for (size_t u = 0; u < buf.size() && aff; ++u) aff = buf[u] - buf[0] == off[u];
+        }
+        kp.maff.push_back(aff ? off : std::vector<int>{});
     }
     kp.family = Family::Macro;
     kp.G = G;
@@ -811,6 +846,7 @@ int int_dim(int a) { return a; }
 // Resolves a femgpu_schedule (TilingParams + B200 knobs) into a launch plan.
 namespace {
 KernelPlan resolve_schedule_impl(Instance& I, const femgpu_schedule* s);
+
 }
 
 
@@ -940,6 +976,8 @@ KernelPlan resolve_schedule_impl(Instance& I, const femgpu_schedule* s) {
                 kp.group_entries.push_back(static_cast<int>(I.group_maps[g].size() / I.cells));
                 kp.group_cap.push_back(M.unique[g]);
                 kp.mpat.push_back(M.pattern[g]);
+                const bool aff = macro_affine_enabled() && !(s->reserved[0] & FEMGPU_FLAG_INDEX_LOADS);
+                kp.maff.push_back(aff && g < M.aoff.size() ? M.aoff[g] : std::vector<int>{});
             }
             kp.tgroup = I.test_group;
             kp.cgroup = sig.affine ? I.coord_group : -1;

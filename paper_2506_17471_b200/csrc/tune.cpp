@@ -80,7 +80,7 @@ std::pair<long long, long long> map_instr(const Signature& sig) {
 std::string tune_key(const Instance& I) {
     const Signature& sig = I.sig;
     std::ostringstream k;
-    k << "v17|" << sig.dim << "|" << sig.Q << "|" << sig.nW << "|" << sig.Tw << "|" << I.cells << "|" << I.output_size;
+    k << "v18|" << sig.dim << "|" << sig.Q << "|" << sig.nW << "|" << sig.Tw << "|" << I.cells << "|" << I.output_size;
     for (size_t i = 0; i < sig.sdofs.size(); ++i) k << "|s" << sig.sdofs[i] << ":" << sig.sterms[i];
     for (size_t i = 0; i < sig.vdofs.size(); ++i) {
         k << "|v" << sig.vdofs[i] << ":" << sig.vterms[i];
@@ -122,6 +122,7 @@ std::string describe_plan(const KernelPlan& kp) {
         case Family::Macro:
             s << "femgpu_macro G=" << kp.G << " block=" << kp.block << (kp.qmajor ? " q-major" : "")
               << (kp.qmajor && !(kp.qmopt & 16) ? " unrolled" : "") << ((kp.qmopt & 16384) ? " 2q/trip" : "")
+              << (std::any_of(kp.maff.begin(), kp.maff.end(), [](const std::vector<int>& a) { return !a.empty(); }) ? " affine-idx" : "")
               << (kp.msplit > 1 ? " split=" + std::to_string(kp.msplit) : std::string())
               << (!kp.merge.empty() ? " warp-merge=" + std::to_string(kp.merge.size()) : std::string()) << (kp.ysmem ? " y-smem" : "");
             break;
@@ -529,6 +530,29 @@ void autotune(Instance& I) {
     if (!first.empty()) {
         I.auto_sched = C[first[win].second].s;
         log << "; re-timed top " << top << ", winner " << C[first[win].second].label;
+        // a macro winner on an affine index pattern: its twin that loads every index instead
+        // (the offset form changes register allocation; C5-hyp-P1 measured it 1.6 % slower)
+        const KernelPlan& wk = C[first[win].second].kp;
+        const bool aff = wk.family == Family::Macro &&
+                         std::any_of(wk.maff.begin(), wk.maff.end(), [](const std::vector<int>& a) { return !a.empty(); });
+        if (aff) {
+            femgpu_schedule tw = I.auto_sched;
+            tw.reserved[0] |= FEMGPU_FLAG_INDEX_LOADS;
+            try {
+                const KernelPlan kt = resolve_schedule(I, &tw);
+                run_action(I, kt, I.d_y, I.stream);  // JIT + module load outside the timing
+                const int reps = reps_of[first[win].second];
+                double ta = 1e300, tl = 1e300;
+                for (int round = 0; round < 2; ++round) {
+                    ta = std::min(ta, time_it(wk, reps));
+                    tl = std::min(tl, time_it(kt, reps));
+                }
+                log << "; affine index offsets " << us(ta) << " us vs index loads " << us(tl) << " us";
+                if (tl < ta) I.auto_sched = tw;
+            } catch (const Error& e) {
+                if (e.code != FEMGPU_E_INFEASIBLE && e.code != FEMGPU_E_JIT) throw;
+            }
+        }
     }
     // ---- rank agreement of the model with the measurements (Spearman over the timed candidates)
     double rho = 0.0;

@@ -201,3 +201,29 @@ def test_scpt_rolled_quadrature_loop(oracle, form, dim, deg, Q, n):
     with fg.GpuInstance(p) as g:
         for G in (1, 2):
             close(g.action(fg.TilingParams.scpt(scatter=abi.SCATTER_ATOMIC, group_cells=G, stage_smem=4)), ref)
+
+
+@pytest.mark.parametrize("form,dim,deg,Q,n,G", [("laplace", 3, 2, 4, 4, 6), ("mass", 2, 1, 3, 16, 4), ("advection", 3, 1, 4, 4, 6),
+                                                ("helmholtz_coef", 2, 3, 12, 6, 4)])
+@pytest.mark.parametrize("stage", [0, 3])
+def test_macro_affine_offsets_match_index_loads(oracle, form, dim, deg, Q, n, G, stage):
+    """Macro kernels on a lattice-numbered mesh: one index load per map group plus compile-time
+    offsets (the default) and the twin that loads every index agree with the reference."""
+    p = fg.mesh_problem(form, dim, deg, Q, n)
+    ref = oracle.reference_action(p)
+    with fg.GpuInstance(p) as g:
+        for loads in (False, True):
+            s = fg.TilingParams.scpt(scatter=abi.SCATTER_MACRO, group_cells=G, stage_smem=stage, index_loads=loads)
+            assert ("affine-idx" in g.describe(s)) != loads
+            close(g.action(s), ref)
+
+
+def test_automatic_schedule_keeps_its_index_mode_through_the_python_schedule():
+    p = fg.config_problem("C2", n=40)  # 384k cells: timed automatic schedule, macro winner
+    with fg.GpuInstance(p) as g:
+        y = g.action()
+        s = g.default_schedule()
+        d = g.describe()
+        if d.startswith("femgpu_macro"):
+            assert ("affine-idx" in d.split(" | ")[0]) != s.index_loads
+        assert rel_l2(g.action(s), y) <= 1e-12

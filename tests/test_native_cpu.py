@@ -127,3 +127,26 @@ def test_reference_counters_through_the_abi_equal_golden(case):
     (golden vectors written by the reference build, form.hpp:463-472)."""
     p = synth(case)
     assert tuple(fg.reference_counters(p)) == tuple(GOLDEN["counters:" + key(case)])
+
+
+@pytest.mark.parametrize("stage", [0, 3])
+def test_macro_affine_index_pattern(stage):
+    """A lattice-numbered structured mesh: every cell group's unique nodes are one base plus fixed
+    offsets, so the macro kernels load one index per map group (MacroLayout::aoff);
+    FEMGPU_FLAG_INDEX_LOADS and a renumbered mesh fall back to one load per unique node."""
+    p = fg.mesh_problem("laplace", 3, 2, 4, 3)
+    s = fg.TilingParams.scpt(scatter=abi.SCATTER_MACRO, group_cells=6, stage_smem=stage)
+    body = fg.emit_source(p, s).split("_checked(")[0]
+    assert "const int igb" in body and body.count("__ldg(&P.gidx") == 2  # node map + coordinate map
+    s.index_loads = True
+    body = fg.emit_source(p, s).split("_checked(")[0]
+    assert "igb" not in body and body.count("__ldg(&P.gidx") > 27
+    s.index_loads = False
+    rng = np.random.default_rng(3)
+    perm = rng.permutation(p.scalar_inputs[0].size).astype(np.int32)
+    maps = {id(m): m for m in (p.connectivity.scalar_maps[0], p.connectivity.test_map)}
+    for m in maps.values():
+        m.indices[:] = perm[m.indices]
+    body = fg.emit_source(p, s).split("_checked(")[0]
+    assert body.count("const int igb") == 1  # only the (unpermuted) coordinate map stays affine
+    fg.jit_check(p, s)
