@@ -994,10 +994,6 @@ void emit_tile_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const 
     o.line("}");
 }
 
-// Macro-element kernel: one thread per group of G cells sharing the compile-time pattern.
-// Gathers each unique node of the group once, computes the G cells in order with the
-// per-cell operation order of the reference, accumulates y per unique node in registers
-// (cells ascending), and issues one red.global.add.f64 per unique test DOF.
 // Affine index pattern of a map group (MacroLayout::aoff): one index load per cell group, the
 // unique nodes at compile-time offsets from it (address arithmetic folds into the loads' immediates).
 bool macro_affine(const KernelPlan& kp, int g) {
@@ -1017,6 +1013,10 @@ std::string macro_index(const KernelPlan& kp, int g, int u) {
     return off ? "(igb" + S(g) + " + " + S(off) + ")" : "igb" + S(g);
 }
 
+// Macro-element kernel: one thread per group of G cells sharing the compile-time pattern.
+// Gathers each unique node of the group once, computes the G cells in order with the
+// per-cell operation order of the reference, accumulates y per unique node in registers
+// (cells ascending), and issues one red.global.add.f64 per unique test DOF.
 void emit_macro_kernel(Out& o, const Signature& sig, const KernelPlan& kp, const MapUse& use, bool unroll_q,
                        const std::string& name, long long smem_tab_off, long long ysmem_off = 0) {
     const int D = sig.dim;

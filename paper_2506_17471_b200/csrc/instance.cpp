@@ -786,6 +786,7 @@ void host_macro_plan(const femgpu_problem* p, const Signature& sig, KernelPlan& 
     kp.qmajor = (s->reserved[3] & 0xff) == 3;
     kp.msplit = kp.qmajor ? std::max(1, (s->reserved[3] >> 8) & 0xff) : 1;
     kp.qmopt = kp.qmajor ? (s->reserved[3] >> 16) & 0xffff : 0;
+    if (kp.qmajor && kp.msplit == 1 && (kp.qmopt & 96)) kp.maff.assign(kp.maff.size(), {});  // as resolve_schedule
     kp.block = s->block_cells > 0 ? s->block_cells : 64;
     check_macro_split(kp);
     const int reg_target = s->reserved[1] > 0 ? s->reserved[1] : 168;
@@ -979,6 +980,8 @@ KernelPlan resolve_schedule_impl(Instance& I, const femgpu_schedule* s) {
                 const bool aff = macro_affine_enabled() && !(s->reserved[0] & FEMGPU_FLAG_INDEX_LOADS);
                 kp.maff.push_back(aff && g < M.aoff.size() ? M.aoff[g] : std::vector<int>{});
             }
+            // the persistent / cp.async-staged q-major variants loop over groups: no base offsets
+            if (kp.qmajor && kp.msplit == 1 && (kp.qmopt & 96)) kp.maff.assign(kp.maff.size(), {});
             kp.tgroup = I.test_group;
             kp.cgroup = sig.affine ? I.coord_group : -1;
             for (const auto& sp : I.sspaces) kp.sgroup.push_back(sp.group);
